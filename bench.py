@@ -1,0 +1,387 @@
+"""Benchmark of the B200 MLMC level-correction sampler (driver contract).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...        (N > 1)
+
+Workload (BASELINE.json configs[1], "C2"): GBM dS = 0.05 S dt + 0.2 S dW,
+S0 = 1, T = 1; levels 0..10; fp32 low-precision legs with the linear:16
+approximate inverse CDF; with and without Kahan; 2^22 paths per level per
+GPU (weak scaling); every path runs all four coupled legs and all three
+moment families -- exactly what the reference's estimate_level_stats /
+run_coupled_paths return (mlmc.hpp:67-149).  One "step" = the whole sweep
+(11 levels x 2 Kahan settings = 22 level launches).  Path bases follow the
+reference's four-way experiment (experiments.hpp:185-194): (l << 40) |
+(kahan << 36).
+
+metric: fine path-steps per second (paths x 2^level, summed over the sweep).
+value:  device-timed (CUDA events on the launching stream), parameters and
+        tables already resident, max over ranks.
+e2e:    through the public API (lpmc_level_partials + gather + fold +
+        LevelStats per level), host buffers, wall clock with syncs.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Euler-Maruyama path-steps/sec per MLMC level & precision; % of FP roofline"
+UNIT = "path-steps/s"
+LEVELS = list(range(0, 11))
+KAHAN = (False, True)
+PATHS_PER_GPU = 1 << 22
+SEED = 1
+WORKLOAD = ("BASELINE config 2: GBM(mu=0.05, sigma=0.2, S0=1, T=1), levels 0..10, fp32 bar legs, "
+            "linear:16 approximate inverse CDF, +-Kahan, 2^22 paths per level per GPU, all four "
+            "coupled legs (fp64 exact + fp32 approx, fine + coarse) -> d_hat, d_bar, d_four "
+            "moments (estimate_level_stats semantics)")
+PROFILE_CONST = os.path.join(ROOT, "profiles", "fp64_ops_per_path_step.json")
+
+
+def path_base(level: int, kahan: bool) -> int:
+    return (level << 40) | (int(kahan) << 36)
+
+
+def fine_steps(level: int, n: int) -> int:
+    return n << level
+
+
+# --------------------------------------------------------------- clocks -----
+class ClockSampler:
+    """nvidia-smi sampling during the timed region (recipe's clocks line)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        try:
+            fd, self.path = tempfile.mkstemp(suffix=".csv")
+            os.close(fd)
+            self.f = open(self.path, "w")
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.f.close()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        with open(self.path) as f:
+            for line in f:
+                parts = [p.strip() for p in line.split(",")]
+                if len(parts) < 9:
+                    continue
+                try:
+                    sm.append(float(parts[1]))
+                    mx.append(float(parts[2]))
+                except ValueError:
+                    continue
+                for name, v in zip(names, parts[5:9]):
+                    if v.lower().startswith("active"):
+                        reasons.add(name)
+        os.unlink(self.path)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------------ reference -----
+def run_reference(args, rank: int) -> None:
+    """--impl reference: the reference's own CPU run_coupled_paths (oracle/_ref,
+    compiled from /root/reference's headers) on all host cores, on a bounded
+    sample of the same workload; the oracle restatement if _ref is absent."""
+    if rank != 0:
+        return
+    from oracle.bind import Oracle, Reference
+    threads = os.cpu_count() or 1
+    sample = 1 << 13  # paths per (level, kahan) per step
+    if Reference.available():
+        R = Reference()
+        kind = "reference"
+
+        def one(level, kahan):
+            rc, msg, _ = R.run_coupled_paths(level=level, mantissa_bits=23, approx="linear:16",
+                                             kahan=kahan, n=sample, seed=SEED,
+                                             path_base=path_base(level, kahan), threads=threads)
+            assert rc == 0, msg
+    else:
+        O = Oracle()
+        kind = "port"
+
+        def one(level, kahan):
+            cfg = O.config(level=level, mantissa_bits=23, approx="linear:16", kahan=kahan,
+                           seed=SEED)
+            rc, _, _ = O.run_sequential(cfg, sample, path_base(level, kahan), threads=threads)
+            assert rc == 0
+
+    work = sum(fine_steps(l, sample) for l in LEVELS for _ in KAHAN)
+    for _ in range(args.warmup):
+        for l in LEVELS:
+            for k in KAHAN:
+                one(l, k)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        for l in LEVELS:
+            for k in KAHAN:
+                one(l, k)
+    dt = time.perf_counter() - t0
+    value = work * args.steps / dt
+    desc = (f"{sample} paths per (level, kahan) per step, levels 0..10, +-Kahan, fp32 linear:16, "
+            f"all four legs; {threads} threads")
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64+f32", "data": "synthetic (seeded counter RNG)",
+            "impl": "reference",
+            "config": {"workload": WORKLOAD, "sample_paths_per_level": sample},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind,
+                             "sample": desc},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def cpu_baseline_sample() -> dict:
+    """The reference timed on this host on a bounded sample (~10-30 core-s)."""
+    from oracle.bind import Oracle, Reference
+    threads = os.cpu_count() or 1
+    sample = 1 << 14
+    work = sum(fine_steps(l, sample) for l in LEVELS for _ in KAHAN)
+    t0 = time.perf_counter()
+    if Reference.available():
+        R = Reference()
+        kind = "reference"
+        for l in LEVELS:
+            for k in KAHAN:
+                rc, msg, _ = R.run_coupled_paths(level=l, mantissa_bits=23, approx="linear:16",
+                                                 kahan=k, n=sample, seed=SEED,
+                                                 path_base=path_base(l, k), threads=threads)
+                assert rc == 0, msg
+    else:
+        O = Oracle()
+        kind = "port"
+        for l in LEVELS:
+            for k in KAHAN:
+                cfg = O.config(level=l, mantissa_bits=23, approx="linear:16", kahan=k, seed=SEED)
+                rc, _, _ = O.run_sequential(cfg, sample, path_base(l, k), threads=threads)
+                assert rc == 0
+    dt = time.perf_counter() - t0
+    return {"value": work / dt, "unit": UNIT, "cores": threads, "kind": kind,
+            "sample": f"{sample} paths per (level 0..10, +-Kahan) = {work:.3e} fine path-steps, "
+                      f"all four legs, {dt:.2f} s wall on {threads} threads"}
+
+
+# ------------------------------------------------------------------ ours ----
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        run_reference(args, rank)
+        return
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_2012_09739_b200 as L
+    from paper_2012_09739_b200.sharded import allgather_partials, shard_chunks
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    model = L.make_gbm(0.05, 0.2, 1.0, 1.0)
+    spec = L.PrecisionSpec.fp32()
+    approx = L.InvCdfApprox.parse("linear:16")
+    n_total = PATHS_PER_GPU * world  # weak scaling
+    n_chunks = n_total // (1 << 18)
+    c0, c1 = shard_chunks(n_chunks, rank, world)
+    cfgs = [(l, k) for l in LEVELS for k in KAHAN]
+    plans = {(l, k): L.LevelPlan(model, l, spec, approx, k, n_total, SEED, path_base(l, k),
+                                 chunks=(c0, c1), device=local) for (l, k) in cfgs}
+    stream = torch.cuda.current_stream(dev)
+    sptr = stream.cuda_stream
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+    def sweep(events=None):
+        for (l, k) in cfgs:
+            if events is not None:
+                events[(l, k)][0].record(stream)
+            plans[(l, k)].launch(sptr)
+            if events is not None:
+                events[(l, k)][1].record(stream)
+
+    def gather_all():
+        out = {}
+        for (l, k) in cfgs:
+            part = plans[(l, k)].collect_partials()
+            full = allgather_partials(part, n_chunks, None, dev) if world > 1 else part
+            out[(l, k)] = L.fold_partials(full)
+        return out
+
+    # warm-up (also a correctness pass of the collective path)
+    for _ in range(max(args.warmup, 1)):
+        sweep()
+        torch.cuda.synchronize(dev)
+        results = gather_all()
+
+    clocks = ClockSampler(local)
+    if rank == 0:
+        clocks.start()
+    L.reset_launch_count()
+    per_step_ms = []
+    per_cfg_ms = {c: [] for c in cfgs}
+    barrier()
+    torch.cuda.synchronize(dev)
+    for _ in range(args.steps):
+        flush.zero_()  # L2 flush (256 MiB > 126 MB L2), outside the events
+        ev = {c: (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+              for c in cfgs}
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t0.record(stream)
+        sweep(ev)
+        t1.record(stream)
+        torch.cuda.synchronize(dev)
+        per_step_ms.append(t0.elapsed_time(t1))
+        for c in cfgs:
+            per_cfg_ms[c].append(ev[c][0].elapsed_time(ev[c][1]))
+        results = gather_all()  # results of every timed step are produced
+    barrier()
+    torch.cuda.synchronize(dev)
+    launches = L.launch_count()
+    clk = clocks.stop() if rank == 0 else {}
+
+    step_ms = sum(per_step_ms) / len(per_step_ms)
+    t = torch.tensor([step_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    step_ms_max = float(t.item())
+    work_total = sum(fine_steps(l, n_total) for (l, k) in cfgs)
+    value = work_total / (step_ms_max * 1e-3)
+
+    # ---- e2e through the public API (host buffers, syncs, gather, fold) ----
+    lib = L.api.N.load()
+    e2e_steps = max(1, min(args.steps, 3))
+    barrier()
+    torch.cuda.synchronize(dev)
+    w0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        for (l, k) in cfgs:
+            part = L.level_partials(model, l, spec, approx, k, n_total, SEED, path_base(l, k),
+                                    c0, c1, device=local)
+            full = allgather_partials(part, n_total // (1 << 18), None, dev) if world > 1 \
+                else part
+            m = L.fold_partials(full)
+            L.level_stats_from_moments(m, l, spec, k, n_total)
+    torch.cuda.synchronize(dev)
+    barrier()
+    e2e_s = (time.perf_counter() - w0) / e2e_steps
+    te = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_value = work_total / float(te.item())
+    table_bytes = 7 * 16 * 8
+    h2d = len(cfgs) * (table_bytes + 12)  # table + failure-word/flag init
+    d2h = len(cfgs) * ((c1 - c0) * 15 * 8 + 12)
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    # ---- roofline of the dominant kernel (level 10) --------------------------
+    peaks = L.measure_pipe_peaks(local)
+    dom = [(10, False), (10, True)]
+    dom_ms = statistics.mean(statistics.mean(per_cfg_ms[c]) for c in dom)
+    dom_steps = fine_steps(10, (c1 - c0) * (1 << 18))
+    ops_per_step = None
+    if os.path.exists(PROFILE_CONST):
+        with open(PROFILE_CONST) as f:
+            ops_per_step = json.load(f).get("fp64_lane_ops_per_path_step")
+    if ops_per_step:
+        achieved = ops_per_step * dom_steps / (dom_ms * 1e-3)
+        roof = {"bound": "fp64", "achieved": achieved / 1e12, "peak": peaks["fp64_ops_per_s"] / 1e12,
+                "unit": "Tops/s (fp64 lane-ops)", "frac": achieved / peaks["fp64_ops_per_s"],
+                "traffic": None,
+                "note": "non-tensor FP64-pipe bound (neither HBM nor tensor): per-path state in "
+                        "registers, 0 bytes per path-step; ops/step from ncu "
+                        "(profiles/fp64_ops_per_path_step.json), peak = measured FMA lane rate"}
+    else:
+        roof = {"bound": "fp64", "achieved": None, "peak": peaks["fp64_ops_per_s"] / 1e12,
+                "unit": "Tops/s (fp64 lane-ops)", "frac": None, "traffic": None,
+                "note": "ops per path-step not yet profiled"}
+
+    cpu = None if args.no_cpu_baseline else cpu_baseline_sample()
+    per_level = {}
+    for l in LEVELS:
+        ms = sum(statistics.mean(per_cfg_ms[(l, k)]) for k in KAHAN)
+        per_level[str(l)] = fine_steps(l, (c1 - c0) * (1 << 18)) * 2 / (ms * 1e-3)
+    out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": step_ms_max, "higher_is_better": True,
+           "scaling": "weak", "vs_baseline": None, "dtype": "f64+f32",
+           "data": "synthetic (seeded counter-based RNG; no dataset)",
+           "config": {"workload": WORKLOAD, "paths_per_level_per_gpu": PATHS_PER_GPU,
+                      "levels": "0..10", "kahan": [False, True], "precision": "fp32",
+                      "approx": "linear:16", "legs": "all", "reduce": "tree",
+                      "parallelism": f"paths sharded by 2^18-path chunks over {world} GPU(s); "
+                                     "one all_gather of chunk moments",
+                      "l2": "flushed between timed steps (256 MiB write); kernels read no "
+                            "input tensors"},
+           "gpu_launches": int(launches),
+           "clocks": clk,
+           "roofline": roof,
+           "pipe_peaks_measured": peaks,
+           "per_level_path_steps_per_s_per_gpu": per_level,
+           "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
+                   "d2h_bytes_per_step": d2h},
+           "cpu_baseline": cpu,
+           "check": {"v_hat_l10": results[(10, False)].d_hat.variance(),
+                     "v_bar_l10": results[(10, False)].d_bar.variance(),
+                     "V_bar_l10": results[(10, False)].d_four.variance(),
+                     "V_bar_l10_kahan": results[(10, True)].d_four.variance()}}
+    print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

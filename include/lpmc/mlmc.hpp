@@ -1,0 +1,146 @@
+// Drop-in for the level-sampling part of the reference's lpmc/mlmc.hpp
+// (proj/include/lpmc/mlmc.hpp:20-149): CostModel, LevelStats,
+// CoupledMoments, run_coupled_paths, estimate_level_stats.  Both entry points
+// keep the reference signatures; the work runs on the sm_100a kernels behind
+// lpmc_run_coupled_paths / lpmc_estimate_level_stats.  `threads` only
+// scheduled the CPU reference and never changed its result (mlmc.hpp:4-5);
+// it is accepted and ignored.
+//
+// Extension: an optional trailing DeviceOptions selects legs, payoff,
+// reduction order, device and stream.
+#pragma once
+
+#include <cstdint>
+#include <stdexcept>
+
+#include "../lpmc_b200.h"
+#include "error.hpp"
+#include "invcdf_approx.hpp"
+#include "sde.hpp"
+#include "softfloat.hpp"
+#include "stats.hpp"
+
+namespace lpmc {
+
+struct CostModel {
+  double cycles_exact_rng = 3.5;
+  double cycles_approx_rng_single = 0.5;
+  double cycles_approx_rng_half = 0.25;
+  double kahan_overhead_factor = 1.4;
+  double per_step_arithmetic = 0.0;
+
+  double approx_rng_cycles(const PrecisionSpec& spec) const {
+    return spec.mantissa_bits <= 10 ? cycles_approx_rng_half : cycles_approx_rng_single;
+  }
+  lpmc_cost_model c_abi() const {
+    return lpmc_cost_model{cycles_exact_rng, cycles_approx_rng_single, cycles_approx_rng_half,
+                           kahan_overhead_factor, per_step_arithmetic};
+  }
+};
+
+struct LevelStats {
+  int level = 0;
+  double mean_hat = 0.0, v_hat = 0.0, v_hat_stderr = 0.0;
+  double mean_bar = 0.0, v_bar = 0.0, v_bar_stderr = 0.0;
+  double mean_four = 0.0, V_bar = 0.0, V_bar_stderr = 0.0;
+  double c_hat = 0.0, c_bar = 0.0, C_bar = 0.0;
+  std::uint64_t m_hat = 0, m_bar = 0, M_bar = 0;
+};
+
+struct CoupledMoments {
+  MomentAccumulator d_hat;
+  MomentAccumulator d_bar;
+  MomentAccumulator d_four;
+
+  void merge(const CoupledMoments& other) {
+    d_hat.merge(other.d_hat);
+    d_bar.merge(other.d_bar);
+    d_four.merge(other.d_four);
+  }
+};
+
+// Extension knobs (defaults reproduce the reference).
+struct DeviceOptions {
+  unsigned legs = LPMC_LEGS_ALL;
+  int payoff = LPMC_PAYOFF_TERMINAL;
+  double strike = 1.0;
+  int reduce = LPMC_REDUCE_TREE;
+  int device = -1;
+  void* stream = nullptr;
+
+  lpmc_options c_abi() const { return lpmc_options{legs, payoff, strike, reduce, device, stream}; }
+};
+
+namespace detail {
+inline lpmc_gbm gbm_of(const SdeModel& model) {
+  if (!model.gbm)
+    throw std::invalid_argument("the device sampler supports GBM models built by make_gbm");
+  return lpmc_gbm{model.gbm->mu, model.gbm->sigma, model.x0, model.horizon};
+}
+}  // namespace detail
+
+inline CoupledMoments run_coupled_paths(const SdeModel& model, int level,
+                                        const PrecisionSpec& spec_low,
+                                        const InvCdfApprox* approx, bool kahan,
+                                        std::uint64_t n_paths, std::uint64_t seed,
+                                        std::uint64_t path_base, int threads = 1,
+                                        const DeviceOptions& options = {}) {
+  (void)threads;
+  const lpmc_gbm g = detail::gbm_of(model);
+  const lpmc_precision p = spec_low.c_abi();
+  const lpmc_options o = options.c_abi();
+  lpmc_invcdf_table t{};
+  if (approx != nullptr) t = approx->c_abi();
+  lpmc_moments acc[3];
+  lpmc_error err{};
+  detail::throw_status(lpmc_run_coupled_paths(&g, level, &p, approx ? &t : nullptr, kahan ? 1 : 0,
+                                              n_paths, seed, path_base, &o, acc, &err),
+                       err);
+  CoupledMoments m;
+  m.d_hat = MomentAccumulator(acc[0]);
+  m.d_bar = MomentAccumulator(acc[1]);
+  m.d_four = MomentAccumulator(acc[2]);
+  return m;
+}
+
+inline LevelStats estimate_level_stats(const SdeModel& model, int level,
+                                       const PrecisionSpec& spec_low,
+                                       const InvCdfApprox* approx, bool kahan,
+                                       std::uint64_t n_paths, std::uint64_t seed,
+                                       const CostModel& cost = {}, int threads = 1,
+                                       std::uint64_t path_base = 0,
+                                       const DeviceOptions& options = {}) {
+  (void)threads;
+  const lpmc_gbm g = detail::gbm_of(model);
+  const lpmc_precision p = spec_low.c_abi();
+  const lpmc_options o = options.c_abi();
+  const lpmc_cost_model c = cost.c_abi();
+  lpmc_invcdf_table t{};
+  if (approx != nullptr) t = approx->c_abi();
+  lpmc_level_stats s{};
+  lpmc_error err{};
+  detail::throw_status(lpmc_estimate_level_stats(&g, level, &p, approx ? &t : nullptr,
+                                                 kahan ? 1 : 0, n_paths, seed, &c, path_base, &o,
+                                                 &s, &err),
+                       err);
+  LevelStats r;
+  r.level = s.level;
+  r.mean_hat = s.mean_hat;
+  r.v_hat = s.v_hat;
+  r.v_hat_stderr = s.v_hat_stderr;
+  r.mean_bar = s.mean_bar;
+  r.v_bar = s.v_bar;
+  r.v_bar_stderr = s.v_bar_stderr;
+  r.mean_four = s.mean_four;
+  r.V_bar = s.V_bar;
+  r.V_bar_stderr = s.V_bar_stderr;
+  r.c_hat = s.c_hat;
+  r.c_bar = s.c_bar;
+  r.C_bar = s.C_bar;
+  r.m_hat = s.m_hat;
+  r.m_bar = s.m_bar;
+  r.M_bar = s.M_bar;
+  return r;
+}
+
+}  // namespace lpmc

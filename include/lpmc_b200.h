@@ -1,0 +1,286 @@
+/*
+ * lpmc_b200.h — C-ABI of the B200-native MLMC level-correction sampler.
+ *
+ * This is the drop-in boundary under the reference's level-sampling entry
+ * points (reference: /root/reference/proj/include/lpmc/mlmc.hpp).  Plain C
+ * types only: pointers, sizes and PODs; no CUDA or C++ types in signatures.
+ * The C++ headers in include/lpmc/ (the reference-compatible API) and the
+ * Python package paper_2012_09739_b200 both bind to exactly these symbols.
+ *
+ * Replaced reference interfaces (file:line under /root/reference/proj):
+ *   lpmc_run_coupled_paths      <- run_coupled_paths       include/lpmc/mlmc.hpp:67-111
+ *   lpmc_estimate_level_stats   <- estimate_level_stats    include/lpmc/mlmc.hpp:113-149
+ *   lpmc_simulate_paths         <- simulate_coupled        include/lpmc/sde.hpp:211-284
+ *                                  (batched per-path dump, for parity only)
+ *   lpmc_invcdf_build           <- InvCdfApprox::build     include/lpmc/invcdf_approx.hpp:101-145
+ *   lpmc_invcdf_eval            <- InvCdfApprox::operator() include/lpmc/invcdf_approx.hpp:44-50
+ *   lpmc_round_to_precision     <- round_to_precision      include/lpmc/softfloat.hpp:69-80
+ *   lpmc_moments_add / _merge   <- MomentAccumulator::add / merge  include/lpmc/stats.hpp:15-54
+ *   lpmc_level_partials +       <- the batch loop + index-order merge of
+ *   lpmc_fold_partials             run_coupled_paths (mlmc.hpp:74-110), split
+ *                                  so paths can be sharded over GPUs/ranks
+ *
+ * Error contract: every entry point returns an lpmc_status.  The values map
+ * one-to-one onto the exception types the reference throws
+ * (std::invalid_argument, std::domain_error, std::runtime_error); the
+ * message text in lpmc_error.message is the reference's what() string.
+ * LPMC_CUDA_ERROR / LPMC_NO_DEVICE have no reference counterpart: there is no
+ * CPU fallback, a device failure is reported, never papered over.
+ */
+#ifndef LPMC_B200_H_
+#define LPMC_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LPMC_B200_ABI_VERSION 1
+
+typedef enum lpmc_status {
+  LPMC_OK = 0,
+  LPMC_INVALID_ARGUMENT = 1, /* std::invalid_argument */
+  LPMC_DOMAIN_ERROR = 2,     /* std::domain_error     */
+  LPMC_RUNTIME_ERROR = 3,    /* std::runtime_error    */
+  LPMC_CUDA_ERROR = 4,       /* device/driver failure */
+  LPMC_NO_DEVICE = 5         /* no usable sm_100 device */
+} lpmc_status;
+
+/* Which first failure a path hit (lpmc_error.kind). */
+typedef enum lpmc_fail_kind {
+  LPMC_FAIL_NONE = 0,
+  LPMC_FAIL_UNIFORM_IS_ONE = 1, /* u == 1.0 reached exact_inv_cdf (gaussian.hpp:60-61) */
+  LPMC_FAIL_NONFINITE = 2,      /* non-finite operand (softfloat.hpp:70)               */
+  LPMC_FAIL_NONFINITE_STATE = 3 /* IEEE-half legs only: non-finite state (sde.hpp:120)  */
+} lpmc_fail_kind;
+
+typedef struct lpmc_error {
+  int32_t status;      /* lpmc_status */
+  int32_t kind;        /* lpmc_fail_kind, for sampler failures */
+  uint64_t path_index; /* global path index (path_base + i) of the first failing path */
+  uint64_t step;       /* fine step index of the first failure in that path */
+  char message[192];   /* reference what() text, or a CUDA error string */
+} lpmc_error;
+
+/* GBM dS = mu S dt + sigma S dW on [0, horizon] (make_gbm, sde.hpp:32-44). */
+typedef struct lpmc_gbm {
+  double mu, sigma, x0, horizon;
+} lpmc_gbm;
+
+typedef enum lpmc_approx_kind {
+  LPMC_APPROX_LINEAR = 0,  /* InvCdfApprox::Kind::linear */
+  LPMC_APPROX_CUBIC = 1,   /* InvCdfApprox::Kind::cubic  */
+  LPMC_APPROX_CONSTANT = 2 /* extension (BASELINE config 3): degree-0 Legendre projection */
+} lpmc_approx_kind;
+
+/*
+ * Host copy of an InvCdfApprox table (invcdf_approx.hpp:92-98).  The device
+ * layout is private; the library uploads what it needs per call.
+ */
+typedef struct lpmc_invcdf_table {
+  int32_t kind;           /* lpmc_approx_kind */
+  int32_t interval_count; /* K, a power of two >= 2 */
+  double w_max;
+  double step_w;
+  double tail_value;
+  const double* breakpoints; /* K ascending interior breakpoints in (1/2, 1) */
+  const double* coeff;       /* K x 4 Legendre coefficients, row-major */
+} lpmc_invcdf_table;
+
+/*
+ * Arithmetic of the low-precision ("bar") legs.  mantissa_bits follows
+ * PrecisionSpec (softfloat.hpp:18-64): 1..51 = emulated round-to-nearest-even
+ * with an unbounded exponent, >= 52 = the binary64 carrier.  ieee_half = 1
+ * selects native IEEE binary16 legs (BASELINE config 3; requires
+ * mantissa_bits == 10): subnormals and the 65504 overflow are IEEE, so these
+ * legs are pinned against an IEEE restatement, not the emulated reference.
+ */
+typedef struct lpmc_precision {
+  int32_t mantissa_bits;
+  int32_t ieee_half;
+} lpmc_precision;
+
+enum {
+  LPMC_LEGS_HAT = 1, /* carrier legs, exact Gaussians: d_hat only */
+  LPMC_LEGS_BAR = 2, /* low-precision legs: d_bar only            */
+  LPMC_LEGS_ALL = 3  /* all four legs (the reference always runs these) */
+};
+
+enum {
+  LPMC_PAYOFF_TERMINAL = 0, /* P(S) = S_T (the reference's quantity) */
+  LPMC_PAYOFF_CALL = 1      /* extension (config 4): max(S_T - strike, 0) in fp64 */
+};
+
+enum {
+  LPMC_REDUCE_TREE = 0,      /* fixed two-pass/Pebay tree; GPU-count independent */
+  LPMC_REDUCE_SEQUENTIAL = 1 /* the reference's own add/merge order, bitwise */
+};
+
+typedef struct lpmc_options {
+  uint32_t legs;  /* LPMC_LEGS_*; 0 means LPMC_LEGS_ALL */
+  int32_t payoff; /* LPMC_PAYOFF_* */
+  double strike;  /* for LPMC_PAYOFF_CALL */
+  int32_t reduce; /* LPMC_REDUCE_* */
+  int32_t device; /* CUDA ordinal; -1 = current device */
+  void* stream;   /* cudaStream_t to launch on; NULL = the library's stream */
+} lpmc_options;
+
+/* Raw MomentAccumulator state (stats.hpp:84-89). */
+typedef struct lpmc_moments {
+  uint64_t n;
+  double mean, m2, m3, m4;
+} lpmc_moments;
+
+/* CostModel (mlmc.hpp:20-34). */
+typedef struct lpmc_cost_model {
+  double cycles_exact_rng;
+  double cycles_approx_rng_single;
+  double cycles_approx_rng_half;
+  double kahan_overhead_factor;
+  double per_step_arithmetic;
+} lpmc_cost_model;
+
+/* LevelStats (mlmc.hpp:36-51). */
+typedef struct lpmc_level_stats {
+  int32_t level;
+  double mean_hat, v_hat, v_hat_stderr;
+  double mean_bar, v_bar, v_bar_stderr;
+  double mean_four, V_bar, V_bar_stderr;
+  double c_hat, c_bar, C_bar;
+  uint64_t m_hat, m_bar, M_bar;
+} lpmc_level_stats;
+
+/* Paths per reduction batch and batches per chunk (the fixed merge tree). */
+#define LPMC_BATCH_PATHS 256u
+#define LPMC_CHUNK_BATCHES 1024u
+#define LPMC_CHUNK_PATHS (LPMC_BATCH_PATHS * LPMC_CHUNK_BATCHES)
+
+/* ---- version / device ---------------------------------------------------- */
+int32_t lpmc_abi_version(void);
+/* Number of visible sm_100 devices (0 on a CPU-only host). */
+int32_t lpmc_device_count(void);
+/* Kernel launches issued by this thread since the last reset (bench evidence). */
+uint64_t lpmc_launch_count(void);
+void lpmc_reset_launch_count(void);
+void lpmc_default_options(lpmc_options* opts);
+void lpmc_default_cost_model(lpmc_cost_model* cost);
+
+/* ---- host-side numerics (no GPU needed) --------------------------------- */
+/* round_to_precision (softfloat.hpp:69-80). */
+lpmc_status lpmc_round_to_precision(double x, int32_t mantissa_bits, double* out, lpmc_error* err);
+/*
+ * InvCdfApprox::build (invcdf_approx.hpp:101-145), same operation order, so
+ * the table is bitwise the reference's.  breakpoints: K doubles; coeff: 4K.
+ */
+lpmc_status lpmc_invcdf_build(int32_t kind, int32_t interval_count, double* breakpoints,
+                              double* coeff, double* w_max, double* step_w, double* tail_value,
+                              lpmc_error* err);
+/* InvCdfApprox::operator() on the host (invcdf_approx.hpp:44-90). */
+lpmc_status lpmc_invcdf_eval(const lpmc_invcdf_table* table, double u, double* out,
+                             lpmc_error* err);
+/* MomentAccumulator::add / merge (stats.hpp:15-54), bitwise. */
+void lpmc_moments_add(lpmc_moments* acc, double x);
+void lpmc_moments_merge(lpmc_moments* acc, const lpmc_moments* other);
+/*
+ * Index-order fold of per-chunk partials (3 per chunk: d_hat, d_bar, d_four),
+ * the run_coupled_paths merge (mlmc.hpp:108-110).  out: 3 accumulators.
+ */
+void lpmc_fold_partials(const lpmc_moments* partials, uint64_t n_chunks, lpmc_moments* out);
+/* LevelStats from three accumulators + the cost model (mlmc.hpp:125-148). */
+void lpmc_level_stats_from_moments(const lpmc_moments* acc3, int32_t level,
+                                   const lpmc_precision* prec, int32_t kahan,
+                                   const lpmc_cost_model* cost, uint64_t n_paths,
+                                   lpmc_level_stats* out);
+
+/* ---- device sampler ------------------------------------------------------ */
+/*
+ * run_coupled_paths (mlmc.hpp:67-111): n_paths coupled fine/coarse x
+ * exact/approx paths at `level`; table == NULL selects the exact inverse CDF
+ * for the bar legs.  out: 3 accumulators (d_hat, d_bar, d_four).
+ */
+lpmc_status lpmc_run_coupled_paths(const lpmc_gbm* model, int32_t level,
+                                   const lpmc_precision* prec, const lpmc_invcdf_table* table,
+                                   int32_t kahan, uint64_t n_paths, uint64_t seed,
+                                   uint64_t path_base, const lpmc_options* opts,
+                                   lpmc_moments* out, lpmc_error* err);
+
+/* estimate_level_stats (mlmc.hpp:113-149).  cost may be NULL (defaults). */
+lpmc_status lpmc_estimate_level_stats(const lpmc_gbm* model, int32_t level,
+                                      const lpmc_precision* prec,
+                                      const lpmc_invcdf_table* table, int32_t kahan,
+                                      uint64_t n_paths, uint64_t seed,
+                                      const lpmc_cost_model* cost, uint64_t path_base,
+                                      const lpmc_options* opts, lpmc_level_stats* out,
+                                      lpmc_error* err);
+
+/*
+ * Shard entry point: chunk accumulators for chunks [chunk_begin, chunk_end)
+ * of an n_paths run (chunk c = paths [c*LPMC_CHUNK_PATHS, ...) relative to
+ * path_base).  out: 3*(chunk_end-chunk_begin) accumulators, chunk-major.
+ * Folding every rank's chunks with lpmc_fold_partials in chunk order gives
+ * the same bits as lpmc_run_coupled_paths for any number of ranks.
+ */
+lpmc_status lpmc_level_partials(const lpmc_gbm* model, int32_t level,
+                                const lpmc_precision* prec, const lpmc_invcdf_table* table,
+                                int32_t kahan, uint64_t n_paths, uint64_t seed,
+                                uint64_t path_base, uint64_t chunk_begin, uint64_t chunk_end,
+                                const lpmc_options* opts, lpmc_moments* out, lpmc_error* err);
+
+/*
+ * Per-path dump for parity tests: out4 = n x {x_hat_fine, x_hat_coarse,
+ * x_bar_fine, x_bar_coarse} as simulate_coupled returns them (sde.hpp:279-283),
+ * host memory.  z_out (optional, n x 2^level) receives the exact Gaussians
+ * the hat legs consumed, so the CPU can replay those legs bit for bit.
+ */
+lpmc_status lpmc_simulate_paths(const lpmc_gbm* model, int32_t level, const lpmc_precision* prec,
+                                const lpmc_invcdf_table* table, int32_t kahan, uint64_t n_paths,
+                                uint64_t seed, uint64_t path_base, const lpmc_options* opts,
+                                double* out4, double* z_out, lpmc_error* err);
+
+/*
+ * Exact Gaussians / approximate Gaussians for host-provided uniforms, on the
+ * device (the kernels' own device functions; parity tests of a2/a3).
+ */
+lpmc_status lpmc_device_inv_cdf(const double* u, uint64_t n, const lpmc_invcdf_table* table,
+                                double* out, const lpmc_options* opts, lpmc_error* err);
+
+/*
+ * Measured lane-operation rates of the current B200 (roofline denominators
+ * for this non-tensor path): out4 = {fp64 FMA, fp32 FMA, fp16 (per half lane,
+ * HFMA2), 64-bit integer multiply-add} operations per second.
+ */
+lpmc_status lpmc_measure_pipe_peaks(int32_t device, double* out4, lpmc_error* err);
+
+/* ---- plans: device-resident repeated launches (bench / sweeps) ---------- */
+typedef struct lpmc_plan lpmc_plan;
+
+lpmc_status lpmc_plan_create(const lpmc_gbm* model, int32_t level, const lpmc_precision* prec,
+                             const lpmc_invcdf_table* table, int32_t kahan, uint64_t n_paths,
+                             uint64_t seed, uint64_t path_base, const lpmc_options* opts,
+                             lpmc_plan** plan, lpmc_error* err);
+/* A plan over chunks [chunk_begin, chunk_end) only (one rank's shard). */
+lpmc_status lpmc_plan_create_range(const lpmc_gbm* model, int32_t level,
+                                   const lpmc_precision* prec, const lpmc_invcdf_table* table,
+                                   int32_t kahan, uint64_t n_paths, uint64_t seed,
+                                   uint64_t path_base, uint64_t chunk_begin, uint64_t chunk_end,
+                                   const lpmc_options* opts, lpmc_plan** plan, lpmc_error* err);
+/* Enqueue the level's kernels on `stream` (NULL = plan's stream); no sync. */
+lpmc_status lpmc_plan_launch(lpmc_plan* plan, void* stream, lpmc_error* err);
+/* Wait, copy the partials back, fold, and map device failures to errors. */
+lpmc_status lpmc_plan_collect(lpmc_plan* plan, lpmc_moments* out, lpmc_error* err);
+/* Wait and copy back the raw chunk partials (3 per chunk, chunk-major),
+ * unfolded, for a cross-rank gather. */
+lpmc_status lpmc_plan_collect_partials(lpmc_plan* plan, lpmc_moments* out, lpmc_error* err);
+/* Number of chunks the plan covers. */
+uint64_t lpmc_plan_chunk_count(const lpmc_plan* plan);
+/* Number of kernels one lpmc_plan_launch enqueues. */
+int32_t lpmc_plan_kernels_per_launch(const lpmc_plan* plan);
+void lpmc_plan_destroy(lpmc_plan* plan);
+
+#ifdef __cplusplus
+} /* extern "C" */
+#endif
+
+#endif /* LPMC_B200_H_ */

@@ -1,0 +1,80 @@
+"""Build the in-tree native library paper_2012_09739_b200/liblpmc_b200.so.
+
+    python -m paper_2012_09739_b200.build          # or __graft_entry__.build()
+
+* csrc/lpmc_kernels.cu -> nvcc -gencode arch=compute_100a,code=sm_100a
+  -O3 -fmad=false -lineinfo (no FMA contraction: the reference rounds every
+  operation separately)
+* csrc/lpmc_host.cpp   -> g++ -O2 -ffp-contract=off (host numerics that must
+  be bitwise the reference's: table build, constant rounding, moment merges)
+* linked with the static CUDA runtime so the .so only needs the driver.
+
+Sources are compiled only when newer than the library.
+"""
+from __future__ import annotations
+
+import os
+import shutil
+import subprocess
+import sys
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+CSRC = os.path.join(PKG, "csrc")
+LIB = os.path.join(PKG, "liblpmc_b200.so")
+BUILD = os.path.join(PKG, "_build")
+INCLUDE = os.path.join(os.path.dirname(PKG), "include")
+
+CUDA_HOME = os.environ.get("CUDA_HOME", "/usr/local/cuda")
+NVCC = os.path.join(CUDA_HOME, "bin", "nvcc")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+NVCC_FLAGS = ARCH + ["-O3", "-fmad=false", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
+                     "-Xptxas", "-warn-spills"]
+CXX_FLAGS = ["-O2", "-ffp-contract=off", "-fno-fast-math", "-std=c++17", "-fPIC", "-Wall",
+             "-Wextra", f"-I{CUDA_HOME}/include"]
+
+SOURCES_CU = ["lpmc_kernels.cu"]
+SOURCES_CXX = ["lpmc_host.cpp"]
+HEADERS = ["lpmc_internal.h", os.path.join("..", "..", "include", "lpmc_b200.h")]
+
+
+def _newer(target: str, deps: list[str]) -> bool:
+    if not os.path.exists(target):
+        return True
+    t = os.path.getmtime(target)
+    return any(os.path.getmtime(d) > t for d in deps)
+
+
+def _run(cmd: list[str]) -> None:
+    print(" ".join(cmd), flush=True)
+    subprocess.check_call(cmd)
+
+
+def build(force: bool = False, verbose_ptxas: bool = False) -> str:
+    os.makedirs(BUILD, exist_ok=True)
+    hdrs = [os.path.join(CSRC, h) for h in HEADERS]
+    objs = []
+    for src in SOURCES_CU:
+        s = os.path.join(CSRC, src)
+        o = os.path.join(BUILD, src + ".o")
+        if force or _newer(o, [s] + hdrs):
+            extra = ["-Xptxas", "-v"] if verbose_ptxas else []
+            _run([NVCC] + NVCC_FLAGS + extra + ["-c", s, "-o", o])
+        objs.append(o)
+    cxx = os.environ.get("CXX", shutil.which("g++") or "g++")
+    for src in SOURCES_CXX:
+        s = os.path.join(CSRC, src)
+        o = os.path.join(BUILD, src + ".o")
+        if force or _newer(o, [s] + hdrs):
+            _run([cxx] + CXX_FLAGS + ["-c", s, "-o", o])
+        objs.append(o)
+    if force or _newer(LIB, objs):
+        tmp = LIB + ".tmp"
+        _run([cxx, "-shared", "-o", tmp] + objs +
+             [f"-L{CUDA_HOME}/lib64", "-lcudart_static", "-ldl", "-lrt", "-lpthread",
+              "-Wl,--no-undefined"])
+        os.replace(tmp, LIB)
+    return LIB
+
+
+if __name__ == "__main__":
+    build(force="--force" in sys.argv, verbose_ptxas="-v" in sys.argv)

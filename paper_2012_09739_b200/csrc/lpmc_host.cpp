@@ -1,0 +1,1193 @@
+// Host side of the C-ABI (include/lpmc_b200.h): argument checking with the
+// reference's error contract, host numerics that must be bitwise the
+// reference's (table build, rounding of the per-level constants, moment
+// merges), device contexts, plans, and the index-order fold.
+//
+// Compiled with -O2 -ffp-contract=off (never contract: every double op here
+// mirrors a reference op 1:1).  No CPU sampling fallback
+// exists: if the device path fails, the call fails.
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <array>
+#include <cmath>
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "../../include/lpmc_b200.h"
+#include "lpmc_internal.h"
+
+namespace lpmc_b200 {
+namespace {
+
+constexpr uint64_t kBatch = LPMC_BATCH_PATHS;
+constexpr uint64_t kChunkBatches = LPMC_CHUNK_BATCHES;
+constexpr uint64_t kChunkPaths = LPMC_CHUNK_PATHS;
+constexpr uint64_t kSliceChunks = 64;     // paths per launch slice = 2^24
+constexpr uint64_t kSeqSliceChunks = 16;  // sequential mode keeps per-path diffs
+constexpr int kMaxK = 1024;
+
+thread_local uint64_t t_launches = 0;
+
+// ------------------------------------------------------------ errors -------
+lpmc_status fail(lpmc_error* err, lpmc_status st, const std::string& msg, int kind = 0,
+                 uint64_t path = 0, uint64_t step = 0) {
+  if (err != nullptr) {
+    err->status = st;
+    err->kind = kind;
+    err->path_index = path;
+    err->step = step;
+    std::snprintf(err->message, sizeof(err->message), "%s", msg.c_str());
+  }
+  return st;
+}
+
+lpmc_status ok(lpmc_error* err) {
+  if (err != nullptr) {
+    err->status = LPMC_OK;
+    err->kind = 0;
+    err->path_index = 0;
+    err->step = 0;
+    err->message[0] = '\0';
+  }
+  return LPMC_OK;
+}
+
+lpmc_status cuda_fail(lpmc_error* err, cudaError_t e, const char* where) {
+  return fail(err, LPMC_CUDA_ERROR, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+// --------------------------------------------------- host numerics ---------
+// round_to_precision (softfloat.hpp:69-80): RNE to m+1 significant bits,
+// unbounded exponent.  Returns false for a non-finite operand.
+bool round_prec(double x, int m, double* out) {
+  if (!std::isfinite(x)) return false;
+  if (x == 0.0 || m >= 52) {
+    *out = x;
+    return true;
+  }
+  int e = 0;
+  const double frac = std::frexp(x, &e);
+  const int p = m + 1;
+  *out = std::ldexp(std::nearbyint(std::ldexp(frac, p)), e - p);
+  return true;
+}
+
+// double -> IEEE binary16 bits, one round-to-nearest-even (== __double2half).
+uint16_t half_bits(double x) {
+  const uint16_t sign = std::signbit(x) ? 0x8000 : 0;
+  const double ax = std::fabs(x);
+  if (std::isnan(x)) return 0x7e00;
+  if (ax == 0.0) return sign;
+  if (ax < 0x1p-14) {  // subnormal range: units of 2^-24
+    const double q = std::nearbyint(ax * 0x1p24);
+    return static_cast<uint16_t>(sign | static_cast<uint16_t>(q));  // q == 1024 -> min normal
+  }
+  int e = 0;
+  const double f = std::frexp(ax, &e);  // ax = f 2^e, f in [1/2, 1)
+  double r = std::nearbyint(f * 2048.0);
+  if (r == 2048.0) {
+    r = 1024.0;
+    e += 1;
+  }
+  const int ef = e - 1 + 15;
+  if (ef >= 31 || std::isinf(x)) return static_cast<uint16_t>(sign | 0x7c00);
+  return static_cast<uint16_t>(sign | (ef << 10) | (static_cast<int>(r) - 1024));
+}
+
+// gauss_legendre (quadrature.hpp:17-41): Newton on the Legendre recurrence.
+void gauss_legendre_rule(int n, std::vector<double>& x_out, std::vector<double>& w_out) {
+  x_out.assign(n, 0.0);
+  w_out.assign(n, 0.0);
+  for (int i = 0; i < n; ++i) {
+    double x = std::cos(M_PI * (i + 0.75) / (n + 0.5));
+    double deriv = 0.0;
+    for (int iter = 0; iter < 100; ++iter) {
+      double p_prev = 1.0;
+      double p_cur = x;
+      for (int k = 2; k <= n; ++k) {
+        const double p_next = ((2.0 * k - 1.0) * x * p_cur - (k - 1.0) * p_prev) / k;
+        p_prev = p_cur;
+        p_cur = p_next;
+      }
+      deriv = n * (x * p_cur - p_prev) / (x * x - 1.0);
+      const double dx = p_cur / deriv;
+      x -= dx;
+      if (std::fabs(dx) < 1e-15) break;
+    }
+    x_out[i] = x;
+    w_out[i] = 2.0 / ((1.0 - x * x) * deriv * deriv);
+  }
+}
+
+// Host exact inverse CDF, used only to build tables (invcdf_approx.hpp:128);
+// same Acklam + Newton expression trees as gaussian.hpp:26-65.
+double host_phi_inv_lower(double u) {
+  double x;
+  if (u < 0.02425) {
+    const double q = std::sqrt(-2.0 * std::log(u));
+    const double num = ((((-7.784894002430293e-03 * q + -3.223964580411365e-01) * q +
+                          -2.400758277161838e+00) * q + -2.549732539343734e+00) * q +
+                        4.374664141464968e+00) * q + 2.938163982698783e+00;
+    const double den = (((7.784695709041462e-03 * q + 3.224671290700398e-01) * q +
+                         2.445134137142996e+00) * q + 3.754408661907416e+00) * q + 1.0;
+    x = num / den;
+  } else {
+    const double q = u - 0.5;
+    const double r = q * q;
+    const double num = ((((-3.969683028665376e+01 * r + 2.209460984245205e+02) * r +
+                          -2.759285104469687e+02) * r + 1.383577518672690e+02) * r +
+                        -3.066479806614716e+01) * r + 2.506628277459239e+00;
+    const double den = ((((-5.447609879822406e+01 * r + 1.615858368580409e+02) * r +
+                          -1.556989798598866e+02) * r + 6.680131188771972e+01) * r +
+                        -1.328068155288572e+01) * r + 1.0;
+    x = num * q / den;
+  }
+  const double resid = 0.5 * std::erfc(-x * 0.7071067811865475244) - u;
+  const double dens = 0.3989422804014326779 * std::exp(-0.5 * x * x);
+  return x - resid / dens;
+}
+
+double host_phi_inv(double u) {
+  if (u == 0.5) return 0.0;
+  return u > 0.5 ? -host_phi_inv_lower(1.0 - u) : host_phi_inv_lower(u);
+}
+
+bool valid_interval_count(int k) { return k >= 2 && (k & (k - 1)) == 0; }
+
+// The reference's interval index J(v) for v = 1 - u' (invcdf_approx.hpp:75-79),
+// K meaning "tail".
+int reference_index(double v, int K, double w_max, double step_w) {
+  const double w = -std::log2(v);
+  if (w >= w_max) return K;
+  int j = static_cast<int>((w - 1.0) / step_w);
+  if (j < 0) j = 0;
+  if (j >= K) j = K - 1;
+  return j;
+}
+
+// v-thresholds T_k = max{v on the 2^-53 grid in (0, 1/2] : J(v) >= k}, k=1..K
+// (T_K = tail).  J is non-increasing in v, so a bisection over the grid
+// integer g (v = g 2^-53) reproduces the reference on every reachable v.
+std::vector<double> index_thresholds(int K, double w_max, double step_w) {
+  static std::mutex mu;
+  static std::map<std::tuple<int, double, double>, std::vector<double>> cache;
+  std::lock_guard<std::mutex> lock(mu);
+  auto key = std::make_tuple(K, w_max, step_w);
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
+  std::vector<double> thr(K, 0.0);
+  const uint64_t g_max = 1ull << 52;  // v = 1/2
+  for (int k = 1; k <= K; ++k) {
+    auto pred = [&](uint64_t g) { return reference_index(std::ldexp(double(g), -53), K, w_max, step_w) >= k; };
+    if (!pred(1)) {
+      thr[k - 1] = 0.0;
+      continue;
+    }
+    uint64_t lo = 1, hi = g_max;  // pred(lo) true
+    if (pred(hi)) {
+      lo = hi;
+    } else {
+      while (hi - lo > 1) {
+        const uint64_t mid = lo + (hi - lo) / 2;
+        if (pred(mid)) lo = mid; else hi = mid;
+      }
+    }
+    thr[k - 1] = std::ldexp(double(lo), -53);
+  }
+  cache.emplace(key, thr);
+  return thr;
+}
+
+struct HostTable {
+  int K = 0, degree = 1, dyadic = 0;
+  double tail = 0.0;
+  std::vector<double> rows;  // kTableRows * K
+};
+
+lpmc_status prepare_table(const lpmc_invcdf_table* t, HostTable* out, lpmc_error* err) {
+  if (t->kind < 0 || t->kind > 2)
+    return fail(err, LPMC_INVALID_ARGUMENT, "bad approximation kind");
+  if (!valid_interval_count(t->interval_count))
+    return fail(err, LPMC_INVALID_ARGUMENT, "interval count must be a power of two >= 2");
+  if (t->interval_count > kMaxK)
+    return fail(err, LPMC_INVALID_ARGUMENT, "device tables support interval counts up to 1024");
+  if (t->breakpoints == nullptr || t->coeff == nullptr)
+    return fail(err, LPMC_INVALID_ARGUMENT, "table has no coefficients");
+  const int K = t->interval_count;
+  out->K = K;
+  out->degree = t->kind == LPMC_APPROX_CUBIC ? 3 : 1;
+  out->tail = t->tail_value;
+  bool dyadic = t->step_w == 1.0 && t->w_max == static_cast<double>(K + 1);
+  for (int j = 0; dyadic && j < K; ++j) dyadic = t->breakpoints[j] == 1.0 - std::ldexp(1.0, -(j + 2));
+  out->dyadic = dyadic ? 1 : 0;
+  out->rows.assign(static_cast<size_t>(kTableRows) * K, 0.0);
+  double* a = out->rows.data();
+  double* w = a + K;
+  for (int j = 0; j < K; ++j) {
+    a[j] = j == 0 ? 0.5 : t->breakpoints[j - 1];
+    w[j] = dyadic ? std::ldexp(1.0, j + 2) : t->breakpoints[j] - a[j];
+    for (int c = 0; c < 4; ++c) out->rows[static_cast<size_t>(2 + c) * K + j] = t->coeff[4 * j + c];
+  }
+  if (!dyadic) {
+    const std::vector<double> thr = index_thresholds(K, t->w_max, t->step_w);
+    std::copy(thr.begin(), thr.end(), out->rows.begin() + 6 * K);
+  }
+  return LPMC_OK;
+}
+
+// --------------------------------------------------------- moments ---------
+struct Moments {
+  uint64_t n = 0;
+  double mean = 0.0, m2 = 0.0, m3 = 0.0, m4 = 0.0;
+};
+
+// MomentAccumulator::merge (stats.hpp:29-54); identical expression trees so
+// the fold is bitwise the reference's.
+void merge_into(Moments& a, const Moments& b) {
+  if (b.n == 0) return;
+  if (a.n == 0) {
+    a = b;
+    return;
+  }
+  const double na = static_cast<double>(a.n);
+  const double nb = static_cast<double>(b.n);
+  const double n = na + nb;
+  const double d = b.mean - a.mean;
+  const double d2 = d * d;
+  const double m2 = a.m2 + b.m2 + d2 * na * nb / n;
+  const double m3 = a.m3 + b.m3 + d2 * d * na * nb * (na - nb) / (n * n) +
+                    3.0 * d * (na * b.m2 - nb * a.m2) / n;
+  const double m4 = a.m4 + b.m4 + d2 * d2 * na * nb * (na * na - na * nb + nb * nb) / (n * n * n) +
+                    6.0 * d2 * (na * na * b.m2 + nb * nb * a.m2) / (n * n) +
+                    4.0 * d * (na * b.m3 - nb * a.m3) / n;
+  a.mean += d * nb / n;
+  a.m2 = m2;
+  a.m3 = m3;
+  a.m4 = m4;
+  a.n += b.n;
+}
+
+Moments from_device(const double* p) {
+  Moments m;
+  m.n = static_cast<uint64_t>(p[0]);
+  m.mean = p[1];
+  m.m2 = p[2];
+  m.m3 = p[3];
+  m.m4 = p[4];
+  return m;
+}
+
+lpmc_moments to_abi(const Moments& m) { return lpmc_moments{m.n, m.mean, m.m2, m.m3, m.m4}; }
+Moments from_abi(const lpmc_moments& m) {
+  Moments r;
+  r.n = m.n;
+  r.mean = m.mean;
+  r.m2 = m.m2;
+  r.m3 = m.m3;
+  r.m4 = m.m4;
+  return r;
+}
+
+// ------------------------------------------------------- run spec ----------
+struct RunSpec {
+  LevelArgs args{};
+  BarArith arith = BarArith::kCarrier;
+  bool kahan = false;
+  int reduce = LPMC_REDUCE_TREE;
+  uint64_t n_paths = 0;
+  uint64_t chunk_begin = 0, chunk_end = 0;  // chunk range this run covers
+  HostTable table;
+  bool has_table = false;
+  int device = -1;
+  bool ieee = false;
+};
+
+bool in_native_range(double c, double lo, double hi) {
+  const double a = std::fabs(c);
+  return a == 0.0 || (a >= lo && a <= hi);
+}
+
+lpmc_status build_spec(const lpmc_gbm* model, int32_t level, const lpmc_precision* prec,
+                       const lpmc_invcdf_table* table, int32_t kahan, uint64_t n_paths,
+                       uint64_t seed, uint64_t path_base, const lpmc_options* opts,
+                       RunSpec* spec, lpmc_error* err) {
+  if (model == nullptr || prec == nullptr)
+    return fail(err, LPMC_INVALID_ARGUMENT, "null model or precision");
+  if (level < 0) return fail(err, LPMC_INVALID_ARGUMENT, "level must be >= 0");  // sde.hpp:215
+  if (level > 40) return fail(err, LPMC_INVALID_ARGUMENT, "level must be <= 40");
+  const int m = prec->mantissa_bits;
+  if (m < 1) return fail(err, LPMC_INVALID_ARGUMENT, "mantissa_bits must be >= 1");
+  lpmc_options o;
+  lpmc_default_options(&o);
+  if (opts != nullptr) o = *opts;
+  if (o.legs == 0) o.legs = LPMC_LEGS_ALL;
+  if (o.legs > 3) return fail(err, LPMC_INVALID_ARGUMENT, "bad legs mask");
+  if (o.payoff != LPMC_PAYOFF_TERMINAL && o.payoff != LPMC_PAYOFF_CALL)
+    return fail(err, LPMC_INVALID_ARGUMENT, "bad payoff");
+  if (o.reduce != LPMC_REDUCE_TREE && o.reduce != LPMC_REDUCE_SEQUENTIAL)
+    return fail(err, LPMC_INVALID_ARGUMENT, "bad reduction mode");
+  if (prec->ieee_half && m != 10)
+    return fail(err, LPMC_INVALID_ARGUMENT, "ieee_half requires mantissa_bits == 10");
+
+  RunSpec& s = *spec;
+  s = RunSpec{};
+  s.n_paths = n_paths;
+  s.kahan = kahan != 0;
+  s.reduce = o.reduce;
+  s.device = o.device;
+  s.ieee = prec->ieee_half != 0;
+  if (table != nullptr) {
+    const lpmc_status st = prepare_table(table, &s.table, err);
+    if (st != LPMC_OK) return st;
+    s.has_table = true;
+  }
+  LevelArgs& A = s.args;
+  A.seed_key = 0;
+  {  // mix64(seed + golden) (uniform.hpp:23), hoisted out of every path
+    uint64_t z = seed + 0x9e3779b97f4a7c15ull;
+    z ^= z >> 33;
+    z *= 0xff51afd7ed558ccdull;
+    z ^= z >> 33;
+    z *= 0xc4ceb9fe1a85ec53ull;
+    z ^= z >> 33;
+    A.seed_key = z;
+  }
+  A.path_base = path_base;
+  A.n_paths = n_paths;
+  A.level = level;
+  A.legs = static_cast<int32_t>(o.legs);
+  // per-level constants (sde.hpp:217-224)
+  const double dtf = std::ldexp(model->horizon, -level);
+  const double sdtf = std::sqrt(dtf);
+  const double dtc = 2.0 * dtf;
+  A.mu = model->mu;
+  A.sigma = model->sigma;
+  A.x0 = model->x0;
+  A.dtf = dtf;
+  A.sdtf = sdtf;
+  A.dtc = dtc;
+  const double consts[6] = {model->mu, model->sigma, model->x0, dtf, sdtf, dtc};
+  double low[6];
+  for (int i = 0; i < 6; ++i) {
+    if (!std::isfinite(consts[i]))
+      return fail(err, LPMC_DOMAIN_ERROR, "non-finite operand", LPMC_FAIL_NONFINITE, path_base, 0);
+    if (s.ieee) {
+      low[i] = 0.0;
+    } else if (!round_prec(consts[i], m, &low[i])) {
+      return fail(err, LPMC_DOMAIN_ERROR, "non-finite operand", LPMC_FAIL_NONFINITE, path_base, 0);
+    }
+  }
+  A.mu_l = low[0];
+  A.sigma_l = low[1];
+  A.x0_l = low[2];
+  A.dtf_l = low[3];
+  A.sdtf_l = low[4];
+  A.dtc_l = low[5];
+  A.h_mu = half_bits(consts[0]);
+  A.h_sigma = half_bits(consts[1]);
+  A.h_x0 = half_bits(consts[2]);
+  A.h_dtf = half_bits(consts[3]);
+  A.h_sdtf = half_bits(consts[4]);
+  A.h_dtc = half_bits(consts[5]);
+  A.mantissa_bits = m;
+  A.payoff = o.payoff;
+  A.strike = o.strike;
+  if (s.has_table) {
+    A.K = s.table.K;
+    A.degree = s.table.degree;
+    A.dyadic = s.table.dyadic;
+    A.tail = s.table.tail;
+  }
+  // bar arithmetic; native fp32 paths only inside the guarded range
+  const bool native_ok = in_native_range(low[0], 0x1p-20, 0x1p20) &&
+                         in_native_range(low[1], 0x1p-20, 0x1p20) &&
+                         in_native_range(low[2], 0x1p-20, 0x1p20) &&
+                         in_native_range(low[3], 0x1p-40, 0x1p20) &&
+                         in_native_range(low[4], 0x1p-20, 0x1p20) &&
+                         in_native_range(low[5], 0x1p-40, 0x1p20);
+  if (s.ieee) {
+    s.arith = BarArith::kHalf2;
+  } else if (m >= 52) {
+    s.arith = BarArith::kCarrier;
+  } else if (m == 23 && native_ok) {
+    s.arith = BarArith::kF32;
+  } else if (m <= 10 && native_ok) {
+    s.arith = BarArith::kF32Round;
+  } else {
+    s.arith = BarArith::kF64Round;
+  }
+  const uint64_t n_chunks = (n_paths + kChunkPaths - 1) / kChunkPaths;
+  s.chunk_begin = 0;
+  s.chunk_end = n_chunks;
+  return LPMC_OK;
+}
+
+// --------------------------------------------------- device state ----------
+template <typename T>
+struct DevBuf {
+  T* ptr = nullptr;
+  size_t cap = 0;
+  cudaError_t ensure(size_t n) {
+    if (n <= cap) return cudaSuccess;
+    if (ptr != nullptr) cudaFree(ptr);
+    ptr = nullptr;
+    cap = 0;
+    const size_t want = std::max(n, static_cast<size_t>(16));
+    cudaError_t e = cudaMalloc(reinterpret_cast<void**>(&ptr), want * sizeof(T));
+    if (e == cudaSuccess) cap = want;
+    return e;
+  }
+  void release() {
+    if (ptr != nullptr) cudaFree(ptr);
+    ptr = nullptr;
+    cap = 0;
+  }
+};
+
+struct Buffers {
+  DevBuf<double> table, batch_acc, chunk_acc, path_diff, seq_acc;
+  DevBuf<unsigned long long> err_key;
+  DevBuf<unsigned int> range_flag;
+  std::vector<double> host_parts;
+  void release() {
+    table.release();
+    batch_acc.release();
+    chunk_acc.release();
+    path_diff.release();
+    seq_acc.release();
+    err_key.release();
+    range_flag.release();
+  }
+};
+
+struct DeviceCtx {
+  std::mutex mu;
+  cudaStream_t stream = nullptr;
+  Buffers scratch;
+  bool configured = false;
+};
+
+std::mutex g_ctx_mu;
+std::map<int, std::unique_ptr<DeviceCtx>> g_ctx;
+
+struct DeviceGuard {
+  int prev = -1;
+  bool changed = false;
+  cudaError_t set(int dev) {
+    cudaError_t e = cudaGetDevice(&prev);
+    if (e != cudaSuccess) return e;
+    if (dev >= 0 && dev != prev) {
+      e = cudaSetDevice(dev);
+      changed = e == cudaSuccess;
+    }
+    return e;
+  }
+  ~DeviceGuard() {
+    if (changed) cudaSetDevice(prev);
+  }
+};
+
+lpmc_status get_ctx(int device, DeviceCtx** out, int* resolved, lpmc_error* err) {
+  int count = 0;
+  cudaError_t e = cudaGetDeviceCount(&count);
+  if (e != cudaSuccess || count == 0)
+    return fail(err, LPMC_NO_DEVICE, "no CUDA device available (the sampler has no CPU fallback)");
+  int dev = device;
+  if (dev < 0) {
+    e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return cuda_fail(err, e, "cudaGetDevice");
+  }
+  if (dev >= count) return fail(err, LPMC_INVALID_ARGUMENT, "device ordinal out of range");
+  std::lock_guard<std::mutex> lock(g_ctx_mu);
+  auto& slot = g_ctx[dev];
+  if (!slot) {
+    cudaDeviceProp prop{};
+    e = cudaGetDeviceProperties(&prop, dev);
+    if (e != cudaSuccess) return cuda_fail(err, e, "cudaGetDeviceProperties");
+    if (prop.major != 10)
+      return fail(err, LPMC_NO_DEVICE, "device is not sm_100 (B200); kernels are built for sm_100a only");
+    auto ctx = std::make_unique<DeviceCtx>();
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(dev);
+    e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = static_cast<cudaError_t>(configure_kernels());
+    cudaSetDevice(prev);
+    if (e != cudaSuccess) return cuda_fail(err, e, "device setup");
+    ctx->configured = true;
+    slot = std::move(ctx);
+  }
+  *out = slot.get();
+  *resolved = dev;
+  return LPMC_OK;
+}
+
+// -------------------------------------------------------- enqueue ----------
+struct Enqueued {
+  uint64_t n_chunks = 0;        // chunk partials produced (tree)
+  uint64_t n_batches_seq = 0;   // batch accumulators produced (sequential)
+  int kernels = 0;
+};
+
+cudaError_t enqueue_run(const RunSpec& s, Buffers& B, cudaStream_t st, Enqueued* q) {
+  cudaError_t e;
+  *q = Enqueued{};
+  if ((e = B.err_key.ensure(1)) != cudaSuccess) return e;
+  if ((e = B.range_flag.ensure(1)) != cudaSuccess) return e;
+  if ((e = cudaMemsetAsync(B.err_key.ptr, 0xff, sizeof(unsigned long long), st)) != cudaSuccess) return e;
+  if ((e = cudaMemsetAsync(B.range_flag.ptr, 0, sizeof(unsigned int), st)) != cudaSuccess) return e;
+  LevelArgs A = s.args;
+  A.err_key = B.err_key.ptr;
+  A.range_flag = B.range_flag.ptr;
+  A.table = nullptr;
+  if (s.has_table) {
+    if ((e = B.table.ensure(s.table.rows.size())) != cudaSuccess) return e;
+    if ((e = cudaMemcpyAsync(B.table.ptr, s.table.rows.data(), s.table.rows.size() * sizeof(double),
+                             cudaMemcpyHostToDevice, st)) != cudaSuccess)
+      return e;
+    A.table = B.table.ptr;
+  }
+  const uint64_t n_batches_total = (s.n_paths + kBatch - 1) / kBatch;
+  const uint64_t chunks = s.chunk_end - s.chunk_begin;
+  if (chunks == 0) return cudaSuccess;
+  const bool seq = s.reduce == LPMC_REDUCE_SEQUENTIAL;
+  const uint64_t slice_chunks = seq ? kSeqSliceChunks : kSliceChunks;
+  if (seq) {
+    const uint64_t b0 = s.chunk_begin * kChunkBatches;
+    const uint64_t b1 = std::min(s.chunk_end * kChunkBatches, n_batches_total);
+    if ((e = B.seq_acc.ensure(15 * (b1 - b0))) != cudaSuccess) return e;
+    if ((e = B.path_diff.ensure(2 * std::min(b1 - b0, slice_chunks * kChunkBatches) * kBatch)) != cudaSuccess)
+      return e;
+    q->n_batches_seq = b1 - b0;
+  } else {
+    if ((e = B.chunk_acc.ensure(15 * chunks)) != cudaSuccess) return e;
+    if ((e = B.batch_acc.ensure(15 * std::min(chunks, slice_chunks) * kChunkBatches)) != cudaSuccess)
+      return e;
+    q->n_chunks = chunks;
+  }
+  for (uint64_t c0 = s.chunk_begin; c0 < s.chunk_end; c0 += slice_chunks) {
+    const uint64_t c1 = std::min(c0 + slice_chunks, s.chunk_end);
+    const uint64_t b0 = c0 * kChunkBatches;
+    const uint64_t b1 = std::min(c1 * kChunkBatches, n_batches_total);
+    LevelArgs S = A;
+    S.batch0 = b0;
+    S.n_batches = b1 - b0;
+    S.batch_acc = seq ? nullptr : B.batch_acc.ptr;
+    S.path_diff = seq ? B.path_diff.ptr : nullptr;
+    S.path_out = nullptr;
+    S.z_out = nullptr;
+    LaunchResult r = launch_paths(S, s.arith, s.kahan, st);
+    q->kernels += r.kernels;
+    if (r.cuda_error != 0) return static_cast<cudaError_t>(r.cuda_error);
+    if (seq) {
+      const uint64_t paths_slice = std::min(b1 * kBatch, s.n_paths) - b0 * kBatch;
+      r = launch_sequential_batches(B.path_diff.ptr, paths_slice,
+                                    B.seq_acc.ptr + 15 * (b0 - s.chunk_begin * kChunkBatches), st);
+    } else {
+      r = launch_chunk_reduce(B.batch_acc.ptr, b1 - b0, c1 - c0,
+                              B.chunk_acc.ptr + 15 * (c0 - s.chunk_begin), st);
+    }
+    q->kernels += r.kernels;
+    if (r.cuda_error != 0) return static_cast<cudaError_t>(r.cuda_error);
+  }
+  t_launches += static_cast<uint64_t>(q->kernels);
+  return cudaSuccess;
+}
+
+// Map the device failure word to the reference's exception (first failing
+// path in path order, as the serial reference would throw).
+lpmc_status failure_from_key(const RunSpec& s, unsigned long long key, lpmc_error* err) {
+  const uint64_t local = key >> 24;
+  const int kind = static_cast<int>((key >> 22) & 3u);
+  const uint64_t step = key & ((1ull << 22) - 1);
+  const uint64_t path = s.args.path_base + local;
+  if (kind == LPMC_FAIL_UNIFORM_IS_ONE)
+    return fail(err, LPMC_DOMAIN_ERROR, "exact_inv_cdf requires u in (0, 1)", kind, path, step);
+  if (kind == LPMC_FAIL_NONFINITE_STATE)
+    return fail(err, LPMC_RUNTIME_ERROR, "non-finite state at step " + std::to_string(step), kind,
+                path, step);
+  return fail(err, LPMC_DOMAIN_ERROR, "non-finite operand", LPMC_FAIL_NONFINITE, path, step);
+}
+
+// Wait, check failure flags, copy partials back.  *rerun set when native
+// legs left their range (the caller re-runs with the exact emulation).
+lpmc_status collect_run(const RunSpec& s, Buffers& B, cudaStream_t st, const Enqueued& q,
+                        std::vector<Moments>* parts, bool* rerun, lpmc_error* err) {
+  *rerun = false;
+  unsigned long long key = ~0ull;
+  unsigned int range = 0;
+  cudaError_t e = cudaMemcpyAsync(&key, B.err_key.ptr, sizeof key, cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(&range, B.range_flag.ptr, sizeof range, cudaMemcpyDeviceToHost, st);
+  const uint64_t n_acc = q.n_batches_seq ? q.n_batches_seq : q.n_chunks;
+  const double* src = q.n_batches_seq ? B.seq_acc.ptr : B.chunk_acc.ptr;
+  B.host_parts.resize(15 * n_acc);
+  if (e == cudaSuccess && n_acc > 0)
+    e = cudaMemcpyAsync(B.host_parts.data(), src, 15 * n_acc * sizeof(double),
+                        cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return cuda_fail(err, e, "level sampler");
+  if (range != 0 && (s.arith == BarArith::kF32 || s.arith == BarArith::kF32Round)) {
+    *rerun = true;
+    return LPMC_OK;
+  }
+  if (key != ~0ull) return failure_from_key(s, key, err);
+  parts->resize(3 * n_acc);
+  for (uint64_t i = 0; i < 3 * n_acc; ++i) (*parts)[i] = from_device(B.host_parts.data() + 5 * i);
+  return LPMC_OK;
+}
+
+void mask_legs(const RunSpec& s, std::vector<Moments>& parts) {
+  const int legs = s.args.legs;
+  for (size_t i = 0; i < parts.size(); ++i) {
+    const int f = static_cast<int>(i % 3);
+    const bool keep = f == 0 ? (legs & 1) : (f == 1 ? (legs & 2) : ((legs & 3) == 3));
+    if (!keep) parts[i] = Moments{};
+  }
+}
+
+// Full synchronous run on one device: enqueue, collect, fallback re-run.
+lpmc_status run_sync(RunSpec& s, void* user_stream, std::vector<Moments>* parts, lpmc_error* err) {
+  DeviceCtx* ctx = nullptr;
+  int dev = -1;
+  lpmc_status stt = get_ctx(s.device, &ctx, &dev, err);
+  if (stt != LPMC_OK) return stt;
+  DeviceGuard guard;
+  cudaError_t e = guard.set(dev);
+  if (e != cudaSuccess) return cuda_fail(err, e, "cudaSetDevice");
+  std::lock_guard<std::mutex> lock(ctx->mu);
+  cudaStream_t st = user_stream != nullptr ? static_cast<cudaStream_t>(user_stream) : ctx->stream;
+  for (int attempt = 0; attempt < 2; ++attempt) {
+    Enqueued q;
+    e = enqueue_run(s, ctx->scratch, st, &q);
+    if (e != cudaSuccess) return cuda_fail(err, e, "launch");
+    bool rerun = false;
+    stt = collect_run(s, ctx->scratch, st, q, parts, &rerun, err);
+    if (stt != LPMC_OK) return stt;
+    if (!rerun) {
+      mask_legs(s, *parts);
+      return ok(err);
+    }
+    s.arith = BarArith::kF64Round;  // exact emulation outside the native range
+  }
+  return fail(err, LPMC_RUNTIME_ERROR, "native range fallback did not converge");
+}
+
+void fold(const std::vector<Moments>& parts, lpmc_moments* out3) {
+  Moments acc[3];
+  for (size_t i = 0; i < parts.size(); ++i) merge_into(acc[i % 3], parts[i]);
+  for (int f = 0; f < 3; ++f) out3[f] = to_abi(acc[f]);
+}
+
+}  // namespace
+}  // namespace lpmc_b200
+
+using namespace lpmc_b200;
+
+// ============================================================ C-ABI ========
+extern "C" {
+
+int32_t lpmc_abi_version(void) { return LPMC_B200_ABI_VERSION; }
+
+int32_t lpmc_device_count(void) {
+  int count = 0;
+  if (cudaGetDeviceCount(&count) != cudaSuccess) return 0;
+  int n = 0;
+  for (int d = 0; d < count; ++d) {
+    cudaDeviceProp p{};
+    if (cudaGetDeviceProperties(&p, d) == cudaSuccess && p.major == 10) ++n;
+  }
+  return n;
+}
+
+uint64_t lpmc_launch_count(void) { return t_launches; }
+void lpmc_reset_launch_count(void) { t_launches = 0; }
+
+void lpmc_default_options(lpmc_options* o) {
+  o->legs = LPMC_LEGS_ALL;
+  o->payoff = LPMC_PAYOFF_TERMINAL;
+  o->strike = 1.0;
+  o->reduce = LPMC_REDUCE_TREE;
+  o->device = -1;
+  o->stream = nullptr;
+}
+
+void lpmc_default_cost_model(lpmc_cost_model* c) {  // mlmc.hpp:20-28
+  c->cycles_exact_rng = 3.5;
+  c->cycles_approx_rng_single = 0.5;
+  c->cycles_approx_rng_half = 0.25;
+  c->kahan_overhead_factor = 1.4;
+  c->per_step_arithmetic = 0.0;
+}
+
+lpmc_status lpmc_round_to_precision(double x, int32_t m, double* out, lpmc_error* err) {
+  if (m < 1) return fail(err, LPMC_INVALID_ARGUMENT, "mantissa_bits must be >= 1");
+  if (!round_prec(x, m, out)) return fail(err, LPMC_DOMAIN_ERROR, "non-finite operand");
+  return ok(err);
+}
+
+lpmc_status lpmc_invcdf_build(int32_t kind, int32_t K, double* bp, double* coeff, double* w_max,
+                              double* step_w, double* tail, lpmc_error* err) {
+  // InvCdfApprox::build (invcdf_approx.hpp:101-145), same op order.
+  if (!valid_interval_count(K))
+    return fail(err, LPMC_INVALID_ARGUMENT, "interval count must be a power of two >= 2");
+  if (kind < 0 || kind > 2) return fail(err, LPMC_INVALID_ARGUMENT, "bad approximation kind");
+  std::vector<double> nodes, weights;
+  gauss_legendre_rule(32, nodes, weights);
+  const double wm = std::min(static_cast<double>(K + 1), 45.0);
+  const double sw = (wm - 1.0) / K;
+  double left = 0.5;
+  for (int j = 0; j < K; ++j) {
+    const double w_hi = 1.0 + (j + 1) * sw;
+    const double right = 1.0 - std::exp2(-w_hi);
+    bp[j] = right;
+    std::array<double, 4> c{0.0, 0.0, 0.0, 0.0};
+    for (size_t i = 0; i < nodes.size(); ++i) {
+      const double t = nodes[i];
+      const double u = 0.5 * (left + right) + 0.5 * (right - left) * t;
+      const double f = weights[i] * host_phi_inv(u);
+      const double p2 = 1.5 * t * t - 0.5;
+      const double p3 = t * (2.5 * t * t - 1.5);
+      c[0] += 0.5 * f;
+      if (kind != LPMC_APPROX_CONSTANT) c[1] += 1.5 * f * t;
+      if (kind == LPMC_APPROX_CUBIC) {
+        c[2] += 2.5 * f * p2;
+        c[3] += 3.5 * f * p3;
+      }
+    }
+    for (int k = 0; k < 4; ++k) coeff[4 * j + k] = c[k];
+    left = right;
+  }
+  const double* last = coeff + 4 * (K - 1);
+  *tail = last[0] + last[1] + last[2] + last[3];
+  *w_max = wm;
+  *step_w = sw;
+  return ok(err);
+}
+
+lpmc_status lpmc_invcdf_eval(const lpmc_invcdf_table* t, double u, double* out, lpmc_error* err) {
+  // InvCdfApprox::operator() / eval_upper (invcdf_approx.hpp:44-90)
+  if (!(u > 0.0 && u < 1.0))
+    return fail(err, LPMC_DOMAIN_ERROR, "approx_inv_cdf requires u in (0, 1)");
+  if (u == 0.5) {
+    *out = 0.0;
+    return ok(err);
+  }
+  const bool lower = u < 0.5;
+  const double up = lower ? 1.0 - u : u;
+  const int j_or_tail = reference_index(1.0 - up, t->interval_count, t->w_max, t->step_w);
+  double r;
+  if (j_or_tail == t->interval_count) {
+    r = t->tail_value;
+  } else {
+    const int j = j_or_tail;
+    const double a = j == 0 ? 0.5 : t->breakpoints[j - 1];
+    const double b = t->breakpoints[j];
+    double s = 2.0 * (up - a) / (b - a) - 1.0;
+    if (s < -1.0) s = -1.0;
+    if (s > 1.0) s = 1.0;
+    const double* c = t->coeff + 4 * j;
+    const double p2 = 1.5 * s * s - 0.5;
+    const double p3 = s * (2.5 * s * s - 1.5);
+    r = c[0] + c[1] * s + c[2] * p2 + c[3] * p3;
+  }
+  *out = lower ? -r : r;
+  return ok(err);
+}
+
+void lpmc_moments_add(lpmc_moments* acc, double x) {  // stats.hpp:15-27
+  const uint64_t prior = acc->n;
+  acc->n += 1;
+  const double dn = static_cast<double>(acc->n);
+  const double delta = x - acc->mean;
+  const double dl = delta / dn;
+  const double dl2 = dl * dl;
+  const double t1 = delta * dl * static_cast<double>(prior);
+  acc->mean += dl;
+  acc->m4 += t1 * dl2 * (dn * dn - 3.0 * dn + 3.0) + 6.0 * dl2 * acc->m2 - 4.0 * dl * acc->m3;
+  acc->m3 += t1 * dl * (dn - 2.0) - 3.0 * dl * acc->m2;
+  acc->m2 += t1;
+}
+
+void lpmc_moments_merge(lpmc_moments* acc, const lpmc_moments* other) {
+  Moments a = from_abi(*acc);
+  merge_into(a, from_abi(*other));
+  *acc = to_abi(a);
+}
+
+void lpmc_fold_partials(const lpmc_moments* partials, uint64_t n_chunks, lpmc_moments* out) {
+  Moments acc[3];
+  for (uint64_t i = 0; i < 3 * n_chunks; ++i) merge_into(acc[i % 3], from_abi(partials[i]));
+  for (int f = 0; f < 3; ++f) out[f] = to_abi(acc[f]);
+}
+
+void lpmc_level_stats_from_moments(const lpmc_moments* acc3, int32_t level,
+                                   const lpmc_precision* prec, int32_t kahan,
+                                   const lpmc_cost_model* cost_in, uint64_t n_paths,
+                                   lpmc_level_stats* s) {
+  // estimate_level_stats (mlmc.hpp:125-148); MomentAccumulator getters
+  // (stats.hpp:56-82).
+  lpmc_cost_model cost;
+  lpmc_default_cost_model(&cost);
+  if (cost_in != nullptr) cost = *cost_in;
+  auto mean = [](const lpmc_moments& a) { return a.n ? a.mean : 0.0; };
+  auto var = [](const lpmc_moments& a) { return a.n < 2 ? 0.0 : a.m2 / static_cast<double>(a.n - 1); };
+  auto var_se = [&](const lpmc_moments& a) {
+    if (a.n < 2) return 0.0;
+    const double v = var(a);
+    double spread = a.m4 / static_cast<double>(a.n) - v * v;
+    if (spread < 0.0) spread = 0.0;
+    return std::sqrt(spread / static_cast<double>(a.n));
+  };
+  const double n_fine = std::ldexp(1.0, level);
+  const double steps = level == 0 ? n_fine : 1.5 * n_fine;
+  s->level = level;
+  s->mean_hat = mean(acc3[0]);
+  s->v_hat = var(acc3[0]);
+  s->v_hat_stderr = var_se(acc3[0]);
+  s->mean_bar = mean(acc3[1]);
+  s->v_bar = var(acc3[1]);
+  s->v_bar_stderr = var_se(acc3[1]);
+  s->mean_four = mean(acc3[2]);
+  s->V_bar = var(acc3[2]);
+  s->V_bar_stderr = var_se(acc3[2]);
+  const double approx_cycles = prec->mantissa_bits <= 10 ? cost.cycles_approx_rng_half
+                                                         : cost.cycles_approx_rng_single;
+  s->c_hat = n_fine * cost.cycles_exact_rng + steps * cost.per_step_arithmetic;
+  s->c_bar = n_fine * approx_cycles * (kahan ? cost.kahan_overhead_factor : 1.0) +
+             steps * cost.per_step_arithmetic;
+  s->C_bar = s->c_hat + s->c_bar;
+  s->m_hat = s->m_bar = s->M_bar = n_paths;
+}
+
+lpmc_status lpmc_run_coupled_paths(const lpmc_gbm* model, int32_t level,
+                                   const lpmc_precision* prec, const lpmc_invcdf_table* table,
+                                   int32_t kahan, uint64_t n_paths, uint64_t seed,
+                                   uint64_t path_base, const lpmc_options* opts,
+                                   lpmc_moments* out, lpmc_error* err) {
+  for (int f = 0; f < 3; ++f) out[f] = lpmc_moments{0, 0.0, 0.0, 0.0, 0.0};
+  if (n_paths == 0) return ok(err);  // mlmc.hpp:75: no batches, nothing simulated
+  RunSpec s;
+  lpmc_status st = build_spec(model, level, prec, table, kahan, n_paths, seed, path_base, opts,
+                              &s, err);
+  if (st != LPMC_OK) return st;
+  std::vector<Moments> parts;
+  st = run_sync(s, opts ? opts->stream : nullptr, &parts, err);
+  if (st != LPMC_OK) return st;
+  Moments acc[3];
+  for (size_t i = 0; i < parts.size(); ++i) merge_into(acc[i % 3], parts[i]);
+  for (int f = 0; f < 3; ++f) out[f] = to_abi(acc[f]);
+  return ok(err);
+}
+
+lpmc_status lpmc_estimate_level_stats(const lpmc_gbm* model, int32_t level,
+                                      const lpmc_precision* prec,
+                                      const lpmc_invcdf_table* table, int32_t kahan,
+                                      uint64_t n_paths, uint64_t seed,
+                                      const lpmc_cost_model* cost, uint64_t path_base,
+                                      const lpmc_options* opts, lpmc_level_stats* out,
+                                      lpmc_error* err) {
+  if (n_paths < 2) return fail(err, LPMC_INVALID_ARGUMENT, "need at least 2 paths");  // mlmc.hpp:121
+  lpmc_moments acc[3];
+  lpmc_status st = lpmc_run_coupled_paths(model, level, prec, table, kahan, n_paths, seed,
+                                          path_base, opts, acc, err);
+  if (st != LPMC_OK) return st;
+  lpmc_level_stats_from_moments(acc, level, prec, kahan, cost, n_paths, out);
+  return ok(err);
+}
+
+lpmc_status lpmc_level_partials(const lpmc_gbm* model, int32_t level,
+                                const lpmc_precision* prec, const lpmc_invcdf_table* table,
+                                int32_t kahan, uint64_t n_paths, uint64_t seed,
+                                uint64_t path_base, uint64_t chunk_begin, uint64_t chunk_end,
+                                const lpmc_options* opts, lpmc_moments* out, lpmc_error* err) {
+  const uint64_t n_chunks = (n_paths + LPMC_CHUNK_PATHS - 1) / LPMC_CHUNK_PATHS;
+  if (chunk_end > n_chunks || chunk_begin > chunk_end)
+    return fail(err, LPMC_INVALID_ARGUMENT, "chunk range outside the run");
+  if (chunk_begin == chunk_end) return ok(err);
+  lpmc_options o;
+  lpmc_default_options(&o);
+  if (opts != nullptr) o = *opts;
+  o.reduce = LPMC_REDUCE_TREE;  // chunk partials are defined by the tree
+  RunSpec s;
+  lpmc_status st = build_spec(model, level, prec, table, kahan, n_paths, seed, path_base, &o, &s, err);
+  if (st != LPMC_OK) return st;
+  s.chunk_begin = chunk_begin;
+  s.chunk_end = chunk_end;
+  std::vector<Moments> parts;
+  st = run_sync(s, o.stream, &parts, err);
+  if (st != LPMC_OK) return st;
+  for (size_t i = 0; i < parts.size(); ++i) out[i] = to_abi(parts[i]);
+  return ok(err);
+}
+
+lpmc_status lpmc_simulate_paths(const lpmc_gbm* model, int32_t level, const lpmc_precision* prec,
+                                const lpmc_invcdf_table* table, int32_t kahan, uint64_t n_paths,
+                                uint64_t seed, uint64_t path_base, const lpmc_options* opts,
+                                double* out4, double* z_out, lpmc_error* err) {
+  if (n_paths == 0) return ok(err);
+  if (n_paths > (1ull << 26)) return fail(err, LPMC_INVALID_ARGUMENT, "path dump limited to 2^26 paths");
+  RunSpec s;
+  lpmc_status st = build_spec(model, level, prec, table, kahan, n_paths, seed, path_base, opts, &s, err);
+  if (st != LPMC_OK) return st;
+  DeviceCtx* ctx = nullptr;
+  int dev = -1;
+  st = get_ctx(s.device, &ctx, &dev, err);
+  if (st != LPMC_OK) return st;
+  DeviceGuard guard;
+  cudaError_t e = guard.set(dev);
+  if (e != cudaSuccess) return cuda_fail(err, e, "cudaSetDevice");
+  std::lock_guard<std::mutex> lock(ctx->mu);
+  cudaStream_t stream = (opts && opts->stream) ? static_cast<cudaStream_t>(opts->stream) : ctx->stream;
+  const uint64_t zcount = z_out ? n_paths << level : 0;
+  DevBuf<double> d_out, d_z;
+  Buffers& B = ctx->scratch;
+  for (int attempt = 0; attempt < 2; ++attempt) {
+    if ((e = d_out.ensure(4 * n_paths)) != cudaSuccess) break;
+    if (zcount && (e = d_z.ensure(zcount)) != cudaSuccess) break;
+    if ((e = B.err_key.ensure(1)) != cudaSuccess) break;
+    if ((e = B.range_flag.ensure(1)) != cudaSuccess) break;
+    cudaMemsetAsync(B.err_key.ptr, 0xff, sizeof(unsigned long long), stream);
+    cudaMemsetAsync(B.range_flag.ptr, 0, sizeof(unsigned int), stream);
+    LevelArgs A = s.args;
+    A.err_key = B.err_key.ptr;
+    A.range_flag = B.range_flag.ptr;
+    A.table = nullptr;
+    if (s.has_table) {
+      if ((e = B.table.ensure(s.table.rows.size())) != cudaSuccess) break;
+      cudaMemcpyAsync(B.table.ptr, s.table.rows.data(), s.table.rows.size() * sizeof(double),
+                      cudaMemcpyHostToDevice, stream);
+      A.table = B.table.ptr;
+    }
+    A.batch0 = 0;
+    A.n_batches = (n_paths + kBatch - 1) / kBatch;
+    A.batch_acc = nullptr;
+    A.path_diff = nullptr;
+    A.path_out = d_out.ptr;
+    A.z_out = zcount ? d_z.ptr : nullptr;
+    LaunchResult r = launch_paths(A, s.arith, s.kahan, stream);
+    t_launches += r.kernels;
+    if (r.cuda_error != 0) {
+      e = static_cast<cudaError_t>(r.cuda_error);
+      break;
+    }
+    unsigned long long key = ~0ull;
+    unsigned int range = 0;
+    cudaMemcpyAsync(&key, B.err_key.ptr, sizeof key, cudaMemcpyDeviceToHost, stream);
+    cudaMemcpyAsync(&range, B.range_flag.ptr, sizeof range, cudaMemcpyDeviceToHost, stream);
+    cudaMemcpyAsync(out4, d_out.ptr, 4 * n_paths * sizeof(double), cudaMemcpyDeviceToHost, stream);
+    if (zcount) cudaMemcpyAsync(z_out, d_z.ptr, zcount * sizeof(double), cudaMemcpyDeviceToHost, stream);
+    if ((e = cudaStreamSynchronize(stream)) != cudaSuccess) break;
+    if (range != 0 && (s.arith == BarArith::kF32 || s.arith == BarArith::kF32Round)) {
+      s.arith = BarArith::kF64Round;
+      continue;
+    }
+    d_out.release();
+    d_z.release();
+    if (key != ~0ull) return failure_from_key(s, key, err);
+    return ok(err);
+  }
+  d_out.release();
+  d_z.release();
+  return cuda_fail(err, e, "path dump");
+}
+
+lpmc_status lpmc_device_inv_cdf(const double* u, uint64_t n, const lpmc_invcdf_table* table,
+                                double* out, const lpmc_options* opts, lpmc_error* err) {
+  if (n == 0) return ok(err);
+  HostTable ht;
+  if (table != nullptr) {
+    lpmc_status st = prepare_table(table, &ht, err);
+    if (st != LPMC_OK) return st;
+  }
+  DeviceCtx* ctx = nullptr;
+  int dev = -1;
+  lpmc_status st = get_ctx(opts ? opts->device : -1, &ctx, &dev, err);
+  if (st != LPMC_OK) return st;
+  DeviceGuard guard;
+  cudaError_t e = guard.set(dev);
+  if (e != cudaSuccess) return cuda_fail(err, e, "cudaSetDevice");
+  std::lock_guard<std::mutex> lock(ctx->mu);
+  cudaStream_t stream = ctx->stream;
+  DevBuf<double> du, dout, dtab;
+  if ((e = du.ensure(n)) == cudaSuccess && (e = dout.ensure(n)) == cudaSuccess &&
+      (table == nullptr || (e = dtab.ensure(ht.rows.size())) == cudaSuccess)) {
+    cudaMemcpyAsync(du.ptr, u, n * sizeof(double), cudaMemcpyHostToDevice, stream);
+    if (table != nullptr)
+      cudaMemcpyAsync(dtab.ptr, ht.rows.data(), ht.rows.size() * sizeof(double),
+                      cudaMemcpyHostToDevice, stream);
+    LaunchResult r = launch_inv_cdf(du.ptr, n, table ? dtab.ptr : nullptr, ht.K, ht.degree,
+                                    ht.dyadic, ht.tail, table ? nullptr : dout.ptr,
+                                    table ? dout.ptr : nullptr, stream);
+    t_launches += r.kernels;
+    e = static_cast<cudaError_t>(r.cuda_error);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(out, dout.ptr, n * sizeof(double), cudaMemcpyDeviceToHost, stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
+  }
+  du.release();
+  dout.release();
+  dtab.release();
+  if (e != cudaSuccess) return cuda_fail(err, e, "inv_cdf");
+  return ok(err);
+}
+
+lpmc_status lpmc_measure_pipe_peaks(int32_t device, double* out4, lpmc_error* err) {
+  DeviceCtx* ctx = nullptr;
+  int dev = -1;
+  lpmc_status st = get_ctx(device, &ctx, &dev, err);
+  if (st != LPMC_OK) return st;
+  DeviceGuard guard;
+  cudaError_t e = guard.set(dev);
+  if (e != cudaSuccess) return cuda_fail(err, e, "cudaSetDevice");
+  std::lock_guard<std::mutex> lock(ctx->mu);
+  e = static_cast<cudaError_t>(measure_pipe_peaks(out4));
+  if (e != cudaSuccess) return cuda_fail(err, e, "pipe peaks");
+  return ok(err);
+}
+
+// ------------------------------------------------------------- plans -------
+struct lpmc_plan {
+  RunSpec spec;
+  Buffers buffers;
+  Enqueued last;
+  int device = -1;
+  cudaStream_t own_stream = nullptr;
+  cudaStream_t last_stream = nullptr;
+  bool launched = false;
+};
+
+lpmc_status lpmc_plan_create(const lpmc_gbm* model, int32_t level, const lpmc_precision* prec,
+                             const lpmc_invcdf_table* table, int32_t kahan, uint64_t n_paths,
+                             uint64_t seed, uint64_t path_base, const lpmc_options* opts,
+                             lpmc_plan** plan, lpmc_error* err) {
+  const uint64_t n_chunks = (n_paths + LPMC_CHUNK_PATHS - 1) / LPMC_CHUNK_PATHS;
+  return lpmc_plan_create_range(model, level, prec, table, kahan, n_paths, seed, path_base, 0,
+                                n_chunks, opts, plan, err);
+}
+
+lpmc_status lpmc_plan_create_range(const lpmc_gbm* model, int32_t level,
+                                   const lpmc_precision* prec, const lpmc_invcdf_table* table,
+                                   int32_t kahan, uint64_t n_paths, uint64_t seed,
+                                   uint64_t path_base, uint64_t chunk_begin, uint64_t chunk_end,
+                                   const lpmc_options* opts, lpmc_plan** plan, lpmc_error* err) {
+  *plan = nullptr;
+  if (n_paths == 0) return fail(err, LPMC_INVALID_ARGUMENT, "plan needs n_paths > 0");
+  const uint64_t n_chunks = (n_paths + LPMC_CHUNK_PATHS - 1) / LPMC_CHUNK_PATHS;
+  if (chunk_end > n_chunks || chunk_begin >= chunk_end)
+    return fail(err, LPMC_INVALID_ARGUMENT, "chunk range outside the run");
+  auto p = std::make_unique<lpmc_plan>();
+  lpmc_status st = build_spec(model, level, prec, table, kahan, n_paths, seed, path_base, opts,
+                              &p->spec, err);
+  if (st != LPMC_OK) return st;
+  if (chunk_begin != 0 || chunk_end != n_chunks) p->spec.reduce = LPMC_REDUCE_TREE;
+  p->spec.chunk_begin = chunk_begin;
+  p->spec.chunk_end = chunk_end;
+  DeviceCtx* ctx = nullptr;
+  st = get_ctx(p->spec.device, &ctx, &p->device, err);
+  if (st != LPMC_OK) return st;
+  DeviceGuard guard;
+  cudaError_t e = guard.set(p->device);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&p->own_stream, cudaStreamNonBlocking);
+  if (e != cudaSuccess) return cuda_fail(err, e, "plan stream");
+  // Pre-allocate by a dry enqueue on the plan's stream, then wait.
+  Enqueued q;
+  e = enqueue_run(p->spec, p->buffers, p->own_stream, &q);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(p->own_stream);
+  if (e != cudaSuccess) return cuda_fail(err, e, "plan warm-up");
+  t_launches -= static_cast<uint64_t>(q.kernels);
+  *plan = p.release();
+  return ok(err);
+}
+
+lpmc_status lpmc_plan_launch(lpmc_plan* p, void* stream, lpmc_error* err) {
+  DeviceGuard guard;
+  cudaError_t e = guard.set(p->device);
+  if (e != cudaSuccess) return cuda_fail(err, e, "cudaSetDevice");
+  cudaStream_t st = stream != nullptr ? static_cast<cudaStream_t>(stream) : p->own_stream;
+  e = enqueue_run(p->spec, p->buffers, st, &p->last);
+  if (e != cudaSuccess) return cuda_fail(err, e, "plan launch");
+  p->last_stream = st;
+  p->launched = true;
+  return ok(err);
+}
+
+lpmc_status lpmc_plan_collect(lpmc_plan* p, lpmc_moments* out, lpmc_error* err) {
+  if (!p->launched) return fail(err, LPMC_INVALID_ARGUMENT, "plan was not launched");
+  DeviceGuard guard;
+  cudaError_t e = guard.set(p->device);
+  if (e != cudaSuccess) return cuda_fail(err, e, "cudaSetDevice");
+  std::vector<Moments> parts;
+  bool rerun = false;
+  lpmc_status st = collect_run(p->spec, p->buffers, p->last_stream, p->last, &parts, &rerun, err);
+  if (st != LPMC_OK) return st;
+  if (rerun) {
+    RunSpec s = p->spec;
+    s.arith = BarArith::kF64Round;
+    Enqueued q;
+    e = enqueue_run(s, p->buffers, p->last_stream, &q);
+    if (e != cudaSuccess) return cuda_fail(err, e, "fallback launch");
+    st = collect_run(s, p->buffers, p->last_stream, q, &parts, &rerun, err);
+    if (st != LPMC_OK) return st;
+  }
+  mask_legs(p->spec, parts);
+  fold(parts, out);
+  p->launched = false;
+  return ok(err);
+}
+
+lpmc_status lpmc_plan_collect_partials(lpmc_plan* p, lpmc_moments* out, lpmc_error* err) {
+  if (!p->launched) return fail(err, LPMC_INVALID_ARGUMENT, "plan was not launched");
+  if (p->spec.reduce != LPMC_REDUCE_TREE)
+    return fail(err, LPMC_INVALID_ARGUMENT, "partials need the tree reduction");
+  DeviceGuard guard;
+  cudaError_t e = guard.set(p->device);
+  if (e != cudaSuccess) return cuda_fail(err, e, "cudaSetDevice");
+  std::vector<Moments> parts;
+  bool rerun = false;
+  lpmc_status st = collect_run(p->spec, p->buffers, p->last_stream, p->last, &parts, &rerun, err);
+  if (st != LPMC_OK) return st;
+  if (rerun) {
+    RunSpec s = p->spec;
+    s.arith = BarArith::kF64Round;
+    Enqueued q;
+    e = enqueue_run(s, p->buffers, p->last_stream, &q);
+    if (e != cudaSuccess) return cuda_fail(err, e, "fallback launch");
+    st = collect_run(s, p->buffers, p->last_stream, q, &parts, &rerun, err);
+    if (st != LPMC_OK) return st;
+  }
+  mask_legs(p->spec, parts);
+  for (size_t i = 0; i < parts.size(); ++i) out[i] = to_abi(parts[i]);
+  p->launched = false;
+  return ok(err);
+}
+
+uint64_t lpmc_plan_chunk_count(const lpmc_plan* p) { return p->spec.chunk_end - p->spec.chunk_begin; }
+
+int32_t lpmc_plan_kernels_per_launch(const lpmc_plan* p) {
+  const uint64_t chunks = p->spec.chunk_end - p->spec.chunk_begin;
+  const uint64_t slice = p->spec.reduce == LPMC_REDUCE_SEQUENTIAL ? kSeqSliceChunks : kSliceChunks;
+  return static_cast<int32_t>(2 * ((chunks + slice - 1) / slice));
+}
+
+void lpmc_plan_destroy(lpmc_plan* p) {
+  if (p == nullptr) return;
+  DeviceGuard guard;
+  guard.set(p->device);
+  if (p->own_stream != nullptr) {
+    cudaStreamSynchronize(p->own_stream);
+    cudaStreamDestroy(p->own_stream);
+  }
+  p->buffers.release();
+  delete p;
+}
+
+}  // extern "C"

@@ -1,0 +1,79 @@
+// Internal interface between the host library (lpmc_host.cpp, plain C++) and
+// the sm_100a kernels (lpmc_kernels.cu).  Not part of the public ABI.
+#pragma once
+
+#include <cstdint>
+
+namespace lpmc_b200 {
+
+// Arithmetic of the low-precision ("bar") legs as the kernels implement it.
+enum class BarArith : int {
+  kCarrier = 0,   // m >= 52: binary64 ops (the reference's carrier)
+  kF32 = 1,       // m == 23: native fp32 __f*_rn (bit-exact inside the guarded range)
+  kF32Round = 2,  // m <= 10: fp32 op + RNE to m+1 bits (innocuous double rounding)
+  kF64Round = 3,  // any m < 52: binary64 op + integer RNE to m+1 bits (exact emulation)
+  kHalf2 = 4      // native IEEE binary16, two paths per thread (__h*2_rn)
+};
+
+// Device table layout (doubles, K = interval_count):
+//   [0K,1K) left endpoint a_j   [1K,2K) 2^(j+2) (dyadic) or b_j - a_j
+//   [2K..6K) c0, c1, c2, c3     [6K,7K) v-thresholds T_1..T_{K-1}, T_tail
+constexpr int kTableRows = 7;
+
+struct LevelArgs {
+  uint64_t seed_key;   // mix64(seed + 0x9e37...) (uniform.hpp:23), hoisted per launch
+  uint64_t path_base;  // global path index of local path 0
+  uint64_t n_paths;    // paths of the whole run (local indices 0..n_paths-1)
+  uint64_t batch0;     // first batch (256 paths) this launch covers
+  uint64_t n_batches;  // batches in this launch
+  int32_t level;
+  int32_t legs;        // 1 hat, 2 bar, 3 both
+  // carrier legs (sde.hpp:219-221)
+  double mu, sigma, x0, dtf, sdtf, dtc;
+  // bar-leg constants already rounded into the low precision (sde.hpp:222-224, :232)
+  double mu_l, sigma_l, x0_l, dtf_l, sdtf_l, dtc_l;
+  // IEEE binary16 bit patterns of the same constants (kHalf2 only)
+  uint16_t h_mu, h_sigma, h_x0, h_dtf, h_sdtf, h_dtc;
+  int32_t mantissa_bits;
+  // approximation table (nullptr = exact inverse CDF for the bar legs)
+  const double* table;
+  int32_t K, degree, dyadic;
+  double tail;
+  // payoff on terminal values (extension)
+  int32_t payoff;
+  double strike;
+  // outputs
+  double* batch_acc;             // tree mode: n_batches x 3 x 5
+  double* path_diff;             // sequential mode: slice paths x 2 (d_hat, d_bar)
+  double* path_out;              // dump: n x 4
+  double* z_out;                 // dump: n x 2^level
+  unsigned long long* err_key;   // atomicMin: (local path << 24) | (kind << 22) | step
+  unsigned int* range_flag;      // native bar legs left the guarded exponent range
+};
+
+struct LaunchResult {
+  int cuda_error;  // cudaError_t
+  int kernels;     // kernels enqueued
+};
+
+// Enqueue the path kernel for one launch slice.  arith/kahan/exact select the
+// template instance.  smem_table_bytes = 7*K*8 or 0.
+LaunchResult launch_paths(const LevelArgs& args, BarArith arith, bool kahan, void* stream);
+// Chunk tree over batch accumulators: chunks [0, n_chunks) of batches
+// [0, n_batches) in `batch_acc` -> chunk_acc (n_chunks x 3 x 5).
+LaunchResult launch_chunk_reduce(const double* batch_acc, uint64_t n_batches, uint64_t n_chunks,
+                                 double* chunk_acc, void* stream);
+// Reference-order batch accumulation of per-path (d_hat, d_bar).
+LaunchResult launch_sequential_batches(const double* path_diff, uint64_t n_paths,
+                                       double* batch_acc, void* stream);
+// Exact / approximate inverse CDF of host-given uniforms (parity hooks).
+LaunchResult launch_inv_cdf(const double* u, uint64_t n, const double* table, int K, int degree,
+                            int dyadic, double tail, double* out_exact, double* out_approx,
+                            void* stream);
+// Max dynamic shared memory the path kernels were configured for.
+int configure_kernels();
+// Lane-op rates on the current device: fp64 FMA, fp32 FMA, half2 HFMA2
+// (per half lane), 64-bit integer multiply-add.  Returns cudaError_t.
+int measure_pipe_peaks(double* out4);
+
+}  // namespace lpmc_b200

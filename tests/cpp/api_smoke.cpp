@@ -1,0 +1,108 @@
+// Drop-in check: code written against the reference's C++ API
+// (proj/include/lpmc: mlmc.hpp / invcdf_approx.hpp / softfloat.hpp / sde.hpp)
+// compiles unchanged against include/lpmc and runs on liblpmc_b200.
+// Shaped after the reference's own unit tests (tests/test_mlmc.cpp:72-95,
+// 191-202; tests/test_randvar.cpp:106-139; tests/test_softfloat.cpp:55-64).
+//
+//   api_smoke --host-only   host numerics only (no GPU)
+//   api_smoke               + device sampling (needs a B200)
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <stdexcept>
+
+#include "lpmc/mlmc.hpp"
+
+using namespace lpmc;
+
+static int g_fail = 0;
+#define CHECK(c)                                              \
+  do {                                                        \
+    if (!(c)) {                                               \
+      std::printf("FAIL %s:%d %s\n", __FILE__, __LINE__, #c); \
+      ++g_fail;                                               \
+    }                                                         \
+  } while (0)
+
+template <typename E, typename F>
+static bool throws(F&& f) {
+  try {
+    f();
+  } catch (const E&) {
+    return true;
+  } catch (...) {
+    return false;
+  }
+  return false;
+}
+
+int main(int argc, char** argv) {
+  const bool host_only = argc > 1 && std::strcmp(argv[1], "--host-only") == 0;
+
+  // softfloat ties (test_softfloat.cpp:55-64)
+  PrecisionSpec half{10};
+  CHECK(round_to_precision(1.0 + 0x1p-11, half) == 1.0);
+  CHECK(round_to_precision(1.0 + 3 * 0x1p-11, half) == 1.0 + 0x1p-9);
+  CHECK(PrecisionSpec::parse("fp22").mantissa_bits == 16);
+  CHECK(throws<std::invalid_argument>([] { PrecisionSpec::parse("fp8"); }));
+
+  // approximation validation and evaluation (test_randvar.cpp:106-139)
+  CHECK(throws<std::invalid_argument>([] { InvCdfApprox::build(InvCdfApprox::Kind::linear, 3); }));
+  CHECK(InvCdfApprox::parse("linear:8").interval_count() == 8);
+  CHECK(InvCdfApprox::parse("cubic:64").degree() == 3);
+  auto approx8 = InvCdfApprox::build(InvCdfApprox::Kind::linear, 8);
+  CHECK(approx8(0.5) == 0.0);
+  CHECK(throws<std::domain_error>([&] { approx8(1.0); }));
+  CHECK(approx8(0.3) == -approx8(0.7));
+
+  // moments (stats.hpp)
+  MomentAccumulator acc;
+  for (int i = 0; i < 100; ++i) acc.add(0.01 * i);
+  CHECK(acc.count() == 100);
+  CHECK(std::fabs(acc.mean() - 0.495) < 1e-14);
+
+  if (host_only) {
+    std::printf(g_fail ? "host-only FAILED\n" : "host-only ok\n");
+    return g_fail ? 1 : 0;
+  }
+
+  // estimate_level_stats: costs and the degenerate model (test_mlmc.cpp:72-95)
+  SdeModel det = make_gbm(0.05, 0.0);
+  CostModel cost;
+  cost.per_step_arithmetic = 0.25;
+  auto s = estimate_level_stats(det, 3, PrecisionSpec::carrier(), nullptr, false, 64, 1, cost);
+  CHECK(s.v_hat == 0.0 && s.v_bar == 0.0 && s.V_bar == 0.0);
+  CHECK(std::fabs(s.c_hat - (8 * 3.5 + 12 * 0.25)) < 1e-12);
+  CHECK(std::fabs(s.c_bar - (8 * 0.5 + 12 * 0.25)) < 1e-12);
+  CHECK(s.m_hat == 64);
+  CHECK(throws<std::invalid_argument>(
+      [&] { estimate_level_stats(det, 0, PrecisionSpec::fp16(), nullptr, false, 1, 1, cost); }));
+
+  // thread-count independent moments (test_mlmc.cpp:191-202)
+  SdeModel gbm = make_gbm();
+  auto approx = InvCdfApprox::parse("linear:64");
+  auto one = run_coupled_paths(gbm, 4, PrecisionSpec::fp16(), &approx, false, 1000, 5, 0, 1);
+  auto three = run_coupled_paths(gbm, 4, PrecisionSpec::fp16(), &approx, false, 1000, 5, 0, 3);
+  CHECK(one.d_bar.mean() == three.d_bar.mean());
+  CHECK(one.d_bar.variance() == three.d_bar.variance());
+  CHECK(one.d_four.variance() == three.d_four.variance());
+  CHECK(one.d_hat.count() == 1000);
+
+  // carrier + exact: four-way correction vanishes (test_mlmc.cpp:225-230)
+  auto c = run_coupled_paths(gbm, 3, PrecisionSpec::carrier(), nullptr, false, 4096, 3, 0);
+  CHECK(c.d_four.variance() == 0.0);
+
+  // non-finite operand -> std::domain_error (test_sde.cpp:168-173 shape)
+  SdeModel blow = make_gbm(1e30, 0.0, 1e300);
+  CHECK(throws<std::domain_error>(
+      [&] { run_coupled_paths(blow, 4, PrecisionSpec::carrier(), nullptr, false, 8, 1, 0); }));
+
+  // non-GBM models are rejected (no CPU fallback)
+  SdeModel custom = gbm;
+  custom.gbm.reset();
+  CHECK(throws<std::invalid_argument>(
+      [&] { run_coupled_paths(custom, 2, PrecisionSpec::fp32(), nullptr, false, 8, 1, 0); }));
+
+  std::printf(g_fail ? "device FAILED\n" : "device ok\n");
+  return g_fail ? 1 : 0;
+}

@@ -1,0 +1,293 @@
+"""Parity of the sm_100a sampler with the reference (golden vectors from the
+unmodified reference, tests/golden/) and with the C oracle that restates it
+(oracle/lpmc_oracle.c, pinned in test_oracle.py).  Every call goes through the
+C-ABI (include/lpmc_b200.h) into liblpmc_b200.so.
+
+Parity contract:
+* approximate Gaussians, table index, bar legs with a table: bit-exact;
+* all four legs given the device's own exact Gaussians: bit-exact (oracle
+  replay);
+* exact Gaussians vs glibc: |dz| <= 64 eps (max(u_low, tiny) / pdf(z) + |z|),
+  i.e. libm last-ulp differences propagated through the Newton step;
+* tree-reduced moments: bit-exact vs the restated tree on the device's own
+  per-path values; vs the reference's sequential order: variance relative
+  1e-12 (1e-10 for d_four), means |dm| <= 1e-12 sqrt(var) + 1e-300;
+* sequential-reduced moments: bit-exact vs the reference order.
+"""
+from __future__ import annotations
+
+import math
+
+import numpy as np
+import pytest
+
+from conftest import bits, unhex
+
+pytestmark = pytest.mark.gpu
+
+EPS = 2.0 ** -52
+
+
+def spec(lib, m, ieee=False):
+    return lib.PrecisionSpec(m, ieee)
+
+
+def table(lib, name):
+    return None if name == "exact" else lib.InvCdfApprox.parse(name)
+
+
+def z_tolerance(u, z):
+    ul = np.minimum(u, 1.0 - u)
+    pdf = np.exp(-0.5 * z * z) / math.sqrt(2 * math.pi)
+    return 64 * EPS * (np.maximum(ul, 1e-300) / np.maximum(pdf, 1e-300) + np.abs(z))
+
+
+# ------------------------------------------------------------ a2 / a3 ------
+def test_exact_inv_cdf_vs_glibc(gpu, golden):
+    u = unhex(golden["gauss"]["u"])
+    zr = unhex(golden["gauss"]["z"])
+    ok = (u > 0) & (u < 1)
+    zg = gpu.device_inv_cdf(u[ok])
+    d = np.abs(zg - zr[ok])
+    assert np.all(d <= z_tolerance(u[ok], zr[ok])), float(np.max(d))
+    same = np.mean(bits(zg) == bits(zr[ok]))
+    print(f"exact Z bitwise equal to glibc on {same:.4f} of draws; max |dz| {np.max(d):.3e}")
+    assert zg[np.where(u[ok] == 0.5)[0]].tolist() == [0.0]
+    # antisymmetry of the reflection is bitwise (gaussian.hpp:62-64)
+    up = np.random.default_rng(1).uniform(0.5, 1.0, 20000)
+    assert np.array_equal(bits(gpu.device_inv_cdf(up)), bits(-gpu.device_inv_cdf(1.0 - up)))
+
+
+@pytest.mark.parametrize("name", ["linear:2", "linear:8", "linear:16", "linear:32", "cubic:16",
+                                  "linear:64", "cubic:64", "linear:1024"])
+def test_approx_inv_cdf_bitexact(gpu, golden, oracle, name):
+    g = golden["tables"][name]
+    u = unhex(golden["tables_u"])
+    t = gpu.InvCdfApprox.parse(name)
+    assert np.array_equal(bits(t.breakpoints()), bits(unhex(g["bp"])))
+    assert np.array_equal(bits(t.coefficients().reshape(-1)), bits(unhex(g["coeff"])))
+    assert np.array_equal(bits(gpu.device_inv_cdf(u, t)), bits(unhex(g["z"])))
+    # every breakpoint +- 48 grid steps, both halves (the index edge cases)
+    bp = t.breakpoints()
+    sel = bp if len(bp) <= 64 else bp[:: len(bp) // 64]
+    k = np.arange(-48, 49) * 2.0 ** -53
+    uu = np.concatenate([(b + k) for b in sel] + [np.array([0.5, 0.5 + 2 ** -53, 0.5 - 2 ** -54])])
+    uu = uu[(uu > 0.5) & (uu < 1.0)]
+    uu = np.concatenate([uu, 1.0 - uu])
+    want = np.array([oracle.approx(name, x) for x in uu])
+    assert np.array_equal(bits(gpu.device_inv_cdf(uu, t)), bits(want))
+
+
+# --------------------------------------------------------------- a7 --------
+def _cases(golden):
+    return [p for p in golden["paths"]]
+
+
+@pytest.mark.parametrize("idx", range(0, 160))
+def test_paths_vs_reference(gpu, golden, oracle, idx):
+    cases = _cases(golden)
+    if idx >= len(cases):
+        pytest.skip("fewer golden cases")
+    c = cases[idx]
+    want = unhex(c["out"]).reshape(-1, 4)
+    n = want.shape[0]
+    model = gpu.make_gbm()
+    out, z = gpu.simulate_paths(model, c["level"], spec(gpu, c["m"]), table(gpu, c["approx"]),
+                                bool(c["kahan"]), n, c["seed"], c["path_base"], want_z=True)
+    # (1) all four legs bitwise == the oracle replayed on the device's own Z
+    cfg = oracle.config(level=c["level"], mantissa_bits=c["m"], approx=c["approx"],
+                        kahan=c["kahan"], seed=c["seed"])
+    rep, _, fails = oracle.simulate(cfg, c["path_base"], n, z_in=z)
+    assert not fails
+    assert np.array_equal(bits(out), bits(rep))
+    # (2) with a table the bar legs do not depend on libm: bitwise == reference
+    if c["approx"] != "exact":
+        assert np.array_equal(bits(out[:, 2:]), bits(want[:, 2:]))
+    # (3) carrier legs within libm tolerance of the reference
+    np.testing.assert_allclose(out[:, :2], want[:, :2], rtol=1e-12, atol=1e-300)
+
+
+def test_reference_unit_pins(gpu):
+    """test_sde.cpp:98-173 on the device."""
+    model = gpu.make_gbm()
+    car = gpu.PrecisionSpec.carrier()
+    # degenerate coupling: carrier + exact => bar legs == hat legs bitwise
+    for level in (1, 3, 6):
+        o = gpu.simulate_paths(model, level, car, None, False, 64, 21, 5)
+        assert np.array_equal(bits(o[:, 2]), bits(o[:, 0]))
+        assert np.array_equal(bits(o[:, 3]), bits(o[:, 1]))
+    # level 0: coarse legs are exactly 0
+    o = gpu.simulate_paths(model, 0, gpu.PrecisionSpec.fp16(), None, False, 16, 3, 0)
+    assert np.all(o[:, 1] == 0.0) and np.all(o[:, 3] == 0.0) and np.all(o[:, 0] != 0.0)
+    # level-1 coarse leg by hand (test_sde.cpp:110-128)
+    o, z = gpu.simulate_paths(model, 1, car, None, False, 1, 33, 4, want_z=True)
+    s = math.sqrt(0.5)
+    dwc = s * z[0, 0] + s * z[0, 1]
+    assert o[0, 1] == 1.0 + (0.05 * 1.0 * 1.0 + 0.2 * 1.0 * dwc)
+    # sigma = 0 closed form in the carrier (test_sde.cpp:49-58)
+    det = gpu.make_gbm(0.05, 0.0)
+    o = gpu.simulate_paths(det, 10, car, None, False, 4, 1, 0)
+    assert np.allclose(o[:, 0], (1.0 + 0.05 * 2 ** -10) ** 1024, rtol=1e-12)
+
+
+# ------------------------------------------------------------ moments ------
+def _moment_close(got, want, var_rtol):
+    n, mean, m2 = want[0], want[1], want[2]
+    assert got[0] == n
+    if n < 2:
+        return
+    var_w = m2 / (n - 1)
+    var_g = got[2] / (n - 1)
+    assert abs(var_g - var_w) <= var_rtol * abs(var_w) + 1e-300, (var_g, var_w)
+    assert abs(got[1] - mean) <= 1e-12 * math.sqrt(max(var_w, 0.0)) + 1e-300, (got[1], mean)
+
+
+@pytest.mark.parametrize("idx", range(8))
+def test_level_moments_vs_reference(gpu, golden, idx):
+    c = golden["moments"][idx]
+    want = [(a[0], *unhex(a[1:])) for a in c["acc"]]
+    model = gpu.make_gbm()
+    args = (model, c["level"], spec(gpu, c["m"]), table(gpu, c["approx"]), bool(c["kahan"]),
+            c["n"], c["seed"], c["path_base"])
+    tree = gpu.run_coupled_paths(*args)
+    seq = gpu.run_coupled_paths(*args, reduce="sequential")
+    for fam, rt in ((0, 1e-12), (1, 1e-12), (2, 1e-10)):
+        for got in (tree, seq):
+            acc = (got.d_hat, got.d_bar, got.d_four)[fam].state()
+            _moment_close(acc, want[fam], rt)
+    if c["approx"] != "exact":  # bar paths bit-exact -> reference-order moments bit-exact
+        assert seq.d_bar.state() == tuple(want[1])
+    print(f"config {idx}: v_hat={tree.d_hat.variance():.10e} ref={want[0][2] / (want[0][0] - 1):.10e}")
+
+
+@pytest.mark.parametrize("level,m,approx,kahan,n,base", [
+    (0, 23, "linear:16", False, 1, 0),
+    (1, 10, "linear:16", True, 255, 7),
+    (2, 7, "cubic:64", False, 257, 1 << 40),
+    (3, 23, "exact", True, 4099, 3),
+    (5, 16, "linear:16", False, 70001, 11),
+    (4, 52, "exact", False, 2 * 262144 + 513, 0),
+])
+def test_moments_bitexact_on_device_paths(gpu, oracle, level, m, approx, kahan, n, base):
+    """Tree and sequential moments are bitwise the restated reductions of
+    the device's own per-path differences (ragged n, multi-chunk)."""
+    model = gpu.make_gbm()
+    sp, tb = spec(gpu, m), table(gpu, approx)
+    out = gpu.simulate_paths(model, level, sp, tb, kahan, n, 9, base)
+    dh = out[:, 0] - (out[:, 1] if level else 0.0)
+    db = out[:, 2] - (out[:, 3] if level else 0.0)
+    tree = gpu.run_coupled_paths(model, level, sp, tb, kahan, n, 9, base)
+    seq = gpu.run_coupled_paths(model, level, sp, tb, kahan, n, 9, base, reduce="sequential")
+    want_tree = oracle.tree_from_values(dh, db)
+    want_seq = oracle.sequential_from_values(dh, db)
+    assert [tree.d_hat.state(), tree.d_bar.state(), tree.d_four.state()] == want_tree
+    assert [seq.d_hat.state(), seq.d_bar.state(), seq.d_four.state()] == want_seq
+
+
+def test_partials_any_split_bitwise(gpu):
+    model = gpu.make_gbm()
+    sp, tb = gpu.PrecisionSpec.fp32(), gpu.InvCdfApprox.parse("linear:16")
+    n = 3 * 262144 + 1000
+    args = (model, 2, sp, tb, True, n, 5, 17)
+    whole = gpu.level_partials(*args, 0, 4)
+    for cut in (1, 2, 3):
+        a = gpu.level_partials(*args, 0, cut)
+        b = gpu.level_partials(*args, cut, 4)
+        assert np.array_equal(bits(np.concatenate([a, b])), bits(whole))
+    folded = gpu.fold_partials(whole)
+    run = gpu.run_coupled_paths(*args)
+    assert folded.d_bar.state() == run.d_bar.state()
+    assert folded.d_four.state() == run.d_four.state()
+
+
+def test_plan_equals_call(gpu):
+    model = gpu.make_gbm()
+    sp, tb = gpu.PrecisionSpec.fp32(), gpu.InvCdfApprox.parse("linear:16")
+    plan = gpu.LevelPlan(model, 6, sp, tb, False, 100000, 1, 6 << 40)
+    plan.launch()
+    a = plan.collect()
+    plan.launch()
+    b = plan.collect()
+    plan.close()
+    c = gpu.run_coupled_paths(model, 6, sp, tb, False, 100000, 1, 6 << 40)
+    assert a.d_hat.state() == b.d_hat.state() == c.d_hat.state()
+    assert a.d_four.state() == c.d_four.state()
+
+
+# ------------------------------------------------- extensions (configs) ----
+@pytest.mark.parametrize("level", [0, 1, 4, 8])
+@pytest.mark.parametrize("approx", ["linear:16", "constant:16", "exact"])
+@pytest.mark.parametrize("kahan", [False, True])
+def test_ieee_half2_legs_vs_ieee_oracle(gpu, oracle, level, approx, kahan):
+    model = gpu.make_gbm()
+    n = 1000
+    out, z = gpu.simulate_paths(model, level, gpu.PrecisionSpec.fp16_ieee(), table(gpu, approx),
+                                kahan, n, 3, 100, want_z=True)
+    cfg = oracle.config(level=level, mantissa_bits=10, approx=approx, kahan=kahan, seed=3,
+                        ieee_half=True)
+    rep, _, fails = oracle.simulate(cfg, 100, n, z_in=z)
+    assert not fails
+    assert np.array_equal(bits(out), bits(rep))
+
+
+@pytest.mark.parametrize("legs", ["hat", "bar", "all"])
+@pytest.mark.parametrize("payoff", ["terminal", "call"])
+def test_legs_and_payoff(gpu, oracle, legs, payoff):
+    model = gpu.make_gbm()
+    level, n = 5, 5000
+    sp, tb = gpu.PrecisionSpec.fp16(), gpu.InvCdfApprox.parse("constant:16")
+    full, z = gpu.simulate_paths(model, level, sp, tb, True, n, 4, 50, want_z=True)
+    mom = gpu.run_coupled_paths(model, level, sp, tb, True, n, 4, 50, legs=legs, payoff=payoff,
+                                strike=1.0)
+    P = (lambda x: np.maximum(x - 1.0, 0.0)) if payoff == "call" else (lambda x: x)
+    dh = P(full[:, 0]) - P(full[:, 1])
+    db = P(full[:, 2]) - P(full[:, 3])
+    want = oracle.tree_from_values(dh if legs != "bar" else np.zeros(n),
+                                   db if legs != "hat" else np.zeros(n),
+                                   {"hat": 1, "bar": 2, "all": 3}[legs])
+    assert [mom.d_hat.state(), mom.d_bar.state(), mom.d_four.state()] == want
+
+
+def test_native_range_fallback_exact(gpu, oracle):
+    """fp32 legs whose state leaves [2^-32, 2^33) are re-run in the exact
+    emulation and still match the unbounded-exponent reference bitwise."""
+    model = gpu.make_gbm(25.0, 0.2)
+    out, z = gpu.simulate_paths(model, 4, gpu.PrecisionSpec.fp32(), None, True, 300, 2, 0,
+                                want_z=True)
+    assert np.max(out[:, 2]) > 2.0 ** 33
+    cfg = oracle.config(level=4, mantissa_bits=23, kahan=True, seed=2, mu=25.0)
+    rep, _, fails = oracle.simulate(cfg, 0, 300, z_in=z)
+    assert not fails and np.array_equal(bits(out), bits(rep))
+
+
+# ----------------------------------------------------------- errors --------
+def test_error_contract(gpu, golden):
+    model = gpu.make_gbm()
+    car = gpu.PrecisionSpec.carrier()
+    errs = {(e["call"], e["n"], e["level"]): e for e in golden["errors"]}
+    with pytest.raises(gpu.InvalidArgument, match=errs[("estimate_level_stats", 1, 3)]["msg"]):
+        gpu.estimate_level_stats(model, 3, car, None, False, 1, 1)
+    with pytest.raises(gpu.InvalidArgument, match=errs[("run_coupled_paths", 4, -1)]["msg"]):
+        gpu.run_coupled_paths(model, -1, car, None, False, 4, 1, 0)
+    empty = gpu.run_coupled_paths(model, -1, car, None, False, 0, 1, 0)
+    assert empty.d_hat.count() == 0
+    bad = gpu.make_gbm(1e30, 0.0, 1e300)
+    with pytest.raises(gpu.DomainError, match=errs[("run_coupled_paths", 8, 4)]["msg"]) as ei:
+        gpu.run_coupled_paths(bad, 4, car, None, False, 8, 1, 0)
+    assert ei.value.path_index == 0
+    with pytest.raises(gpu.InvalidArgument):
+        gpu.run_coupled_paths(model, 2, gpu.PrecisionSpec(23, True), None, False, 8, 1, 0)
+
+
+def test_level_stats_costs(gpu, golden):
+    model = gpu.make_gbm()
+    for c in golden["level_stats"]:
+        want = unhex(c["out"])
+        cost = gpu.CostModel(per_step_arithmetic=c["per_step_arithmetic"])
+        s = gpu.estimate_level_stats(model, c["level"], spec(gpu, c["m"]), table(gpu, c["approx"]),
+                                     bool(c["kahan"]), c["n"], 1, cost)
+        got = [s.mean_hat, s.v_hat, s.v_hat_stderr, s.mean_bar, s.v_bar, s.v_bar_stderr,
+               s.mean_four, s.V_bar, s.V_bar_stderr, s.c_hat, s.c_bar, s.C_bar, s.m_hat, s.m_bar,
+               s.M_bar, s.level]
+        np.testing.assert_array_equal(got[9:], want[9:])  # costs and counts exact
+        np.testing.assert_allclose(got[:9], want[:9], rtol=1e-9, atol=1e-15)
