@@ -237,8 +237,12 @@ def main():
     cfgs = [(l, k) for l in LEVELS for k in KAHAN]
     plans = {(l, k): L.LevelPlan(model, l, spec, approx, k, n_total, SEED, path_base(l, k),
                                  chunks=(c0, c1), device=local) for (l, k) in cfgs}
-    stream = torch.cuda.current_stream(dev)
+    # A dedicated stream: torch's legacy default stream has handle 0, which
+    # the C-ABI reads as "the plan's own stream".
+    stream = torch.cuda.Stream(dev)
+    torch.cuda.set_stream(stream)
     sptr = stream.cuda_stream
+    assert sptr != 0
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 
     def sweep(events=None):

@@ -251,11 +251,11 @@ def test_legs_and_payoff(gpu, oracle, legs, payoff):
 def test_native_range_fallback_exact(gpu, oracle):
     """fp32 legs whose state leaves [2^-32, 2^33) are re-run in the exact
     emulation and still match the unbounded-exponent reference bitwise."""
-    model = gpu.make_gbm(25.0, 0.2)
+    model = gpu.make_gbm(80.0, 0.2)  # EM growth (1 + 80/16)^16 ~ 3e12 > 2^33
     out, z = gpu.simulate_paths(model, 4, gpu.PrecisionSpec.fp32(), None, True, 300, 2, 0,
                                 want_z=True)
     assert np.max(out[:, 2]) > 2.0 ** 33
-    cfg = oracle.config(level=4, mantissa_bits=23, kahan=True, seed=2, mu=25.0)
+    cfg = oracle.config(level=4, mantissa_bits=23, kahan=True, seed=2, mu=80.0)
     rep, _, fails = oracle.simulate(cfg, 0, 300, z_in=z)
     assert not fails and np.array_equal(bits(out), bits(rep))
 

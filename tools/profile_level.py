@@ -1,0 +1,41 @@
+"""One level launch of the sampler, for ncu (-k regex:level_kernel -s 1 -c 1).
+
+    python tools/profile_level.py --level 10 --prec fp32 --approx linear:16
+Launch 0 warms up, launch 1 is the profiled one; both are the C2 level config.
+"""
+from __future__ import annotations
+
+import argparse
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import paper_2012_09739_b200 as L  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--level", type=int, default=10)
+    ap.add_argument("--prec", default="fp32")
+    ap.add_argument("--approx", default="linear:16")
+    ap.add_argument("--kahan", type=int, default=0)
+    ap.add_argument("--legs", default="all")
+    ap.add_argument("--n", type=int, default=1 << 22)
+    ap.add_argument("--launches", type=int, default=2)
+    a = ap.parse_args()
+    spec = L.PrecisionSpec.parse(a.prec)
+    approx = None if a.approx == "exact" else L.InvCdfApprox.parse(a.approx)
+    plan = L.LevelPlan(L.make_gbm(), a.level, spec, approx, bool(a.kahan), a.n, 1,
+                       (a.level << 40) | (a.kahan << 36), legs=a.legs)
+    for _ in range(a.launches):
+        plan.launch()
+        m = plan.collect()
+    print(f"level {a.level} {a.prec} {a.approx} kahan={a.kahan} legs={a.legs} n={a.n}: "
+          f"v_hat={m.d_hat.variance():.6e} v_bar={m.d_bar.variance():.6e} "
+          f"V_bar={m.d_four.variance():.6e}")
+    plan.close()
+
+
+if __name__ == "__main__":
+    main()
