@@ -253,6 +253,18 @@ lpmc_status lpmc_device_inv_cdf(const double* u, uint64_t n, const lpmc_invcdf_t
  */
 lpmc_status lpmc_measure_pipe_peaks(int32_t device, double* out4, lpmc_error* err);
 
+/*
+ * Diagnostics of the device math on host-given inputs: op 0 = exact inverse
+ * CDF (the sampler's), 1 = approximate inverse CDF (table required), 2 = the
+ * reference's Acklam+Newton formula on CUDA libdevice, 3 = erfc core on
+ * t in [0, 6.5).
+ */
+lpmc_status lpmc_device_math(int32_t op, const double* in, uint64_t n,
+                             const lpmc_invcdf_table* table, double* out,
+                             const lpmc_options* opts, lpmc_error* err);
+/* Host evaluation of the same erfc core (bitwise equal to op 3). */
+double lpmc_erfc_core(double t);
+
 /* ---- plans: device-resident repeated launches (bench / sweeps) ---------- */
 typedef struct lpmc_plan lpmc_plan;
 

@@ -139,6 +139,8 @@ SIGNATURES = {
                                    _u64, _u64, _P(Options), _dp, _dp, _P(Error)]),
     "lpmc_device_inv_cdf": (_i32, [_dp, _u64, _P(InvCdfTable), _dp, _P(Options), _P(Error)]),
     "lpmc_measure_pipe_peaks": (_i32, [_i32, _dp, _P(Error)]),
+    "lpmc_device_math": (_i32, [_i32, _dp, _u64, _P(InvCdfTable), _dp, _P(Options), _P(Error)]),
+    "lpmc_erfc_core": (C.c_double, [C.c_double]),
     "lpmc_plan_create": (_i32, [_P(Gbm), _i32, _P(Precision), _P(InvCdfTable), _i32, _u64, _u64,
                                 _u64, _P(Options), _P(C.c_void_p), _P(Error)]),
     "lpmc_plan_create_range": (_i32, [_P(Gbm), _i32, _P(Precision), _P(InvCdfTable), _i32, _u64,

@@ -473,6 +473,25 @@ def device_inv_cdf(u: np.ndarray, approx: Optional[InvCdfApprox] = None,
     return out
 
 
+def device_math(op: str, x: np.ndarray, approx: Optional[InvCdfApprox] = None,
+                device: Optional[int] = None) -> np.ndarray:
+    """Diagnostics: op in {"exact", "approx", "exact_libdevice", "erfc"}."""
+    ops = {"exact": 0, "approx": 1, "exact_libdevice": 2, "erfc": 3}
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    out = np.zeros_like(x)
+    err = N.Error()
+    opts = _options(device=device)
+    N.check(N.load().lpmc_device_math(ops[op], x.ctypes.data_as(N._dp), len(x),
+                                      _table_ptr(approx), out.ctypes.data_as(N._dp),
+                                      C.byref(opts), C.byref(err)), err)
+    return out
+
+
+def erfc_core(t: float) -> float:
+    """Host evaluation of the device erfc core (bitwise the device's)."""
+    return float(N.load().lpmc_erfc_core(float(t)))
+
+
 class LevelPlan:
     """Device-resident repeated launches of one level (buffers and table
     stay in HBM).  launch() only enqueues; collect() waits and folds."""

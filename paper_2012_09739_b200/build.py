@@ -34,7 +34,8 @@ CXX_FLAGS = ["-O2", "-ffp-contract=off", "-fno-fast-math", "-std=c++17", "-fPIC"
 
 SOURCES_CU = ["lpmc_kernels.cu"]
 SOURCES_CXX = ["lpmc_host.cpp"]
-HEADERS = ["lpmc_internal.h", os.path.join("..", "..", "include", "lpmc_b200.h")]
+HEADERS = ["lpmc_internal.h", "lpmc_math.cuh", "lpmc_math_coef.h",
+           os.path.join("..", "..", "include", "lpmc_b200.h")]
 
 
 def _newer(target: str, deps: list[str]) -> bool:

@@ -24,6 +24,7 @@
 
 #include "../../include/lpmc_b200.h"
 #include "lpmc_internal.h"
+#include "lpmc_math.cuh"
 
 namespace lpmc_b200 {
 namespace {
@@ -1000,9 +1001,12 @@ lpmc_status lpmc_simulate_paths(const lpmc_gbm* model, int32_t level, const lpmc
   return cuda_fail(err, e, "path dump");
 }
 
-lpmc_status lpmc_device_inv_cdf(const double* u, uint64_t n, const lpmc_invcdf_table* table,
-                                double* out, const lpmc_options* opts, lpmc_error* err) {
+lpmc_status lpmc_device_math(int32_t op, const double* u, uint64_t n,
+                             const lpmc_invcdf_table* table, double* out,
+                             const lpmc_options* opts, lpmc_error* err) {
   if (n == 0) return ok(err);
+  if (op < 0 || op > 3) return fail(err, LPMC_INVALID_ARGUMENT, "bad math op");
+  if (op == 1 && table == nullptr) return fail(err, LPMC_INVALID_ARGUMENT, "op 1 needs a table");
   HostTable ht;
   if (table != nullptr) {
     lpmc_status st = prepare_table(table, &ht, err);
@@ -1025,8 +1029,7 @@ lpmc_status lpmc_device_inv_cdf(const double* u, uint64_t n, const lpmc_invcdf_t
       cudaMemcpyAsync(dtab.ptr, ht.rows.data(), ht.rows.size() * sizeof(double),
                       cudaMemcpyHostToDevice, stream);
     LaunchResult r = launch_inv_cdf(du.ptr, n, table ? dtab.ptr : nullptr, ht.K, ht.degree,
-                                    ht.dyadic, ht.tail, table ? nullptr : dout.ptr,
-                                    table ? dout.ptr : nullptr, stream);
+                                    ht.dyadic, ht.tail, op, dout.ptr, stream);
     t_launches += r.kernels;
     e = static_cast<cudaError_t>(r.cuda_error);
     if (e == cudaSuccess)
@@ -1038,6 +1041,16 @@ lpmc_status lpmc_device_inv_cdf(const double* u, uint64_t n, const lpmc_invcdf_t
   dtab.release();
   if (e != cudaSuccess) return cuda_fail(err, e, "inv_cdf");
   return ok(err);
+}
+
+lpmc_status lpmc_device_inv_cdf(const double* u, uint64_t n, const lpmc_invcdf_table* table,
+                                double* out, const lpmc_options* opts, lpmc_error* err) {
+  return lpmc_device_math(table ? 1 : 0, u, n, table, out, opts, err);
+}
+
+double lpmc_erfc_core(double t) {
+  if (!(t >= 0.0 && t < math::kFastTMax)) return std::erfc(t);
+  return math::erfc_fast(t, math::kErfcxTableHost);
 }
 
 lpmc_status lpmc_measure_pipe_peaks(int32_t device, double* out4, lpmc_error* err) {

@@ -67,9 +67,9 @@ LaunchResult launch_chunk_reduce(const double* batch_acc, uint64_t n_batches, ui
 LaunchResult launch_sequential_batches(const double* path_diff, uint64_t n_paths,
                                        double* batch_acc, void* stream);
 // Exact / approximate inverse CDF of host-given uniforms (parity hooks).
+// op 0 exact, 1 approximate (table), 2 libdevice reference formula, 3 erfc core.
 LaunchResult launch_inv_cdf(const double* u, uint64_t n, const double* table, int K, int degree,
-                            int dyadic, double tail, double* out_exact, double* out_approx,
-                            void* stream);
+                            int dyadic, double tail, int op, double* out, void* stream);
 // Max dynamic shared memory the path kernels were configured for.
 int configure_kernels();
 // Lane-op rates on the current device: fp64 FMA, fp32 FMA, half2 HFMA2

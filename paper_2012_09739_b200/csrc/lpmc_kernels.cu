@@ -29,6 +29,7 @@
 #include <cstdint>
 
 #include "lpmc_internal.h"
+#include "lpmc_math.cuh"
 
 namespace lpmc_b200 {
 namespace {
@@ -54,39 +55,13 @@ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
 }
 
 // ------------------------------------------------ exact inverse CDF --------
-// Acklam's rational initialiser + one Newton step on Phi, for u in (0, 1/2].
-__device__ __forceinline__ double phi_inv_lower(double u) {
-  double x;
-  if (u < 0.02425) {
-    const double q = sqrt(-2.0 * log(u));
-    const double num = ((((-7.784894002430293e-03 * q + -3.223964580411365e-01) * q +
-                          -2.400758277161838e+00) * q + -2.549732539343734e+00) * q +
-                        4.374664141464968e+00) * q + 2.938163982698783e+00;
-    const double den = (((7.784695709041462e-03 * q + 3.224671290700398e-01) * q +
-                         2.445134137142996e+00) * q + 3.754408661907416e+00) * q + 1.0;
-    x = num / den;
-  } else {
-    const double q = u - 0.5;
-    const double r = q * q;
-    const double num = ((((-3.969683028665376e+01 * r + 2.209460984245205e+02) * r +
-                          -2.759285104469687e+02) * r + 1.383577518672690e+02) * r +
-                        -3.066479806614716e+01) * r + 2.506628277459239e+00;
-    const double den = ((((-5.447609879822406e+01 * r + 1.615858368580409e+02) * r +
-                          -1.556989798598866e+02) * r + 6.680131188771972e+01) * r +
-                        -1.328068155288572e+01) * r + 1.0;
-    x = num * q / den;
-  }
-  const double resid = 0.5 * erfc(-x * 0.7071067811865475244) - u;
-  const double dens = 0.3989422804014326779 * exp(-0.5 * x * x);
-  return x - resid / dens;
-}
+// math::phi_inv (lpmc_math.cuh): Acklam + one Newton step with a
+// constant-bank erfc; the erfcx coefficient table is staged in shared memory.
+using math::phi_inv;
+constexpr int kErfcxWords = math::kErfcxRows * math::kErfcxN;
 
-// Reflection about 1/2 exactly as gaussian.hpp:62-64 (1-u is exact there).
-__device__ __forceinline__ double phi_inv(double u) {
-  const bool upper = u > 0.5;
-  const double r = phi_inv_lower(upper ? 1.0 - u : u);
-  const double z = upper ? -r : r;
-  return u == 0.5 ? 0.0 : z;
+__device__ __forceinline__ void stage_erfcx(double* s_erfcx) {
+  for (int i = threadIdx.x; i < kErfcxWords; i += blockDim.x) s_erfcx[i] = math::kErfcxTable[i];
 }
 
 // ------------------------------------------- approximate inverse CDF -------
@@ -404,7 +379,7 @@ __device__ __forceinline__ void note_fail(uint64_t& fk, bool bad, uint64_t n, ui
 }
 
 template <class Arith, bool KAHAN, int LEGS, bool APPROX>
-__global__ void __launch_bounds__(kBatch / Arith::NP)
+__global__ void __launch_bounds__(kBatch / Arith::NP, 3 * Arith::NP)
     level_kernel(const __grid_constant__ LevelArgs A) {
   using T = typename Arith::T;
   constexpr int NP = Arith::NP;
@@ -413,12 +388,14 @@ __global__ void __launch_bounds__(kBatch / Arith::NP)
   constexpr bool kNeedExact = kHat || !APPROX;
 
   extern __shared__ double s_table[];
+  __shared__ double s_erfcx[kNeedExact ? kErfcxWords : 1];
+  if constexpr (kNeedExact) stage_erfcx(s_erfcx);
   TableView tab{};
   if constexpr (APPROX) {
     for (int i = threadIdx.x; i < kTableRows * A.K; i += blockDim.x) s_table[i] = A.table[i];
-    __syncthreads();
     tab = table_view(s_table, A.K, A.degree, A.dyadic, A.tail);
   }
+  __syncthreads();
 
   const Arith ar(A);
   const uint64_t batch = A.batch0 + blockIdx.x;
@@ -461,7 +438,7 @@ __global__ void __launch_bounds__(kBatch / Arith::NP)
       const uint64_t top = w >> 11;
       note_fail(fk[p], top == kTopDraw, n, kStageDraw);
       const double u = __dadd_rn(__dmul_rn(__ull2double_rn(top), 0x1p-53), 0x1p-54);
-      z[p] = kNeedExact ? phi_inv(u) : 0.0;
+      z[p] = kNeedExact ? phi_inv(u, s_erfcx) : 0.0;
       if (A.z_out != nullptr && valid[p]) A.z_out[local[p] * zstride + n] = z[p];
       if constexpr (APPROX) {
         zl[p] = approx_inv(tab, u);
@@ -709,18 +686,29 @@ __global__ void sequential_batch_kernel(const double* __restrict__ path_diff, ui
   store_acc(batch_acc + 15 * b + 5 * f, a);
 }
 
+// op 0: exact Gaussian (product path), 1: approximate (table), 2: the
+// reference's formula on libdevice, 3: erfc core on t in [0, 6.5).
 __global__ void inv_cdf_kernel(const double* __restrict__ u, uint64_t n,
                                const double* __restrict__ table, int K, int degree, int dyadic,
-                               double tail, double* __restrict__ out_exact,
-                               double* __restrict__ out_approx) {
+                               double tail, int op, double* __restrict__ out) {
+  __shared__ double s_erfcx[kErfcxWords];
+  stage_erfcx(s_erfcx);
+  __syncthreads();
   const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const double x = u[i];
-  if (out_exact != nullptr) out_exact[i] = phi_inv(x);
-  if (out_approx != nullptr && table != nullptr) {
+  double r = 0.0;
+  if (op == 0) {
+    r = phi_inv(x, s_erfcx);
+  } else if (op == 1) {
     const TableView t = table_view(table, K, degree, dyadic, tail);
-    out_approx[i] = approx_inv(t, x);
+    r = approx_inv(t, x);
+  } else if (op == 2) {
+    r = math::phi_inv_libdevice(x);
+  } else {
+    r = math::erfc_fast(x, s_erfcx);
   }
+  out[i] = r;
 }
 
 // ------------------------------------------------------ pipe peaks ---------
@@ -839,7 +827,10 @@ cudaError_t configure_arith() {
 }  // namespace
 
 int configure_kernels() {
-  cudaError_t e = configure_arith<ArithCarrier>();
+  // math constants live in an uninitialised __constant__ block (see
+  // lpmc_math.cuh): upload them for the current device first
+  cudaError_t e = cudaMemcpyToSymbol(math::kMath, math::kMathHost, sizeof(math::kMathHost));
+  if (e == cudaSuccess) e = configure_arith<ArithCarrier>();
   if (e == cudaSuccess) e = configure_arith<ArithF32>();
   if (e == cudaSuccess) e = configure_arith<ArithF32Round>();
   if (e == cudaSuccess) e = configure_arith<ArithF64Round>();
@@ -918,11 +909,10 @@ int measure_pipe_peaks(double* out4) {
 }
 
 LaunchResult launch_inv_cdf(const double* u, uint64_t n, const double* table, int K, int degree,
-                            int dyadic, double tail, double* out_exact, double* out_approx,
-                            void* stream) {
+                            int dyadic, double tail, int op, double* out, void* stream) {
   const unsigned blocks = static_cast<unsigned>((n + 255) / 256);
   inv_cdf_kernel<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(
-      u, n, table, K, degree, dyadic, tail, out_exact, out_approx);
+      u, n, table, K, degree, dyadic, tail, op, out);
   return {static_cast<int>(cudaGetLastError()), 1};
 }
 

@@ -1,0 +1,320 @@
+// Device math for the exact Gaussian: the reference's Acklam + one Newton
+// step (gaussian.hpp:26-65), restated for the sm_100a issue budget.
+//
+// Why not libdevice: its erfc/exp keep their polynomial coefficients as
+// 64-bit literals, which ptxas rematerialises through uniform moves on every
+// loop iteration (136 UMOV per warp-step, 24% of all issue slots in the v0
+// kernel, profiles/r01_v0_summary.md), and their range branches diverge.
+// Here every coefficient is a constant-bank operand (__constant__) or a
+// shared-memory load, and the hot path has one branch (Acklam's tail).
+//
+// Accuracy design:
+//  * Newton squares the initial error, so x0 (Acklam) only needs ~1e-12:
+//    its division/log/sqrt use MUFU seeds + Newton refinement.
+//  * The correction (Phi(x0) - u) / pdf needs Phi(x0) to ~1 ulp of u, and
+//    1/pdf to ~1e-10 only.  Phi(x0) = erfc(t)/2, t = -x0/sqrt(2), with
+//    erfc(t) = 2^k p(r) G(t): t^2 split exactly by FMA, exp(-t^2) = 2^k p(r)
+//    by a degree-11 minimax polynomial, and G = erfcx by 26 degree-11
+//    piecewise polynomials (tools/fit_math.py, 7e-18 relative).  1/pdf is
+//    sqrt(2 pi) 2^-k / p(r): the same exponential, no second exp, no division.
+//  * t > 6.5 (u < 1e-20; never drawn by the sampler, whose u >= 2^-54) takes
+//    a libdevice slow path.
+//
+// All functions are __host__ __device__ so tests/cpp/math_accuracy.cpp can
+// check the erfc core on the CPU against mpmath; the core uses only IEEE
+// fma/mul/add and integer bit operations, hence is bitwise the same there.
+#pragma once
+
+#include <cstdint>
+#include <cstring>
+#include <cmath>
+
+#include "lpmc_math_coef.h"
+
+#ifdef __CUDACC__
+#define LPMC_HD __host__ __device__ __forceinline__
+#else
+#define LPMC_HD inline
+#endif
+
+namespace lpmc_b200 {
+namespace math {
+
+LPMC_HD double fmad(double a, double b, double c) {
+#ifdef __CUDA_ARCH__
+  return __fma_rn(a, b, c);
+#else
+  return std::fma(a, b, c);
+#endif
+}
+
+LPMC_HD uint64_t bits(double x) {
+#ifdef __CUDA_ARCH__
+  return static_cast<uint64_t>(__double_as_longlong(x));
+#else
+  uint64_t b;
+  std::memcpy(&b, &x, 8);
+  return b;
+#endif
+}
+
+LPMC_HD double from_bits(uint64_t b) {
+#ifdef __CUDA_ARCH__
+  return __longlong_as_double(static_cast<long long>(b));
+#else
+  double x;
+  std::memcpy(&x, &b, 8);
+  return x;
+#endif
+}
+
+// 1/d to ~1 ulp: hardware seed (MUFU.RCP64H) + two Newton steps.
+LPMC_HD double rcp_refined(double d) {
+#ifdef __CUDA_ARCH__
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(d));
+  double e = fmad(-d, r, 1.0);
+  r = fmad(r, e, r);
+  e = fmad(-d, r, 1.0);
+  return fmad(r, e, r);
+#else
+  return 1.0 / d;
+#endif
+}
+
+// 1/d to ~2^-44: seed + one Newton step (for the Newton correction only).
+LPMC_HD double rcp_coarse(double d) {
+#ifdef __CUDA_ARCH__
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(d));
+  const double e = fmad(-d, r, 1.0);
+  return fmad(r, e, r);
+#else
+  return 1.0 / d;
+#endif
+}
+
+// sqrt(y), y > 0, to ~2^-44 (Acklam tail only).
+LPMC_HD double sqrt_coarse(double y) {
+#ifdef __CUDA_ARCH__
+  double r;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(y));
+  const double h = 0.5 * y;
+  r = r * fmad(-h * r, r, 1.5);
+  return y * r;
+#else
+  return std::sqrt(y);
+#endif
+}
+
+// Scalar coefficients, one constant block.  On the device it is deliberately
+// NOT statically initialised: ptxas constant-folds initialised __constant__
+// data back into 64-bit immediates (uniform-register moves again); uploaded
+// at context creation (upload_constants), every use is a c[0x3][...] operand.
+enum : int {
+  kOffAckA = 0,                     // Acklam central numerator a0..a5   (gaussian.hpp:28-30)
+  kOffAckB = 6,                     // Acklam central denominator b0..b4 (:31-33)
+  kOffAckC = 11,                    // Acklam tail numerator c0..c5      (:34-36)
+  kOffAckD = 17,                    // Acklam tail denominator d0..d3    (:37-38)
+  kOffLogS = 21,                    // 2/(2i+1), i = 0..6: log(m) = s sum s^2i 2/(2i+1)
+  kOffExp = 28,                     // exp minimax, LPMC_EXP_DEG + 1 terms
+  kOffMisc = kOffExp + LPMC_EXP_DEG + 1,
+  kLog2e = kOffMisc + 0,            // log2(e)
+  kLn2Hi = kOffMisc + 1,            // ln 2 split: 32 significant bits (k * hi exact)
+  kLn2Lo = kOffMisc + 2,
+  kLn2 = kOffMisc + 3,
+  kInvSqrt2 = kOffMisc + 4,         // gaussian.hpp:15 literal
+  kSqrt2Pi = kOffMisc + 5,
+  kTailU = kOffMisc + 6,            // Acklam's u_low = 0.02425 (gaussian.hpp:38)
+  kSqrtHalfBits = kOffMisc + 7,     // unused slot (alignment)
+  kMathCount = kOffMisc + 8
+};
+
+static const double kMathHost[kMathCount] = {
+    -3.969683028665376e+01, 2.209460984245205e+02, -2.759285104469687e+02,
+    1.383577518672690e+02, -3.066479806614716e+01, 2.506628277459239e+00,
+    -5.447609879822406e+01, 1.615858368580409e+02, -1.556989798598866e+02,
+    6.680131188771972e+01, -1.328068155288572e+01,
+    -7.784894002430293e-03, -3.223964580411365e-01, -2.400758277161838e+00,
+    -2.549732539343734e+00, 4.374664141464968e+00, 2.938163982698783e+00,
+    7.784695709041462e-03, 3.224671290700398e-01, 2.445134137142996e+00,
+    3.754408661907416e+00,
+    2.0, 2.0 / 3.0, 2.0 / 5.0, 2.0 / 7.0, 2.0 / 9.0, 2.0 / 11.0, 2.0 / 13.0,
+    LPMC_EXP_COEF_LIST,
+    1.4426950408889634, 6.93147180369123816490e-01, 1.90821492927058770002e-10,
+    6.93147180559945309417e-01, 0.7071067811865475244, 2.5066282746310002, 0.02425, 0.0};
+static const double kErfcxTableHost[(LPMC_ERFCX_DEG + 2) * LPMC_ERFCX_INTERVALS] = LPMC_ERFCX_COEF;
+
+#ifdef __CUDACC__
+__constant__ double kMath[kMathCount];
+__device__ const double kErfcxTable[(LPMC_ERFCX_DEG + 2) * LPMC_ERFCX_INTERVALS] = LPMC_ERFCX_COEF;
+#endif
+
+#ifdef __CUDA_ARCH__
+#define LPMC_K(i) kMath[i]
+#else
+#define LPMC_K(i) kMathHost[i]
+#endif
+
+constexpr int kErfcxRows = LPMC_ERFCX_DEG + 2;
+constexpr int kErfcxN = LPMC_ERFCX_INTERVALS;
+constexpr double kFastTMax = 6.5;  // 26 intervals of 1/4
+
+// exp(-(th + tl)) = 2^k p, p in [2^-1/2, 2^1/2], for th in [0, 708].
+struct ExpSplit {
+  double p;
+  int k;
+};
+
+LPMC_HD ExpSplit exp_neg(double th, double tl) {
+  const double kShift = 6755399441055744.0;  // 1.5 * 2^52 (an encodable immediate)
+  const double kd = fmad(-th, LPMC_K(kLog2e), kShift) - kShift;  // round(-th log2 e)
+  const int k = static_cast<int>(kd);
+  double r = fmad(kd, -LPMC_K(kLn2Hi), -th);
+  r = fmad(kd, -LPMC_K(kLn2Lo), r);
+  r = r - tl;
+  double q = LPMC_K(kOffExp + LPMC_EXP_DEG);
+#ifdef __CUDA_ARCH__
+#pragma unroll
+#endif
+  for (int i = LPMC_EXP_DEG - 1; i >= 0; --i) q = fmad(q, r, LPMC_K(kOffExp + i));
+  return ExpSplit{q, k};
+}
+
+// erfcx(t) for t in [0, 6.5) from a [kErfcxRows][kErfcxN] coefficient table.
+LPMC_HD double erfcx_piecewise(double t, const double* tab) {
+  int j = static_cast<int>(t * 4.0);
+  j = j < kErfcxN - 1 ? j : kErfcxN - 1;
+  const double s = t - (0.25 * j + 0.125);
+  double q = tab[LPMC_ERFCX_DEG * kErfcxN + j];
+#ifdef __CUDA_ARCH__
+#pragma unroll
+#endif
+  for (int i = LPMC_ERFCX_DEG - 1; i >= 1; --i) q = fmad(q, s, tab[i * kErfcxN + j]);
+  const double lo = tab[(LPMC_ERFCX_DEG + 1) * kErfcxN + j];
+  return tab[j] + fmad(q, s, lo);
+}
+
+// 2^k x for |k| <= 1022 and a normal result (the fast path has |k| <= 62).
+LPMC_HD double scale(double x, int k) {
+  return x * from_bits(static_cast<uint64_t>(1023 + k) << 52);
+}
+
+// erfc(t), 0 <= t < 6.5 (host/device identical).
+LPMC_HD double erfc_fast(double t, const double* tab) {
+  const double th = t * t;
+  const double tl = fmad(t, t, -th);
+  const ExpSplit e = exp_neg(th, tl);
+  return scale(e.p * erfcx_piecewise(t, tab), e.k);
+}
+
+#ifdef __CUDACC__
+// The reference's own formula on libdevice (slow path, t > 6.5 only).
+__device__ __forceinline__ double phi_inv_lower_libdevice(double u) {
+  double x;
+  if (u < 0.02425) {
+    const double q = sqrt(-2.0 * log(u));
+    const double num = ((((-7.784894002430293e-03 * q + -3.223964580411365e-01) * q +
+                          -2.400758277161838e+00) * q + -2.549732539343734e+00) * q +
+                        4.374664141464968e+00) * q + 2.938163982698783e+00;
+    const double den = (((7.784695709041462e-03 * q + 3.224671290700398e-01) * q +
+                         2.445134137142996e+00) * q + 3.754408661907416e+00) * q + 1.0;
+    x = num / den;
+  } else {
+    const double q = u - 0.5;
+    const double r = q * q;
+    const double num = ((((-3.969683028665376e+01 * r + 2.209460984245205e+02) * r +
+                          -2.759285104469687e+02) * r + 1.383577518672690e+02) * r +
+                        -3.066479806614716e+01) * r + 2.506628277459239e+00;
+    const double den = ((((-5.447609879822406e+01 * r + 1.615858368580409e+02) * r +
+                          -1.556989798598866e+02) * r + 6.680131188771972e+01) * r +
+                        -1.328068155288572e+01) * r + 1.0;
+    x = num * q / den;
+  }
+  const double resid = 0.5 * erfc(-x * 0.7071067811865475244) - u;
+  const double dens = 0.3989422804014326779 * exp(-0.5 * x * x);
+  return x - resid / dens;
+}
+
+// log(u) for normal u > 0 to ~1e-13 absolute (Acklam tail only).
+__device__ __forceinline__ double log_coarse(double u) {
+  const uint64_t b = bits(u);
+  int e = static_cast<int>(b >> 52) - 1023;
+  uint64_t mb = (b & 0x000FFFFFFFFFFFFFull) | 0x3FF0000000000000ull;  // m in [1, 2)
+  if (mb > 0x3FF6A09E667F3BCDull) {  // m > sqrt(2): use m/2, e+1
+    mb -= 0x0010000000000000ull;
+    e += 1;
+  }
+  const double m = from_bits(mb);
+  const double f = m - 1.0;
+  const double s = f * rcp_coarse(2.0 + f);
+  const double s2 = s * s;
+  double p = LPMC_K(kOffLogS + 6);
+#pragma unroll
+  for (int i = 5; i >= 0; --i) p = fmad(p, s2, LPMC_K(kOffLogS + i));
+  return fmad(static_cast<double>(e), LPMC_K(kLn2), s * p);
+}
+
+// Acklam's initial approximation for u in (0, 1/2] (gaussian.hpp:26-51),
+// to ~1e-12 relative of the reference's x0.
+__device__ __forceinline__ double acklam_lower(double u) {
+  if (u < LPMC_K(kTailU)) {
+    const double q = sqrt_coarse(-2.0 * log_coarse(u));
+    double num = LPMC_K(kOffAckC);
+#pragma unroll
+    for (int i = 1; i < 6; ++i) num = fmad(num, q, LPMC_K(kOffAckC + i));
+    double den = LPMC_K(kOffAckD);
+#pragma unroll
+    for (int i = 1; i < 4; ++i) den = fmad(den, q, LPMC_K(kOffAckD + i));
+    den = fmad(den, q, 1.0);
+    return num * rcp_refined(den);
+  }
+  const double q = u - 0.5;
+  const double r = q * q;
+  double num = LPMC_K(kOffAckA);
+#pragma unroll
+  for (int i = 1; i < 6; ++i) num = fmad(num, r, LPMC_K(kOffAckA + i));
+  double den = LPMC_K(kOffAckB);
+#pragma unroll
+  for (int i = 1; i < 5; ++i) den = fmad(den, r, LPMC_K(kOffAckB + i));
+  den = fmad(den, r, 1.0);
+  return (num * q) * rcp_refined(den);
+}
+
+// exact_inv_cdf lower half (gaussian.hpp:26-55) for u in (0, 1/2]:
+// Acklam x0, then x0 - (Phi(x0) - u) / pdf(x0) with Phi(x0) = erfc(t)/2,
+// t = (-x0) * (1/sqrt 2) rounded exactly as the reference rounds it.
+__device__ __forceinline__ double phi_inv_lower_fast(double u, const double* erfcx_tab) {
+  const double x0 = acklam_lower(u);
+  const double t = -x0 * LPMC_K(kInvSqrt2);
+  if (!(t < kFastTMax)) return phi_inv_lower_libdevice(u);
+  const double th = t * t;
+  const double tl = fmad(t, t, -th);
+  const ExpSplit e = exp_neg(th, tl);
+  const double pg = e.p * erfcx_piecewise(t, erfcx_tab);
+  const double cdf = scale(pg, e.k - 1);  // 0.5 erfc(t)
+  const double resid = cdf - u;
+  // 1/pdf(x0) = sqrt(2 pi) exp(t^2) = sqrt(2 pi) 2^-k / p
+  const double inv_pdf = scale(LPMC_K(kSqrt2Pi) * rcp_coarse(e.p), -e.k);
+  return x0 - resid * inv_pdf;
+}
+
+// Reflection about 1/2 exactly as gaussian.hpp:62-64 (1-u is exact there).
+__device__ __forceinline__ double phi_inv(double u, const double* erfcx_tab) {
+  const bool upper = u > 0.5;
+  const double r = phi_inv_lower_fast(upper ? 1.0 - u : u, erfcx_tab);
+  const double z = upper ? -r : r;
+  return u == 0.5 ? 0.0 : z;
+}
+
+// The same with the reference's formula on libdevice (diagnostics only).
+__device__ __forceinline__ double phi_inv_libdevice(double u) {
+  const bool upper = u > 0.5;
+  const double r = phi_inv_lower_libdevice(upper ? 1.0 - u : u);
+  const double z = upper ? -r : r;
+  return u == 0.5 ? 0.0 : z;
+}
+#endif
+
+}  // namespace math
+}  // namespace lpmc_b200

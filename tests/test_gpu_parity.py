@@ -58,6 +58,32 @@ def test_exact_inv_cdf_vs_glibc(gpu, golden):
     assert np.array_equal(bits(gpu.device_inv_cdf(up)), bits(-gpu.device_inv_cdf(1.0 - up)))
 
 
+def test_device_erfc_core_equals_host(gpu):
+    """The device erfc core is the same IEEE operation sequence as the host
+    evaluation that test_math_host.py checks against mpmath."""
+    rng = np.random.default_rng(5)
+    t = np.concatenate([rng.uniform(0, 6.5, 20000), np.arange(26) * 0.25])
+    dev = gpu.api.device_math("erfc", t)
+    host = np.array([gpu.api.erfc_core(x) for x in t])
+    assert np.array_equal(bits(dev), bits(host))
+
+
+def test_exact_z_agreement_report(gpu, ref):
+    """Bitwise agreement of the device exact Gaussians with glibc's, for the
+    product path and for the reference's formula on libdevice (context)."""
+    u = np.concatenate([ref.uniforms(77, p, 2048) for p in range(64)])
+    zr = ref.exact_inv_cdf(u)
+    fast = gpu.device_inv_cdf(u)
+    libd = gpu.api.device_math("exact_libdevice", u)
+    f_eq = np.mean(bits(fast) == bits(zr))
+    l_eq = np.mean(bits(libd) == bits(zr))
+    f_ulp = np.abs(bits(fast).astype(np.int64) - bits(zr).astype(np.int64))
+    print(f"\nZ == glibc: product path {f_eq:.4f} (max {f_ulp.max()} ulp), "
+          f"libdevice formula {l_eq:.4f}")
+    assert np.all(np.abs(fast - zr) <= z_tolerance(u, zr))
+    assert f_eq > 0.5
+
+
 @pytest.mark.parametrize("name", ["linear:2", "linear:8", "linear:16", "linear:32", "cubic:16",
                                   "linear:64", "cubic:64", "linear:1024"])
 def test_approx_inv_cdf_bitexact(gpu, golden, oracle, name):
