@@ -27,15 +27,15 @@ INCLUDE = os.path.join(os.path.dirname(PKG), "include")
 CUDA_HOME = os.environ.get("CUDA_HOME", "/usr/local/cuda")
 NVCC = os.path.join(CUDA_HOME, "bin", "nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-NVCC_FLAGS = ARCH + ["-O3", "-fmad=false", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
-                     "-Xptxas", "-warn-spills"]
+NVCC_FLAGS = ARCH + ["-O3", "-fmad=false", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC"]
 CXX_FLAGS = ["-O2", "-ffp-contract=off", "-fno-fast-math", "-std=c++17", "-fPIC", "-Wall",
              "-Wextra", f"-I{CUDA_HOME}/include"]
 
-SOURCES_CU = ["lpmc_kernels.cu"]
+SOURCES_CU = ["lpmc_kernels.cu", "lpmc_level_carrier.cu", "lpmc_level_f32.cu",
+              "lpmc_level_f32r.cu", "lpmc_level_f64r.cu", "lpmc_level_half2.cu"]
 SOURCES_CXX = ["lpmc_host.cpp"]
-HEADERS = ["lpmc_internal.h", "lpmc_math.cuh", "lpmc_math_coef.h",
-           os.path.join("..", "..", "include", "lpmc_b200.h")]
+HEADERS = ["lpmc_internal.h", "lpmc_math.cuh", "lpmc_math_coef.h", "lpmc_device.cuh",
+           "lpmc_level.cuh", os.path.join("..", "..", "include", "lpmc_b200.h")]
 
 
 def _newer(target: str, deps: list[str]) -> bool:
@@ -54,13 +54,18 @@ def build(force: bool = False, verbose_ptxas: bool = False) -> str:
     os.makedirs(BUILD, exist_ok=True)
     hdrs = [os.path.join(CSRC, h) for h in HEADERS]
     objs = []
+    jobs = []
     for src in SOURCES_CU:
         s = os.path.join(CSRC, src)
         o = os.path.join(BUILD, src + ".o")
         if force or _newer(o, [s] + hdrs):
             extra = ["-Xptxas", "-v"] if verbose_ptxas else []
-            _run([NVCC] + NVCC_FLAGS + extra + ["-c", s, "-o", o])
+            jobs.append([NVCC] + NVCC_FLAGS + extra + ["-c", s, "-o", o])
         objs.append(o)
+    if jobs:  # one translation unit per bar arithmetic: compile in parallel
+        from concurrent.futures import ThreadPoolExecutor
+        with ThreadPoolExecutor(max_workers=min(len(jobs), os.cpu_count() or 1)) as ex:
+            list(ex.map(_run, jobs))
     cxx = os.environ.get("CXX", shutil.which("g++") or "g++")
     for src in SOURCES_CXX:
         s = os.path.join(CSRC, src)

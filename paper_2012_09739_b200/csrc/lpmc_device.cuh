@@ -1,0 +1,420 @@
+// Device building blocks of the level sampler (shared by every kernel TU):
+// counter RNG, approximate inverse CDF, emulated rounding, bar-leg arithmetic
+// policies, the fixed batch-moment tree and the Pebay merge.
+//
+// Reference cross-walk (file:line under /root/reference/proj/include/lpmc):
+//   mix64 / stream_word / next      uniform.hpp:13-41
+//   InvCdfApprox::operator()        invcdf_approx.hpp:44-90
+//   round_to_precision / fp_*       softfloat.hpp:69-111
+//   MomentAccumulator add/merge     stats.hpp:15-54
+#pragma once
+
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "lpmc_internal.h"
+#include "lpmc_math.cuh"
+
+namespace lpmc_b200 {
+namespace dev {
+
+constexpr int kBatch = 256;
+constexpr int kChunkBatches = 1024;
+constexpr int kChunkThreads = 512;
+constexpr uint64_t kTopDraw = 0x1FFFFFFFFFFFFFull;  // (w >> 11) that rounds u to 1.0
+constexpr uint64_t kNoFail = ~0ull;
+constexpr int kErfcxWords = math::kErfcxRows * math::kErfcxN;
+
+enum : uint32_t { kStageDraw = 0, kStageHatFine = 1, kStageBarFine = 2, kStageHatCoarse = 3,
+                  kStageBarCoarse = 4 };
+enum : uint32_t { kKindU1 = 1, kKindNonFinite = 2, kKindState = 3 };
+
+// ---------------------------------------------------------------- RNG ------
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z ^= z >> 33;
+  z *= 0xff51afd7ed558ccdull;
+  z ^= z >> 33;
+  z *= 0xc4ceb9fe1a85ec53ull;
+  z ^= z >> 33;
+  return z;
+}
+
+// key of path i: mix64(mix64(seed + phi) ^ mix64(i + c2)) (uniform.hpp:23-24),
+// the first factor hoisted by the host (LevelArgs::seed_key).
+__device__ __forceinline__ uint64_t path_key(uint64_t seed_key, uint64_t path) {
+  return mix64(seed_key ^ mix64(path + 0xbf58476d1ce4e5b9ull));
+}
+
+// u = (w >> 11) 2^-53 + 2^-54 with w = mix64(mix64(key + ctr c3)); the
+// running kc = key + ctr c3 is strength-reduced (uniform.hpp:25, :38-41).
+__device__ __forceinline__ double next_uniform(uint64_t& kc, bool& top) {
+  const uint64_t w = mix64(mix64(kc));
+  kc += 0x94d049bb133111ebull;
+  const uint64_t b = w >> 11;
+  top = b == kTopDraw;
+  return __dadd_rn(__dmul_rn(__ull2double_rn(b), 0x1p-53), 0x1p-54);
+}
+
+__device__ __forceinline__ void stage_erfcx(double* s_erfcx) {
+  for (int i = threadIdx.x; i < kErfcxWords; i += blockDim.x) s_erfcx[i] = math::kErfcxTable[i];
+}
+
+// ------------------------------------------- approximate inverse CDF -------
+// Shared-memory table, kTableRows rows of `stride` doubles (stride 32 for the
+// dyadic layout K <= 32, K otherwise): a_j, w_j, c0..c3, v-thresholds.
+struct TableView {
+  const double* base;
+  int stride, K, degree, dyadic, simple;
+  double tail;
+};
+
+// InvCdfApprox::operator() (invcdf_approx.hpp:44-90).
+//  * dyadic tables (K <= 32, w_max = K+1): the reference's j = floor(-log2 v)
+//    - 1 read from the exponent of v = 1 - u' (exact on the 2^-53 grid,
+//    SURVEY.md §A3); u' in [a_j, b_j) so t in [-1, 1) and the reference's
+//    clamps are no-ops; 2(u'-a)/(b-a) = 2(u'-a) 2^(j+2) exactly.
+//  * general K: index from host thresholds that reproduce the reference's
+//    log2-based index on every representable v; division and clamps as the
+//    reference.
+//  * `simple` (host-proved: every c0 != 0 and c2 = c3 = +0): the reference's
+//    (c0 + c1 t) + 0 p2 + 0 p3 equals c0 + c1 t including the sign of zero.
+__device__ __forceinline__ double approx_inv(const TableView& t, double u) {
+  const bool lower = u < 0.5;
+  const double up = lower ? 1.0 - u : u;  // fl(1-u) for the lower half (:47-49)
+  const double v = 1.0 - up;              // exact (Sterbenz)
+  double r;
+  if (t.dyadic) {
+    const uint64_t vb = static_cast<uint64_t>(__double_as_longlong(v));
+    const int e = static_cast<int>(vb >> 52) - 1023;
+    const int fl = (vb & 0xFFFFFFFFFFFFFull) == 0 ? -e : -e - 1;  // floor(-log2 v) >= 1
+    const int j = min(fl - 1, t.K - 1);
+    const double* b = t.base + j;
+    const double s = __dsub_rn(__dmul_rn(__dmul_rn(2.0, __dsub_rn(up, b[0])), b[32]), 1.0);
+    r = __dadd_rn(b[64], __dmul_rn(b[96], s));
+    if (t.degree == 3 || (!t.simple && r == 0.0)) {
+      const double p2 = 1.5 * s * s - 0.5;
+      const double p3 = s * (2.5 * s * s - 1.5);
+      r = r + b[128] * p2 + b[160] * p3;
+    }
+    r = fl >= t.K + 1 ? t.tail : r;  // w >= w_max: clamped tail
+  } else {
+    const int S = t.stride;
+    const double* thr = t.base + 6 * S;
+    int lo = 0, hi = t.K - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (v <= thr[mid]) lo = mid + 1; else hi = mid;
+    }
+    const int j = lo;
+    const double* b = t.base + j;
+    double s = (2.0 * (up - b[0])) / b[S];
+    s = s - 1.0;
+    s = s < -1.0 ? -1.0 : s;
+    s = s > 1.0 ? 1.0 : s;
+    r = b[2 * S] + b[3 * S] * s;
+    if (t.degree == 3 || (!t.simple && r == 0.0)) {
+      const double p2 = 1.5 * s * s - 0.5;
+      const double p3 = s * (2.5 * s * s - 1.5);
+      r = r + b[4 * S] * p2 + b[5 * S] * p3;
+    }
+    r = v <= thr[t.K - 1] ? t.tail : r;
+  }
+  r = lower ? -r : r;
+  return u == 0.5 ? 0.0 : r;
+}
+
+// ----------------------------------------------- rounding helpers ---------
+// RNE of a binary64 value to m+1 significant bits by integer arithmetic on
+// its pattern (== round_to_precision, softfloat.hpp:69-80, for normal
+// operands; binary64 subnormals are scaled the way frexp/ldexp handle them).
+__device__ __forceinline__ double rne64(double x, uint32_t d, uint64_t half_m1, uint64_t keep) {
+  uint64_t b = static_cast<uint64_t>(__double_as_longlong(x));
+  if (((b >> 52) & 0x7ff) == 0 && (b << 1) != 0) {
+    const double y = x * 0x1p64;
+    uint64_t c = static_cast<uint64_t>(__double_as_longlong(y));
+    c = (c + half_m1 + ((c >> d) & 1ull)) & keep;
+    return __longlong_as_double(static_cast<long long>(c)) * 0x1p-64;
+  }
+  b = (b + half_m1 + ((b >> d) & 1ull)) & keep;
+  return __longlong_as_double(static_cast<long long>(b));
+}
+
+__device__ __forceinline__ float rne32(float x, uint32_t d, uint32_t half_m1, uint32_t keep) {
+  uint32_t b = __float_as_uint(x);
+  b = (b + half_m1 + ((b >> d) & 1u)) & keep;
+  return __uint_as_float(b);
+}
+
+__device__ __forceinline__ bool nonfinite64(double x) {
+  return (__double2hiint(x) & 0x7ff00000) == 0x7ff00000;
+}
+__device__ __forceinline__ bool nonfinite32(float x) {
+  return (__float_as_uint(x) & 0x7f800000u) == 0x7f800000u;
+}
+
+// ------------------------------------------------------ bar arithmetic -----
+// Policies: T (state type), NP (paths per thread), mul/add/sub in the target
+// precision, lift(z[NP]) = R(z) packed, get(x, p) -> double, bad(x) ->
+// bitmask of non-finite lanes.  Native fp32 policies also track the state
+// exponent range: they are bit-exact with the unbounded-exponent reference
+// while states stay in [2^-32, 2^33) (no intermediate can then be subnormal
+// or overflow); otherwise the host re-runs
+// the level in the exact kF64Round emulation.
+struct RangeNone {
+  __device__ void track(double) {}
+  __device__ void track(float) {}
+  __device__ void track(__half2) {}
+  __device__ bool bad() const { return false; }
+};
+struct RangeF32 {
+  uint32_t lo = 0xffffffffu, hi = 0u;
+  __device__ void track(float x) {
+    const uint32_t b = __float_as_uint(x) & 0x7fffffffu;
+    lo = min(lo, b);
+    hi = max(hi, b);
+  }
+  __device__ bool bad() const { return hi >= 0x50000000u || lo < 0x2f800000u; }
+};
+
+struct ArithCarrier {  // m >= 52
+  using T = double;
+  using Range = RangeNone;
+  static constexpr int NP = 1;
+  static constexpr bool kIeee = false;
+  __device__ explicit ArithCarrier(const LevelArgs&) {}
+  __device__ T c(double d, uint16_t) const { return d; }
+  __device__ T zero() const { return 0.0; }
+  __device__ T mul(T a, T b) const { return __dmul_rn(a, b); }
+  __device__ T add(T a, T b) const { return __dadd_rn(a, b); }
+  __device__ T sub(T a, T b) const { return __dsub_rn(a, b); }
+  __device__ T lift(const double (&z)[1]) const { return z[0]; }
+  __device__ double get(T x, int) const { return x; }
+  __device__ uint32_t bad(T x) const { return nonfinite64(x) ? 1u : 0u; }
+};
+
+struct ArithF32 {  // m == 23, native
+  using T = float;
+  using Range = RangeF32;
+  static constexpr int NP = 1;
+  static constexpr bool kIeee = false;
+  __device__ explicit ArithF32(const LevelArgs&) {}
+  __device__ T c(double d, uint16_t) const { return static_cast<float>(d); }  // exact
+  __device__ T zero() const { return 0.0f; }
+  __device__ T mul(T a, T b) const { return __fmul_rn(a, b); }
+  __device__ T add(T a, T b) const { return __fadd_rn(a, b); }
+  __device__ T sub(T a, T b) const { return __fsub_rn(a, b); }
+  __device__ T lift(const double (&z)[1]) const { return __double2float_rn(z[0]); }
+  __device__ double get(T x, int) const { return static_cast<double>(x); }
+  __device__ uint32_t bad(T x) const { return nonfinite32(x) ? 1u : 0u; }
+};
+
+struct ArithF32Round {  // m <= 10: fp32 op (correctly rounded), then RNE to m+1 bits
+  using T = float;
+  using Range = RangeF32;
+  static constexpr int NP = 1;
+  static constexpr bool kIeee = false;
+  uint32_t d, half_m1, keep;
+  uint32_t d64;
+  uint64_t half_m1_64, keep64;
+  __device__ explicit ArithF32Round(const LevelArgs& A) {
+    d = 23u - static_cast<uint32_t>(A.mantissa_bits);
+    half_m1 = (1u << (d - 1)) - 1u;
+    keep = ~((1u << d) - 1u);
+    d64 = 52u - static_cast<uint32_t>(A.mantissa_bits);
+    half_m1_64 = (1ull << (d64 - 1)) - 1ull;
+    keep64 = ~((1ull << d64) - 1ull);
+  }
+  __device__ T c(double dd, uint16_t) const { return static_cast<float>(dd); }
+  __device__ T zero() const { return 0.0f; }
+  __device__ T mul(T a, T b) const { return rne32(__fmul_rn(a, b), d, half_m1, keep); }
+  __device__ T add(T a, T b) const { return rne32(__fadd_rn(a, b), d, half_m1, keep); }
+  __device__ T sub(T a, T b) const { return rne32(__fsub_rn(a, b), d, half_m1, keep); }
+  // R(z) from the full binary64 value: one rounding (softfloat.hpp:69)
+  __device__ T lift(const double (&z)[1]) const {
+    return __double2float_rn(rne64(z[0], d64, half_m1_64, keep64));
+  }
+  __device__ double get(T x, int) const { return static_cast<double>(x); }
+  __device__ uint32_t bad(T x) const { return nonfinite32(x) ? 1u : 0u; }
+};
+
+struct ArithF64Round {  // any m < 52: binary64 op, then integer RNE (exact emulation)
+  using T = double;
+  using Range = RangeNone;
+  static constexpr int NP = 1;
+  static constexpr bool kIeee = false;
+  uint32_t d;
+  uint64_t half_m1, keep;
+  __device__ explicit ArithF64Round(const LevelArgs& A) {
+    d = 52u - static_cast<uint32_t>(A.mantissa_bits);
+    half_m1 = (1ull << (d - 1)) - 1ull;
+    keep = ~((1ull << d) - 1ull);
+  }
+  __device__ T c(double dd, uint16_t) const { return dd; }
+  __device__ T zero() const { return 0.0; }
+  __device__ T mul(T a, T b) const { return rne64(__dmul_rn(a, b), d, half_m1, keep); }
+  __device__ T add(T a, T b) const { return rne64(__dadd_rn(a, b), d, half_m1, keep); }
+  __device__ T sub(T a, T b) const { return rne64(__dsub_rn(a, b), d, half_m1, keep); }
+  __device__ T lift(const double (&z)[1]) const { return rne64(z[0], d, half_m1, keep); }
+  __device__ double get(T x, int) const { return x; }
+  __device__ uint32_t bad(T x) const { return nonfinite64(x) ? 1u : 0u; }
+};
+
+struct ArithHalf2 {  // native IEEE binary16, two paths per thread
+  using T = __half2;
+  using Range = RangeNone;
+  static constexpr int NP = 2;
+  static constexpr bool kIeee = true;
+  __device__ explicit ArithHalf2(const LevelArgs&) {}
+  __device__ T c(double, uint16_t bits) const {
+    const __half h = __ushort_as_half(bits);
+    return __halves2half2(h, h);
+  }
+  __device__ T zero() const { return __float2half2_rn(0.0f); }
+  __device__ T mul(T a, T b) const { return __hmul2_rn(a, b); }
+  __device__ T add(T a, T b) const { return __hadd2_rn(a, b); }
+  __device__ T sub(T a, T b) const { return __hsub2_rn(a, b); }
+  __device__ T lift(const double (&z)[2]) const {
+    return __halves2half2(__double2half(z[0]), __double2half(z[1]));
+  }
+  __device__ double get(T x, int p) const {
+    return static_cast<double>(__half2float(p == 0 ? __low2half(x) : __high2half(x)));
+  }
+  __device__ uint32_t bad(T x) const {
+    const uint32_t b = *reinterpret_cast<const uint32_t*>(&x);
+    return (((b & 0x7c00u) == 0x7c00u) ? 1u : 0u) | (((b & 0x7c000000u) == 0x7c000000u) ? 2u : 0u);
+  }
+};
+
+// --------------------------------------------------------- block tree ------
+// Fixed reduction of a 256-path batch: slot s = threadIdx.x + p*blockDim.x;
+// per 32-slot group an xor butterfly, then an xor butterfly over the 8 group
+// sums.  Pass 1 gives the mean, pass 2 the central power sums.  Restated
+// bit for bit in oracle/lpmc_oracle.c (batch_acc).
+__device__ __forceinline__ double warp_sum(double x, int first) {
+  for (int k = first; k >= 1; k >>= 1) x = __dadd_rn(x, __shfl_xor_sync(0xffffffffu, x, k));
+  return x;
+}
+
+template <int NP>
+__device__ void batch_moments(const double (&vh)[NP], const double (&vb)[NP],
+                              const bool (&valid)[NP], int count, double* out15) {
+  __shared__ double s_grp[9][8];
+  __shared__ double s_mean[3];
+  constexpr int kWarps = kBatch / NP / 32;
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  double v[3][NP];
+#pragma unroll
+  for (int p = 0; p < NP; ++p) {
+    v[0][p] = valid[p] ? vh[p] : 0.0;
+    v[1][p] = valid[p] ? vb[p] : 0.0;
+    v[2][p] = valid[p] ? __dsub_rn(vh[p], vb[p]) : 0.0;
+  }
+#pragma unroll
+  for (int f = 0; f < 3; ++f)
+#pragma unroll
+    for (int p = 0; p < NP; ++p) {
+      const double s = warp_sum(v[f][p], 16);
+      if (lane == 0) s_grp[f][warp + p * kWarps] = s;
+    }
+  __syncthreads();
+  if (warp == 0) {
+#pragma unroll
+    for (int f = 0; f < 3; ++f) {
+      const double g = warp_sum(lane < 8 ? s_grp[f][lane] : 0.0, 4);
+      if (lane == 0) s_mean[f] = __ddiv_rn(g, static_cast<double>(count));
+    }
+  }
+  __syncthreads();
+  const double mean[3] = {s_mean[0], s_mean[1], s_mean[2]};
+#pragma unroll
+  for (int f = 0; f < 3; ++f)
+#pragma unroll
+    for (int p = 0; p < NP; ++p) {
+      const double dv = valid[p] ? __dsub_rn(v[f][p], mean[f]) : 0.0;
+      const double d2 = __dmul_rn(dv, dv);
+      const double d3 = __dmul_rn(d2, dv);
+      const double d4 = __dmul_rn(d2, d2);
+      const double s2 = warp_sum(d2, 16);
+      const double s3 = warp_sum(d3, 16);
+      const double s4 = warp_sum(d4, 16);
+      if (lane == 0) {
+        s_grp[3 * f + 0][warp + p * kWarps] = s2;
+        s_grp[3 * f + 1][warp + p * kWarps] = s3;
+        s_grp[3 * f + 2][warp + p * kWarps] = s4;
+      }
+    }
+  __syncthreads();
+  if (warp == 0) {
+#pragma unroll
+    for (int q = 0; q < 9; ++q) {
+      const double g = warp_sum(lane < 8 ? s_grp[q][lane] : 0.0, 4);
+      if (lane == 0) out15[5 * (q / 3) + 2 + (q % 3)] = g;
+    }
+    if (lane == 0) {
+#pragma unroll
+      for (int f = 0; f < 3; ++f) {
+        out15[5 * f + 0] = static_cast<double>(count);
+        out15[5 * f + 1] = mean[f];
+      }
+    }
+  }
+}
+
+// ----------------------------------------------------------- moments -------
+struct Acc {
+  double n, mean, m2, m3, m4;
+};
+
+// MomentAccumulator::merge (stats.hpp:29-54), same expression trees.
+__device__ __forceinline__ void acc_merge(Acc& a, const Acc& b) {
+  if (b.n == 0.0) return;
+  if (a.n == 0.0) {
+    a = b;
+    return;
+  }
+  const double na = a.n, nb = b.n;
+  const double n = na + nb;
+  const double d = b.mean - a.mean;
+  const double d2 = d * d;
+  const double m2 = a.m2 + b.m2 + d2 * na * nb / n;
+  const double m3 = a.m3 + b.m3 + d2 * d * na * nb * (na - nb) / (n * n) +
+                    3.0 * d * (na * b.m2 - nb * a.m2) / n;
+  const double m4 = a.m4 + b.m4 + d2 * d2 * na * nb * (na * na - na * nb + nb * nb) / (n * n * n) +
+                    6.0 * d2 * (na * na * b.m2 + nb * nb * a.m2) / (n * n) +
+                    4.0 * d * (na * b.m3 - nb * a.m3) / n;
+  a.mean = a.mean + d * nb / n;
+  a.m2 = m2;
+  a.m3 = m3;
+  a.m4 = m4;
+  a.n = n;
+}
+
+// MomentAccumulator::add (stats.hpp:15-27), same expression trees.
+__device__ __forceinline__ void acc_add(Acc& a, double x) {
+  const double before = a.n;
+  const double dn = a.n + 1.0;
+  a.n = dn;
+  const double delta = x - a.mean;
+  const double dl = delta / dn;
+  const double dl2 = dl * dl;
+  const double t1 = delta * dl * before;
+  a.mean = a.mean + dl;
+  a.m4 = a.m4 + (t1 * dl2 * (dn * dn - 3.0 * dn + 3.0) + 6.0 * dl2 * a.m2 - 4.0 * dl * a.m3);
+  a.m3 = a.m3 + (t1 * dl * (dn - 2.0) - 3.0 * dl * a.m2);
+  a.m2 = a.m2 + t1;
+}
+
+__device__ __forceinline__ Acc load_acc(const double* p) { return Acc{p[0], p[1], p[2], p[3], p[4]}; }
+__device__ __forceinline__ void store_acc(double* p, const Acc& a) {
+  p[0] = a.n;
+  p[1] = a.mean;
+  p[2] = a.m2;
+  p[3] = a.m3;
+  p[4] = a.m4;
+}
+
+}  // namespace dev
+}  // namespace lpmc_b200

@@ -209,9 +209,9 @@ std::vector<double> index_thresholds(int K, double w_max, double step_w) {
 }
 
 struct HostTable {
-  int K = 0, degree = 1, dyadic = 0;
+  int K = 0, degree = 1, dyadic = 0, stride = 0, simple = 0;
   double tail = 0.0;
-  std::vector<double> rows;  // kTableRows * K
+  std::vector<double> rows;  // kTableRows * stride
 };
 
 lpmc_status prepare_table(const lpmc_invcdf_table* t, HostTable* out, lpmc_error* err) {
@@ -230,17 +230,27 @@ lpmc_status prepare_table(const lpmc_invcdf_table* t, HostTable* out, lpmc_error
   bool dyadic = t->step_w == 1.0 && t->w_max == static_cast<double>(K + 1);
   for (int j = 0; dyadic && j < K; ++j) dyadic = t->breakpoints[j] == 1.0 - std::ldexp(1.0, -(j + 2));
   out->dyadic = dyadic ? 1 : 0;
-  out->rows.assign(static_cast<size_t>(kTableRows) * K, 0.0);
+  const int S = dyadic ? kDyadicStride : K;  // dyadic K <= 32: fixed stride, immediate offsets
+  out->stride = S;
+  // signed-zero fix-up provably unnecessary (see dev::approx_inv)
+  bool simple = t->kind != LPMC_APPROX_CUBIC;
+  for (int j = 0; simple && j < K; ++j) {
+    const double* c = t->coeff + 4 * j;
+    simple = c[0] != 0.0 && c[2] == 0.0 && !std::signbit(c[2]) && c[3] == 0.0 &&
+             !std::signbit(c[3]);
+  }
+  out->simple = simple ? 1 : 0;
+  out->rows.assign(static_cast<size_t>(kTableRows) * S, 0.0);
   double* a = out->rows.data();
-  double* w = a + K;
+  double* w = a + S;
   for (int j = 0; j < K; ++j) {
     a[j] = j == 0 ? 0.5 : t->breakpoints[j - 1];
     w[j] = dyadic ? std::ldexp(1.0, j + 2) : t->breakpoints[j] - a[j];
-    for (int c = 0; c < 4; ++c) out->rows[static_cast<size_t>(2 + c) * K + j] = t->coeff[4 * j + c];
+    for (int c = 0; c < 4; ++c) out->rows[static_cast<size_t>(2 + c) * S + j] = t->coeff[4 * j + c];
   }
   if (!dyadic) {
     const std::vector<double> thr = index_thresholds(K, t->w_max, t->step_w);
-    std::copy(thr.begin(), thr.end(), out->rows.begin() + 6 * K);
+    std::copy(thr.begin(), thr.end(), out->rows.begin() + 6 * S);
   }
   return LPMC_OK;
 }
@@ -406,6 +416,8 @@ lpmc_status build_spec(const lpmc_gbm* model, int32_t level, const lpmc_precisio
     A.K = s.table.K;
     A.degree = s.table.degree;
     A.dyadic = s.table.dyadic;
+    A.table_stride = s.table.stride;
+    A.table_simple = s.table.simple;
     A.tail = s.table.tail;
   }
   // bar arithmetic; native fp32 paths only inside the guarded range
@@ -586,7 +598,7 @@ cudaError_t enqueue_run(const RunSpec& s, Buffers& B, cudaStream_t st, Enqueued*
     S.path_diff = seq ? B.path_diff.ptr : nullptr;
     S.path_out = nullptr;
     S.z_out = nullptr;
-    LaunchResult r = launch_paths(S, s.arith, s.kahan, st);
+    LaunchResult r = launch_paths(S, s.arith, s.kahan, false, st);
     q->kernels += r.kernels;
     if (r.cuda_error != 0) return static_cast<cudaError_t>(r.cuda_error);
     if (seq) {
@@ -974,7 +986,7 @@ lpmc_status lpmc_simulate_paths(const lpmc_gbm* model, int32_t level, const lpmc
     A.path_diff = nullptr;
     A.path_out = d_out.ptr;
     A.z_out = zcount ? d_z.ptr : nullptr;
-    LaunchResult r = launch_paths(A, s.arith, s.kahan, stream);
+    LaunchResult r = launch_paths(A, s.arith, s.kahan, true, stream);
     t_launches += r.kernels;
     if (r.cuda_error != 0) {
       e = static_cast<cudaError_t>(r.cuda_error);
@@ -1029,7 +1041,7 @@ lpmc_status lpmc_device_math(int32_t op, const double* u, uint64_t n,
       cudaMemcpyAsync(dtab.ptr, ht.rows.data(), ht.rows.size() * sizeof(double),
                       cudaMemcpyHostToDevice, stream);
     LaunchResult r = launch_inv_cdf(du.ptr, n, table ? dtab.ptr : nullptr, ht.K, ht.degree,
-                                    ht.dyadic, ht.tail, op, dout.ptr, stream);
+                                    ht.dyadic, ht.stride, ht.simple, ht.tail, op, dout.ptr, stream);
     t_launches += r.kernels;
     e = static_cast<cudaError_t>(r.cuda_error);
     if (e == cudaSuccess)

@@ -1,8 +1,13 @@
 // Internal interface between the host library (lpmc_host.cpp, plain C++) and
-// the sm_100a kernels (lpmc_kernels.cu).  Not part of the public ABI.
+// the sm_100a kernels (lpmc_kernels.cu, lpmc_level_*.cu).  Not part of the
+// public ABI.
 #pragma once
 
 #include <cstdint>
+
+#ifdef __CUDACC__
+#include <cuda_runtime.h>
+#endif
 
 namespace lpmc_b200 {
 
@@ -15,10 +20,12 @@ enum class BarArith : int {
   kHalf2 = 4      // native IEEE binary16, two paths per thread (__h*2_rn)
 };
 
-// Device table layout (doubles, K = interval_count):
-//   [0K,1K) left endpoint a_j   [1K,2K) 2^(j+2) (dyadic) or b_j - a_j
-//   [2K..6K) c0, c1, c2, c3     [6K,7K) v-thresholds T_1..T_{K-1}, T_tail
+// Device table layout: kTableRows rows of `table_stride` doubles
+// (stride 32 for dyadic tables, K otherwise):
+//   row 0 left endpoint a_j      row 1 2^(j+2) (dyadic) or b_j - a_j
+//   rows 2..5 c0, c1, c2, c3     row 6 v-thresholds T_1..T_{K-1}, T_tail (general K)
 constexpr int kTableRows = 7;
+constexpr int kDyadicStride = 32;
 
 struct LevelArgs {
   uint64_t seed_key;   // mix64(seed + 0x9e37...) (uniform.hpp:23), hoisted per launch
@@ -38,6 +45,8 @@ struct LevelArgs {
   // approximation table (nullptr = exact inverse CDF for the bar legs)
   const double* table;
   int32_t K, degree, dyadic;
+  int32_t table_stride;  // 32 (dyadic) or K
+  int32_t table_simple;  // every c0 != 0 and c2 = c3 = +0: no signed-zero fix-up
   double tail;
   // payoff on terminal values (extension)
   int32_t payoff;
@@ -56,9 +65,10 @@ struct LaunchResult {
   int kernels;     // kernels enqueued
 };
 
-// Enqueue the path kernel for one launch slice.  arith/kahan/exact select the
-// template instance.  smem_table_bytes = 7*K*8 or 0.
-LaunchResult launch_paths(const LevelArgs& args, BarArith arith, bool kahan, void* stream);
+// Enqueue the path kernel for one launch slice; dump selects the instance
+// that writes path_out / z_out.
+LaunchResult launch_paths(const LevelArgs& args, BarArith arith, bool kahan, bool dump,
+                          void* stream);
 // Chunk tree over batch accumulators: chunks [0, n_chunks) of batches
 // [0, n_batches) in `batch_acc` -> chunk_acc (n_chunks x 3 x 5).
 LaunchResult launch_chunk_reduce(const double* batch_acc, uint64_t n_batches, uint64_t n_chunks,
@@ -69,11 +79,26 @@ LaunchResult launch_sequential_batches(const double* path_diff, uint64_t n_paths
 // Exact / approximate inverse CDF of host-given uniforms (parity hooks).
 // op 0 exact, 1 approximate (table), 2 libdevice reference formula, 3 erfc core.
 LaunchResult launch_inv_cdf(const double* u, uint64_t n, const double* table, int K, int degree,
-                            int dyadic, double tail, int op, double* out, void* stream);
-// Max dynamic shared memory the path kernels were configured for.
+                            int dyadic, int stride, int simple, double tail, int op, double* out,
+                            void* stream);
+// Upload constants and set kernel attributes on the current device.
 int configure_kernels();
 // Lane-op rates on the current device: fp64 FMA, fp32 FMA, half2 HFMA2
 // (per half lane), 64-bit integer multiply-add.  Returns cudaError_t.
 int measure_pipe_peaks(double* out4);
+
+#ifdef __CUDACC__
+// per-arithmetic translation units (lpmc_level_*.cu)
+cudaError_t launch_level_carrier(const LevelArgs& A, bool kahan, bool dump, void* stream);
+cudaError_t launch_level_f32(const LevelArgs& A, bool kahan, bool dump, void* stream);
+cudaError_t launch_level_f32r(const LevelArgs& A, bool kahan, bool dump, void* stream);
+cudaError_t launch_level_f64r(const LevelArgs& A, bool kahan, bool dump, void* stream);
+cudaError_t launch_level_half2(const LevelArgs& A, bool kahan, bool dump, void* stream);
+cudaError_t configure_level_carrier();
+cudaError_t configure_level_f32();
+cudaError_t configure_level_f32r();
+cudaError_t configure_level_f64r();
+cudaError_t configure_level_half2();
+#endif
 
 }  // namespace lpmc_b200

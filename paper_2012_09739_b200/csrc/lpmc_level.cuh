@@ -1,0 +1,389 @@
+// The coupled level sampler: simulate_coupled (sde.hpp:211-284) for 256
+// paths per CTA (one path per thread, two for the IEEE-half2 legs), reduced
+// to per-batch central moments in the same CTA.
+//
+// Hot loop per coarse step m (two fine draws):
+//   RNG for both draws -> exact Gaussians for both (phi_inv_multi: branch-free
+//   central Acklam, one warp-uniform tail pass, interleaved Newton) ->
+//   approximate Gaussians -> fine legs x2 -> coarse legs.
+// State stays in registers.  Failure bookkeeping in the hot loop is two
+// bits (a u == 1 draw; a native-range excursion); non-finite values are
+// absorbing, so a non-finite end state <=> a non-finite operation somewhere.
+// Only a path that may have failed is replayed (noinline, CHECKED) to find
+// its first failing step in the reference's serial order.
+#pragma once
+
+#include "lpmc_device.cuh"
+
+namespace lpmc_b200 {
+namespace dev {
+
+template <int NP>
+struct PathEnd {
+  double hf[NP], hc[NP], bf[NP], bc[NP];
+  uint64_t fk[NP];   // CHECKED: first failure (n << 3 | stage), kNoFail if none
+  bool suspect[NP];  // lean: the path may have failed
+  bool range_bad;    // native bar legs left the exact range
+};
+
+__device__ __forceinline__ void note_fail(uint64_t& fk, bool bad, uint64_t n, uint32_t stage) {
+  if (bad) {
+    const uint64_t ord = (n << 3) | stage;
+    fk = ord < fk ? ord : fk;
+  }
+}
+
+// H draws per path starting at fine index n0: uniforms, exact Gaussians (hat
+// legs, or bar legs without a table), R(approx) packed for the bar legs
+// (sde.hpp:256-258).
+template <class Arith, bool APPROX, bool NEED_EXACT, bool BAR, bool CHECKED, bool DUMP, int H>
+__device__ __forceinline__ void gen_draws(const LevelArgs& A, const TableView& tab,
+                                          const double* s_erfcx, const Arith& ar,
+                                          uint64_t (&kc)[Arith::NP], bool (&u1)[Arith::NP],
+                                          uint64_t (&fk)[Arith::NP],
+                                          const uint64_t (&local)[Arith::NP],
+                                          const bool (&valid)[Arith::NP], uint64_t n0,
+                                          double (&z)[2][Arith::NP],
+                                          typename Arith::T (&zb)[2]) {
+  constexpr int NP = Arith::NP;
+  constexpr int D = H * NP;
+  double u[D];
+#pragma unroll
+  for (int h = 0; h < H; ++h)
+#pragma unroll
+    for (int p = 0; p < NP; ++p) {
+      bool top;
+      u[h * NP + p] = next_uniform(kc[p], top);
+      if constexpr (CHECKED) {
+        note_fail(fk[p], top, n0 + h, kStageDraw);
+      } else {
+        u1[p] |= top;
+      }
+    }
+  double zz[D];
+  if constexpr (NEED_EXACT) {
+    math::phi_inv_multi<D>(u, zz, s_erfcx);
+  } else {
+#pragma unroll
+    for (int d = 0; d < D; ++d) zz[d] = 0.0;
+  }
+#pragma unroll
+  for (int h = 0; h < H; ++h) {
+    double zl[NP];
+#pragma unroll
+    for (int p = 0; p < NP; ++p) {
+      z[h][p] = zz[h * NP + p];
+      if constexpr (DUMP) {
+        if (A.z_out != nullptr && valid[p])
+          A.z_out[local[p] * (1ull << A.level) + n0 + h] = z[h][p];
+      }
+      if constexpr (APPROX) {
+        zl[p] = approx_inv(tab, u[h * NP + p]);
+      } else {
+        zl[p] = z[h][p];
+      }
+    }
+    if constexpr (BAR) zb[h] = ar.lift(zl);
+  }
+}
+
+template <class Arith, bool KAHAN, int LEGS, bool APPROX, bool CHECKED, bool DUMP>
+__device__ __forceinline__ void simulate(const LevelArgs& A, const TableView& tab,
+                                         const double* s_erfcx,
+                                         const uint64_t (&local)[Arith::NP],
+                                         const bool (&valid)[Arith::NP],
+                                         PathEnd<Arith::NP>& R) {
+  using T = typename Arith::T;
+  constexpr int NP = Arith::NP;
+  constexpr bool kHat = (LEGS & 1) != 0;
+  constexpr bool kBar = (LEGS & 2) != 0;
+  constexpr bool kNeedExact = kHat || !APPROX;
+
+  const Arith ar(A);
+  typename Arith::Range range;
+  uint64_t kc[NP];
+  bool u1[NP];
+  uint64_t fk[NP];
+  double xhf[NP], xhc[NP];
+#pragma unroll
+  for (int p = 0; p < NP; ++p) {
+    kc[p] = path_key(A.seed_key, A.path_base + local[p]);
+    u1[p] = false;
+    fk[p] = kNoFail;
+    xhf[p] = A.x0;
+    xhc[p] = A.x0;
+  }
+  const T mu_l = ar.c(A.mu_l, A.h_mu), sg_l = ar.c(A.sigma_l, A.h_sigma);
+  const T dtf_l = ar.c(A.dtf_l, A.h_dtf), sdtf_l = ar.c(A.sdtf_l, A.h_sdtf);
+  const T dtc_l = ar.c(A.dtc_l, A.h_dtc);
+  T xbf = ar.c(A.x0_l, A.h_x0);
+  T xbc = xbf;
+  T cmpf = ar.zero(), cmpc = ar.zero();
+
+  // em_step (sde.hpp:60-68), carrier legs
+  auto hat_fine = [&](const double (&z)[NP], uint64_t n) {
+#pragma unroll
+    for (int p = 0; p < NP; ++p) {
+      const double x = xhf[p];
+      const double drift = __dmul_rn(__dmul_rn(A.mu, x), A.dtf);
+      const double diff = __dmul_rn(__dmul_rn(__dmul_rn(A.sigma, x), A.sdtf), z[p]);
+      xhf[p] = __dadd_rn(x, __dadd_rn(drift, diff));
+      if constexpr (CHECKED) note_fail(fk[p], nonfinite64(xhf[p]), n, kStageHatFine);
+    }
+  };
+  // em_step / em_step_kahan (sde.hpp:60-68, 96-105), bar precision
+  auto bar_fine = [&](T zb, uint64_t n) {
+    const T x = xbf;
+    const T drift = ar.mul(ar.mul(mu_l, x), dtf_l);
+    const T diff = ar.mul(ar.mul(ar.mul(sg_l, x), sdtf_l), zb);
+    const T inc = ar.add(drift, diff);
+    if constexpr (KAHAN) {  // kahan_accumulate (sde.hpp:85-92)
+      const T y = ar.sub(inc, cmpf);
+      const T s = ar.add(x, y);
+      cmpf = ar.sub(ar.sub(s, x), y);
+      xbf = s;
+    } else {
+      xbf = ar.add(x, inc);
+    }
+    range.track(xbf);
+    if constexpr (CHECKED) {
+      const uint32_t m = ar.bad(xbf);
+#pragma unroll
+      for (int p = 0; p < NP; ++p) note_fail(fk[p], (m >> p) & 1u, n, kStageBarFine);
+    }
+  };
+  // em_step_dw / em_step_kahan_dw (sde.hpp:72-80, 107-116)
+  auto coarse = [&](const double (&z0)[NP], const double (&z1)[NP], T zb0, T zb1, uint64_t n) {
+    if constexpr (kHat) {
+#pragma unroll
+      for (int p = 0; p < NP; ++p) {
+        const double dw = __dadd_rn(__dmul_rn(A.sdtf, z0[p]), __dmul_rn(A.sdtf, z1[p]));
+        const double x = xhc[p];
+        const double drift = __dmul_rn(__dmul_rn(A.mu, x), A.dtc);
+        const double diff = __dmul_rn(__dmul_rn(A.sigma, x), dw);
+        xhc[p] = __dadd_rn(x, __dadd_rn(drift, diff));
+        if constexpr (CHECKED) note_fail(fk[p], nonfinite64(xhc[p]), n, kStageHatCoarse);
+      }
+    }
+    if constexpr (kBar) {
+      const T dw = ar.add(ar.mul(sdtf_l, zb0), ar.mul(sdtf_l, zb1));
+      const T x = xbc;
+      const T drift = ar.mul(ar.mul(mu_l, x), dtc_l);
+      const T diff = ar.mul(ar.mul(sg_l, x), dw);
+      const T inc = ar.add(drift, diff);
+      if constexpr (KAHAN) {
+        const T y = ar.sub(inc, cmpc);
+        const T s = ar.add(x, y);
+        cmpc = ar.sub(ar.sub(s, x), y);
+        xbc = s;
+      } else {
+        xbc = ar.add(x, inc);
+      }
+      range.track(xbc);
+      if constexpr (CHECKED) {
+        const uint32_t m = ar.bad(xbc);
+#pragma unroll
+        for (int p = 0; p < NP; ++p) note_fail(fk[p], (m >> p) & 1u, n, kStageBarCoarse);
+      }
+    }
+  };
+
+  if (A.level == 0) {  // sde.hpp:237-249: one draw, fine legs only, coarse := 0
+    double z[2][NP];
+    T zb[2] = {ar.zero(), ar.zero()};
+    gen_draws<Arith, APPROX, kNeedExact, kBar, CHECKED, DUMP, 1>(A, tab, s_erfcx, ar, kc, u1, fk,
+                                                                 local, valid, 0, z, zb);
+    if constexpr (kHat) hat_fine(z[0], 0);
+    if constexpr (kBar) bar_fine(zb[0], 0);
+  } else {
+    const uint64_t halves = 1ull << (A.level - 1);
+    for (uint64_t m = 0; m < halves; ++m) {  // sde.hpp:251-277
+      double z[2][NP];
+      T zb[2] = {ar.zero(), ar.zero()};
+      gen_draws<Arith, APPROX, kNeedExact, kBar, CHECKED, DUMP, 2>(A, tab, s_erfcx, ar, kc, u1,
+                                                                   fk, local, valid, 2 * m, z, zb);
+      if constexpr (kHat) hat_fine(z[0], 2 * m);
+      if constexpr (kBar) bar_fine(zb[0], 2 * m);
+      if constexpr (kHat) hat_fine(z[1], 2 * m + 1);
+      if constexpr (kBar) bar_fine(zb[1], 2 * m + 1);
+      coarse(z[0], z[1], zb[0], zb[1], 2 * m + 1);
+    }
+  }
+
+  const uint32_t bad_f = kBar ? ar.bad(xbf) : 0u;
+  const uint32_t bad_c = (kBar && A.level > 0) ? ar.bad(xbc) : 0u;
+#pragma unroll
+  for (int p = 0; p < NP; ++p) {
+    R.hf[p] = kHat ? xhf[p] : 0.0;
+    R.hc[p] = (kHat && A.level > 0) ? xhc[p] : 0.0;
+    R.bf[p] = kBar ? ar.get(xbf, p) : 0.0;
+    R.bc[p] = (kBar && A.level > 0) ? ar.get(xbc, p) : 0.0;
+    R.fk[p] = fk[p];
+    const bool hat_bad = kHat && (nonfinite64(R.hf[p]) || nonfinite64(R.hc[p]));
+    R.suspect[p] = u1[p] || hat_bad || ((bad_f >> p) & 1u) || ((bad_c >> p) & 1u);
+  }
+  R.range_bad = range.bad();
+}
+
+// Exact first failure of this thread's paths (only called for suspects).
+template <class Arith, bool KAHAN, int LEGS, bool APPROX>
+__device__ __noinline__ void replay_checked(const LevelArgs& A, TableView tab,
+                                            const double* s_erfcx,
+                                            const uint64_t (&local)[Arith::NP],
+                                            const bool (&valid)[Arith::NP],
+                                            uint64_t (&fk)[Arith::NP]) {
+  PathEnd<Arith::NP> R;
+  simulate<Arith, KAHAN, LEGS, APPROX, true, false>(A, tab, s_erfcx, local, valid, R);
+#pragma unroll
+  for (int p = 0; p < Arith::NP; ++p) fk[p] = R.fk[p];
+}
+
+// 256 threads x 4 CTAs per SM (64 registers) for one path per thread; the
+// half2 instances (two paths, four draws per coarse step) get 128 threads x
+// 4 CTAs (128 registers) so they do not spill.
+template <class Arith, bool KAHAN, int LEGS, bool APPROX, bool DUMP>
+__global__ void __launch_bounds__(kBatch / Arith::NP, 4)
+    level_kernel(const __grid_constant__ LevelArgs A) {
+  constexpr int NP = Arith::NP;
+  constexpr bool kHat = (LEGS & 1) != 0;
+  constexpr bool kBar = (LEGS & 2) != 0;
+  constexpr bool kNeedExact = kHat || !APPROX;
+
+  extern __shared__ double s_table[];
+  __shared__ double s_erfcx[kNeedExact ? kErfcxWords : 1];
+  if constexpr (kNeedExact) stage_erfcx(s_erfcx);
+  TableView tab{};
+  if constexpr (APPROX) {
+    for (int i = threadIdx.x; i < kTableRows * A.table_stride; i += blockDim.x)
+      s_table[i] = A.table[i];
+    tab = TableView{s_table, A.table_stride, A.K, A.degree, A.dyadic, A.table_simple, A.tail};
+  }
+  __syncthreads();
+
+  const uint64_t batch = A.batch0 + blockIdx.x;
+  const uint64_t first = batch * kBatch;
+  const uint64_t left = A.n_paths - first;
+  const int count = left < kBatch ? static_cast<int>(left) : kBatch;
+  uint64_t local[NP];
+  bool valid[NP];
+#pragma unroll
+  for (int p = 0; p < NP; ++p) {
+    const int slot = threadIdx.x + p * blockDim.x;
+    local[p] = first + slot;
+    valid[p] = slot < count;
+  }
+
+  PathEnd<NP> R;
+  simulate<Arith, KAHAN, LEGS, APPROX, false, DUMP>(A, tab, s_erfcx, local, valid, R);
+
+  bool any_suspect = false;
+#pragma unroll
+  for (int p = 0; p < NP; ++p) any_suspect |= valid[p] && R.suspect[p];
+  if (any_suspect) {  // rare: exact first failure in the reference's serial order
+    uint64_t fk[NP];
+    replay_checked<Arith, KAHAN, LEGS, APPROX>(A, tab, s_erfcx, local, valid, fk);
+#pragma unroll
+    for (int p = 0; p < NP; ++p) {
+      if (!valid[p] || fk[p] == kNoFail) continue;
+      const uint64_t n = fk[p] >> 3;
+      const uint32_t stage = static_cast<uint32_t>(fk[p] & 7u);
+      uint32_t kind = stage == kStageDraw ? kKindU1 : kKindNonFinite;
+      if (Arith::kIeee && (stage == kStageBarFine || stage == kStageBarCoarse)) kind = kKindState;
+      const uint64_t step = n < (1ull << 22) ? n : (1ull << 22) - 1;
+      atomicMin(A.err_key, static_cast<unsigned long long>(
+                               (local[p] << 24) | (static_cast<uint64_t>(kind) << 22) | step));
+    }
+  }
+  if (R.range_bad) atomicOr(A.range_flag, 1u);
+
+  // terminal values -> payoff -> per-path differences (mlmc.hpp:86-90)
+  double dh[NP], db[NP];
+#pragma unroll
+  for (int p = 0; p < NP; ++p) {
+    if constexpr (DUMP) {
+      if (A.path_out != nullptr && valid[p]) {
+        double* o = A.path_out + 4 * local[p];
+        o[0] = R.hf[p];
+        o[1] = R.hc[p];
+        o[2] = R.bf[p];
+        o[3] = R.bc[p];
+      }
+    }
+    double pf_h = R.hf[p], pc_h = R.hc[p], pf_b = R.bf[p], pc_b = R.bc[p];
+    if (A.payoff == 1) {
+      pf_h = fmax(__dsub_rn(R.hf[p], A.strike), 0.0);
+      pf_b = fmax(__dsub_rn(R.bf[p], A.strike), 0.0);
+      pc_h = A.level > 0 ? fmax(__dsub_rn(R.hc[p], A.strike), 0.0) : 0.0;
+      pc_b = A.level > 0 ? fmax(__dsub_rn(R.bc[p], A.strike), 0.0) : 0.0;
+    }
+    dh[p] = kHat ? __dsub_rn(pf_h, pc_h) : 0.0;
+    db[p] = kBar ? __dsub_rn(pf_b, pc_b) : 0.0;
+  }
+  if (A.path_diff != nullptr) {
+#pragma unroll
+    for (int p = 0; p < NP; ++p)
+      if (valid[p]) {
+        const uint64_t r = local[p] - A.batch0 * kBatch;  // slice-relative
+        A.path_diff[2 * r + 0] = dh[p];
+        A.path_diff[2 * r + 1] = db[p];
+      }
+  }
+  if (A.batch_acc != nullptr) batch_moments<NP>(dh, db, valid, count, A.batch_acc + 15 * blockIdx.x);
+}
+
+// ------------------------------------------------------- per-arith glue ----
+constexpr int kMaxTableK = 1024;
+constexpr int kMaxDynSmem = kTableRows * kMaxTableK * 8;
+
+template <class Arith, bool KAHAN, int LEGS, bool APPROX, bool DUMP>
+cudaError_t launch_one(const LevelArgs& A, cudaStream_t s) {
+  const size_t smem = APPROX ? static_cast<size_t>(kTableRows) * A.table_stride * sizeof(double) : 0;
+  level_kernel<Arith, KAHAN, LEGS, APPROX, DUMP>
+      <<<static_cast<unsigned>(A.n_batches), kBatch / Arith::NP, smem, s>>>(A);
+  return cudaGetLastError();
+}
+
+template <class Arith, bool KAHAN, int LEGS, bool DUMP>
+cudaError_t pick_approx(const LevelArgs& A, cudaStream_t s) {
+  return A.table != nullptr ? launch_one<Arith, KAHAN, LEGS, true, DUMP>(A, s)
+                            : launch_one<Arith, KAHAN, LEGS, false, DUMP>(A, s);
+}
+
+template <class Arith, bool KAHAN, bool DUMP>
+cudaError_t pick_legs(const LevelArgs& A, cudaStream_t s) {
+  if (A.legs == 2) return pick_approx<Arith, KAHAN, 2, DUMP>(A, s);
+  return pick_approx<Arith, KAHAN, 3, DUMP>(A, s);
+}
+
+// Launch the path kernel of one bar arithmetic (legs 2 / 3).
+template <class Arith>
+cudaError_t launch_level(const LevelArgs& A, bool kahan, bool dump, cudaStream_t s) {
+  if (dump) return kahan ? pick_legs<Arith, true, true>(A, s) : pick_legs<Arith, false, true>(A, s);
+  return kahan ? pick_legs<Arith, true, false>(A, s) : pick_legs<Arith, false, false>(A, s);
+}
+
+template <class Arith, bool KAHAN, int LEGS, bool DUMP>
+cudaError_t configure_one() {
+  return cudaFuncSetAttribute(level_kernel<Arith, KAHAN, LEGS, true, DUMP>,
+                              cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem);
+}
+
+template <class Arith>
+cudaError_t configure_level() {
+  cudaError_t e = cudaSuccess;
+  auto acc = [&](cudaError_t x) {
+    if (e == cudaSuccess) e = x;
+  };
+  acc(configure_one<Arith, false, 2, false>());
+  acc(configure_one<Arith, true, 2, false>());
+  acc(configure_one<Arith, false, 3, false>());
+  acc(configure_one<Arith, true, 3, false>());
+  acc(configure_one<Arith, false, 2, true>());
+  acc(configure_one<Arith, true, 2, true>());
+  acc(configure_one<Arith, false, 3, true>());
+  acc(configure_one<Arith, true, 3, true>());
+  return e;
+}
+
+}  // namespace dev
+}  // namespace lpmc_b200

@@ -1,0 +1,22 @@
+// Level-kernel instances for the ArithCarrier bar arithmetic (see lpmc_level.cuh).
+// One translation unit per arithmetic so the build compiles them in parallel.
+#include "lpmc_level.cuh"
+
+namespace lpmc_b200 {
+
+cudaError_t launch_level_carrier(const LevelArgs& A, bool kahan, bool dump, void* stream) {
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (A.legs == 1) {  // carrier legs only: precision, Kahan and table do not apply
+    return dump ? dev::launch_one<dev::ArithCarrier, false, 1, false, true>(A, s)
+                : dev::launch_one<dev::ArithCarrier, false, 1, false, false>(A, s);
+  }
+  return dev::launch_level<dev::ArithCarrier>(A, kahan, dump, s);
+}
+
+cudaError_t configure_level_carrier() {
+  cudaError_t e = math::upload_math_constants();
+  if (e == cudaSuccess) e = dev::configure_level<dev::ArithCarrier>();
+  return e;
+}
+
+}  // namespace lpmc_b200

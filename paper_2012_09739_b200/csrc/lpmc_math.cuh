@@ -146,8 +146,15 @@ static const double kMathHost[kMathCount] = {
 static const double kErfcxTableHost[(LPMC_ERFCX_DEG + 2) * LPMC_ERFCX_INTERVALS] = LPMC_ERFCX_COEF;
 
 #ifdef __CUDACC__
-__constant__ double kMath[kMathCount];
-__device__ const double kErfcxTable[(LPMC_ERFCX_DEG + 2) * LPMC_ERFCX_INTERVALS] = LPMC_ERFCX_COEF;
+// TU-local (static): every kernel translation unit has its own copy and
+// uploads it in its configure function (upload_math_constants).
+static __constant__ double kMath[kMathCount];
+static __device__ const double kErfcxTable[(LPMC_ERFCX_DEG + 2) * LPMC_ERFCX_INTERVALS] =
+    LPMC_ERFCX_COEF;
+
+static inline cudaError_t upload_math_constants() {
+  return cudaMemcpyToSymbol(kMath, kMathHost, sizeof(kMathHost));
+}
 #endif
 
 #ifdef __CUDA_ARCH__
@@ -255,21 +262,11 @@ __device__ __forceinline__ double log_coarse(double u) {
   return fmad(static_cast<double>(e), LPMC_K(kLn2), s * p);
 }
 
-// Acklam's initial approximation for u in (0, 1/2] (gaussian.hpp:26-51),
-// to ~1e-12 relative of the reference's x0.
-__device__ __forceinline__ double acklam_lower(double u) {
-  if (u < LPMC_K(kTailU)) {
-    const double q = sqrt_coarse(-2.0 * log_coarse(u));
-    double num = LPMC_K(kOffAckC);
-#pragma unroll
-    for (int i = 1; i < 6; ++i) num = fmad(num, q, LPMC_K(kOffAckC + i));
-    double den = LPMC_K(kOffAckD);
-#pragma unroll
-    for (int i = 1; i < 4; ++i) den = fmad(den, q, LPMC_K(kOffAckD + i));
-    den = fmad(den, q, 1.0);
-    return num * rcp_refined(den);
-  }
-  const double q = u - 0.5;
+// Acklam's initial approximation (gaussian.hpp:26-51) for v in (0, 1/2], to
+// ~1e-12 relative of the reference's x0 (Newton squares that away).
+// Central branch, v >= 0.02425: evaluated branch-free for every draw.
+__device__ __forceinline__ double acklam_central(double v) {
+  const double q = v - 0.5;
   const double r = q * q;
   double num = LPMC_K(kOffAckA);
 #pragma unroll
@@ -281,30 +278,77 @@ __device__ __forceinline__ double acklam_lower(double u) {
   return (num * q) * rcp_refined(den);
 }
 
-// exact_inv_cdf lower half (gaussian.hpp:26-55) for u in (0, 1/2]:
-// Acklam x0, then x0 - (Phi(x0) - u) / pdf(x0) with Phi(x0) = erfc(t)/2,
-// t = (-x0) * (1/sqrt 2) rounded exactly as the reference rounds it.
-__device__ __forceinline__ double phi_inv_lower_fast(double u, const double* erfcx_tab) {
-  const double x0 = acklam_lower(u);
-  const double t = -x0 * LPMC_K(kInvSqrt2);
-  if (!(t < kFastTMax)) return phi_inv_lower_libdevice(u);
+// Tail branch, v < 0.02425 (4.85% of draws).
+__device__ __forceinline__ double acklam_tail(double v) {
+  const double q = sqrt_coarse(-2.0 * log_coarse(v));
+  double num = LPMC_K(kOffAckC);
+#pragma unroll
+  for (int i = 1; i < 6; ++i) num = fmad(num, q, LPMC_K(kOffAckC + i));
+  double den = LPMC_K(kOffAckD);
+#pragma unroll
+  for (int i = 1; i < 4; ++i) den = fmad(den, q, LPMC_K(kOffAckD + i));
+  den = fmad(den, q, 1.0);
+  return num * rcp_refined(den);
+}
+
+// The Newton step of gaussian.hpp:52-53, x0 - (Phi(x0) - v) / pdf(x0), with
+// Phi(x0) = erfc(t)/2 and t = (-x0) * (1/sqrt 2) rounded as the reference
+// rounds it.  *slow is set when t >= 6.5 (v < ~1e-20: outside the sampler's
+// range); the caller then redoes that draw on libdevice.
+__device__ __forceinline__ double newton_fast(double x0, double v, const double* erfcx_tab,
+                                              bool* slow) {
+  const double t0 = -x0 * LPMC_K(kInvSqrt2);
+  *slow = !(t0 < kFastTMax);
+  const double t = *slow ? 0.0 : t0;
   const double th = t * t;
   const double tl = fmad(t, t, -th);
   const ExpSplit e = exp_neg(th, tl);
   const double pg = e.p * erfcx_piecewise(t, erfcx_tab);
   const double cdf = scale(pg, e.k - 1);  // 0.5 erfc(t)
-  const double resid = cdf - u;
+  const double resid = cdf - v;
   // 1/pdf(x0) = sqrt(2 pi) exp(t^2) = sqrt(2 pi) 2^-k / p
   const double inv_pdf = scale(LPMC_K(kSqrt2Pi) * rcp_coarse(e.p), -e.k);
   return x0 - resid * inv_pdf;
 }
 
-// Reflection about 1/2 exactly as gaussian.hpp:62-64 (1-u is exact there).
-__device__ __forceinline__ double phi_inv(double u, const double* erfcx_tab) {
-  const bool upper = u > 0.5;
-  const double r = phi_inv_lower_fast(upper ? 1.0 - u : u, erfcx_tab);
-  const double z = upper ? -r : r;
-  return u == 0.5 ? 0.0 : z;
+// exact_inv_cdf (gaussian.hpp:59-65) for D independent draws of one thread.
+// The central rational runs for all draws; the tail rational (log, sqrt)
+// runs in warp-uniform passes, one pending tail draw per lane per pass, so a
+// warp pays for it about once per coarse step instead of once per draw with
+// one lane active.  Must be called by every active lane of the warp.
+template <int D>
+__device__ __forceinline__ void phi_inv_multi(const double (&u)[D], double (&z)[D],
+                                              const double* erfcx_tab) {
+  double v[D], x0[D];
+  uint32_t pend = 0;
+#pragma unroll
+  for (int d = 0; d < D; ++d) {
+    v[d] = u[d] > 0.5 ? 1.0 - u[d] : u[d];  // exact (gaussian.hpp:63)
+    x0[d] = acklam_central(v[d]);
+    if (v[d] < LPMC_K(kTailU)) pend |= 1u << d;
+  }
+  const unsigned mask = __activemask();
+  while (__any_sync(mask, pend != 0)) {
+    double vs = 0.01;  // lanes with nothing pending evaluate a harmless value
+#pragma unroll
+    for (int d = D - 1; d >= 0; --d)
+      if (pend & (1u << d)) vs = v[d];
+    const double xt = acklam_tail(vs);
+    const uint32_t low = pend & (0u - pend);
+#pragma unroll
+    for (int d = 0; d < D; ++d)
+      if (low == (1u << d)) x0[d] = xt;
+    pend &= pend - 1u;
+  }
+  bool slow[D];
+#pragma unroll
+  for (int d = 0; d < D; ++d) z[d] = newton_fast(x0[d], v[d], erfcx_tab, &slow[d]);
+#pragma unroll
+  for (int d = 0; d < D; ++d) {
+    if (slow[d]) z[d] = phi_inv_lower_libdevice(v[d]);
+    const double r = u[d] > 0.5 ? -z[d] : z[d];
+    z[d] = u[d] == 0.5 ? 0.0 : r;
+  }
 }
 
 // The same with the reference's formula on libdevice (diagnostics only).
