@@ -43,8 +43,8 @@ __device__ __forceinline__ void gen_draws(const LevelArgs& A, const TableView& t
                                           uint64_t (&fk)[Arith::NP],
                                           const uint64_t (&local)[Arith::NP],
                                           const bool (&valid)[Arith::NP], uint64_t n0,
-                                          double (&z)[2][Arith::NP],
-                                          typename Arith::T (&zb)[2]) {
+                                          double (&z)[4][Arith::NP],
+                                          typename Arith::T (&zb)[4]) {
   constexpr int NP = Arith::NP;
   constexpr int D = H * NP;
   double u[D];
@@ -188,25 +188,49 @@ __device__ __forceinline__ void simulate(const LevelArgs& A, const TableView& ta
     }
   };
 
+  // The draws of G coarse steps are generated together (more independent
+  // chains to hide FP64 latency, one Acklam tail pass per batch); the legs
+  // then consume them in the reference's order (sde.hpp:251-277).
+#ifndef LPMC_COARSE_PER_BATCH
+#define LPMC_COARSE_PER_BATCH 2
+#endif
+  constexpr int G = NP == 1 ? LPMC_COARSE_PER_BATCH : 1;  // coarse steps per batch
   if (A.level == 0) {  // sde.hpp:237-249: one draw, fine legs only, coarse := 0
-    double z[2][NP];
-    T zb[2] = {ar.zero(), ar.zero()};
+    double z[4][NP];
+    T zb[4];
     gen_draws<Arith, APPROX, kNeedExact, kBar, CHECKED, DUMP, 1>(A, tab, s_erfcx, ar, kc, u1, fk,
                                                                  local, valid, 0, z, zb);
     if constexpr (kHat) hat_fine(z[0], 0);
     if constexpr (kBar) bar_fine(zb[0], 0);
   } else {
     const uint64_t halves = 1ull << (A.level - 1);
-    for (uint64_t m = 0; m < halves; ++m) {  // sde.hpp:251-277
-      double z[2][NP];
-      T zb[2] = {ar.zero(), ar.zero()};
+    uint64_t m = 0;
+    if (halves >= G) {
+      for (; m < halves; m += G) {
+        double z[4][NP];
+        T zb[4];
+        gen_draws<Arith, APPROX, kNeedExact, kBar, CHECKED, DUMP, 2 * G>(
+            A, tab, s_erfcx, ar, kc, u1, fk, local, valid, 2 * m, z, zb);
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+          const uint64_t n = 2 * (m + g);
+          if constexpr (kHat) hat_fine(z[2 * g], n);
+          if constexpr (kBar) bar_fine(zb[2 * g], n);
+          if constexpr (kHat) hat_fine(z[2 * g + 1], n + 1);
+          if constexpr (kBar) bar_fine(zb[2 * g + 1], n + 1);
+          coarse(z[2 * g], z[2 * g + 1], zb[2 * g], zb[2 * g + 1], n + 1);
+        }
+      }
+    } else {  // level 1 with G = 2: a single coarse step
+      double z[4][NP];
+      T zb[4];
       gen_draws<Arith, APPROX, kNeedExact, kBar, CHECKED, DUMP, 2>(A, tab, s_erfcx, ar, kc, u1,
-                                                                   fk, local, valid, 2 * m, z, zb);
-      if constexpr (kHat) hat_fine(z[0], 2 * m);
-      if constexpr (kBar) bar_fine(zb[0], 2 * m);
-      if constexpr (kHat) hat_fine(z[1], 2 * m + 1);
-      if constexpr (kBar) bar_fine(zb[1], 2 * m + 1);
-      coarse(z[0], z[1], zb[0], zb[1], 2 * m + 1);
+                                                                   fk, local, valid, 0, z, zb);
+      if constexpr (kHat) hat_fine(z[0], 0);
+      if constexpr (kBar) bar_fine(zb[0], 0);
+      if constexpr (kHat) hat_fine(z[1], 1);
+      if constexpr (kBar) bar_fine(zb[1], 1);
+      coarse(z[0], z[1], zb[0], zb[1], 1);
     }
   }
 
@@ -241,8 +265,11 @@ __device__ __noinline__ void replay_checked(const LevelArgs& A, TableView tab,
 // 256 threads x 4 CTAs per SM (64 registers) for one path per thread; the
 // half2 instances (two paths, four draws per coarse step) get 128 threads x
 // 4 CTAs (128 registers) so they do not spill.
+#ifndef LPMC_LEVEL_MIN_CTAS
+#define LPMC_LEVEL_MIN_CTAS 3
+#endif
 template <class Arith, bool KAHAN, int LEGS, bool APPROX, bool DUMP>
-__global__ void __launch_bounds__(kBatch / Arith::NP, 4)
+__global__ void __launch_bounds__(kBatch / Arith::NP, LPMC_LEVEL_MIN_CTAS)
     level_kernel(const __grid_constant__ LevelArgs A) {
   constexpr int NP = Arith::NP;
   constexpr bool kHat = (LEGS & 1) != 0;
