@@ -33,27 +33,52 @@ __device__ __forceinline__ void note_fail(uint64_t& fk, bool bad, uint64_t n, ui
   }
 }
 
-// H draws per path starting at fine index n0: uniforms, exact Gaussians (hat
-// legs, or bar legs without a table), R(approx) packed for the bar legs
-// (sde.hpp:256-258).
-template <class Arith, bool APPROX, bool NEED_EXACT, bool BAR, bool CHECKED, bool DUMP, int H>
+// Uniforms of H draws x NP paths (draw-major), with their u == 1 bits.
+template <int D>
+struct Uniforms {
+  double u[D];
+  uint32_t top;
+};
+
+template <int NP, int H>
+__device__ __forceinline__ void draw_uniforms(uint64_t (&kc)[NP], Uniforms<H * NP>& U) {
+  U.top = 0u;
+#pragma unroll
+  for (int h = 0; h < H; ++h)
+#pragma unroll
+    for (int p = 0; p < NP; ++p) {
+      bool top;
+      U.u[h * NP + p] = next_uniform(kc[p], top);
+      U.top |= (top ? 1u : 0u) << (h * NP + p);
+    }
+}
+
+// H draws per path starting at fine index n0 from pre-drawn uniforms `cur`:
+// exact Gaussians (hat legs, or bar legs without a table) and R(approx)
+// packed for the bar legs (sde.hpp:256-258).  With PREFETCH the uniforms of
+// the next batch are drawn between the Acklam stage and the Newton stage, so
+// the integer RNG interleaves with FP64 work instead of forming its own
+// phase (software pipelining across batches).
+template <class Arith, bool APPROX, bool NEED_EXACT, bool BAR, bool CHECKED, bool DUMP, int H,
+          bool PREFETCH>
 __device__ __forceinline__ void gen_draws(const LevelArgs& A, const TableView& tab,
                                           const double* s_erfcx, const Arith& ar,
                                           uint64_t (&kc)[Arith::NP], bool (&u1)[Arith::NP],
                                           uint64_t (&fk)[Arith::NP],
                                           const uint64_t (&local)[Arith::NP],
                                           const bool (&valid)[Arith::NP], uint64_t n0,
+                                          const Uniforms<H * Arith::NP>& cur,
+                                          Uniforms<H * Arith::NP>& next,
                                           double (&z)[4][Arith::NP],
                                           typename Arith::T (&zb)[4]) {
   constexpr int NP = Arith::NP;
   constexpr int D = H * NP;
-  double u[D];
+  const double(&u)[D] = cur.u;
 #pragma unroll
   for (int h = 0; h < H; ++h)
 #pragma unroll
     for (int p = 0; p < NP; ++p) {
-      bool top;
-      u[h * NP + p] = next_uniform(kc[p], top);
+      const bool top = (cur.top >> (h * NP + p)) & 1u;
       if constexpr (CHECKED) {
         note_fail(fk[p], top, n0 + h, kStageDraw);
       } else {
@@ -62,8 +87,12 @@ __device__ __forceinline__ void gen_draws(const LevelArgs& A, const TableView& t
     }
   double zz[D];
   if constexpr (NEED_EXACT) {
-    math::phi_inv_multi<D>(u, zz, s_erfcx);
+    double v[D], x0[D];
+    math::phi_inv_stage1<D>(u, v, x0);
+    if constexpr (PREFETCH) draw_uniforms<NP, H>(kc, next);
+    math::phi_inv_stage2<D>(u, v, x0, zz, s_erfcx);
   } else {
+    if constexpr (PREFETCH) draw_uniforms<NP, H>(kc, next);
 #pragma unroll
     for (int d = 0; d < D; ++d) zz[d] = 0.0;
   }
@@ -198,19 +227,26 @@ __device__ __forceinline__ void simulate(const LevelArgs& A, const TableView& ta
   if (A.level == 0) {  // sde.hpp:237-249: one draw, fine legs only, coarse := 0
     double z[4][NP];
     T zb[4];
-    gen_draws<Arith, APPROX, kNeedExact, kBar, CHECKED, DUMP, 1>(A, tab, s_erfcx, ar, kc, u1, fk,
-                                                                 local, valid, 0, z, zb);
+    Uniforms<NP> cur, unused;
+    draw_uniforms<NP, 1>(kc, cur);
+    gen_draws<Arith, APPROX, kNeedExact, kBar, CHECKED, DUMP, 1, false>(
+        A, tab, s_erfcx, ar, kc, u1, fk, local, valid, 0, cur, unused, z, zb);
     if constexpr (kHat) hat_fine(z[0], 0);
     if constexpr (kBar) bar_fine(zb[0], 0);
   } else {
     const uint64_t halves = 1ull << (A.level - 1);
-    uint64_t m = 0;
     if (halves >= G) {
-      for (; m < halves; m += G) {
+      // the batch after the last is drawn too (never consumed, its u == 1
+      // bits never recorded): the price of a branch-free pipeline
+      Uniforms<2 * G * NP> cur;
+      draw_uniforms<NP, 2 * G>(kc, cur);
+      for (uint64_t m = 0; m < halves; m += G) {
         double z[4][NP];
         T zb[4];
-        gen_draws<Arith, APPROX, kNeedExact, kBar, CHECKED, DUMP, 2 * G>(
-            A, tab, s_erfcx, ar, kc, u1, fk, local, valid, 2 * m, z, zb);
+        Uniforms<2 * G * NP> next;
+        gen_draws<Arith, APPROX, kNeedExact, kBar, CHECKED, DUMP, 2 * G, true>(
+            A, tab, s_erfcx, ar, kc, u1, fk, local, valid, 2 * m, cur, next, z, zb);
+        cur = next;
 #pragma unroll
         for (int g = 0; g < G; ++g) {
           const uint64_t n = 2 * (m + g);
@@ -224,8 +260,10 @@ __device__ __forceinline__ void simulate(const LevelArgs& A, const TableView& ta
     } else {  // level 1 with G = 2: a single coarse step
       double z[4][NP];
       T zb[4];
-      gen_draws<Arith, APPROX, kNeedExact, kBar, CHECKED, DUMP, 2>(A, tab, s_erfcx, ar, kc, u1,
-                                                                   fk, local, valid, 0, z, zb);
+      Uniforms<2 * NP> cur, unused;
+      draw_uniforms<NP, 2>(kc, cur);
+      gen_draws<Arith, APPROX, kNeedExact, kBar, CHECKED, DUMP, 2, false>(
+          A, tab, s_erfcx, ar, kc, u1, fk, local, valid, 0, cur, unused, z, zb);
       if constexpr (kHat) hat_fine(z[0], 0);
       if constexpr (kBar) bar_fine(zb[0], 0);
       if constexpr (kHat) hat_fine(z[1], 1);

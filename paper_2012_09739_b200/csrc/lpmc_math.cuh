@@ -316,10 +316,10 @@ __device__ __forceinline__ double newton_fast(double x0, double v, const double*
 // runs in warp-uniform passes, one pending tail draw per lane per pass, so a
 // warp pays for it about once per coarse step instead of once per draw with
 // one lane active.  Must be called by every active lane of the warp.
+// Stage 1: reflection and Acklam x0 (central for all, tail pass for the rest).
 template <int D>
-__device__ __forceinline__ void phi_inv_multi(const double (&u)[D], double (&z)[D],
-                                              const double* erfcx_tab) {
-  double v[D], x0[D];
+__device__ __forceinline__ void phi_inv_stage1(const double (&u)[D], double (&v)[D],
+                                               double (&x0)[D]) {
   uint32_t pend = 0;
 #pragma unroll
   for (int d = 0; d < D; ++d) {
@@ -340,15 +340,34 @@ __device__ __forceinline__ void phi_inv_multi(const double (&u)[D], double (&z)[
       if (low == (1u << d)) x0[d] = xt;
     pend &= pend - 1u;
   }
+}
+
+// Out of line: keeps the never-taken libdevice path out of the hot loop's
+// instruction footprint (one copy per kernel instead of one per draw).
+__device__ __noinline__ double phi_inv_lower_slow(double v) { return phi_inv_lower_libdevice(v); }
+
+// Stage 2: the Newton step, libdevice fix-up of out-of-range draws, sign.
+template <int D>
+__device__ __forceinline__ void phi_inv_stage2(const double (&u)[D], const double (&v)[D],
+                                               const double (&x0)[D], double (&z)[D],
+                                               const double* erfcx_tab) {
   bool slow[D];
 #pragma unroll
   for (int d = 0; d < D; ++d) z[d] = newton_fast(x0[d], v[d], erfcx_tab, &slow[d]);
 #pragma unroll
   for (int d = 0; d < D; ++d) {
-    if (slow[d]) z[d] = phi_inv_lower_libdevice(v[d]);
+    if (slow[d]) z[d] = phi_inv_lower_slow(v[d]);
     const double r = u[d] > 0.5 ? -z[d] : z[d];
     z[d] = u[d] == 0.5 ? 0.0 : r;
   }
+}
+
+template <int D>
+__device__ __forceinline__ void phi_inv_multi(const double (&u)[D], double (&z)[D],
+                                              const double* erfcx_tab) {
+  double v[D], x0[D];
+  phi_inv_stage1<D>(u, v, x0);
+  phi_inv_stage2<D>(u, v, x0, z, erfcx_tab);
 }
 
 // The same with the reference's formula on libdevice (diagnostics only).
