@@ -344,7 +344,9 @@ __device__ __forceinline__ void phi_inv_stage1(const double (&u)[D], double (&v)
 
 // Out of line: keeps the never-taken libdevice path out of the hot loop's
 // instruction footprint (one copy per kernel instead of one per draw).
-__device__ __noinline__ double phi_inv_lower_slow(double v) { return phi_inv_lower_libdevice(v); }
+static __device__ __noinline__ double phi_inv_lower_slow(double v) {
+  return phi_inv_lower_libdevice(v);
+}
 
 // Stage 2: the Newton step, libdevice fix-up of out-of-range draws, sign.
 template <int D>

@@ -2,6 +2,7 @@
 cd $GRAFT_REPO_ROOT
 mkdir -p gpurun_out
 TAG=${1:-iter}
+python -m paper_2012_09739_b200.build > gpurun_out/build_${TAG}.log 2>&1 || { echo BUILD FAILED; tail -20 gpurun_out/build_${TAG}.log; exit 1; }
 timeout 1200 python -m pytest tests -m gpu -q -p no:cacheprovider -rs -s -k "agreement or erfc_core" > gpurun_out/pytest_${TAG}_report.log 2>&1
 timeout 1200 python -m pytest tests -m gpu -q -p no:cacheprovider > gpurun_out/pytest_${TAG}.log 2>&1; echo "pytest exit $?" >> gpurun_out/pytest_${TAG}.log
 timeout 600 python bench.py --steps 3 --warmup 2 > gpurun_out/bench_${TAG}.log 2>&1; echo "bench exit $?" >> gpurun_out/bench_${TAG}.log
