@@ -304,7 +304,7 @@ __device__ __noinline__ void replay_checked(const LevelArgs& A, TableView tab,
 // half2 instances (two paths, four draws per coarse step) get 128 threads x
 // 4 CTAs (128 registers) so they do not spill.
 #ifndef LPMC_LEVEL_MIN_CTAS
-#define LPMC_LEVEL_MIN_CTAS 3
+#define LPMC_LEVEL_MIN_CTAS 4
 #endif
 template <class Arith, bool KAHAN, int LEGS, bool APPROX, bool DUMP>
 __global__ void __launch_bounds__(kBatch / Arith::NP, LPMC_LEVEL_MIN_CTAS)
