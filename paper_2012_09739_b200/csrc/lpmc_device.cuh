@@ -25,7 +25,8 @@ constexpr int kChunkBatches = 1024;
 constexpr int kChunkThreads = 512;
 constexpr uint64_t kTopDraw = 0x1FFFFFFFFFFFFFull;  // (w >> 11) that rounds u to 1.0
 constexpr uint64_t kNoFail = ~0ull;
-constexpr int kErfcxWords = math::kErfcxRows * math::kErfcxN;
+constexpr int kMathWords = math::kMathTableWords;
+constexpr uint64_t kHalfDraw = 1ull << 52;  // (w >> 11) that rounds u to exactly 1/2
 
 enum : uint32_t { kStageDraw = 0, kStageHatFine = 1, kStageBarFine = 2, kStageHatCoarse = 3,
                   kStageBarCoarse = 4 };
@@ -49,21 +50,26 @@ __device__ __forceinline__ uint64_t path_key(uint64_t seed_key, uint64_t path) {
 
 // u = (w >> 11) 2^-53 + 2^-54 with w = mix64(mix64(key + ctr c3)); the
 // running kc = key + ctr c3 is strength-reduced (uniform.hpp:25, :38-41).
-__device__ __forceinline__ double next_uniform(uint64_t& kc, bool& top) {
+// top: the draw rounds to u == 1 (the reference throws, gaussian.hpp:60);
+// half: it rounds to exactly u == 1/2 (both transforms return exactly 0).
+__device__ __forceinline__ double next_uniform(uint64_t& kc, bool& top, bool& half) {
   const uint64_t w = mix64(mix64(kc));
   kc += 0x94d049bb133111ebull;
   const uint64_t b = w >> 11;
   top = b == kTopDraw;
+  half = b == kHalfDraw;
   return __dadd_rn(__dmul_rn(__ull2double_rn(b), 0x1p-53), 0x1p-54);
 }
 
-__device__ __forceinline__ void stage_erfcx(double* s_erfcx) {
-  for (int i = threadIdx.x; i < kErfcxWords; i += blockDim.x) s_erfcx[i] = math::kErfcxTable[i];
+// erfcx records + 2^(j/64) pairs into (16-byte aligned) shared memory
+__device__ __forceinline__ void stage_math(double* s_math) {
+  for (int i = threadIdx.x; i < kMathWords; i += blockDim.x) s_math[i] = math::kMathTable[i];
 }
 
 // ------------------------------------------- approximate inverse CDF -------
-// Shared-memory table, kTableRows rows of `stride` doubles (stride 32 for the
-// dyadic layout K <= 32, K otherwise): a_j, w_j, c0..c3, v-thresholds.
+// Shared-memory table.  Dyadic layout (K <= 32): one 6-double record per
+// interval {a_j, 2^(j+2), c0, c1, c2, c3} (128-bit loads).  General layout:
+// kTableRows rows of `stride` = K doubles: a_j, b_j - a_j, c0..c3, v-thresholds.
 struct TableView {
   const double* base;
   int stride, K, degree, dyadic, simple;
@@ -80,6 +86,8 @@ struct TableView {
 //    reference.
 //  * `simple` (host-proved: every c0 != 0 and c2 = c3 = +0): the reference's
 //    (c0 + c1 t) + 0 p2 + 0 p3 equals c0 + c1 t including the sign of zero.
+//  * EXACT_HALF: exactly 0 at u = 1/2; the hot loop replays such draws.
+template <bool EXACT_HALF = true>
 __device__ __forceinline__ double approx_inv(const TableView& t, double u) {
   const bool lower = u < 0.5;
   const double up = lower ? 1.0 - u : u;  // fl(1-u) for the lower half (:47-49)
@@ -90,13 +98,16 @@ __device__ __forceinline__ double approx_inv(const TableView& t, double u) {
     const int e = static_cast<int>(vb >> 52) - 1023;
     const int fl = (vb & 0xFFFFFFFFFFFFFull) == 0 ? -e : -e - 1;  // floor(-log2 v) >= 1
     const int j = min(fl - 1, t.K - 1);
-    const double* b = t.base + j;
-    const double s = __dsub_rn(__dmul_rn(__dmul_rn(2.0, __dsub_rn(up, b[0])), b[32]), 1.0);
-    r = __dadd_rn(b[64], __dmul_rn(b[96], s));
+    const double* b = t.base + 6 * j;
+    const math::D2 aw = math::load2(b);
+    const math::D2 c01 = math::load2(b + 2);
+    const double s = __dsub_rn(__dmul_rn(__dmul_rn(2.0, __dsub_rn(up, aw.a)), aw.b), 1.0);
+    r = __dadd_rn(c01.a, __dmul_rn(c01.b, s));
     if (t.degree == 3 || (!t.simple && r == 0.0)) {
+      const math::D2 c23 = math::load2(b + 4);
       const double p2 = 1.5 * s * s - 0.5;
       const double p3 = s * (2.5 * s * s - 1.5);
-      r = r + b[128] * p2 + b[160] * p3;
+      r = r + c23.a * p2 + c23.b * p3;
     }
     r = fl >= t.K + 1 ? t.tail : r;  // w >= w_max: clamped tail
   } else {
@@ -122,7 +133,8 @@ __device__ __forceinline__ double approx_inv(const TableView& t, double u) {
     r = v <= thr[t.K - 1] ? t.tail : r;
   }
   r = lower ? -r : r;
-  return u == 0.5 ? 0.0 : r;
+  if constexpr (EXACT_HALF) r = u == 0.5 ? 0.0 : r;
+  return r;
 }
 
 // ----------------------------------------------- rounding helpers ---------

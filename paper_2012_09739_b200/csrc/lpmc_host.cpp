@@ -230,8 +230,7 @@ lpmc_status prepare_table(const lpmc_invcdf_table* t, HostTable* out, lpmc_error
   bool dyadic = t->step_w == 1.0 && t->w_max == static_cast<double>(K + 1);
   for (int j = 0; dyadic && j < K; ++j) dyadic = t->breakpoints[j] == 1.0 - std::ldexp(1.0, -(j + 2));
   out->dyadic = dyadic ? 1 : 0;
-  const int S = dyadic ? kDyadicStride : K;  // dyadic K <= 32: fixed stride, immediate offsets
-  out->stride = S;
+  out->stride = K;
   // signed-zero fix-up provably unnecessary (see dev::approx_inv)
   bool simple = t->kind != LPMC_APPROX_CUBIC;
   for (int j = 0; simple && j < K; ++j) {
@@ -240,17 +239,24 @@ lpmc_status prepare_table(const lpmc_invcdf_table* t, HostTable* out, lpmc_error
              !std::signbit(c[3]);
   }
   out->simple = simple ? 1 : 0;
-  out->rows.assign(static_cast<size_t>(kTableRows) * S, 0.0);
-  double* a = out->rows.data();
-  double* w = a + S;
-  for (int j = 0; j < K; ++j) {
-    a[j] = j == 0 ? 0.5 : t->breakpoints[j - 1];
-    w[j] = dyadic ? std::ldexp(1.0, j + 2) : t->breakpoints[j] - a[j];
-    for (int c = 0; c < 4; ++c) out->rows[static_cast<size_t>(2 + c) * S + j] = t->coeff[4 * j + c];
-  }
-  if (!dyadic) {
+  auto left = [&](int j) { return j == 0 ? 0.5 : t->breakpoints[j - 1]; };
+  if (dyadic) {  // records {a, 2^(j+2), c0, c1, c2, c3}
+    out->rows.assign(static_cast<size_t>(kDyadicRecord) * K, 0.0);
+    for (int j = 0; j < K; ++j) {
+      double* r = out->rows.data() + kDyadicRecord * j;
+      r[0] = left(j);
+      r[1] = std::ldexp(1.0, j + 2);
+      for (int c = 0; c < 4; ++c) r[2 + c] = t->coeff[4 * j + c];
+    }
+  } else {  // rows of K
+    out->rows.assign(static_cast<size_t>(kTableRows) * K, 0.0);
+    for (int j = 0; j < K; ++j) {
+      out->rows[j] = left(j);
+      out->rows[static_cast<size_t>(K) + j] = t->breakpoints[j] - left(j);
+      for (int c = 0; c < 4; ++c) out->rows[static_cast<size_t>(2 + c) * K + j] = t->coeff[4 * j + c];
+    }
     const std::vector<double> thr = index_thresholds(K, t->w_max, t->step_w);
-    std::copy(thr.begin(), thr.end(), out->rows.begin() + 6 * S);
+    std::copy(thr.begin(), thr.end(), out->rows.begin() + 6 * static_cast<size_t>(K));
   }
   return LPMC_OK;
 }
@@ -417,6 +423,7 @@ lpmc_status build_spec(const lpmc_gbm* model, int32_t level, const lpmc_precisio
     A.degree = s.table.degree;
     A.dyadic = s.table.dyadic;
     A.table_stride = s.table.stride;
+    A.table_words = static_cast<int32_t>(s.table.rows.size());
     A.table_simple = s.table.simple;
     A.tail = s.table.tail;
   }
@@ -1062,7 +1069,7 @@ lpmc_status lpmc_device_inv_cdf(const double* u, uint64_t n, const lpmc_invcdf_t
 
 double lpmc_erfc_core(double t) {
   if (!(t >= 0.0 && t < math::kFastTMax)) return std::erfc(t);
-  return math::erfc_fast(t, math::kErfcxTableHost);
+  return math::erfc_fast(t, math::kMathTableHost);
 }
 
 lpmc_status lpmc_measure_pipe_peaks(int32_t device, double* out4, lpmc_error* err) {

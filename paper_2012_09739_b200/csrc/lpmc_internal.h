@@ -20,12 +20,12 @@ enum class BarArith : int {
   kHalf2 = 4      // native IEEE binary16, two paths per thread (__h*2_rn)
 };
 
-// Device table layout: kTableRows rows of `table_stride` doubles
-// (stride 32 for dyadic tables, K otherwise):
-//   row 0 left endpoint a_j      row 1 2^(j+2) (dyadic) or b_j - a_j
-//   rows 2..5 c0, c1, c2, c3     row 6 v-thresholds T_1..T_{K-1}, T_tail (general K)
+// Device table layouts (doubles):
+//   dyadic (K <= 32): K records {a_j, 2^(j+2), c0, c1, c2, c3} (kDyadicRecord)
+//   general: kTableRows rows of K: a_j, b_j - a_j, c0, c1, c2, c3,
+//            v-thresholds T_1..T_{K-1}, T_tail
 constexpr int kTableRows = 7;
-constexpr int kDyadicStride = 32;
+constexpr int kDyadicRecord = 6;
 
 struct LevelArgs {
   uint64_t seed_key;   // mix64(seed + 0x9e37...) (uniform.hpp:23), hoisted per launch
@@ -45,7 +45,8 @@ struct LevelArgs {
   // approximation table (nullptr = exact inverse CDF for the bar legs)
   const double* table;
   int32_t K, degree, dyadic;
-  int32_t table_stride;  // 32 (dyadic) or K
+  int32_t table_stride;  // general layout: K (rows of K doubles)
+  int32_t table_words;   // doubles to stage into shared memory
   int32_t table_simple;  // every c0 != 0 and c2 = c3 = +0: no signed-zero fix-up
   double tail;
   // payoff on terminal values (extension)

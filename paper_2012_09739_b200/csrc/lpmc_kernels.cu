@@ -74,8 +74,8 @@ __global__ void inv_cdf_kernel(const double* __restrict__ u, uint64_t n,
                                const double* __restrict__ table, int K, int degree, int dyadic,
                                int stride, int simple, double tail, int op,
                                double* __restrict__ out) {
-  __shared__ double s_erfcx[kErfcxWords];
-  stage_erfcx(s_erfcx);
+  __shared__ __align__(16) double s_math[kMathWords];
+  stage_math(s_math);
   __syncthreads();
   const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   const bool in = i < n;
@@ -83,7 +83,7 @@ __global__ void inv_cdf_kernel(const double* __restrict__ u, uint64_t n,
   double r = 0.0;
   if (op == 0) {
     double uu[1] = {x}, zz[1];
-    math::phi_inv_multi<1>(uu, zz, s_erfcx);
+    math::phi_inv_multi<1>(uu, zz, s_math);
     r = zz[0];
   } else if (op == 1) {
     const TableView t{table, stride, K, degree, dyadic, simple, tail};
@@ -91,7 +91,7 @@ __global__ void inv_cdf_kernel(const double* __restrict__ u, uint64_t n,
   } else if (op == 2) {
     r = math::phi_inv_libdevice(x);
   } else {
-    r = math::erfc_fast(x, s_erfcx);
+    r = math::erfc_fast(x, s_math);
   }
   if (in) out[i] = r;
 }

@@ -33,23 +33,26 @@ __device__ __forceinline__ void note_fail(uint64_t& fk, bool bad, uint64_t n, ui
   }
 }
 
-// Uniforms of H draws x NP paths (draw-major), with their u == 1 bits.
+// Uniforms of H draws x NP paths (draw-major), with their u == 1 bits (top)
+// and u == 1/2 bits (half).
 template <int D>
 struct Uniforms {
   double u[D];
-  uint32_t top;
+  uint32_t top, half;
 };
 
 template <int NP, int H>
 __device__ __forceinline__ void draw_uniforms(uint64_t (&kc)[NP], Uniforms<H * NP>& U) {
   U.top = 0u;
+  U.half = 0u;
 #pragma unroll
   for (int h = 0; h < H; ++h)
 #pragma unroll
     for (int p = 0; p < NP; ++p) {
-      bool top;
-      U.u[h * NP + p] = next_uniform(kc[p], top);
+      bool top, half;
+      U.u[h * NP + p] = next_uniform(kc[p], top, half);
       U.top |= (top ? 1u : 0u) << (h * NP + p);
+      U.half |= (half ? 1u : 0u) << (h * NP + p);
     }
 }
 
@@ -62,7 +65,7 @@ __device__ __forceinline__ void draw_uniforms(uint64_t (&kc)[NP], Uniforms<H * N
 template <class Arith, bool APPROX, bool NEED_EXACT, bool BAR, bool CHECKED, bool DUMP, int H,
           bool PREFETCH>
 __device__ __forceinline__ void gen_draws(const LevelArgs& A, const TableView& tab,
-                                          const double* s_erfcx, const Arith& ar,
+                                          const double* s_math, const Arith& ar,
                                           uint64_t (&kc)[Arith::NP], bool (&u1)[Arith::NP],
                                           uint64_t (&fk)[Arith::NP],
                                           const uint64_t (&local)[Arith::NP],
@@ -78,11 +81,11 @@ __device__ __forceinline__ void gen_draws(const LevelArgs& A, const TableView& t
   for (int h = 0; h < H; ++h)
 #pragma unroll
     for (int p = 0; p < NP; ++p) {
-      const bool top = (cur.top >> (h * NP + p)) & 1u;
+      const uint32_t bit = 1u << (h * NP + p);
       if constexpr (CHECKED) {
-        note_fail(fk[p], top, n0 + h, kStageDraw);
-      } else {
-        u1[p] |= top;
+        note_fail(fk[p], (cur.top & bit) != 0u, n0 + h, kStageDraw);
+      } else {  // u == 1 or u == 1/2: the path is replayed exactly
+        u1[p] |= ((cur.top | cur.half) & bit) != 0u;
       }
     }
   double zz[D];
@@ -90,7 +93,7 @@ __device__ __forceinline__ void gen_draws(const LevelArgs& A, const TableView& t
     double v[D], x0[D];
     math::phi_inv_stage1<D>(u, v, x0);
     if constexpr (PREFETCH) draw_uniforms<NP, H>(kc, next);
-    math::phi_inv_stage2<D>(u, v, x0, zz, s_erfcx);
+    math::phi_inv_stage2<D, CHECKED>(u, v, x0, zz, s_math);
   } else {
     if constexpr (PREFETCH) draw_uniforms<NP, H>(kc, next);
 #pragma unroll
@@ -107,7 +110,7 @@ __device__ __forceinline__ void gen_draws(const LevelArgs& A, const TableView& t
           A.z_out[local[p] * (1ull << A.level) + n0 + h] = z[h][p];
       }
       if constexpr (APPROX) {
-        zl[p] = approx_inv(tab, u[h * NP + p]);
+        zl[p] = approx_inv<CHECKED>(tab, u[h * NP + p]);
       } else {
         zl[p] = z[h][p];
       }
@@ -118,7 +121,7 @@ __device__ __forceinline__ void gen_draws(const LevelArgs& A, const TableView& t
 
 template <class Arith, bool KAHAN, int LEGS, bool APPROX, bool CHECKED, bool DUMP>
 __device__ __forceinline__ void simulate(const LevelArgs& A, const TableView& tab,
-                                         const double* s_erfcx,
+                                         const double* s_math,
                                          const uint64_t (&local)[Arith::NP],
                                          const bool (&valid)[Arith::NP],
                                          PathEnd<Arith::NP>& R) {
@@ -230,7 +233,7 @@ __device__ __forceinline__ void simulate(const LevelArgs& A, const TableView& ta
     Uniforms<NP> cur, unused;
     draw_uniforms<NP, 1>(kc, cur);
     gen_draws<Arith, APPROX, kNeedExact, kBar, CHECKED, DUMP, 1, false>(
-        A, tab, s_erfcx, ar, kc, u1, fk, local, valid, 0, cur, unused, z, zb);
+        A, tab, s_math, ar, kc, u1, fk, local, valid, 0, cur, unused, z, zb);
     if constexpr (kHat) hat_fine(z[0], 0);
     if constexpr (kBar) bar_fine(zb[0], 0);
   } else {
@@ -245,7 +248,7 @@ __device__ __forceinline__ void simulate(const LevelArgs& A, const TableView& ta
         T zb[4];
         Uniforms<2 * G * NP> next;
         gen_draws<Arith, APPROX, kNeedExact, kBar, CHECKED, DUMP, 2 * G, true>(
-            A, tab, s_erfcx, ar, kc, u1, fk, local, valid, 2 * m, cur, next, z, zb);
+            A, tab, s_math, ar, kc, u1, fk, local, valid, 2 * m, cur, next, z, zb);
         cur = next;
 #pragma unroll
         for (int g = 0; g < G; ++g) {
@@ -263,7 +266,7 @@ __device__ __forceinline__ void simulate(const LevelArgs& A, const TableView& ta
       Uniforms<2 * NP> cur, unused;
       draw_uniforms<NP, 2>(kc, cur);
       gen_draws<Arith, APPROX, kNeedExact, kBar, CHECKED, DUMP, 2, false>(
-          A, tab, s_erfcx, ar, kc, u1, fk, local, valid, 0, cur, unused, z, zb);
+          A, tab, s_math, ar, kc, u1, fk, local, valid, 0, cur, unused, z, zb);
       if constexpr (kHat) hat_fine(z[0], 0);
       if constexpr (kBar) bar_fine(zb[0], 0);
       if constexpr (kHat) hat_fine(z[1], 1);
@@ -287,17 +290,16 @@ __device__ __forceinline__ void simulate(const LevelArgs& A, const TableView& ta
   R.range_bad = range.bad();
 }
 
-// Exact first failure of this thread's paths (only called for suspects).
+// Exact replay of this thread's paths (only for suspects: a u == 1 or
+// u == 1/2 draw, or a non-finite end state): exact transforms and the first
+// failure in the reference's serial order.
 template <class Arith, bool KAHAN, int LEGS, bool APPROX>
 __device__ __noinline__ void replay_checked(const LevelArgs& A, TableView tab,
-                                            const double* s_erfcx,
+                                            const double* s_math,
                                             const uint64_t (&local)[Arith::NP],
                                             const bool (&valid)[Arith::NP],
-                                            uint64_t (&fk)[Arith::NP]) {
-  PathEnd<Arith::NP> R;
-  simulate<Arith, KAHAN, LEGS, APPROX, true, false>(A, tab, s_erfcx, local, valid, R);
-#pragma unroll
-  for (int p = 0; p < Arith::NP; ++p) fk[p] = R.fk[p];
+                                            PathEnd<Arith::NP>& R) {
+  simulate<Arith, KAHAN, LEGS, APPROX, true, false>(A, tab, s_math, local, valid, R);
 }
 
 // 256 threads x 4 CTAs per SM (64 registers) for one path per thread; the
@@ -314,13 +316,12 @@ __global__ void __launch_bounds__(kBatch / Arith::NP, LPMC_LEVEL_MIN_CTAS)
   constexpr bool kBar = (LEGS & 2) != 0;
   constexpr bool kNeedExact = kHat || !APPROX;
 
-  extern __shared__ double s_table[];
-  __shared__ double s_erfcx[kNeedExact ? kErfcxWords : 1];
-  if constexpr (kNeedExact) stage_erfcx(s_erfcx);
+  extern __shared__ __align__(16) double s_table[];
+  __shared__ __align__(16) double s_math[kNeedExact ? kMathWords : 2];
+  if constexpr (kNeedExact) stage_math(s_math);
   TableView tab{};
   if constexpr (APPROX) {
-    for (int i = threadIdx.x; i < kTableRows * A.table_stride; i += blockDim.x)
-      s_table[i] = A.table[i];
+    for (int i = threadIdx.x; i < A.table_words; i += blockDim.x) s_table[i] = A.table[i];
     tab = TableView{s_table, A.table_stride, A.K, A.degree, A.dyadic, A.table_simple, A.tail};
   }
   __syncthreads();
@@ -339,19 +340,20 @@ __global__ void __launch_bounds__(kBatch / Arith::NP, LPMC_LEVEL_MIN_CTAS)
   }
 
   PathEnd<NP> R;
-  simulate<Arith, KAHAN, LEGS, APPROX, false, DUMP>(A, tab, s_erfcx, local, valid, R);
+  simulate<Arith, KAHAN, LEGS, APPROX, false, DUMP>(A, tab, s_math, local, valid, R);
 
   bool any_suspect = false;
 #pragma unroll
   for (int p = 0; p < NP; ++p) any_suspect |= valid[p] && R.suspect[p];
-  if (any_suspect) {  // rare: exact first failure in the reference's serial order
-    uint64_t fk[NP];
-    replay_checked<Arith, KAHAN, LEGS, APPROX>(A, tab, s_erfcx, local, valid, fk);
+  if (any_suspect) {  // rare: exact values and first failure (serial order)
+    const bool range_bad = R.range_bad;
+    replay_checked<Arith, KAHAN, LEGS, APPROX>(A, tab, s_math, local, valid, R);
+    R.range_bad |= range_bad;
 #pragma unroll
     for (int p = 0; p < NP; ++p) {
-      if (!valid[p] || fk[p] == kNoFail) continue;
-      const uint64_t n = fk[p] >> 3;
-      const uint32_t stage = static_cast<uint32_t>(fk[p] & 7u);
+      if (!valid[p] || R.fk[p] == kNoFail) continue;
+      const uint64_t n = R.fk[p] >> 3;
+      const uint32_t stage = static_cast<uint32_t>(R.fk[p] & 7u);
       uint32_t kind = stage == kStageDraw ? kKindU1 : kKindNonFinite;
       if (Arith::kIeee && (stage == kStageBarFine || stage == kStageBarCoarse)) kind = kKindState;
       const uint64_t step = n < (1ull << 22) ? n : (1ull << 22) - 1;
@@ -402,7 +404,7 @@ constexpr int kMaxDynSmem = kTableRows * kMaxTableK * 8;
 
 template <class Arith, bool KAHAN, int LEGS, bool APPROX, bool DUMP>
 cudaError_t launch_one(const LevelArgs& A, cudaStream_t s) {
-  const size_t smem = APPROX ? static_cast<size_t>(kTableRows) * A.table_stride * sizeof(double) : 0;
+  const size_t smem = APPROX ? static_cast<size_t>(A.table_words) * sizeof(double) : 0;
   level_kernel<Arith, KAHAN, LEGS, APPROX, DUMP>
       <<<static_cast<unsigned>(A.n_batches), kBatch / Arith::NP, smem, s>>>(A);
   return cudaGetLastError();

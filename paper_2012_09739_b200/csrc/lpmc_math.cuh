@@ -110,23 +110,23 @@ LPMC_HD double sqrt_coarse(double y) {
 // Scalar coefficients, one constant block.  On the device it is deliberately
 // NOT statically initialised: ptxas constant-folds initialised __constant__
 // data back into 64-bit immediates (uniform-register moves again); uploaded
-// at context creation (upload_constants), every use is a c[0x3][...] operand.
+// at context creation (upload_math_constants), uses become constant loads.
 enum : int {
   kOffAckA = 0,                     // Acklam central numerator a0..a5   (gaussian.hpp:28-30)
   kOffAckB = 6,                     // Acklam central denominator b0..b4 (:31-33)
   kOffAckC = 11,                    // Acklam tail numerator c0..c5      (:34-36)
   kOffAckD = 17,                    // Acklam tail denominator d0..d3    (:37-38)
   kOffLogS = 21,                    // 2/(2i+1), i = 0..6: log(m) = s sum s^2i 2/(2i+1)
-  kOffExp = 28,                     // exp minimax, LPMC_EXP_DEG + 1 terms
-  kOffMisc = kOffExp + LPMC_EXP_DEG + 1,
-  kLog2e = kOffMisc + 0,            // log2(e)
-  kLn2Hi = kOffMisc + 1,            // ln 2 split: 32 significant bits (k * hi exact)
-  kLn2Lo = kOffMisc + 2,
+  kOffExpm1 = 28,                   // expm1(r)/r, LPMC_EXPM1_DEG + 1 terms
+  kOffMisc = kOffExpm1 + LPMC_EXPM1_DEG + 1,
+  kLog2eN = kOffMisc + 0,           // 64 log2(e)
+  kLn2HiN = kOffMisc + 1,           // ln2/64 split: 32 significant bits (k * hi exact)
+  kLn2LoN = kOffMisc + 2,
   kLn2 = kOffMisc + 3,
   kInvSqrt2 = kOffMisc + 4,         // gaussian.hpp:15 literal
   kSqrt2Pi = kOffMisc + 5,
   kTailU = kOffMisc + 6,            // Acklam's u_low = 0.02425 (gaussian.hpp:38)
-  kSqrtHalfBits = kOffMisc + 7,     // unused slot (alignment)
+  kSpare = kOffMisc + 7,
   kMathCount = kOffMisc + 8
 };
 
@@ -140,17 +140,29 @@ static const double kMathHost[kMathCount] = {
     7.784695709041462e-03, 3.224671290700398e-01, 2.445134137142996e+00,
     3.754408661907416e+00,
     2.0, 2.0 / 3.0, 2.0 / 5.0, 2.0 / 7.0, 2.0 / 9.0, 2.0 / 11.0, 2.0 / 13.0,
-    LPMC_EXP_COEF_LIST,
-    1.4426950408889634, 6.93147180369123816490e-01, 1.90821492927058770002e-10,
+    LPMC_EXPM1_COEF_LIST,
+    92.332482616893657,                       // 64 log2(e)
+    6.93147180369123816490e-01 / 64.0,        // exact scaling of the 32-bit ln2 head
+    1.90821492927058770002e-10 / 64.0,
     6.93147180559945309417e-01, 0.7071067811865475244, 2.5066282746310002, 0.02425, 0.0};
-static const double kErfcxTableHost[(LPMC_ERFCX_DEG + 2) * LPMC_ERFCX_INTERVALS] = LPMC_ERFCX_COEF;
+
+constexpr int kErfcxRow = LPMC_ERFCX_ROW;
+constexpr int kErfcxN = LPMC_ERFCX_INTERVALS;
+constexpr int kErfcxWords = kErfcxRow * kErfcxN;
+constexpr int kExpN = LPMC_EXP_N;
+constexpr int kExpWords = 2 * kExpN;
+constexpr int kMathTableWords = kErfcxWords + kExpWords;  // one shared-memory block
+constexpr double kFastTMax = 6.5;  // 26 intervals of 1/4
+
+// erfcx records, then the 2^(j/64) hi/lo pairs (host copy)
+static const double kMathTableHost[kMathTableWords] = {LPMC_ERFCX_COEF_LIST, LPMC_EXP_TAB_LIST};
 
 #ifdef __CUDACC__
 // TU-local (static): every kernel translation unit has its own copy and
 // uploads it in its configure function (upload_math_constants).
 static __constant__ double kMath[kMathCount];
-static __device__ const double kErfcxTable[(LPMC_ERFCX_DEG + 2) * LPMC_ERFCX_INTERVALS] =
-    LPMC_ERFCX_COEF;
+static __device__ const double kMathTable[kMathTableWords] = {LPMC_ERFCX_COEF_LIST,
+                                                               LPMC_EXP_TAB_LIST};
 
 static inline cudaError_t upload_math_constants() {
   return cudaMemcpyToSymbol(kMath, kMathHost, sizeof(kMathHost));
@@ -163,43 +175,65 @@ static inline cudaError_t upload_math_constants() {
 #define LPMC_K(i) kMathHost[i]
 #endif
 
-constexpr int kErfcxRows = LPMC_ERFCX_DEG + 2;
-constexpr int kErfcxN = LPMC_ERFCX_INTERVALS;
-constexpr double kFastTMax = 6.5;  // 26 intervals of 1/4
+// two adjacent doubles of a 16-byte aligned table (one 128-bit load)
+struct D2 {
+  double a, b;
+};
+LPMC_HD D2 load2(const double* p) {
+#ifdef __CUDA_ARCH__
+  const double2 v = *reinterpret_cast<const double2*>(p);
+  return D2{v.x, v.y};
+#else
+  return D2{p[0], p[1]};
+#endif
+}
 
-// exp(-(th + tl)) = 2^k p, p in [2^-1/2, 2^1/2], for th in [0, 708].
+// exp(-(th + tl)) = 2^k p, p in [2^-1/2, 2^1/2], th in [0, 700]:
+// kf = round(-64 th log2 e) = 64 k + j, r = -th - kf ln2/64 (exact head),
+// p = 2^(j/64) (1 + r P(r)) with the table value as hi + lo.
 struct ExpSplit {
   double p;
   int k;
 };
 
-LPMC_HD ExpSplit exp_neg(double th, double tl) {
+LPMC_HD ExpSplit exp_neg(double th, double tl, const double* tab) {
   const double kShift = 6755399441055744.0;  // 1.5 * 2^52 (an encodable immediate)
-  const double kd = fmad(-th, LPMC_K(kLog2e), kShift) - kShift;  // round(-th log2 e)
-  const int k = static_cast<int>(kd);
-  double r = fmad(kd, -LPMC_K(kLn2Hi), -th);
-  r = fmad(kd, -LPMC_K(kLn2Lo), r);
+  const double kd = fmad(-th, LPMC_K(kLog2eN), kShift) - kShift;
+  const int kf = static_cast<int>(kd);
+  double r = fmad(kd, -LPMC_K(kLn2HiN), -th);  // exact
+  r = fmad(kd, -LPMC_K(kLn2LoN), r);
   r = r - tl;
-  double q = LPMC_K(kOffExp + LPMC_EXP_DEG);
+  double q = LPMC_K(kOffExpm1 + LPMC_EXPM1_DEG);
 #ifdef __CUDA_ARCH__
 #pragma unroll
 #endif
-  for (int i = LPMC_EXP_DEG - 1; i >= 0; --i) q = fmad(q, r, LPMC_K(kOffExp + i));
-  return ExpSplit{q, k};
+  for (int i = LPMC_EXPM1_DEG - 1; i >= 0; --i) q = fmad(q, r, LPMC_K(kOffExpm1 + i));
+  q = q * r;  // expm1(r)
+  const D2 t2 = load2(tab + kErfcxWords + 2 * (kf & (kExpN - 1)));
+  const double p = t2.a + fmad(t2.a, q, t2.b);
+  return ExpSplit{p, kf >> 6};
 }
 
-// erfcx(t) for t in [0, 6.5) from a [kErfcxRows][kErfcxN] coefficient table.
+// erfcx(t) for t in [0, 6.5): interval record j, highest power first.
 LPMC_HD double erfcx_piecewise(double t, const double* tab) {
   int j = static_cast<int>(t * 4.0);
   j = j < kErfcxN - 1 ? j : kErfcxN - 1;
   const double s = t - (0.25 * j + 0.125);
-  double q = tab[LPMC_ERFCX_DEG * kErfcxN + j];
+  const double* rec = tab + kErfcxRow * j;
+  D2 c = load2(rec);
+  double q = fmad(c.a, s, c.b);  // c11 s + c10
 #ifdef __CUDA_ARCH__
 #pragma unroll
 #endif
-  for (int i = LPMC_ERFCX_DEG - 1; i >= 1; --i) q = fmad(q, s, tab[i * kErfcxN + j]);
-  const double lo = tab[(LPMC_ERFCX_DEG + 1) * kErfcxN + j];
-  return tab[j] + fmad(q, s, lo);
+  for (int i = 2; i < 10; i += 2) {  // c9..c2
+    c = load2(rec + i);
+    q = fmad(q, s, c.a);
+    q = fmad(q, s, c.b);
+  }
+  c = load2(rec + 10);  // c1, c0 hi
+  q = fmad(q, s, c.a);
+  const D2 lo = load2(rec + 12);  // c0 lo, 0
+  return c.b + fmad(q, s, lo.a);
 }
 
 // 2^k x for |k| <= 1022 and a normal result (the fast path has |k| <= 62).
@@ -211,7 +245,7 @@ LPMC_HD double scale(double x, int k) {
 LPMC_HD double erfc_fast(double t, const double* tab) {
   const double th = t * t;
   const double tl = fmad(t, t, -th);
-  const ExpSplit e = exp_neg(th, tl);
+  const ExpSplit e = exp_neg(th, tl, tab);
   return scale(e.p * erfcx_piecewise(t, tab), e.k);
 }
 
@@ -294,16 +328,17 @@ __device__ __forceinline__ double acklam_tail(double v) {
 // The Newton step of gaussian.hpp:52-53, x0 - (Phi(x0) - v) / pdf(x0), with
 // Phi(x0) = erfc(t)/2 and t = (-x0) * (1/sqrt 2) rounded as the reference
 // rounds it.  *slow is set when t >= 6.5 (v < ~1e-20: outside the sampler's
-// range); the caller then redoes that draw on libdevice.
-__device__ __forceinline__ double newton_fast(double x0, double v, const double* erfcx_tab,
+// range); the caller then redoes that draw on libdevice (the value computed
+// here for such a lane is garbage but never used, and no operation traps).
+// mtab = the staged math table (erfcx records, then 2^(j/64)).
+__device__ __forceinline__ double newton_fast(double x0, double v, const double* mtab,
                                               bool* slow) {
-  const double t0 = -x0 * LPMC_K(kInvSqrt2);
-  *slow = !(t0 < kFastTMax);
-  const double t = *slow ? 0.0 : t0;
+  const double t = -x0 * LPMC_K(kInvSqrt2);
+  *slow = !(t < kFastTMax);
   const double th = t * t;
   const double tl = fmad(t, t, -th);
-  const ExpSplit e = exp_neg(th, tl);
-  const double pg = e.p * erfcx_piecewise(t, erfcx_tab);
+  const ExpSplit e = exp_neg(th, tl, mtab);
+  const double pg = e.p * erfcx_piecewise(t, mtab);
   const double cdf = scale(pg, e.k - 1);  // 0.5 erfc(t)
   const double resid = cdf - v;
   // 1/pdf(x0) = sqrt(2 pi) exp(t^2) = sqrt(2 pi) 2^-k / p
@@ -349,27 +384,34 @@ static __device__ __noinline__ double phi_inv_lower_slow(double v) {
 }
 
 // Stage 2: the Newton step, libdevice fix-up of out-of-range draws, sign.
-template <int D>
+// EXACT_HALF: return exactly 0 for u == 1/2 (gaussian.hpp:62).  The hot loop
+// instead flags such a draw (probability 2^-53) and has the path replayed
+// with EXACT_HALF, which keeps two selects per draw out of the loop.
+template <int D, bool EXACT_HALF = true>
 __device__ __forceinline__ void phi_inv_stage2(const double (&u)[D], const double (&v)[D],
                                                const double (&x0)[D], double (&z)[D],
-                                               const double* erfcx_tab) {
+                                               const double* mtab) {
   bool slow[D];
 #pragma unroll
-  for (int d = 0; d < D; ++d) z[d] = newton_fast(x0[d], v[d], erfcx_tab, &slow[d]);
+  for (int d = 0; d < D; ++d) z[d] = newton_fast(x0[d], v[d], mtab, &slow[d]);
 #pragma unroll
   for (int d = 0; d < D; ++d) {
     if (slow[d]) z[d] = phi_inv_lower_slow(v[d]);
     const double r = u[d] > 0.5 ? -z[d] : z[d];
-    z[d] = u[d] == 0.5 ? 0.0 : r;
+    if constexpr (EXACT_HALF) {
+      z[d] = u[d] == 0.5 ? 0.0 : r;
+    } else {
+      z[d] = r;
+    }
   }
 }
 
 template <int D>
 __device__ __forceinline__ void phi_inv_multi(const double (&u)[D], double (&z)[D],
-                                              const double* erfcx_tab) {
+                                              const double* mtab) {
   double v[D], x0[D];
   phi_inv_stage1<D>(u, v, x0);
-  phi_inv_stage2<D>(u, v, x0, z, erfcx_tab);
+  phi_inv_stage2<D, true>(u, v, x0, z, mtab);
 }
 
 // The same with the reference's formula on libdevice (diagnostics only).
