@@ -234,6 +234,27 @@ class Oracle:
             out[i] = o2
         return out
 
+    def diffs(self, cfg, path_base: int, n: int):
+        """Per-path (d_hat, d_bar) of paths path_base .. path_base+n-1."""
+        dh = np.zeros(n)
+        db = np.zeros(n)
+        self.lib.orc_diffs.argtypes = [C.POINTER(OrcConfig), _u64, _u64, _dp, _dp]
+        rc = self.lib.orc_diffs(C.byref(cfg), path_base, n, _ptr(dh), _ptr(db))
+        if rc:
+            raise RuntimeError(f"oracle path failure {rc}")
+        return dh, db
+
+    def chunk_partials(self, cfg, n_paths: int, path_base: int, c0: int, c1: int,
+                       chunk_paths: int = 262144):
+        """(c1-c0, 3, 5) chunk accumulators of the device library's tree."""
+        out = []
+        for c in range(c0, c1):
+            a = c * chunk_paths
+            m = min(chunk_paths, n_paths - a)
+            dh, db = self.diffs(cfg, path_base + a, m)
+            out.append(self.tree_from_values(dh, db, cfg.legs))
+        return np.array(out, dtype=np.float64).reshape(-1, 3, 5)
+
     def sequential_from_values(self, d_hat, d_bar):
         d_hat = np.ascontiguousarray(d_hat, dtype=np.float64)
         d_bar = np.ascontiguousarray(d_bar, dtype=np.float64)

@@ -657,3 +657,20 @@ void orc_sequential_from_values(const double* d_hat, const double* d_bar, uint64
     for (int k = 0; k < 3; ++k) orc_moments_merge(&out3[k], &acc[k]);
   }
 }
+
+/* Per-path differences (mlmc.hpp:86-90, payoff applied) for paths
+ * path_base .. path_base+n-1; legs not simulated give 0.  Returns the first
+ * failure kind (0 if none). */
+int orc_diffs(const orc_config* c, uint64_t path_base, uint64_t n, double* d_hat, double* d_bar) {
+  for (uint64_t i = 0; i < n; ++i) {
+    double r[4];
+    uint64_t st = 0;
+    const int f = orc_simulate_coupled(c, path_base + i, r, NULL, &st);
+    if (f != ORC_OK) return f;
+    double h, b;
+    diffs(c, r, &h, &b);
+    d_hat[i] = (c->legs & 1) ? h : 0.0;
+    d_bar[i] = (c->legs & 2) ? b : 0.0;
+  }
+  return ORC_OK;
+}

@@ -78,4 +78,5 @@ int orc_run_tree(const orc_config* c, uint64_t n, uint64_t path_base, orc_moment
 int orc_replay_hat(const orc_config* c, const double* z, double* out2);
 void orc_sequential_from_values(const double* d_hat, const double* d_bar, uint64_t n,
                                 orc_moments* out3);
+int orc_diffs(const orc_config* c, uint64_t path_base, uint64_t n, double* d_hat, double* d_bar);
 #endif

@@ -91,12 +91,14 @@ def full(path: str, path_steps: float | None) -> str:
         src = subprocess.run(["ncu", "-i", path, "--page", "source", "--csv", "--print-source",
                               "sass"], capture_output=True, text=True).stdout
         srows = list(csv.reader(io.StringIO(src)))
-        if len(srows) > 2 and path_steps:
-            sh = srows[1]
+        hdr = [i for i, r in enumerate(srows[:8]) if "Address" in r and "Source" in r]
+        if hdr and path_steps:
+            srows = srows[hdr[0]:]
+            sh = srows[0]
             iS, iE = sh.index("Source"), sh.index("Instructions Executed")
             iW = sh.index("Warp Stall Sampling (All Samples)")
             by, st = collections.Counter(), collections.Counter()
-            for r in srows[2:]:
+            for r in srows[1:]:
                 if len(r) <= iE:
                     continue
                 try:
