@@ -309,7 +309,7 @@ __device__ __forceinline__ double acklam_central(double v) {
 #pragma unroll
   for (int i = 1; i < 5; ++i) den = fmad(den, r, LPMC_K(kOffAckB + i));
   den = fmad(den, r, 1.0);
-  return (num * q) * rcp_refined(den);
+  return (num * q) * rcp_coarse(den);  // ~2^-44: x0 only needs ~1e-12
 }
 
 // Tail branch, v < 0.02425 (4.85% of draws).
@@ -322,7 +322,7 @@ __device__ __forceinline__ double acklam_tail(double v) {
 #pragma unroll
   for (int i = 1; i < 4; ++i) den = fmad(den, q, LPMC_K(kOffAckD + i));
   den = fmad(den, q, 1.0);
-  return num * rcp_refined(den);
+  return num * rcp_coarse(den);
 }
 
 // The Newton step of gaussian.hpp:52-53, x0 - (Phi(x0) - v) / pdf(x0), with
@@ -339,11 +339,14 @@ __device__ __forceinline__ double newton_fast(double x0, double v, const double*
   const double tl = fmad(t, t, -th);
   const ExpSplit e = exp_neg(th, tl, mtab);
   const double pg = e.p * erfcx_piecewise(t, mtab);
-  const double cdf = scale(pg, e.k - 1);  // 0.5 erfc(t)
-  const double resid = cdf - v;
-  // 1/pdf(x0) = sqrt(2 pi) exp(t^2) = sqrt(2 pi) 2^-k / p
-  const double inv_pdf = scale(LPMC_K(kSqrt2Pi) * rcp_coarse(e.p), -e.k);
-  return x0 - resid * inv_pdf;
+  // resid = 0.5 erfc(t) - v = 2^k (pg/2 - v 2^-k); 1/pdf(x0) = sqrt(2 pi)
+  // exp(t^2) = 2^-k sqrt(2 pi) / p.  Both power-of-two factors cancel, and
+  // power-of-two scaling commutes with rounding, so this is bitwise
+  // x0 - RN(RN(cdf - v) RN(sqrt(2 pi) 2^-k / p)) with two fewer FP64 ops.
+  // v 2^-k: an exponent add (v is normal: v >= 2^-54, |k| <= 62).
+  const double v_k = from_bits(bits(v) - (static_cast<uint64_t>(static_cast<int64_t>(e.k)) << 52));
+  const double resid_k = fmad(pg, 0.5, -v_k);
+  return x0 - resid_k * (LPMC_K(kSqrt2Pi) * rcp_coarse(e.p));
 }
 
 // exact_inv_cdf (gaussian.hpp:59-65) for D independent draws of one thread.
