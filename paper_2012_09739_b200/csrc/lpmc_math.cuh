@@ -309,7 +309,7 @@ __device__ __forceinline__ double acklam_central(double v) {
 #pragma unroll
   for (int i = 1; i < 5; ++i) den = fmad(den, r, LPMC_K(kOffAckB + i));
   den = fmad(den, r, 1.0);
-  return (num * q) * rcp_coarse(den);  // ~2^-44: x0 only needs ~1e-12
+  return (num * q) * rcp_refined(den);
 }
 
 // Tail branch, v < 0.02425 (4.85% of draws).
@@ -322,7 +322,7 @@ __device__ __forceinline__ double acklam_tail(double v) {
 #pragma unroll
   for (int i = 1; i < 4; ++i) den = fmad(den, q, LPMC_K(kOffAckD + i));
   den = fmad(den, q, 1.0);
-  return num * rcp_coarse(den);
+  return num * rcp_refined(den);
 }
 
 // The Newton step of gaussian.hpp:52-53, x0 - (Phi(x0) - v) / pdf(x0), with
