@@ -48,16 +48,20 @@ __device__ __forceinline__ uint64_t path_key(uint64_t seed_key, uint64_t path) {
   return mix64(seed_key ^ mix64(path + 0xbf58476d1ce4e5b9ull));
 }
 
-// u = (w >> 11) 2^-53 + 2^-54 with w = mix64(mix64(key + ctr c3)); the
-// running kc = key + ctr c3 is strength-reduced (uniform.hpp:25, :38-41).
-// top: the draw rounds to u == 1 (the reference throws, gaussian.hpp:60);
-// half: it rounds to exactly u == 1/2 (both transforms return exactly 0).
-__device__ __forceinline__ double next_uniform(uint64_t& kc, bool& top, bool& half) {
+// The draw b = w >> 11 of u = b 2^-53 + 2^-54 with w = mix64(mix64(key + ctr
+// c3)); the running kc = key + ctr c3 is strength-reduced (uniform.hpp:25,
+// :38-41).  The hot loop keeps b, not u: everything the transforms take
+// from u is derived from it; the half-plane tests are then integer compares
+// on its high word instead of FP64 compares.
+// b == kTopDraw: u rounds to 1 (the reference throws, gaussian.hpp:60);
+// b == kHalfDraw: u rounds to exactly 1/2 (both transforms return exactly 0).
+__device__ __forceinline__ uint64_t next_draw(uint64_t& kc) {
   const uint64_t w = mix64(mix64(kc));
   kc += 0x94d049bb133111ebull;
-  const uint64_t b = w >> 11;
-  top = b == kTopDraw;
-  half = b == kHalfDraw;
+  return w >> 11;
+}
+
+__device__ __forceinline__ double uniform_of(uint64_t b) {
   return __dadd_rn(__dmul_rn(__ull2double_rn(b), 0x1p-53), 0x1p-54);
 }
 
@@ -68,8 +72,9 @@ __device__ __forceinline__ void stage_math(double* s_math) {
 
 // ------------------------------------------- approximate inverse CDF -------
 // Shared-memory table.  Dyadic layout (K <= 32): one 6-double record per
-// interval {a_j, 2^(j+2), c0, c1, c2, c3} (128-bit loads).  General layout:
-// kTableRows rows of `stride` = K doubles: a_j, b_j - a_j, c0..c3, v-thresholds.
+// interval {3 - 2^(j+3), 2^(j+3), c0, c1, c2, c3} (128-bit loads).  General
+// layout: kTableRows rows of `stride` = K doubles: a_j, b_j - a_j, c0..c3,
+// v-thresholds.
 struct TableView {
   const double* base;
   int stride, K, degree, dyadic, simple;
@@ -79,17 +84,20 @@ struct TableView {
 // InvCdfApprox::operator() (invcdf_approx.hpp:44-90).
 //  * dyadic tables (K <= 32, w_max = K+1): the reference's j = floor(-log2 v)
 //    - 1 read from the exponent of v = 1 - u' (exact on the 2^-53 grid,
-//    SURVEY.md §A3); u' in [a_j, b_j) so t in [-1, 1) and the reference's
-//    clamps are no-ops; 2(u'-a)/(b-a) = 2(u'-a) 2^(j+2) exactly.
+//    SURVEY.md §A3); u' in [a_j, b_j) with a_j = 1 - 2^-(j+1), b_j - a_j =
+//    2^-(j+2), so t in [-1, 1) and the reference's clamps are no-ops.  Its
+//    t = RN(2 (u' - a_j) / (b_j - a_j) - 1) has only that last rounding
+//    (u' - a_j is exact by Sterbenz, the rest are powers of two), and the
+//    exact value is u' 2^(j+3) - (2^(j+3) - 3): one FMA, bitwise equal.
 //  * general K: index from host thresholds that reproduce the reference's
 //    log2-based index on every representable v; division and clamps as the
 //    reference.
 //  * `simple` (host-proved: every c0 != 0 and c2 = c3 = +0): the reference's
 //    (c0 + c1 t) + 0 p2 + 0 p3 equals c0 + c1 t including the sign of zero.
+//  * lower: u < 1/2 (the sampler passes the integer test on its draw).
 //  * EXACT_HALF: exactly 0 at u = 1/2; the hot loop replays such draws.
 template <bool EXACT_HALF = true>
-__device__ __forceinline__ double approx_inv(const TableView& t, double u) {
-  const bool lower = u < 0.5;
+__device__ __forceinline__ double approx_inv(const TableView& t, double u, bool lower) {
   const double up = lower ? 1.0 - u : u;  // fl(1-u) for the lower half (:47-49)
   const double v = 1.0 - up;              // exact (Sterbenz)
   double r;
@@ -99,9 +107,9 @@ __device__ __forceinline__ double approx_inv(const TableView& t, double u) {
     const int fl = (vb & 0xFFFFFFFFFFFFFull) == 0 ? -e : -e - 1;  // floor(-log2 v) >= 1
     const int j = min(fl - 1, t.K - 1);
     const double* b = t.base + 6 * j;
-    const math::D2 aw = math::load2(b);
+    const math::D2 cw = math::load2(b);
     const math::D2 c01 = math::load2(b + 2);
-    const double s = __dsub_rn(__dmul_rn(__dmul_rn(2.0, __dsub_rn(up, aw.a)), aw.b), 1.0);
+    const double s = __fma_rn(up, cw.b, cw.a);
     r = __dadd_rn(c01.a, __dmul_rn(c01.b, s));
     if (t.degree == 3 || (!t.simple && r == 0.0)) {
       const math::D2 c23 = math::load2(b + 4);
@@ -135,6 +143,16 @@ __device__ __forceinline__ double approx_inv(const TableView& t, double u) {
   r = lower ? -r : r;
   if constexpr (EXACT_HALF) r = u == 0.5 ? 0.0 : r;
   return r;
+}
+
+template <bool EXACT_HALF = true>
+__device__ __forceinline__ double approx_inv(const TableView& t, double u) {
+  return approx_inv<EXACT_HALF>(t, u, u < 0.5);
+}
+
+// u < 1/2 <=> b < 2^52 <=> high word < 2^20
+__device__ __forceinline__ bool draw_lower(uint64_t b) {
+  return static_cast<uint32_t>(b >> 32) < (1u << 20);
 }
 
 // ----------------------------------------------- rounding helpers ---------

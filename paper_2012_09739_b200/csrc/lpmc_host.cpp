@@ -227,7 +227,7 @@ lpmc_status prepare_table(const lpmc_invcdf_table* t, HostTable* out, lpmc_error
   out->K = K;
   out->degree = t->kind == LPMC_APPROX_CUBIC ? 3 : 1;
   out->tail = t->tail_value;
-  bool dyadic = t->step_w == 1.0 && t->w_max == static_cast<double>(K + 1);
+  bool dyadic = K <= 32 && t->step_w == 1.0 && t->w_max == static_cast<double>(K + 1);
   for (int j = 0; dyadic && j < K; ++j) dyadic = t->breakpoints[j] == 1.0 - std::ldexp(1.0, -(j + 2));
   out->dyadic = dyadic ? 1 : 0;
   out->stride = K;
@@ -240,12 +240,12 @@ lpmc_status prepare_table(const lpmc_invcdf_table* t, HostTable* out, lpmc_error
   }
   out->simple = simple ? 1 : 0;
   auto left = [&](int j) { return j == 0 ? 0.5 : t->breakpoints[j - 1]; };
-  if (dyadic) {  // records {a, 2^(j+2), c0, c1, c2, c3}
+  if (dyadic) {  // records {3 - 2^(j+3), 2^(j+3), c0, c1, c2, c3} (dev::approx_inv)
     out->rows.assign(static_cast<size_t>(kDyadicRecord) * K, 0.0);
     for (int j = 0; j < K; ++j) {
       double* r = out->rows.data() + kDyadicRecord * j;
-      r[0] = left(j);
-      r[1] = std::ldexp(1.0, j + 2);
+      r[0] = 3.0 - std::ldexp(1.0, j + 3);
+      r[1] = std::ldexp(1.0, j + 3);
       for (int c = 0; c < 4; ++c) r[2 + c] = t->coeff[4 * j + c];
     }
   } else {  // rows of K

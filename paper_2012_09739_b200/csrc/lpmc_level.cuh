@@ -34,7 +34,7 @@ __device__ __forceinline__ void note_fail(uint64_t& fk, bool bad, uint64_t n, ui
 }
 
 // Uniforms of H draws x NP paths (draw-major), with their u == 1 bits (top)
-// and u == 1/2 bits (half).
+// and u == 1/2 bits (half), read off the integer draws.
 template <int D>
 struct Uniforms {
   double u[D];
@@ -49,10 +49,11 @@ __device__ __forceinline__ void draw_uniforms(uint64_t (&kc)[NP], Uniforms<H * N
   for (int h = 0; h < H; ++h)
 #pragma unroll
     for (int p = 0; p < NP; ++p) {
-      bool top, half;
-      U.u[h * NP + p] = next_uniform(kc[p], top, half);
-      U.top |= (top ? 1u : 0u) << (h * NP + p);
-      U.half |= (half ? 1u : 0u) << (h * NP + p);
+      const uint64_t b = next_draw(kc[p]);
+      const int d = h * NP + p;
+      U.u[d] = uniform_of(b);
+      U.top |= (b == kTopDraw ? 1u : 0u) << d;
+      U.half |= (b == kHalfDraw ? 1u : 0u) << d;
     }
 }
 
@@ -91,9 +92,16 @@ __device__ __forceinline__ void gen_draws(const LevelArgs& A, const TableView& t
   double zz[D];
   if constexpr (NEED_EXACT) {
     double v[D], x0[D];
-    math::phi_inv_stage1<D>(u, v, x0);
+    uint32_t neg = 0;
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+      const bool ng = u[d] > 0.5;
+      v[d] = ng ? 1.0 - u[d] : u[d];  // exact (gaussian.hpp:63)
+      neg |= (ng ? 1u : 0u) << d;
+    }
+    math::phi_inv_stage1<D>(v, x0);
     if constexpr (PREFETCH) draw_uniforms<NP, H>(kc, next);
-    math::phi_inv_stage2<D, CHECKED>(u, v, x0, zz, s_math);
+    math::phi_inv_stage2<D, CHECKED>(v, x0, neg, cur.half, zz, s_math);
   } else {
     if constexpr (PREFETCH) draw_uniforms<NP, H>(kc, next);
 #pragma unroll

@@ -354,14 +354,13 @@ __device__ __forceinline__ double newton_fast(double x0, double v, const double*
 // runs in warp-uniform passes, one pending tail draw per lane per pass, so a
 // warp pays for it about once per coarse step instead of once per draw with
 // one lane active.  Must be called by every active lane of the warp.
-// Stage 1: reflection and Acklam x0 (central for all, tail pass for the rest).
+// Stage 1: Acklam x0 of the reflected v = min(u, 1 - u) (gaussian.hpp:63)
+// (central for all, tail pass for the rest).
 template <int D>
-__device__ __forceinline__ void phi_inv_stage1(const double (&u)[D], double (&v)[D],
-                                               double (&x0)[D]) {
+__device__ __forceinline__ void phi_inv_stage1(const double (&v)[D], double (&x0)[D]) {
   uint32_t pend = 0;
 #pragma unroll
   for (int d = 0; d < D; ++d) {
-    v[d] = u[d] > 0.5 ? 1.0 - u[d] : u[d];  // exact (gaussian.hpp:63)
     x0[d] = acklam_central(v[d]);
     if (v[d] < LPMC_K(kTailU)) pend |= 1u << d;
   }
@@ -386,13 +385,14 @@ static __device__ __noinline__ double phi_inv_lower_slow(double v) {
   return phi_inv_lower_libdevice(v);
 }
 
-// Stage 2: the Newton step, libdevice fix-up of out-of-range draws, sign.
-// EXACT_HALF: return exactly 0 for u == 1/2 (gaussian.hpp:62).  The hot loop
-// instead flags such a draw (probability 2^-53) and has the path replayed
-// with EXACT_HALF, which keeps two selects per draw out of the loop.
+// Stage 2: the Newton step, libdevice fix-up of out-of-range draws, sign
+// (bit d of `neg`: u > 1/2).  EXACT_HALF: exactly 0 where bit d of `half`
+// (u == 1/2, gaussian.hpp:62).  The hot loop instead flags such a draw
+// (probability 2^-53) and has the path replayed with EXACT_HALF, which keeps
+// two selects per draw out of the loop.
 template <int D, bool EXACT_HALF = true>
-__device__ __forceinline__ void phi_inv_stage2(const double (&u)[D], const double (&v)[D],
-                                               const double (&x0)[D], double (&z)[D],
+__device__ __forceinline__ void phi_inv_stage2(const double (&v)[D], const double (&x0)[D],
+                                               uint32_t neg, uint32_t half, double (&z)[D],
                                                const double* mtab) {
   bool slow[D];
 #pragma unroll
@@ -400,21 +400,30 @@ __device__ __forceinline__ void phi_inv_stage2(const double (&u)[D], const doubl
 #pragma unroll
   for (int d = 0; d < D; ++d) {
     if (slow[d]) z[d] = phi_inv_lower_slow(v[d]);
-    const double r = u[d] > 0.5 ? -z[d] : z[d];
+    const double r = (neg >> d) & 1u ? -z[d] : z[d];
     if constexpr (EXACT_HALF) {
-      z[d] = u[d] == 0.5 ? 0.0 : r;
+      z[d] = (half >> d) & 1u ? 0.0 : r;
     } else {
       z[d] = r;
     }
   }
 }
 
+// exact_inv_cdf for D arbitrary u (diagnostics; the sampler reflects from
+// its integer draws, dev::draw_reflect).
 template <int D>
 __device__ __forceinline__ void phi_inv_multi(const double (&u)[D], double (&z)[D],
                                               const double* mtab) {
   double v[D], x0[D];
-  phi_inv_stage1<D>(u, v, x0);
-  phi_inv_stage2<D, true>(u, v, x0, z, mtab);
+  uint32_t neg = 0, half = 0;
+#pragma unroll
+  for (int d = 0; d < D; ++d) {
+    v[d] = u[d] > 0.5 ? 1.0 - u[d] : u[d];  // exact (gaussian.hpp:63)
+    neg |= (u[d] > 0.5 ? 1u : 0u) << d;
+    half |= (u[d] == 0.5 ? 1u : 0u) << d;
+  }
+  phi_inv_stage1<D>(v, x0);
+  phi_inv_stage2<D, true>(v, x0, neg, half, z, mtab);
 }
 
 // The same with the reference's formula on libdevice (diagnostics only).
