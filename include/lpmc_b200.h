@@ -19,6 +19,16 @@
  *   lpmc_level_partials +       <- the batch loop + index-order merge of
  *   lpmc_fold_partials             run_coupled_paths (mlmc.hpp:74-110), split
  *                                  so paths can be sharded over GPUs/ranks
+ *   lpmc_run_coupled_many       <- a loop of run_coupled_paths calls (the
+ *                                  callers: mlmc.hpp:254-278,
+ *                                  experiments.hpp:126-143, :185-194), run
+ *                                  concurrently on one device
+ *   lpmc_run_two_way_paths      <- run_batched(simulate_two_way) (experiments.hpp:136-141,
+ *                                  sde.hpp:162-196)
+ *   lpmc_allocate_samples       <- allocate_samples        include/lpmc/mlmc.hpp:165-195
+ *   lpmc_predicted_times        <- predicted_times         include/lpmc/mlmc.hpp:202-213
+ *   lpmc_per_level_speedup      <- per_level_speedup       include/lpmc/mlmc.hpp:223-230
+ *   lpmc_run_nested_estimator   <- run_nested_estimator    include/lpmc/mlmc.hpp:244-283
  *
  * Error contract: every entry point returns an lpmc_status.  The values map
  * one-to-one onto the exception types the reference throws
@@ -105,7 +115,14 @@ typedef struct lpmc_precision {
 enum {
   LPMC_LEGS_HAT = 1, /* carrier legs, exact Gaussians: d_hat only */
   LPMC_LEGS_BAR = 2, /* low-precision legs: d_bar only            */
-  LPMC_LEGS_ALL = 3  /* all four legs (the reference always runs these) */
+  LPMC_LEGS_ALL = 3, /* all four legs (the reference always runs these) */
+  /*
+   * Fine legs only = simulate_two_way (sde.hpp:162-196): the carrier and
+   * the low-precision path at the same level, no coarse legs.  The three
+   * accumulators then hold x_hat, x_bar and x_hat - x_bar (the two-way
+   * experiment's quantity, experiments.hpp:136-141).
+   */
+  LPMC_LEGS_FINE = 4
 };
 
 enum {
@@ -264,6 +281,85 @@ lpmc_status lpmc_device_math(int32_t op, const double* in, uint64_t n,
                              const lpmc_options* opts, lpmc_error* err);
 /* Host evaluation of the same erfc core (bitwise equal to op 3). */
 double lpmc_erfc_core(double t);
+
+/* ---- callers of the level sampler (mlmc.hpp:151-285) --------------------- */
+/* One run of a multi-run call. */
+typedef struct lpmc_run_desc {
+  int32_t level;
+  lpmc_precision prec;
+  int32_t kahan;
+  uint64_t n_paths;
+  uint64_t path_base;
+} lpmc_run_desc;
+
+/*
+ * n_runs run_coupled_paths calls sharing model, table, seed and options,
+ * executed concurrently on one device (one stream per run, up to 16 in
+ * flight; small levels overlap instead of serialising behind host syncs).
+ * out: 3 accumulators per run, run-major.  Results are exactly those of the
+ * separate calls; the first failing run in list order is reported, as a
+ * serial loop would throw it.  opts->stream, if set, is waited on before
+ * the runs start.  Blocking.
+ */
+lpmc_status lpmc_run_coupled_many(const lpmc_gbm* model, const lpmc_invcdf_table* table,
+                                  uint64_t seed, const lpmc_run_desc* runs, uint64_t n_runs,
+                                  const lpmc_options* opts, lpmc_moments* out, lpmc_error* err);
+
+/*
+ * The two-way sampler: MomentAccumulator of x_hat - x_bar over n_paths
+ * simulate_two_way paths (sde.hpp:162-196), batched and merged like
+ * run_batched (experiments.hpp:89-112).  out: 1 accumulator.
+ */
+lpmc_status lpmc_run_two_way_paths(const lpmc_gbm* model, int32_t level,
+                                   const lpmc_precision* prec, const lpmc_invcdf_table* table,
+                                   int32_t kahan, uint64_t n_paths, uint64_t seed,
+                                   uint64_t path_base, const lpmc_options* opts,
+                                   lpmc_moments* out, lpmc_error* err);
+
+enum { LPMC_ALLOCATION_STANDARD = 0, LPMC_ALLOCATION_NESTED = 1 }; /* AllocationKind */
+
+/*
+ * allocate_samples (mlmc.hpp:165-195), bitwise: primary[n_levels];
+ * secondary[n_levels] for the nested kind (may be NULL for standard);
+ * *degenerate = every variance was zero.
+ */
+lpmc_status lpmc_allocate_samples(const lpmc_level_stats* stats, uint64_t n_levels, double eps,
+                                  int32_t kind, uint64_t* primary, uint64_t* secondary,
+                                  int32_t* degenerate, lpmc_error* err);
+/* predicted_times (mlmc.hpp:202-213), bitwise. */
+lpmc_status lpmc_predicted_times(const lpmc_level_stats* stats, uint64_t n_levels, double eps,
+                                 double* t_hat, double* t_bar, lpmc_error* err);
+/* per_level_speedup (mlmc.hpp:223-230), bitwise. */
+lpmc_status lpmc_per_level_speedup(const lpmc_level_stats* stats, double* value,
+                                   int32_t* cost_ratio_only, lpmc_error* err);
+
+/* EstimatorResult (mlmc.hpp:232-239); the arrays are caller-owned with
+ * max_level + 1 entries each (any may be NULL). */
+typedef struct lpmc_estimator_result {
+  double value; /* theta_bar */
+  double eps;
+  double t_hat, t_bar;  /* predicted_times of the pilot stats */
+  int32_t degenerate;   /* Allocation::degenerate */
+  double* level_contributions;
+  lpmc_level_stats* pilot_stats;
+  uint64_t* primary;   /* Allocation::primary */
+  uint64_t* secondary; /* Allocation::secondary */
+} lpmc_estimator_result;
+
+/*
+ * run_nested_estimator (mlmc.hpp:244-283): pilot estimate_level_stats of
+ * pilot_paths per level (path base l << 40), nested allocation, then per
+ * level a two-way pass (phase 1, primary[l] paths) and a four-way pass
+ * (phase 2, secondary[l]); contribution_l = two_way.d_bar.mean() +
+ * (four_way.d_hat.mean() - four_way.d_bar.mean()).  Each pass runs all its
+ * levels concurrently (lpmc_run_coupled_many).  cost may be NULL.
+ */
+lpmc_status lpmc_run_nested_estimator(const lpmc_gbm* model, int32_t max_level,
+                                      const lpmc_precision* prec,
+                                      const lpmc_invcdf_table* table, int32_t kahan, double eps,
+                                      uint64_t seed, const lpmc_cost_model* cost,
+                                      uint64_t pilot_paths, const lpmc_options* opts,
+                                      lpmc_estimator_result* out, lpmc_error* err);
 
 /* ---- plans: device-resident repeated launches (bench / sweeps) ---------- */
 typedef struct lpmc_plan lpmc_plan;

@@ -306,6 +306,21 @@ class Reference:
         L.ref_moments_add.argtypes = [_dp, _u64, _dp]
         L.ref_moments_merge.argtypes = [_dp, _dp, _dp]
         L.ref_hardware_threads.restype = C.c_int
+        _pu = C.POINTER(_u64)
+        _pi = C.POINTER(C.c_int)
+        L.ref_allocate_samples.argtypes = [_dp, _u64, C.c_double, C.c_int, _pu, _pu, _pi,
+                                           C.c_char_p, C.c_int]
+        L.ref_predicted_times.argtypes = [_dp, _u64, C.c_double, _dp, C.c_char_p, C.c_int]
+        L.ref_per_level_speedup.argtypes = [_dp, _dp, _pi, C.c_char_p, C.c_int]
+        L.ref_run_nested_estimator.argtypes = [C.c_double] * 4 + [
+            C.c_int, C.c_int, C.c_char_p, C.c_int, C.c_double, _u64, _u64, C.c_int, _dp, _dp,
+            _dp, _pu, _pu, C.c_char_p, C.c_int]
+        L.ref_simulate_two_way.argtypes = [C.c_double] * 4 + [C.c_int, C.c_int, C.c_char_p,
+                                                              C.c_int, _u64, _u64, _u64, _dp,
+                                                              C.c_char_p, C.c_int]
+        L.ref_two_way_experiment.argtypes = [C.c_double] * 4 + [
+            C.c_char_p, C.c_char_p, C.c_int, C.c_int, C.c_int, _u64, _u64, C.c_int, _dp,
+            C.c_char_p, C.c_int]
 
     def _err(self, rc, msg):
         if rc:
@@ -388,3 +403,82 @@ class Reference:
 
     def hardware_threads(self) -> int:
         return int(self.lib.ref_hardware_threads())
+
+    # --------------------------------------- callers (mlmc.hpp:151-285) ----
+    STATS_FIELDS = ("mean_hat", "v_hat", "v_hat_stderr", "mean_bar", "v_bar", "v_bar_stderr",
+                    "mean_four", "V_bar", "V_bar_stderr", "c_hat", "c_bar", "C_bar", "m_hat",
+                    "m_bar", "M_bar", "level")
+
+    @staticmethod
+    def _stats16(stats) -> np.ndarray:
+        """LevelStats-like objects or dicts -> n x 16 doubles."""
+        rows = []
+        for st in stats:
+            get = st.get if isinstance(st, dict) else (lambda k, st=st: getattr(st, k))
+            rows.append([float(get(k)) for k in Reference.STATS_FIELDS])
+        return np.ascontiguousarray(np.array(rows, dtype=np.float64).reshape(-1, 16))
+
+    def allocate_samples(self, stats, eps, kind):
+        a = self._stats16(stats)
+        n = a.shape[0]
+        prim = (C.c_uint64 * max(1, n))()
+        sec = (C.c_uint64 * max(1, n))()
+        deg = C.c_int()
+        msg = C.create_string_buffer(256)
+        rc = self.lib.ref_allocate_samples(_ptr(a), n, eps, int(kind), prim, sec, C.byref(deg),
+                                           msg, 256)
+        return rc, msg.value.decode(), ([int(x) for x in prim[:n]], [int(x) for x in sec[:n]],
+                                        bool(deg.value))
+
+    def predicted_times(self, stats, eps):
+        a = self._stats16(stats)
+        out = np.zeros(2)
+        msg = C.create_string_buffer(256)
+        rc = self.lib.ref_predicted_times(_ptr(a), a.shape[0], eps, _ptr(out), msg, 256)
+        return rc, msg.value.decode(), (out[0], out[1])
+
+    def per_level_speedup(self, st):
+        a = self._stats16([st])
+        v = C.c_double()
+        flag = C.c_int()
+        msg = C.create_string_buffer(256)
+        rc = self.lib.ref_per_level_speedup(_ptr(a), C.byref(v), C.byref(flag), msg, 256)
+        return rc, msg.value.decode(), (v.value, bool(flag.value))
+
+    def run_nested_estimator(self, *, max_level, mantissa_bits, approx="exact", kahan=False,
+                             eps=1e-2, seed=1, pilot_paths=1000, threads=1, mu=0.05, sigma=0.2,
+                             x0=1.0, horizon=1.0):
+        L = max(0, max_level) + 1
+        out4 = np.zeros(4)
+        contrib = np.zeros(L)
+        pilot = np.zeros(16 * L)
+        prim = (C.c_uint64 * L)()
+        sec = (C.c_uint64 * L)()
+        msg = C.create_string_buffer(256)
+        rc = self.lib.ref_run_nested_estimator(mu, sigma, x0, horizon, max_level, mantissa_bits,
+                                               approx.encode(), int(kahan), eps, seed,
+                                               pilot_paths, threads, _ptr(out4), _ptr(contrib),
+                                               _ptr(pilot), prim, sec, msg, 256)
+        return rc, msg.value.decode(), {
+            "value": out4[0], "t_hat": out4[1], "t_bar": out4[2], "degenerate": bool(out4[3]),
+            "contributions": contrib, "pilot": pilot.reshape(L, 16),
+            "primary": [int(x) for x in prim], "secondary": [int(x) for x in sec]}
+
+    def simulate_two_way(self, *, level, mantissa_bits, approx="exact", kahan=False, seed=1,
+                         path_base=0, n=1, mu=0.05, sigma=0.2, x0=1.0, horizon=1.0):
+        out = np.zeros((n, 2))
+        msg = C.create_string_buffer(256)
+        rc = self.lib.ref_simulate_two_way(mu, sigma, x0, horizon, level, mantissa_bits,
+                                           approx.encode(), int(kahan), seed, path_base, n,
+                                           _ptr(out), msg, 256)
+        return rc, msg.value.decode(), out
+
+    def two_way_experiment(self, *, precision, approx, kahan, level_min, level_max, paths,
+                           seed=1, threads=1, mu=0.05, sigma=0.2, x0=1.0, horizon=1.0):
+        rows = level_max - level_min + 1
+        out = np.zeros(4 * max(rows, 1))
+        msg = C.create_string_buffer(256)
+        rc = self.lib.ref_two_way_experiment(mu, sigma, x0, horizon, precision.encode(),
+                                             approx.encode(), int(kahan), level_min, level_max,
+                                             paths, seed, threads, _ptr(out), msg, 256)
+        return rc, msg.value.decode(), out[:4 * rows].reshape(rows, 4)

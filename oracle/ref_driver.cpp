@@ -29,6 +29,7 @@
 #include <vector>
 
 #define private public
+#include "lpmc/experiments.hpp"
 #include "lpmc/gaussian.hpp"
 #include "lpmc/invcdf_approx.hpp"
 #include "lpmc/mlmc.hpp"
@@ -244,6 +245,147 @@ void ref_moments_merge(const double* a5, const double* b5, double* out5) {
   b.m4_ = b5[4];
   a.merge(b);
   dump_acc(a, out5);
+}
+
+// LevelStats <-> 16 doubles, the ref_estimate_level_stats order.
+static lpmc::LevelStats stats_from16(const double* v) {
+  lpmc::LevelStats s;
+  s.mean_hat = v[0];
+  s.v_hat = v[1];
+  s.v_hat_stderr = v[2];
+  s.mean_bar = v[3];
+  s.v_bar = v[4];
+  s.v_bar_stderr = v[5];
+  s.mean_four = v[6];
+  s.V_bar = v[7];
+  s.V_bar_stderr = v[8];
+  s.c_hat = v[9];
+  s.c_bar = v[10];
+  s.C_bar = v[11];
+  s.m_hat = static_cast<uint64_t>(v[12]);
+  s.m_bar = static_cast<uint64_t>(v[13]);
+  s.M_bar = static_cast<uint64_t>(v[14]);
+  s.level = static_cast<int>(v[15]);
+  return s;
+}
+
+static void stats_to16(const lpmc::LevelStats& s, double* out) {
+  const double v[16] = {s.mean_hat, s.v_hat, s.v_hat_stderr, s.mean_bar, s.v_bar,
+                        s.v_bar_stderr, s.mean_four, s.V_bar, s.V_bar_stderr, s.c_hat,
+                        s.c_bar, s.C_bar, static_cast<double>(s.m_hat),
+                        static_cast<double>(s.m_bar), static_cast<double>(s.M_bar),
+                        static_cast<double>(s.level)};
+  std::memcpy(out, v, sizeof v);
+}
+
+// allocate_samples (mlmc.hpp:165): stats16 = n x 16 doubles; kind 0/1.
+int ref_allocate_samples(const double* stats16, uint64_t n, double eps, int kind,
+                         uint64_t* primary, uint64_t* secondary, int* degenerate, char* msg,
+                         int len) {
+  return guarded(msg, len, [&] {
+    std::vector<lpmc::LevelStats> st;
+    for (uint64_t i = 0; i < n; ++i) st.push_back(stats_from16(stats16 + 16 * i));
+    lpmc::Allocation a = lpmc::allocate_samples(
+        st, eps, kind ? lpmc::AllocationKind::nested : lpmc::AllocationKind::standard);
+    for (size_t i = 0; i < a.primary.size(); ++i) primary[i] = a.primary[i];
+    for (size_t i = 0; i < a.secondary.size(); ++i) secondary[i] = a.secondary[i];
+    *degenerate = a.degenerate ? 1 : 0;
+  });
+}
+
+int ref_predicted_times(const double* stats16, uint64_t n, double eps, double* out2, char* msg,
+                        int len) {
+  return guarded(msg, len, [&] {
+    std::vector<lpmc::LevelStats> st;
+    for (uint64_t i = 0; i < n; ++i) st.push_back(stats_from16(stats16 + 16 * i));
+    lpmc::PredictedTimes t = lpmc::predicted_times(st, eps);
+    out2[0] = t.t_hat;
+    out2[1] = t.t_bar;
+  });
+}
+
+int ref_per_level_speedup(const double* stats16, double* value, int* cost_ratio_only, char* msg,
+                          int len) {
+  return guarded(msg, len, [&] {
+    lpmc::SpeedupResult r = lpmc::per_level_speedup(stats_from16(stats16));
+    *value = r.value;
+    *cost_ratio_only = r.cost_ratio_only ? 1 : 0;
+  });
+}
+
+// run_nested_estimator (mlmc.hpp:244): out = {value, t_hat, t_bar, degenerate};
+// contributions[L+1], pilot16[(L+1) x 16], primary[L+1], secondary[L+1].
+int ref_run_nested_estimator(double mu, double sigma, double x0, double horizon, int max_level,
+                             int mantissa_bits, const char* approx, int kahan, double eps,
+                             uint64_t seed, uint64_t pilot_paths, int threads, double* out4,
+                             double* contributions, double* pilot16, uint64_t* primary,
+                             uint64_t* secondary, char* msg, int len) {
+  return guarded(msg, len, [&] {
+    const lpmc::SdeModel model = lpmc::make_gbm(mu, sigma, x0, horizon);
+    const lpmc::InvCdfApprox* t = table_for(approx);
+    lpmc::EstimatorResult r = lpmc::run_nested_estimator(
+        model, max_level, lpmc::PrecisionSpec{mantissa_bits}, t, kahan != 0, eps, seed,
+        lpmc::CostModel{}, threads, pilot_paths);
+    out4[0] = r.value;
+    out4[1] = r.times.t_hat;
+    out4[2] = r.times.t_bar;
+    out4[3] = r.allocation.degenerate ? 1.0 : 0.0;
+    for (size_t l = 0; l < r.level_contributions.size(); ++l) {
+      contributions[l] = r.level_contributions[l];
+      stats_to16(r.pilot_stats[l], pilot16 + 16 * l);
+      primary[l] = r.allocation.primary[l];
+      secondary[l] = r.allocation.secondary[l];
+    }
+  });
+}
+
+// simulate_two_way (sde.hpp:168) for n consecutive paths: out n x 2 (x_hat, x_bar).
+int ref_simulate_two_way(double mu, double sigma, double x0, double horizon, int level,
+                         int mantissa_bits, const char* approx, int kahan, uint64_t seed,
+                         uint64_t path_base, uint64_t n, double* out, char* msg, int len) {
+  return guarded(msg, len, [&] {
+    const lpmc::SdeModel model = lpmc::make_gbm(mu, sigma, x0, horizon);
+    const lpmc::InvCdfApprox* t = table_for(approx);
+    const lpmc::LevelSpec ls{level, horizon};
+    for (uint64_t i = 0; i < n; ++i) {
+      lpmc::TwoWayResult r = lpmc::simulate_two_way(model, ls, lpmc::PrecisionSpec{mantissa_bits},
+                                                    t, kahan != 0,
+                                                    lpmc::UniformStream(seed, path_base + i));
+      out[2 * i] = r.x_hat;
+      out[2 * i + 1] = r.x_bar;
+    }
+  });
+}
+
+// run_two_way_experiment (experiments.hpp:119) for one precision name and a
+// level range, paths per level broadcast; out = rows x {n_steps, variance,
+// stderr, paths}.
+int ref_two_way_experiment(double mu, double sigma, double x0, double horizon,
+                           const char* precision, const char* approx, int kahan, int level_min,
+                           int level_max, uint64_t paths, uint64_t seed, int threads,
+                           double* out4, char* msg, int len) {
+  return guarded(msg, len, [&] {
+    lpmc::ExperimentConfig c;
+    c.mu = mu;
+    c.sigma = sigma;
+    c.x0 = x0;
+    c.horizon = horizon;
+    c.precisions = {precision};
+    c.approx = approx;
+    c.kahan = kahan != 0;
+    c.level_min = level_min;
+    c.level_max = level_max;
+    if (paths) c.paths = {paths};
+    c.seed = seed;
+    c.threads = threads;
+    std::vector<lpmc::TwoWayRow> rows = lpmc::run_two_way_experiment(c);
+    for (size_t i = 0; i < rows.size(); ++i) {
+      out4[4 * i] = static_cast<double>(rows[i].n_steps);
+      out4[4 * i + 1] = rows[i].variance;
+      out4[4 * i + 2] = rows[i].stderr_variance;
+      out4[4 * i + 3] = static_cast<double>(rows[i].paths);
+    }
+  });
 }
 
 int ref_hardware_threads() { return static_cast<int>(std::thread::hardware_concurrency()); }

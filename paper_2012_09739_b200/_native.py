@@ -24,7 +24,8 @@ LPMC_RUNTIME_ERROR = 3
 LPMC_CUDA_ERROR = 4
 LPMC_NO_DEVICE = 5
 
-LEGS_HAT, LEGS_BAR, LEGS_ALL = 1, 2, 3
+LEGS_HAT, LEGS_BAR, LEGS_ALL, LEGS_FINE = 1, 2, 3, 4
+ALLOCATION_STANDARD, ALLOCATION_NESTED = 0, 1
 PAYOFF_TERMINAL, PAYOFF_CALL = 0, 1
 REDUCE_TREE, REDUCE_SEQUENTIAL = 0, 1
 APPROX_LINEAR, APPROX_CUBIC, APPROX_CONSTANT = 0, 1, 2
@@ -109,6 +110,18 @@ class LevelStatsC(C.Structure):
                 ("C_bar", C.c_double), ("m_hat", _u64), ("m_bar", _u64), ("M_bar", _u64)]
 
 
+class RunDesc(C.Structure):
+    _fields_ = [("level", _i32), ("prec", Precision), ("kahan", _i32), ("n_paths", _u64),
+                ("path_base", _u64)]
+
+
+class EstimatorResultC(C.Structure):
+    _fields_ = [("value", C.c_double), ("eps", C.c_double), ("t_hat", C.c_double),
+                ("t_bar", C.c_double), ("degenerate", _i32), ("level_contributions", _dp),
+                ("pilot_stats", C.POINTER(LevelStatsC)), ("primary", C.POINTER(_u64)),
+                ("secondary", C.POINTER(_u64))]
+
+
 # exported symbol -> (restype, argtypes); the CPU test suite checks every
 # symbol include/lpmc_b200.h declares is exported and bound here.
 _P = C.POINTER
@@ -141,6 +154,17 @@ SIGNATURES = {
     "lpmc_measure_pipe_peaks": (_i32, [_i32, _dp, _P(Error)]),
     "lpmc_device_math": (_i32, [_i32, _dp, _u64, _P(InvCdfTable), _dp, _P(Options), _P(Error)]),
     "lpmc_erfc_core": (C.c_double, [C.c_double]),
+    "lpmc_run_coupled_many": (_i32, [_P(Gbm), _P(InvCdfTable), _u64, _P(RunDesc), _u64,
+                                     _P(Options), _P(Moments), _P(Error)]),
+    "lpmc_run_two_way_paths": (_i32, [_P(Gbm), _i32, _P(Precision), _P(InvCdfTable), _i32, _u64,
+                                      _u64, _u64, _P(Options), _P(Moments), _P(Error)]),
+    "lpmc_allocate_samples": (_i32, [_P(LevelStatsC), _u64, C.c_double, _i32, _P(_u64),
+                                     _P(_u64), _P(_i32), _P(Error)]),
+    "lpmc_predicted_times": (_i32, [_P(LevelStatsC), _u64, C.c_double, _dp, _dp, _P(Error)]),
+    "lpmc_per_level_speedup": (_i32, [_P(LevelStatsC), _dp, _P(_i32), _P(Error)]),
+    "lpmc_run_nested_estimator": (_i32, [_P(Gbm), _i32, _P(Precision), _P(InvCdfTable), _i32,
+                                         C.c_double, _u64, _P(CostModelC), _u64, _P(Options),
+                                         _P(EstimatorResultC), _P(Error)]),
     "lpmc_plan_create": (_i32, [_P(Gbm), _i32, _P(Precision), _P(InvCdfTable), _i32, _u64, _u64,
                                 _u64, _P(Options), _P(C.c_void_p), _P(Error)]),
     "lpmc_plan_create_range": (_i32, [_P(Gbm), _i32, _P(Precision), _P(InvCdfTable), _i32, _u64,

@@ -15,6 +15,16 @@ CoupledMoments              mlmc.hpp:53-63
 CostModel / LevelStats      mlmc.hpp:20-51
 run_coupled_paths           mlmc.hpp:67-111   (device: lpmc_run_coupled_paths)
 estimate_level_stats        mlmc.hpp:113-149  (device: lpmc_estimate_level_stats)
+run_two_way_paths           experiments.hpp:136-141 over sde.hpp:162-196
+                            (device: lpmc_run_two_way_paths)
+AllocationKind/Allocation,  mlmc.hpp:151-195
+allocate_samples
+PredictedTimes,             mlmc.hpp:197-213
+predicted_times
+SpeedupResult,              mlmc.hpp:215-230
+per_level_speedup
+EstimatorResult,            mlmc.hpp:232-283  (device: lpmc_run_nested_estimator)
+run_nested_estimator
 ==========================  ================================================
 
 Every sampling call runs on the sm_100a kernels through the C-ABI; there is
@@ -24,7 +34,9 @@ DomainError (std::domain_error), SamplerRuntimeError (std::runtime_error).
 Extensions beyond the reference (keyword-only, defaults reproduce the
 reference): ``legs`` (hat/bar/all), ``payoff`` ("terminal" | "call") with
 ``strike``, ``reduce`` ("tree" | "sequential"), ``device``, ``stream``, and
-``PrecisionSpec.fp16_ieee()`` for native IEEE-binary16 legs.
+``PrecisionSpec.fp16_ieee()`` for native IEEE-binary16 legs.  ``legs="fine"``
+runs the two-way sampler (fine legs only); ``run_coupled_many`` runs a list of
+levels concurrently on one device.
 """
 from __future__ import annotations
 
@@ -38,7 +50,7 @@ import numpy as np
 from . import _native as N
 from ._native import DomainError, InvalidArgument, SamplerRuntimeError  # noqa: F401
 
-_LEGS = {"hat": N.LEGS_HAT, "bar": N.LEGS_BAR, "all": N.LEGS_ALL}
+_LEGS = {"hat": N.LEGS_HAT, "bar": N.LEGS_BAR, "all": N.LEGS_ALL, "fine": N.LEGS_FINE}
 _PAYOFF = {"terminal": N.PAYOFF_TERMINAL, "call": N.PAYOFF_CALL}
 _REDUCE = {"tree": N.REDUCE_TREE, "sequential": N.REDUCE_SEQUENTIAL}
 
@@ -344,6 +356,9 @@ class LevelStats:
     def from_c(cls, s: N.LevelStatsC) -> "LevelStats":
         return cls(**{name: getattr(s, name) for name, _ in N.LevelStatsC._fields_})
 
+    def _c(self) -> N.LevelStatsC:
+        return N.LevelStatsC(**{name: getattr(self, name) for name, _ in N.LevelStatsC._fields_})
+
 
 # ------------------------------------------------------------ sampling -----
 def _options(legs="all", payoff="terminal", strike=1.0, reduce="tree", device=None,
@@ -392,6 +407,42 @@ def estimate_level_stats(model: SdeModel, level: int, spec_low: PrecisionSpec,
                                                C.byref(cm), int(path_base), C.byref(opts),
                                                C.byref(out), C.byref(err)), err)
     return LevelStats.from_c(out)
+
+
+def run_coupled_many(model: SdeModel, approx: Optional[InvCdfApprox], seed: int, runs,
+                     **ext) -> list:
+    """Several run_coupled_paths calls (same model, table, seed and options)
+    executed concurrently on one device; ``runs`` holds (level, spec_low,
+    kahan, n_paths, path_base) tuples.  Returns one CoupledMoments per run,
+    bitwise those of the separate calls; the first failing run in list order
+    raises, as a serial loop would."""
+    runs = list(runs)
+    descs = (N.RunDesc * max(1, len(runs)))()
+    for i, (level, spec, kahan, n, base) in enumerate(runs):
+        descs[i] = N.RunDesc(int(level), spec._c(), int(bool(kahan)), int(n), int(base))
+    acc = (N.Moments * max(1, 3 * len(runs)))()
+    err = N.Error()
+    opts = _options(**ext)
+    N.check(N.load().lpmc_run_coupled_many(C.byref(_gbm_c(model)), _table_ptr(approx), int(seed),
+                                           descs, len(runs), C.byref(opts), acc, C.byref(err)),
+            err)
+    return [CoupledMoments.from_c3(acc[3 * i:3 * i + 3]) for i in range(len(runs))]
+
+
+def run_two_way_paths(model: SdeModel, level: int, spec_low: PrecisionSpec,
+                      approx: Optional[InvCdfApprox], kahan: bool, n_paths: int, seed: int,
+                      path_base: int, threads: int = 1, **ext) -> MomentAccumulator:
+    """MomentAccumulator of x_hat - x_bar over simulate_two_way paths
+    (sde.hpp:162-196), merged like run_batched (experiments.hpp:89-112)."""
+    out = N.Moments()
+    err = N.Error()
+    opts = _options(**ext)
+    N.check(N.load().lpmc_run_two_way_paths(C.byref(_gbm_c(model)), int(level),
+                                            C.byref(spec_low._c()), _table_ptr(approx),
+                                            int(bool(kahan)), int(n_paths), int(seed),
+                                            int(path_base), C.byref(opts), C.byref(out),
+                                            C.byref(err)), err)
+    return MomentAccumulator.from_c(out)
 
 
 def level_stats_from_moments(m: CoupledMoments, level: int, spec_low: PrecisionSpec,
@@ -573,3 +624,116 @@ def launch_count() -> int:
 
 def reset_launch_count() -> None:
     N.load().lpmc_reset_launch_count()
+
+
+# -------------------------------------- estimator layer (mlmc.hpp:151-285) --
+class AllocationKind:
+    standard = N.ALLOCATION_STANDARD
+    nested = N.ALLOCATION_NESTED
+
+
+@dataclass
+class Allocation:
+    """mlmc.hpp:153-163."""
+    primary: list = field(default_factory=list)
+    secondary: list = field(default_factory=list)
+    degenerate: bool = False
+
+
+@dataclass
+class PredictedTimes:
+    t_hat: float = 0.0
+    t_bar: float = 0.0
+
+
+@dataclass
+class SpeedupResult:
+    value: float = 0.0
+    cost_ratio_only: bool = False
+
+
+@dataclass
+class EstimatorResult:
+    """mlmc.hpp:232-239."""
+    value: float = 0.0
+    level_contributions: list = field(default_factory=list)
+    pilot_stats: list = field(default_factory=list)
+    allocation: Allocation = field(default_factory=Allocation)
+    times: PredictedTimes = field(default_factory=PredictedTimes)
+    eps: float = 0.0
+
+
+def _stats_array(stats):
+    stats = list(stats)
+    arr = (N.LevelStatsC * max(1, len(stats)))()
+    for i, s in enumerate(stats):
+        arr[i] = s._c()
+    return arr, len(stats)
+
+
+def allocate_samples(stats, eps: float, kind: int) -> Allocation:
+    """allocate_samples (mlmc.hpp:165-195), bitwise (host C++)."""
+    arr, n = _stats_array(stats)
+    prim = (C.c_uint64 * max(1, n))()
+    sec = (C.c_uint64 * max(1, n))()
+    deg = C.c_int32()
+    err = N.Error()
+    N.check(N.load().lpmc_allocate_samples(arr, n, float(eps), int(kind), prim, sec,
+                                           C.byref(deg), C.byref(err)), err)
+    return Allocation([int(x) for x in prim[:n]],
+                      [int(x) for x in sec[:n]] if kind == AllocationKind.nested else [],
+                      bool(deg.value))
+
+
+def predicted_times(stats, eps: float) -> PredictedTimes:
+    """predicted_times (mlmc.hpp:202-213), bitwise (host C++)."""
+    arr, n = _stats_array(stats)
+    th, tb = C.c_double(), C.c_double()
+    err = N.Error()
+    N.check(N.load().lpmc_predicted_times(arr, n, float(eps), C.byref(th), C.byref(tb),
+                                          C.byref(err)), err)
+    return PredictedTimes(th.value, tb.value)
+
+
+def per_level_speedup(s: LevelStats) -> SpeedupResult:
+    """per_level_speedup (mlmc.hpp:223-230), bitwise (host C++)."""
+    v = C.c_double()
+    flag = C.c_int32()
+    err = N.Error()
+    N.check(N.load().lpmc_per_level_speedup(C.byref(s._c()), C.byref(v), C.byref(flag),
+                                            C.byref(err)), err)
+    return SpeedupResult(v.value, bool(flag.value))
+
+
+def run_nested_estimator(model: SdeModel, max_level: int, spec_low: PrecisionSpec,
+                         approx: Optional[InvCdfApprox], kahan: bool, eps: float, seed: int,
+                         cost: Optional[CostModel] = None, threads: int = 1,
+                         pilot_paths: int = 1000, **ext) -> EstimatorResult:
+    """run_nested_estimator (mlmc.hpp:244-283) on the device: the pilot pass
+    and the main pass each run all their levels concurrently."""
+    if max_level < 0:
+        raise InvalidArgument("max level must be >= 0")
+    L = int(max_level) + 1
+    contrib = (C.c_double * L)()
+    pilot = (N.LevelStatsC * L)()
+    prim = (C.c_uint64 * L)()
+    sec = (C.c_uint64 * L)()
+    res = N.EstimatorResultC()
+    res.level_contributions = C.cast(contrib, N._dp)
+    res.pilot_stats = C.cast(pilot, C.POINTER(N.LevelStatsC))
+    res.primary = C.cast(prim, C.POINTER(C.c_uint64))
+    res.secondary = C.cast(sec, C.POINTER(C.c_uint64))
+    err = N.Error()
+    opts = _options(**ext)
+    cm = (cost or CostModel())._c()
+    N.check(N.load().lpmc_run_nested_estimator(C.byref(_gbm_c(model)), int(max_level),
+                                               C.byref(spec_low._c()), _table_ptr(approx),
+                                               int(bool(kahan)), float(eps), int(seed),
+                                               C.byref(cm), int(pilot_paths), C.byref(opts),
+                                               C.byref(res), C.byref(err)), err)
+    return EstimatorResult(
+        value=res.value, level_contributions=list(contrib),
+        pilot_stats=[LevelStats.from_c(pilot[i]) for i in range(L)],
+        allocation=Allocation([int(x) for x in prim], [int(x) for x in sec],
+                              bool(res.degenerate)),
+        times=PredictedTimes(res.t_hat, res.t_bar), eps=res.eps)

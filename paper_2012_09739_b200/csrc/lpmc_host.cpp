@@ -347,7 +347,7 @@ lpmc_status build_spec(const lpmc_gbm* model, int32_t level, const lpmc_precisio
   lpmc_default_options(&o);
   if (opts != nullptr) o = *opts;
   if (o.legs == 0) o.legs = LPMC_LEGS_ALL;
-  if (o.legs > 3) return fail(err, LPMC_INVALID_ARGUMENT, "bad legs mask");
+  if (o.legs > 4) return fail(err, LPMC_INVALID_ARGUMENT, "bad legs mask");
   if (o.payoff != LPMC_PAYOFF_TERMINAL && o.payoff != LPMC_PAYOFF_CALL)
     return fail(err, LPMC_INVALID_ARGUMENT, "bad payoff");
   if (o.reduce != LPMC_REDUCE_TREE && o.reduce != LPMC_REDUCE_SEQUENTIAL)
@@ -434,7 +434,9 @@ lpmc_status build_spec(const lpmc_gbm* model, int32_t level, const lpmc_precisio
                          in_native_range(low[3], 0x1p-40, 0x1p20) &&
                          in_native_range(low[4], 0x1p-20, 0x1p20) &&
                          in_native_range(low[5], 0x1p-40, 0x1p20);
-  if (s.ieee) {
+  if (o.legs == LPMC_LEGS_HAT) {
+    s.arith = BarArith::kCarrier;  // carrier legs only: the bar arithmetic is never run
+  } else if (s.ieee) {
     s.arith = BarArith::kHalf2;
   } else if (m >= 52) {
     s.arith = BarArith::kCarrier;
@@ -489,10 +491,22 @@ struct Buffers {
   }
 };
 
+// Streams and buffer sets for concurrent runs (lpmc_run_coupled_many), plus
+// a pinned staging area for their asynchronous read-backs.
+constexpr int kPoolStreams = 16;
+struct StreamPool {
+  cudaStream_t streams[kPoolStreams] = {};
+  Buffers bufs[kPoolStreams];
+  cudaEvent_t start = nullptr;
+  double* pinned = nullptr;
+  size_t pinned_cap = 0;  // doubles
+};
+
 struct DeviceCtx {
   std::mutex mu;
   cudaStream_t stream = nullptr;
   Buffers scratch;
+  StreamPool pool;
   bool configured = false;
 };
 
@@ -558,11 +572,39 @@ struct Enqueued {
   int kernels = 0;
 };
 
+// Grow B to what enqueue_run(s) needs (no-op when already large enough).
+// Runs sharing a buffer set on one stream reserve up front, so no buffer is
+// reallocated under an in-flight kernel.
+cudaError_t reserve(const RunSpec& s, Buffers& B) {
+  cudaError_t e;
+  if ((e = B.err_key.ensure(1)) != cudaSuccess) return e;
+  if ((e = B.range_flag.ensure(1)) != cudaSuccess) return e;
+  if (s.has_table && (e = B.table.ensure(s.table.rows.size())) != cudaSuccess) return e;
+  const uint64_t chunks = s.chunk_end - s.chunk_begin;
+  if (chunks == 0) return cudaSuccess;
+  if (s.reduce == LPMC_REDUCE_SEQUENTIAL) {
+    const uint64_t n_batches_total = (s.n_paths + kBatch - 1) / kBatch;
+    const uint64_t b0 = s.chunk_begin * kChunkBatches;
+    const uint64_t b1 = std::min(s.chunk_end * kChunkBatches, n_batches_total);
+    if ((e = B.seq_acc.ensure(15 * (b1 - b0))) != cudaSuccess) return e;
+    return B.path_diff.ensure(2 * std::min(b1 - b0, kSeqSliceChunks * kChunkBatches) * kBatch);
+  }
+  if ((e = B.chunk_acc.ensure(15 * chunks)) != cudaSuccess) return e;
+  return B.batch_acc.ensure(15 * std::min(chunks, kSliceChunks) * kChunkBatches);
+}
+
+// Accumulators a run produces (chunk partials, or batch accumulators in the
+// sequential mode).
+uint64_t acc_count_of(const RunSpec& s) {
+  if (s.reduce != LPMC_REDUCE_SEQUENTIAL) return s.chunk_end - s.chunk_begin;
+  const uint64_t n_batches_total = (s.n_paths + kBatch - 1) / kBatch;
+  return std::min(s.chunk_end * kChunkBatches, n_batches_total) - s.chunk_begin * kChunkBatches;
+}
+
 cudaError_t enqueue_run(const RunSpec& s, Buffers& B, cudaStream_t st, Enqueued* q) {
   cudaError_t e;
   *q = Enqueued{};
-  if ((e = B.err_key.ensure(1)) != cudaSuccess) return e;
-  if ((e = B.range_flag.ensure(1)) != cudaSuccess) return e;
+  if ((e = reserve(s, B)) != cudaSuccess) return e;
   if ((e = cudaMemsetAsync(B.err_key.ptr, 0xff, sizeof(unsigned long long), st)) != cudaSuccess) return e;
   if ((e = cudaMemsetAsync(B.range_flag.ptr, 0, sizeof(unsigned int), st)) != cudaSuccess) return e;
   LevelArgs A = s.args;
@@ -570,7 +612,6 @@ cudaError_t enqueue_run(const RunSpec& s, Buffers& B, cudaStream_t st, Enqueued*
   A.range_flag = B.range_flag.ptr;
   A.table = nullptr;
   if (s.has_table) {
-    if ((e = B.table.ensure(s.table.rows.size())) != cudaSuccess) return e;
     if ((e = cudaMemcpyAsync(B.table.ptr, s.table.rows.data(), s.table.rows.size() * sizeof(double),
                              cudaMemcpyHostToDevice, st)) != cudaSuccess)
       return e;
@@ -582,16 +623,8 @@ cudaError_t enqueue_run(const RunSpec& s, Buffers& B, cudaStream_t st, Enqueued*
   const bool seq = s.reduce == LPMC_REDUCE_SEQUENTIAL;
   const uint64_t slice_chunks = seq ? kSeqSliceChunks : kSliceChunks;
   if (seq) {
-    const uint64_t b0 = s.chunk_begin * kChunkBatches;
-    const uint64_t b1 = std::min(s.chunk_end * kChunkBatches, n_batches_total);
-    if ((e = B.seq_acc.ensure(15 * (b1 - b0))) != cudaSuccess) return e;
-    if ((e = B.path_diff.ensure(2 * std::min(b1 - b0, slice_chunks * kChunkBatches) * kBatch)) != cudaSuccess)
-      return e;
-    q->n_batches_seq = b1 - b0;
+    q->n_batches_seq = acc_count_of(s);
   } else {
-    if ((e = B.chunk_acc.ensure(15 * chunks)) != cudaSuccess) return e;
-    if ((e = B.batch_acc.ensure(15 * std::min(chunks, slice_chunks) * kChunkBatches)) != cudaSuccess)
-      return e;
     q->n_chunks = chunks;
   }
   for (uint64_t c0 = s.chunk_begin; c0 < s.chunk_end; c0 += slice_chunks) {
@@ -638,38 +671,56 @@ lpmc_status failure_from_key(const RunSpec& s, unsigned long long key, lpmc_erro
   return fail(err, LPMC_DOMAIN_ERROR, "non-finite operand", LPMC_FAIL_NONFINITE, path, step);
 }
 
-// Wait, check failure flags, copy partials back.  *rerun set when native
-// legs left their range (the caller re-runs with the exact emulation).
-lpmc_status collect_run(const RunSpec& s, Buffers& B, cudaStream_t st, const Enqueued& q,
-                        std::vector<Moments>* parts, bool* rerun, lpmc_error* err) {
-  *rerun = false;
-  unsigned long long key = ~0ull;
-  unsigned int range = 0;
-  cudaError_t e = cudaMemcpyAsync(&key, B.err_key.ptr, sizeof key, cudaMemcpyDeviceToHost, st);
-  if (e == cudaSuccess) e = cudaMemcpyAsync(&range, B.range_flag.ptr, sizeof range, cudaMemcpyDeviceToHost, st);
-  const uint64_t n_acc = q.n_batches_seq ? q.n_batches_seq : q.n_chunks;
+uint64_t acc_count(const Enqueued& q) { return q.n_batches_seq ? q.n_batches_seq : q.n_chunks; }
+
+// Device -> host copies of an enqueued run's failure word, range flag and
+// partials into caller memory (pinned for an asynchronous copy).
+cudaError_t enqueue_readback(const Enqueued& q, const Buffers& B, cudaStream_t st,
+                             unsigned long long* key, unsigned int* range, double* parts) {
+  cudaError_t e = cudaMemcpyAsync(key, B.err_key.ptr, sizeof *key, cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(range, B.range_flag.ptr, sizeof *range, cudaMemcpyDeviceToHost, st);
+  const uint64_t n_acc = acc_count(q);
   const double* src = q.n_batches_seq ? B.seq_acc.ptr : B.chunk_acc.ptr;
-  B.host_parts.resize(15 * n_acc);
   if (e == cudaSuccess && n_acc > 0)
-    e = cudaMemcpyAsync(B.host_parts.data(), src, 15 * n_acc * sizeof(double),
-                        cudaMemcpyDeviceToHost, st);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
-  if (e != cudaSuccess) return cuda_fail(err, e, "level sampler");
+    e = cudaMemcpyAsync(parts, src, 15 * n_acc * sizeof(double), cudaMemcpyDeviceToHost, st);
+  return e;
+}
+
+// Failure flags and partials of a finished run.  *rerun set when native
+// legs left their range (the caller re-runs with the exact emulation).
+lpmc_status interpret_run(const RunSpec& s, uint64_t n_acc, unsigned long long key,
+                          unsigned int range, const double* host, std::vector<Moments>* parts,
+                          bool* rerun, lpmc_error* err) {
+  *rerun = false;
   if (range != 0 && (s.arith == BarArith::kF32 || s.arith == BarArith::kF32Round)) {
     *rerun = true;
     return LPMC_OK;
   }
   if (key != ~0ull) return failure_from_key(s, key, err);
   parts->resize(3 * n_acc);
-  for (uint64_t i = 0; i < 3 * n_acc; ++i) (*parts)[i] = from_device(B.host_parts.data() + 5 * i);
+  for (uint64_t i = 0; i < 3 * n_acc; ++i) (*parts)[i] = from_device(host + 5 * i);
   return LPMC_OK;
+}
+
+// Wait, check failure flags, copy partials back.
+lpmc_status collect_run(const RunSpec& s, Buffers& B, cudaStream_t st, const Enqueued& q,
+                        std::vector<Moments>* parts, bool* rerun, lpmc_error* err) {
+  unsigned long long key = ~0ull;
+  unsigned int range = 0;
+  B.host_parts.resize(15 * acc_count(q));
+  cudaError_t e = enqueue_readback(q, B, st, &key, &range, B.host_parts.data());
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return cuda_fail(err, e, "level sampler");
+  return interpret_run(s, acc_count(q), key, range, B.host_parts.data(), parts, rerun, err);
 }
 
 void mask_legs(const RunSpec& s, std::vector<Moments>& parts) {
   const int legs = s.args.legs;
   for (size_t i = 0; i < parts.size(); ++i) {
     const int f = static_cast<int>(i % 3);
-    const bool keep = f == 0 ? (legs & 1) : (f == 1 ? (legs & 2) : ((legs & 3) == 3));
+    const bool keep = legs == LPMC_LEGS_FINE ||
+                      (f == 0 ? (legs & 1) : (f == 1 ? (legs & 2) : ((legs & 3) == 3)));
     if (!keep) parts[i] = Moments{};
   }
 }
@@ -699,6 +750,89 @@ lpmc_status run_sync(RunSpec& s, void* user_stream, std::vector<Moments>* parts,
     s.arith = BarArith::kF64Round;  // exact emulation outside the native range
   }
   return fail(err, LPMC_RUNTIME_ERROR, "native range fallback did not converge");
+}
+
+// Independent runs on one device, concurrently: run i goes to pool stream
+// i % kPoolStreams with that slot's buffers (reserved for the slot's largest
+// run first), every run's read-back is enqueued behind its kernels, and the
+// host waits once.  Results are then interpreted in list order, so the
+// first failure reported is the one a serial loop would hit first; a run
+// whose native legs left their range is re-run in the exact emulation.
+lpmc_status run_many(std::vector<RunSpec>& specs, void* user_stream,
+                     std::vector<std::vector<Moments>>* out, lpmc_error* err) {
+  out->assign(specs.size(), {});
+  if (specs.empty()) return ok(err);
+  DeviceCtx* ctx = nullptr;
+  int dev = -1;
+  lpmc_status stt = get_ctx(specs[0].device, &ctx, &dev, err);
+  if (stt != LPMC_OK) return stt;
+  DeviceGuard guard;
+  cudaError_t e = guard.set(dev);
+  if (e != cudaSuccess) return cuda_fail(err, e, "cudaSetDevice");
+  std::lock_guard<std::mutex> lock(ctx->mu);
+  StreamPool& P = ctx->pool;
+  const size_t n = specs.size();
+  const int used = static_cast<int>(std::min<size_t>(n, kPoolStreams));
+  for (int k = 0; k < used && e == cudaSuccess; ++k)
+    if (P.streams[k] == nullptr) e = cudaStreamCreateWithFlags(&P.streams[k], cudaStreamNonBlocking);
+  if (e == cudaSuccess && P.start == nullptr)
+    e = cudaEventCreateWithFlags(&P.start, cudaEventDisableTiming);
+  if (e != cudaSuccess) return cuda_fail(err, e, "stream pool");
+  // staging layout per run: key, range, 15 doubles per accumulator
+  std::vector<size_t> off(n + 1, 0);
+  for (size_t i = 0; i < n; ++i)
+    off[i + 1] = off[i] + 2 + (specs[i].n_paths ? 15 * acc_count_of(specs[i]) : 0);
+  if (off[n] > P.pinned_cap) {
+    if (P.pinned != nullptr) cudaFreeHost(P.pinned);
+    P.pinned = nullptr;
+    P.pinned_cap = 0;
+    e = cudaMallocHost(reinterpret_cast<void**>(&P.pinned), off[n] * sizeof(double));
+    if (e != cudaSuccess) return cuda_fail(err, e, "pinned staging");
+    P.pinned_cap = off[n];
+  }
+  for (size_t i = 0; i < n && e == cudaSuccess; ++i)
+    if (specs[i].n_paths) e = reserve(specs[i], P.bufs[i % kPoolStreams]);
+  if (e == cudaSuccess && user_stream != nullptr) {
+    e = cudaEventRecord(P.start, static_cast<cudaStream_t>(user_stream));
+    for (int k = 0; k < used && e == cudaSuccess; ++k) e = cudaStreamWaitEvent(P.streams[k], P.start, 0);
+  }
+  std::vector<Enqueued> q(n);
+  for (size_t i = 0; i < n && e == cudaSuccess; ++i) {
+    if (specs[i].n_paths == 0) continue;  // mlmc.hpp:75: nothing simulated
+    const int k = static_cast<int>(i % kPoolStreams);
+    double* stage = P.pinned + off[i];
+    e = enqueue_run(specs[i], P.bufs[k], P.streams[k], &q[i]);
+    if (e == cudaSuccess)
+      e = enqueue_readback(q[i], P.bufs[k], P.streams[k], reinterpret_cast<unsigned long long*>(stage),
+                           reinterpret_cast<unsigned int*>(stage + 1), stage + 2);
+  }
+  for (int k = 0; k < used; ++k) {
+    const cudaError_t s2 = cudaStreamSynchronize(P.streams[k]);
+    if (e == cudaSuccess) e = s2;
+  }
+  if (e != cudaSuccess) return cuda_fail(err, e, "level sampler");
+  for (size_t i = 0; i < n; ++i) {
+    if (specs[i].n_paths == 0) continue;
+    const int k = static_cast<int>(i % kPoolStreams);
+    const double* stage = P.pinned + off[i];
+    unsigned long long key;
+    unsigned int range;
+    std::memcpy(&key, stage, sizeof key);
+    std::memcpy(&range, stage + 1, sizeof range);
+    bool rerun = false;
+    stt = interpret_run(specs[i], acc_count(q[i]), key, range, stage + 2, &(*out)[i], &rerun, err);
+    if (stt != LPMC_OK) return stt;
+    if (rerun) {
+      specs[i].arith = BarArith::kF64Round;
+      Enqueued q2;
+      e = enqueue_run(specs[i], P.bufs[k], P.streams[k], &q2);
+      if (e != cudaSuccess) return cuda_fail(err, e, "fallback launch");
+      stt = collect_run(specs[i], P.bufs[k], P.streams[k], q2, &(*out)[i], &rerun, err);
+      if (stt != LPMC_OK) return stt;
+    }
+    mask_legs(specs[i], (*out)[i]);
+  }
+  return ok(err);
 }
 
 void fold(const std::vector<Moments>& parts, lpmc_moments* out3) {
@@ -921,6 +1055,197 @@ lpmc_status lpmc_estimate_level_stats(const lpmc_gbm* model, int32_t level,
                                           path_base, opts, acc, err);
   if (st != LPMC_OK) return st;
   lpmc_level_stats_from_moments(acc, level, prec, kahan, cost, n_paths, out);
+  return ok(err);
+}
+
+lpmc_status lpmc_run_coupled_many(const lpmc_gbm* model, const lpmc_invcdf_table* table,
+                                  uint64_t seed, const lpmc_run_desc* runs, uint64_t n_runs,
+                                  const lpmc_options* opts, lpmc_moments* out, lpmc_error* err) {
+  if (n_runs == 0) return ok(err);
+  if (runs == nullptr || out == nullptr)
+    return fail(err, LPMC_INVALID_ARGUMENT, "null run list or output");
+  for (uint64_t i = 0; i < 3 * n_runs; ++i) out[i] = lpmc_moments{0, 0.0, 0.0, 0.0, 0.0};
+  // Specs in list order; a run that cannot even be set up ends the list
+  // there (a serial loop would throw at it, after the runs before it).
+  std::vector<RunSpec> specs;
+  specs.reserve(n_runs);
+  lpmc_status setup = LPMC_OK;
+  lpmc_error setup_err{};
+  for (uint64_t i = 0; i < n_runs; ++i) {
+    RunSpec s;
+    if (runs[i].n_paths == 0) {  // run_coupled_paths simulates nothing (mlmc.hpp:75)
+      s.device = opts != nullptr ? opts->device : -1;
+    } else {
+      setup = build_spec(model, runs[i].level, &runs[i].prec, table, runs[i].kahan,
+                         runs[i].n_paths, seed, runs[i].path_base, opts, &s, &setup_err);
+      if (setup != LPMC_OK) break;
+    }
+    specs.push_back(std::move(s));
+  }
+  std::vector<std::vector<Moments>> parts;
+  lpmc_status st = run_many(specs, opts != nullptr ? opts->stream : nullptr, &parts, err);
+  if (st != LPMC_OK) return st;
+  if (setup != LPMC_OK) {
+    if (err != nullptr) *err = setup_err;
+    return setup;
+  }
+  for (size_t i = 0; i < specs.size(); ++i) fold(parts[i], out + 3 * i);
+  return ok(err);
+}
+
+lpmc_status lpmc_run_two_way_paths(const lpmc_gbm* model, int32_t level,
+                                   const lpmc_precision* prec, const lpmc_invcdf_table* table,
+                                   int32_t kahan, uint64_t n_paths, uint64_t seed,
+                                   uint64_t path_base, const lpmc_options* opts,
+                                   lpmc_moments* out, lpmc_error* err) {
+  *out = lpmc_moments{0, 0.0, 0.0, 0.0, 0.0};
+  lpmc_options o;
+  lpmc_default_options(&o);
+  if (opts != nullptr) o = *opts;
+  o.legs = LPMC_LEGS_FINE;
+  lpmc_moments acc[3];
+  const lpmc_status st = lpmc_run_coupled_paths(model, level, prec, table, kahan, n_paths, seed,
+                                                path_base, &o, acc, err);
+  if (st != LPMC_OK) return st;
+  *out = acc[2];  // x_hat - x_bar
+  return ok(err);
+}
+
+lpmc_status lpmc_allocate_samples(const lpmc_level_stats* stats, uint64_t n_levels, double eps,
+                                  int32_t kind, uint64_t* primary, uint64_t* secondary,
+                                  int32_t* degenerate, lpmc_error* err) {
+  // allocate_samples (mlmc.hpp:165-195): same expressions, same order
+  if (stats == nullptr || n_levels == 0) return fail(err, LPMC_INVALID_ARGUMENT, "no level stats");
+  if (!(eps > 0.0)) return fail(err, LPMC_INVALID_ARGUMENT, "eps must be positive");
+  if (kind != LPMC_ALLOCATION_STANDARD && kind != LPMC_ALLOCATION_NESTED)
+    return fail(err, LPMC_INVALID_ARGUMENT, "bad allocation kind");
+  const bool nested = kind == LPMC_ALLOCATION_NESTED;
+  if (primary == nullptr || (nested && secondary == nullptr))
+    return fail(err, LPMC_INVALID_ARGUMENT, "null allocation output");
+  double s = 0.0;
+  for (uint64_t i = 0; i < n_levels; ++i) {
+    const lpmc_level_stats& st = stats[i];
+    if (!nested) {
+      s += std::sqrt(st.v_hat * st.c_hat);
+    } else {
+      s += std::sqrt(st.v_bar * st.c_bar) + std::sqrt(st.V_bar * st.C_bar);
+    }
+  }
+  if (degenerate != nullptr) *degenerate = s == 0.0 ? 1 : 0;
+  const double scale = 2.0 / (eps * eps) * s;
+  for (uint64_t i = 0; i < n_levels; ++i) {
+    const lpmc_level_stats& st = stats[i];
+    const double v1 = nested ? st.v_bar : st.v_hat;
+    const double c1 = nested ? st.c_bar : st.c_hat;
+    const double m1 = v1 > 0.0 ? scale * std::sqrt(v1 / c1) : 0.0;
+    primary[i] = std::max<uint64_t>(1, static_cast<uint64_t>(std::ceil(m1)));
+    if (nested) {
+      const double m2 = st.V_bar > 0.0 ? scale * std::sqrt(st.V_bar / st.C_bar) : 0.0;
+      secondary[i] = std::max<uint64_t>(1, static_cast<uint64_t>(std::ceil(m2)));
+    }
+  }
+  return ok(err);
+}
+
+lpmc_status lpmc_predicted_times(const lpmc_level_stats* stats, uint64_t n_levels, double eps,
+                                 double* t_hat, double* t_bar, lpmc_error* err) {
+  // predicted_times (mlmc.hpp:202-213)
+  if (stats == nullptr || n_levels == 0) return fail(err, LPMC_INVALID_ARGUMENT, "no level stats");
+  if (!(eps > 0.0)) return fail(err, LPMC_INVALID_ARGUMENT, "eps must be positive");
+  double s_hat = 0.0, s_bar = 0.0;
+  for (uint64_t i = 0; i < n_levels; ++i) {
+    const lpmc_level_stats& st = stats[i];
+    s_hat += std::sqrt(st.v_hat * st.c_hat);
+    s_bar += std::sqrt(st.v_bar * st.c_bar) + std::sqrt(st.V_bar * st.C_bar);
+  }
+  const double scale = 2.0 / (eps * eps);
+  *t_hat = scale * s_hat * s_hat;
+  *t_bar = scale * s_bar * s_bar;
+  return ok(err);
+}
+
+lpmc_status lpmc_per_level_speedup(const lpmc_level_stats* s, double* value,
+                                   int32_t* cost_ratio_only, lpmc_error* err) {
+  // per_level_speedup (mlmc.hpp:223-230)
+  if (!(s->v_hat > 0.0) || !(s->c_hat > 0.0))
+    return fail(err, LPMC_INVALID_ARGUMENT, "per_level_speedup needs v_hat, c_hat > 0");
+  if (s->v_bar == 0.0) {
+    *value = s->c_hat / s->c_bar;
+    *cost_ratio_only = 1;
+    return ok(err);
+  }
+  const double ratio = (s->v_bar * s->c_bar) / (s->v_hat * s->c_hat);
+  const double mix = 1.0 + std::sqrt(s->V_bar * s->C_bar / (s->v_bar * s->c_bar));
+  *value = 1.0 / (ratio * mix * mix);
+  *cost_ratio_only = 0;
+  return ok(err);
+}
+
+lpmc_status lpmc_run_nested_estimator(const lpmc_gbm* model, int32_t max_level,
+                                      const lpmc_precision* prec,
+                                      const lpmc_invcdf_table* table, int32_t kahan, double eps,
+                                      uint64_t seed, const lpmc_cost_model* cost,
+                                      uint64_t pilot_paths, const lpmc_options* opts,
+                                      lpmc_estimator_result* out, lpmc_error* err) {
+  // run_nested_estimator (mlmc.hpp:244-283)
+  if (out == nullptr || prec == nullptr) return fail(err, LPMC_INVALID_ARGUMENT, "null argument");
+  out->value = 0.0;
+  out->eps = eps;
+  out->t_hat = out->t_bar = 0.0;
+  out->degenerate = 0;
+  if (max_level < 0) return fail(err, LPMC_INVALID_ARGUMENT, "max level must be >= 0");
+  if (pilot_paths < 2) return fail(err, LPMC_INVALID_ARGUMENT, "need at least 2 paths");  // :121
+  const uint64_t levels = static_cast<uint64_t>(max_level) + 1;
+  auto path_base = [](uint64_t l, uint64_t phase) { return (l << 40) | (phase << 36); };
+  lpmc_options o;
+  lpmc_default_options(&o);
+  if (opts != nullptr) o = *opts;
+  o.legs = LPMC_LEGS_ALL;  // the estimator needs all four legs
+
+  std::vector<lpmc_run_desc> runs;
+  for (uint64_t l = 0; l < levels; ++l)
+    runs.push_back({static_cast<int32_t>(l), *prec, kahan, pilot_paths, path_base(l, 0)});
+  std::vector<lpmc_moments> acc(3 * runs.size());
+  lpmc_status st = lpmc_run_coupled_many(model, table, seed, runs.data(), runs.size(), &o,
+                                         acc.data(), err);
+  if (st != LPMC_OK) return st;
+  std::vector<lpmc_level_stats> stats(levels);
+  for (uint64_t l = 0; l < levels; ++l) {
+    lpmc_level_stats_from_moments(&acc[3 * l], static_cast<int32_t>(l), prec, kahan, cost,
+                                  pilot_paths, &stats[l]);
+    if (out->pilot_stats != nullptr) out->pilot_stats[l] = stats[l];
+  }
+  std::vector<uint64_t> primary(levels), secondary(levels);
+  int32_t degenerate = 0;
+  st = lpmc_allocate_samples(stats.data(), levels, eps, LPMC_ALLOCATION_NESTED, primary.data(),
+                             secondary.data(), &degenerate, err);
+  if (st != LPMC_OK) return st;
+  out->degenerate = degenerate;
+  st = lpmc_predicted_times(stats.data(), levels, eps, &out->t_hat, &out->t_bar, err);
+  if (st != LPMC_OK) return st;
+  for (uint64_t l = 0; l < levels; ++l) {
+    if (out->primary != nullptr) out->primary[l] = primary[l];
+    if (out->secondary != nullptr) out->secondary[l] = secondary[l];
+  }
+
+  runs.clear();
+  for (uint64_t l = 0; l < levels; ++l) {
+    runs.push_back({static_cast<int32_t>(l), *prec, kahan, primary[l], path_base(l, 1)});
+    runs.push_back({static_cast<int32_t>(l), *prec, kahan, secondary[l], path_base(l, 2)});
+  }
+  acc.assign(3 * runs.size(), lpmc_moments{});
+  st = lpmc_run_coupled_many(model, table, seed, runs.data(), runs.size(), &o, acc.data(), err);
+  if (st != LPMC_OK) return st;
+  auto mean = [](const lpmc_moments& a) { return a.n ? a.mean : 0.0; };  // stats.hpp:57
+  double value = 0.0;
+  for (uint64_t l = 0; l < levels; ++l) {
+    const lpmc_moments* two_way = &acc[6 * l];
+    const lpmc_moments* four_way = &acc[6 * l + 3];
+    const double contribution = mean(two_way[1]) + (mean(four_way[0]) - mean(four_way[1]));
+    if (out->level_contributions != nullptr) out->level_contributions[l] = contribution;
+    value += contribution;
+  }
+  out->value = value;
   return ok(err);
 }
 

@@ -135,8 +135,9 @@ __device__ __forceinline__ void simulate(const LevelArgs& A, const TableView& ta
                                          PathEnd<Arith::NP>& R) {
   using T = typename Arith::T;
   constexpr int NP = Arith::NP;
-  constexpr bool kHat = (LEGS & 1) != 0;
-  constexpr bool kBar = (LEGS & 2) != 0;
+  constexpr bool kFineOnly = LEGS == 4;  // simulate_two_way (sde.hpp:162-196)
+  constexpr bool kHat = (LEGS & 1) != 0 || kFineOnly;
+  constexpr bool kBar = (LEGS & 2) != 0 || kFineOnly;
   constexpr bool kNeedExact = kHat || !APPROX;
 
   const Arith ar(A);
@@ -194,7 +195,7 @@ __device__ __forceinline__ void simulate(const LevelArgs& A, const TableView& ta
   };
   // em_step_dw / em_step_kahan_dw (sde.hpp:72-80, 107-116)
   auto coarse = [&](const double (&z0)[NP], const double (&z1)[NP], T zb0, T zb1, uint64_t n) {
-    if constexpr (kHat) {
+    if constexpr (kHat && !kFineOnly) {
 #pragma unroll
       for (int p = 0; p < NP; ++p) {
         const double dw = __dadd_rn(__dmul_rn(A.sdtf, z0[p]), __dmul_rn(A.sdtf, z1[p]));
@@ -205,7 +206,7 @@ __device__ __forceinline__ void simulate(const LevelArgs& A, const TableView& ta
         if constexpr (CHECKED) note_fail(fk[p], nonfinite64(xhc[p]), n, kStageHatCoarse);
       }
     }
-    if constexpr (kBar) {
+    if constexpr (kBar && !kFineOnly) {
       const T dw = ar.add(ar.mul(sdtf_l, zb0), ar.mul(sdtf_l, zb1));
       const T x = xbc;
       const T drift = ar.mul(ar.mul(mu_l, x), dtc_l);
@@ -283,14 +284,15 @@ __device__ __forceinline__ void simulate(const LevelArgs& A, const TableView& ta
     }
   }
 
+  constexpr bool kCoarse = !kFineOnly;
   const uint32_t bad_f = kBar ? ar.bad(xbf) : 0u;
-  const uint32_t bad_c = (kBar && A.level > 0) ? ar.bad(xbc) : 0u;
+  const uint32_t bad_c = (kBar && kCoarse && A.level > 0) ? ar.bad(xbc) : 0u;
 #pragma unroll
   for (int p = 0; p < NP; ++p) {
     R.hf[p] = kHat ? xhf[p] : 0.0;
-    R.hc[p] = (kHat && A.level > 0) ? xhc[p] : 0.0;
+    R.hc[p] = (kHat && kCoarse && A.level > 0) ? xhc[p] : 0.0;
     R.bf[p] = kBar ? ar.get(xbf, p) : 0.0;
-    R.bc[p] = (kBar && A.level > 0) ? ar.get(xbc, p) : 0.0;
+    R.bc[p] = (kBar && kCoarse && A.level > 0) ? ar.get(xbc, p) : 0.0;
     R.fk[p] = fk[p];
     const bool hat_bad = kHat && (nonfinite64(R.hf[p]) || nonfinite64(R.hc[p]));
     R.suspect[p] = u1[p] || hat_bad || ((bad_f >> p) & 1u) || ((bad_c >> p) & 1u);
@@ -320,8 +322,9 @@ template <class Arith, bool KAHAN, int LEGS, bool APPROX, bool DUMP>
 __global__ void __launch_bounds__(kBatch / Arith::NP, LPMC_LEVEL_MIN_CTAS)
     level_kernel(const __grid_constant__ LevelArgs A) {
   constexpr int NP = Arith::NP;
-  constexpr bool kHat = (LEGS & 1) != 0;
-  constexpr bool kBar = (LEGS & 2) != 0;
+  constexpr bool kFineOnly = LEGS == 4;
+  constexpr bool kHat = (LEGS & 1) != 0 || kFineOnly;
+  constexpr bool kBar = (LEGS & 2) != 0 || kFineOnly;
   constexpr bool kNeedExact = kHat || !APPROX;
 
   extern __shared__ __align__(16) double s_table[];
@@ -388,8 +391,8 @@ __global__ void __launch_bounds__(kBatch / Arith::NP, LPMC_LEVEL_MIN_CTAS)
     if (A.payoff == 1) {
       pf_h = fmax(__dsub_rn(R.hf[p], A.strike), 0.0);
       pf_b = fmax(__dsub_rn(R.bf[p], A.strike), 0.0);
-      pc_h = A.level > 0 ? fmax(__dsub_rn(R.hc[p], A.strike), 0.0) : 0.0;
-      pc_b = A.level > 0 ? fmax(__dsub_rn(R.bc[p], A.strike), 0.0) : 0.0;
+      pc_h = (!kFineOnly && A.level > 0) ? fmax(__dsub_rn(R.hc[p], A.strike), 0.0) : 0.0;
+      pc_b = (!kFineOnly && A.level > 0) ? fmax(__dsub_rn(R.bc[p], A.strike), 0.0) : 0.0;
     }
     dh[p] = kHat ? __dsub_rn(pf_h, pc_h) : 0.0;
     db[p] = kBar ? __dsub_rn(pf_b, pc_b) : 0.0;
@@ -427,10 +430,11 @@ cudaError_t pick_approx(const LevelArgs& A, cudaStream_t s) {
 template <class Arith, bool KAHAN, bool DUMP>
 cudaError_t pick_legs(const LevelArgs& A, cudaStream_t s) {
   if (A.legs == 2) return pick_approx<Arith, KAHAN, 2, DUMP>(A, s);
+  if (A.legs == 4) return pick_approx<Arith, KAHAN, 4, DUMP>(A, s);
   return pick_approx<Arith, KAHAN, 3, DUMP>(A, s);
 }
 
-// Launch the path kernel of one bar arithmetic (legs 2 / 3).
+// Launch the path kernel of one bar arithmetic (legs 2 / 3 / 4 = fine only).
 template <class Arith>
 cudaError_t launch_level(const LevelArgs& A, bool kahan, bool dump, cudaStream_t s) {
   if (dump) return kahan ? pick_legs<Arith, true, true>(A, s) : pick_legs<Arith, false, true>(A, s);
@@ -449,6 +453,10 @@ cudaError_t configure_level() {
   auto acc = [&](cudaError_t x) {
     if (e == cudaSuccess) e = x;
   };
+  acc(configure_one<Arith, false, 4, false>());
+  acc(configure_one<Arith, true, 4, false>());
+  acc(configure_one<Arith, false, 4, true>());
+  acc(configure_one<Arith, true, 4, true>());
   acc(configure_one<Arith, false, 2, false>());
   acc(configure_one<Arith, true, 2, false>());
   acc(configure_one<Arith, false, 3, false>());

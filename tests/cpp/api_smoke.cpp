@@ -11,6 +11,7 @@
 #include <cstring>
 #include <stdexcept>
 
+#include "lpmc/experiments.hpp"
 #include "lpmc/mlmc.hpp"
 
 using namespace lpmc;
@@ -61,6 +62,54 @@ int main(int argc, char** argv) {
   CHECK(acc.count() == 100);
   CHECK(std::fabs(acc.mean() - 0.495) < 1e-14);
 
+  // allocation / predicted times / speedup closed forms (test_mlmc.cpp:97-189)
+  {
+    LevelStats a, b;
+    a.level = 0;
+    a.v_hat = 4.0;
+    a.c_hat = 1.0;
+    b.level = 1;
+    b.v_hat = 1.0;
+    b.c_hat = 4.0;
+    auto alloc = allocate_samples({a, b}, 0.1, AllocationKind::standard);
+    CHECK(alloc.primary.size() == 2 && !alloc.degenerate);
+    CHECK(alloc.primary[0] == 1600 && alloc.primary[1] == 400);
+    CHECK(allocate_samples({a}, 0.1, AllocationKind::standard).primary[0] == 800);
+    CHECK(throws<std::invalid_argument>([] { allocate_samples({}, 0.1, AllocationKind::standard); }));
+    CHECK(throws<std::invalid_argument>([&] { allocate_samples({a}, 0.0, AllocationKind::standard); }));
+    LevelStats n;
+    n.v_bar = 1.0;
+    n.c_bar = 1.0;
+    n.V_bar = 0.25;
+    n.C_bar = 4.0;
+    auto nested = allocate_samples({n}, 0.1, AllocationKind::nested);
+    CHECK(nested.primary[0] == 400 && nested.secondary[0] == 100);
+    auto d = allocate_samples({LevelStats{}}, 0.1, AllocationKind::nested);
+    CHECK(d.degenerate && d.primary[0] == 1 && d.secondary[0] == 1);
+    LevelStats t = n;
+    t.v_hat = 4.0;
+    t.c_hat = 1.0;
+    auto pt = predicted_times({t}, 0.1);
+    CHECK(std::fabs(pt.t_hat - 800.0) < 1e-9 && std::fabs(pt.t_bar - 800.0) < 1e-9);
+    CHECK(std::fabs(predicted_times({t, t}, 0.1).t_hat - 4.0 * pt.t_hat) < 1e-9);
+    LevelStats sp;
+    sp.v_hat = 1.0;
+    sp.c_hat = 8.0;
+    sp.v_bar = 1.0;
+    sp.c_bar = 2.0;
+    sp.V_bar = 0.0;
+    sp.C_bar = 10.0;
+    CHECK(std::fabs(per_level_speedup(sp).value - 4.0) < 1e-12 && !per_level_speedup(sp).cost_ratio_only);
+    sp.V_bar = 0.2;
+    const double ratio = (1.0 * 2.0) / (1.0 * 8.0), mix = 1.0 + std::sqrt(0.2 * 10.0 / 2.0);
+    CHECK(std::fabs(per_level_speedup(sp).value - 1.0 / (ratio * mix * mix)) < 1e-12);
+    sp.v_bar = 0.0;
+    CHECK(per_level_speedup(sp).cost_ratio_only && std::fabs(per_level_speedup(sp).value - 4.0) < 1e-12);
+    sp.v_hat = 0.0;
+    CHECK(throws<std::invalid_argument>([&] { per_level_speedup(sp); }));
+    CHECK(ExperimentConfig{}.paths_for_level(11) == 2500);
+  }
+
   if (host_only) {
     std::printf(g_fail ? "host-only FAILED\n" : "host-only ok\n");
     return g_fail ? 1 : 0;
@@ -96,6 +145,39 @@ int main(int argc, char** argv) {
   SdeModel blow = make_gbm(1e30, 0.0, 1e300);
   CHECK(throws<std::domain_error>(
       [&] { run_coupled_paths(blow, 4, PrecisionSpec::carrier(), nullptr, false, 8, 1, 0); }));
+
+  // nested estimator (test_mlmc.cpp:204-236)
+  {
+    SdeModel det0 = make_gbm(0.05, 0.0);
+    auto r = run_nested_estimator(det0, 4, PrecisionSpec::carrier(), nullptr, false, 0.01, 1);
+    CHECK(r.allocation.degenerate);
+    const double expected = std::pow(1.0 + 0.05 * 0x1p-4, 16.0);
+    CHECK(std::fabs(r.value - expected) <= 1e-12 * expected);
+    CHECK(r.level_contributions.size() == 5 && r.pilot_stats.size() == 5);
+    auto rc = run_nested_estimator(gbm, 2, PrecisionSpec::carrier(), nullptr, false, 0.05, 3);
+    for (const auto& st : rc.pilot_stats) CHECK(st.V_bar == 0.0);
+    auto a1024 = InvCdfApprox::parse("linear:1024");
+    auto g = run_nested_estimator(gbm, 6, PrecisionSpec::fp32(), &a1024, false, 0.01, 11);
+    CHECK(std::fabs(g.value - std::exp(0.05)) < 0.04);
+    CHECK(g.times.t_hat > 0.0 && g.times.t_bar > 0.0);
+  }
+
+  // two-way / four-way experiments (experiments.hpp)
+  {
+    ExperimentConfig cfg;
+    cfg.precisions = {"fp16", "fp32"};
+    cfg.approx = "linear:16";
+    cfg.level_min = 0;
+    cfg.level_max = 3;
+    cfg.paths = {2000};
+    auto rows = run_two_way_experiment(cfg);
+    CHECK(rows.size() == 8 && rows[3].n_steps == 8 && rows[4].precision == "fp32");
+    CHECK(rows[0].variance > rows[4].variance);  // fp16 rounding dominates fp32's
+    auto four = run_four_way_experiment(cfg);
+    CHECK(four.rows.size() == 24 && four.high_stats.size() == 4);
+    auto report = run_speedup_report(four.high_stats, four.low_stats, four.low_kahan_stats);
+    CHECK(report.size() == 12);
+  }
 
   // non-GBM models are rejected (no CPU fallback)
   SdeModel custom = gbm;

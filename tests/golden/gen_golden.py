@@ -135,5 +135,118 @@ def main():
     print("wrote", os.path.join(OUT, "reference_vectors.json"))
 
 
+def callers():
+    """Fixtures of the callers above the level sampler:
+    two-way paths and experiment rows, allocation/predicted-time/speedup pins,
+    nested-estimator runs -> callers_vectors.json."""
+    build(ref=True)
+    R = Reference()
+    threads = os.cpu_count() or 1
+
+    two_way_paths = []
+    for level in [0, 1, 3, 6]:
+        for m in [52, 23, 10]:
+            for approx in ["exact", "linear:16", "cubic:64"]:
+                for kahan in [0, 1]:
+                    rc, msg, out = R.simulate_two_way(level=level, mantissa_bits=m, approx=approx,
+                                                      kahan=kahan, seed=3, path_base=77 + level,
+                                                      n=16)
+                    assert rc == 0, msg
+                    two_way_paths.append({"level": level, "m": m, "approx": approx,
+                                          "kahan": kahan, "seed": 3, "path_base": 77 + level,
+                                          "out": hx(out)})
+
+    two_way_rows = []
+    for prec, approx, kahan, lmin, lmax, paths in [("fp16", "linear:16", 0, 0, 6, 2000),
+                                                   ("fp16", "linear:16", 1, 0, 6, 2000),
+                                                   ("fp32", "cubic:64", 0, 0, 4, 3000),
+                                                   ("bf16", "exact", 0, 2, 5, 1500)]:
+        rc, msg, out = R.two_way_experiment(precision=prec, approx=approx, kahan=kahan,
+                                            level_min=lmin, level_max=lmax, paths=paths,
+                                            threads=threads)
+        assert rc == 0, msg
+        two_way_rows.append({"precision": prec, "approx": approx, "kahan": kahan,
+                             "level_min": lmin, "level_max": lmax, "paths": paths,
+                             "rows": [hx(r) for r in out]})
+
+    rng = np.random.default_rng(11)
+
+    def stats_set(n, zero=()):
+        out = []
+        for lv in range(n):
+            d = {k: 0.0 for k in Reference.STATS_FIELDS}
+            d.update(level=lv, v_hat=float(rng.uniform(1e-6, 1e-3)), c_hat=3.5 * 2**lv,
+                     v_bar=float(rng.uniform(1e-6, 1e-3)), c_bar=0.25 * 2**lv * 1.4,
+                     V_bar=float(rng.uniform(1e-9, 1e-5)))
+            d["C_bar"] = d["c_hat"] + d["c_bar"]
+            for k in zero:
+                d[k] = 0.0
+            out.append(d)
+        return out
+
+    sets = [stats_set(6), stats_set(3, zero=("v_bar",)), stats_set(4, zero=("v_hat", "v_bar",
+                                                                            "V_bar")),
+            stats_set(1)]
+    allocation = []
+    for si, st in enumerate(sets):
+        for eps in [1e-3, 2.5e-2]:
+            for kind in [0, 1]:
+                rc, msg, (prim, sec, deg) = R.allocate_samples(st, eps, kind)
+                allocation.append({"set": si, "eps": eps.hex(), "kind": kind, "rc": rc,
+                                   "msg": msg, "primary": prim, "secondary": sec,
+                                   "degenerate": deg})
+    bad_alloc = []
+    for st, eps in [([], 1e-3), (sets[0], 0.0), (sets[0], -1.0)]:
+        rc, msg, _ = R.allocate_samples(st, eps, 1)
+        bad_alloc.append({"n": len(st), "eps": eps.hex(), "rc": rc, "msg": msg})
+    times = []
+    for si, st in enumerate(sets):
+        rc, msg, (th, tb) = R.predicted_times(st, 1e-3)
+        times.append({"set": si, "eps": (1e-3).hex(), "rc": rc, "t_hat": th.hex(),
+                      "t_bar": tb.hex()})
+    speedup = []
+    for si, st in enumerate(sets):
+        for li, row in enumerate(st):
+            rc, msg, (v, flag) = R.per_level_speedup(row)
+            speedup.append({"set": si, "level": li, "rc": rc, "msg": msg, "value": v.hex(),
+                            "cost_ratio_only": flag})
+
+    nested = []
+    for max_level, m, approx, kahan, eps in [(4, 10, "linear:16", 0, 1e-3),
+                                             (3, 23, "linear:16", 1, 2e-3),
+                                             (3, 52, "exact", 0, 5e-3),
+                                             (0, 10, "linear:8", 0, 1e-2)]:
+        rc, msg, r = R.run_nested_estimator(max_level=max_level, mantissa_bits=m, approx=approx,
+                                            kahan=kahan, eps=eps, threads=threads)
+        assert rc == 0, msg
+        nested.append({"max_level": max_level, "m": m, "approx": approx, "kahan": kahan,
+                       "eps": eps.hex(), "seed": 1, "pilot_paths": 1000,
+                       "value": r["value"].hex(), "t_hat": r["t_hat"].hex(),
+                       "t_bar": r["t_bar"].hex(), "degenerate": r["degenerate"],
+                       "contributions": hx(r["contributions"]), "pilot": hx(r["pilot"]),
+                       "primary": r["primary"], "secondary": r["secondary"]})
+    nested_errors = []
+    for max_level, eps, pilot in [(-1, 1e-3, 1000), (2, 0.0, 1000), (2, 1e-3, 1)]:
+        rc, msg, _ = R.run_nested_estimator(max_level=max_level, mantissa_bits=10,
+                                            approx="linear:16", eps=eps, pilot_paths=pilot)
+        nested_errors.append({"max_level": max_level, "eps": eps.hex(), "pilot_paths": pilot,
+                              "rc": rc, "msg": msg})
+
+    doc = {"generator": "tests/golden/gen_golden.py callers (reference: "
+                        "/root/reference/proj/include, oracle/ref_driver.cpp)",
+           "stats_fields": list(Reference.STATS_FIELDS),
+           "stats_sets": [[{k: float(v).hex() for k, v in d.items()} for d in st] for st in sets],
+           "two_way_paths": two_way_paths, "two_way_rows": two_way_rows,
+           "allocation": allocation, "allocation_errors": bad_alloc, "times": times,
+           "speedup": speedup, "nested": nested, "nested_errors": nested_errors}
+    with open(os.path.join(OUT, "callers_vectors.json"), "w") as f:
+        json.dump(doc, f, indent=0)
+    print("wrote", os.path.join(OUT, "callers_vectors.json"))
+
+
 if __name__ == "__main__":
-    main()
+    if sys.argv[1:] == ["callers"]:
+        callers()
+    else:
+        main()
+        callers()

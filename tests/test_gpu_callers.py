@@ -1,0 +1,169 @@
+"""GPU parity of the callers above the level sampler:
+the two-way sampler (simulate_two_way, sde.hpp:162-196) and experiment
+(experiments.hpp:119-151), the concurrent multi-run entry point, and the
+nested estimator (mlmc.hpp:244-283), against fixtures from the unmodified
+reference (tests/golden/callers_vectors.json) and the C oracle.
+
+Contract: as test_gpu_parity.py -- table-driven bar legs bitwise, all legs
+bitwise given the device's own exact Gaussians (oracle replay), carrier legs
+within libm tolerance of glibc; allocation counts equal; estimator
+contributions within 1e-12 absolute (means of O(1e-3)-variance differences).
+"""
+from __future__ import annotations
+
+import json
+import os
+
+import numpy as np
+import pytest
+
+from conftest import ROOT, bits, unhex
+
+pytestmark = pytest.mark.gpu
+
+CALLERS = os.path.join(ROOT, "tests", "golden", "callers_vectors.json")
+
+
+@pytest.fixture(scope="module")
+def cv():
+    with open(CALLERS) as f:
+        return json.load(f)
+
+
+def _table(lib, name):
+    return None if name == "exact" else lib.InvCdfApprox.parse(name)
+
+
+@pytest.mark.parametrize("idx", range(0, 72))
+def test_two_way_paths_vs_reference(gpu, cv, oracle, idx):
+    cases = cv["two_way_paths"]
+    if idx >= len(cases):
+        pytest.skip("fewer cases")
+    c = cases[idx]
+    want = unhex(c["out"]).reshape(-1, 2)
+    n = want.shape[0]
+    out, z = gpu.simulate_paths(gpu.make_gbm(), c["level"], gpu.PrecisionSpec(c["m"]),
+                                _table(gpu, c["approx"]), bool(c["kahan"]), n, c["seed"],
+                                c["path_base"], want_z=True, legs="fine")
+    assert not out[:, [1, 3]].any()  # no coarse legs
+    # the two-way legs are the coupled sampler's fine legs: bitwise == the
+    # oracle's coupled replay on the device's own Gaussians
+    cfg = oracle.config(level=c["level"], mantissa_bits=c["m"], approx=c["approx"],
+                        kahan=c["kahan"], seed=c["seed"])
+    rep, _, fails = oracle.simulate(cfg, c["path_base"], n, z_in=z)
+    assert not fails
+    assert np.array_equal(bits(out[:, [0, 2]]), bits(rep[:, [0, 2]]))
+    if c["approx"] != "exact":
+        assert np.array_equal(bits(out[:, 2]), bits(want[:, 1]))
+    np.testing.assert_allclose(out[:, 0], want[:, 0], rtol=1e-12, atol=1e-300)
+
+
+def test_two_way_moments_sequential_bitwise(gpu, oracle):
+    """lpmc_run_two_way_paths (sequential order) == the reference's
+    run_batched merge of x_hat - x_bar over the device's own paths."""
+    model = gpu.make_gbm()
+    sp, tb = gpu.PrecisionSpec.fp16(), gpu.InvCdfApprox.parse("linear:16")
+    for level, n, base in [(0, 700, 5), (4, 2049, 1 << 40), (7, 513, 123)]:
+        out, _ = gpu.simulate_paths(model, level, sp, tb, True, n, 9, base, legs="fine")
+        m = gpu.run_two_way_paths(model, level, sp, tb, True, n, 9, base, reduce="sequential")
+        want = oracle.sequential_from_values(out[:, 0] - out[:, 2], np.zeros(n))
+        assert m.state() == tuple(want[0])
+
+
+def test_two_way_experiment_vs_reference(gpu, cv):
+    from paper_2012_09739_b200.experiments import ExperimentConfig, run_two_way_experiment
+    for row in cv["two_way_rows"]:
+        cfg = ExperimentConfig(precisions=[row["precision"]], approx=row["approx"],
+                               kahan=bool(row["kahan"]), level_min=row["level_min"],
+                               level_max=row["level_max"], paths=[row["paths"]])
+        got = run_two_way_experiment(cfg, reduce="sequential")
+        want = [unhex(r) for r in row["rows"]]
+        assert len(got) == len(want)
+        for g, w in zip(got, want):
+            assert g.n_steps == int(w[0]) and g.paths == int(w[3])
+            # x_hat carries the device's exact Gaussians: libm-level deviations
+            np.testing.assert_allclose([g.variance, g.stderr_variance], w[1:3], rtol=1e-8)
+
+
+def test_run_coupled_many_equals_separate_calls(gpu):
+    model = gpu.make_gbm()
+    P = gpu.PrecisionSpec
+    tb = gpu.InvCdfApprox.parse("linear:16")
+    runs = []
+    for i in range(21):  # > 16 streams: slots are reused in order
+        level = i % 7
+        spec = [P.fp32(), P.fp16(), P.bf16(), P.carrier()][i % 4]
+        runs.append((level, spec, bool(i % 2), [3000, 1, 0, 70000, 256][i % 5], (i << 36) + 17))
+    many = gpu.run_coupled_many(model, tb, 5, runs)
+    for (level, spec, kahan, n, base), m in zip(runs, many):
+        one = gpu.run_coupled_paths(model, level, spec, tb, kahan, n, 5, base)
+        assert [m.d_hat.state(), m.d_bar.state(), m.d_four.state()] == \
+               [one.d_hat.state(), one.d_bar.state(), one.d_four.state()]
+
+
+def test_run_coupled_many_error_order(gpu):
+    model = gpu.make_gbm()
+    P = gpu.PrecisionSpec
+    car = P.carrier()
+    with pytest.raises(gpu.InvalidArgument, match="level must be >= 0"):
+        gpu.run_coupled_many(model, None, 1, [(2, car, False, 10, 0), (-1, car, False, 4, 0)])
+    # n = 0 runs are skipped without validation, as run_coupled_paths does
+    assert gpu.run_coupled_many(model, None, 1, [(-1, car, False, 0, 0)])[0].d_hat.count() == 0
+    bad = gpu.make_gbm(1e30, 0.0, 1e300)
+    with pytest.raises(gpu.DomainError) as ei:
+        gpu.run_coupled_many(bad, None, 1, [(3, car, False, 0, 5), (3, car, False, 8, 200),
+                                            (3, car, False, 8, 100)])
+    assert ei.value.path_index == 200  # the first failing run in list order
+
+
+@pytest.mark.parametrize("idx", range(4))
+def test_nested_estimator_vs_reference(gpu, cv, idx):
+    n = cv["nested"][idx]
+    r = gpu.run_nested_estimator(gpu.make_gbm(), n["max_level"], gpu.PrecisionSpec(n["m"]),
+                                 _table(gpu, n["approx"]), bool(n["kahan"]),
+                                 float.fromhex(n["eps"]), n["seed"],
+                                 pilot_paths=n["pilot_paths"], reduce="sequential")
+    assert r.allocation.primary == n["primary"]
+    assert r.allocation.secondary == n["secondary"]
+    assert r.allocation.degenerate == n["degenerate"]
+    pilot = unhex(n["pilot"]).reshape(-1, 16)
+    for s, w in zip(r.pilot_stats, pilot):
+        got = [s.mean_hat, s.v_hat, s.v_hat_stderr, s.mean_bar, s.v_bar, s.v_bar_stderr,
+               s.mean_four, s.V_bar, s.V_bar_stderr, s.c_hat, s.c_bar, s.C_bar, s.m_hat,
+               s.m_bar, s.M_bar, s.level]
+        np.testing.assert_array_equal(got[9:], w[9:])
+        if n["approx"] != "exact":  # bar legs bitwise, sequential order
+            assert [s.mean_bar, s.v_bar, s.v_bar_stderr] == list(w[3:6])
+        np.testing.assert_allclose(got[:9], w[:9], rtol=1e-9, atol=1e-15)
+    np.testing.assert_allclose(r.level_contributions, unhex(n["contributions"]), rtol=0,
+                               atol=1e-12)
+    assert abs(r.value - float.fromhex(n["value"])) <= 1e-12
+    np.testing.assert_allclose([r.times.t_hat, r.times.t_bar],
+                               [float.fromhex(n["t_hat"]), float.fromhex(n["t_bar"])], rtol=1e-9)
+
+
+def test_nested_estimator_errors(gpu, cv):
+    for e in cv["nested_errors"]:
+        with pytest.raises(gpu.InvalidArgument, match=e["msg"]):
+            gpu.run_nested_estimator(gpu.make_gbm(), e["max_level"], gpu.PrecisionSpec.fp16(),
+                                     gpu.InvCdfApprox.parse("linear:16"), False,
+                                     float.fromhex(e["eps"]), 1, pilot_paths=e["pilot_paths"])
+
+
+def test_four_way_experiment_matches_level_stats(gpu):
+    """run_four_way_experiment (concurrent) == its definition as three
+    estimate_level_stats calls per level (experiments.hpp:185-194)."""
+    from paper_2012_09739_b200.experiments import ExperimentConfig, run_four_way_experiment
+    cfg = ExperimentConfig(precisions=["fp16", "fp32"], approx="linear:16", level_min=0,
+                           level_max=5, paths=[3000])
+    out = run_four_way_experiment(cfg)
+    assert len(out.rows) == 6 * 6
+    P = gpu.PrecisionSpec
+    tb = gpu.InvCdfApprox.parse("linear:16")
+    for i, level in enumerate(range(0, 6)):
+        for got, spec, kahan, phase in ((out.low_stats[i], P.fp16(), False, 0),
+                                        (out.low_kahan_stats[i], P.fp16(), True, 1),
+                                        (out.high_stats[i], P.fp32(), False, 2)):
+            want = gpu.estimate_level_stats(gpu.make_gbm(), level, spec, tb, kahan, 3000, 1,
+                                            path_base=(level << 40) | (phase << 36))
+            assert got == want
