@@ -64,7 +64,7 @@ def test_two_way_moments_sequential_bitwise(gpu, oracle):
     model = gpu.make_gbm()
     sp, tb = gpu.PrecisionSpec.fp16(), gpu.InvCdfApprox.parse("linear:16")
     for level, n, base in [(0, 700, 5), (4, 2049, 1 << 40), (7, 513, 123)]:
-        out, _ = gpu.simulate_paths(model, level, sp, tb, True, n, 9, base, legs="fine")
+        out = gpu.simulate_paths(model, level, sp, tb, True, n, 9, base, legs="fine")
         m = gpu.run_two_way_paths(model, level, sp, tb, True, n, 9, base, reduce="sequential")
         want = oracle.sequential_from_values(out[:, 0] - out[:, 2], np.zeros(n))
         assert m.state() == tuple(want[0])
@@ -167,3 +167,20 @@ def test_four_way_experiment_matches_level_stats(gpu):
             want = gpu.estimate_level_stats(gpu.make_gbm(), level, spec, tb, kahan, 3000, 1,
                                             path_base=(level << 40) | (phase << 36))
             assert got == want
+
+
+def test_cpp_api_device_part(gpu):
+    """tests/cpp/api_smoke.cpp (reference-shaped C++ unit tests, incl. the
+    nested-estimator pins test_mlmc.cpp:204-236) on the device."""
+    import subprocess
+    import tempfile
+    from paper_2012_09739_b200 import _native as N
+    src = os.path.join(ROOT, "tests", "cpp", "api_smoke.cpp")
+    with tempfile.TemporaryDirectory() as d:
+        exe = os.path.join(d, "api_smoke")
+        subprocess.check_call(["g++", "-std=c++20", "-O1", "-I", os.path.join(ROOT, "include"), src,
+                               "-o", exe, "-L", os.path.dirname(N.LIB_PATH), "-llpmc_b200",
+                               "-Wl,-rpath," + os.path.dirname(N.LIB_PATH)])
+        out = subprocess.run([exe], capture_output=True, text=True, timeout=600)
+        assert out.returncode == 0, out.stdout + out.stderr
+        assert "device ok" in out.stdout
