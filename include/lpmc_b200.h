@@ -29,6 +29,7 @@
  *   lpmc_predicted_times        <- predicted_times         include/lpmc/mlmc.hpp:202-213
  *   lpmc_per_level_speedup      <- per_level_speedup       include/lpmc/mlmc.hpp:223-230
  *   lpmc_run_nested_estimator   <- run_nested_estimator    include/lpmc/mlmc.hpp:244-283
+ *   lpmc_step_error_probe       <- step_error_probe        include/lpmc/sde.hpp:297-344
  *
  * Error contract: every entry point returns an lpmc_status.  The values map
  * one-to-one onto the exception types the reference throws
@@ -360,6 +361,24 @@ lpmc_status lpmc_run_nested_estimator(const lpmc_gbm* model, int32_t max_level,
                                       uint64_t seed, const lpmc_cost_model* cost,
                                       uint64_t pilot_paths, const lpmc_options* opts,
                                       lpmc_estimator_result* out, lpmc_error* err);
+
+/* StepErrorStats (sde.hpp:289-295). */
+typedef struct lpmc_step_error_stats {
+  double mean_eta, mean_abs_eta, mean_eta_prime, mean_abs_eta_prime;
+  uint64_t samples;
+} lpmc_step_error_stats;
+
+/*
+ * step_error_probe (sde.hpp:297-344): per-step rounding residuals eta (outer
+ * add) and eta' (inner sum) along the low-precision paths 0, 1, ... of
+ * `seed` at `level`, n_samples steps in total (the last path truncated).
+ * One path per device thread; the means differ from the reference's single
+ * sequential sum only by summation order.  ieee_half is not supported.
+ */
+lpmc_status lpmc_step_error_probe(const lpmc_gbm* model, int32_t level,
+                                  const lpmc_precision* prec, const lpmc_invcdf_table* table,
+                                  uint64_t n_samples, uint64_t seed, const lpmc_options* opts,
+                                  lpmc_step_error_stats* out, lpmc_error* err);
 
 /* ---- plans: device-resident repeated launches (bench / sweeps) ---------- */
 typedef struct lpmc_plan lpmc_plan;

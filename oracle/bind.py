@@ -318,6 +318,8 @@ class Reference:
         L.ref_simulate_two_way.argtypes = [C.c_double] * 4 + [C.c_int, C.c_int, C.c_char_p,
                                                               C.c_int, _u64, _u64, _u64, _dp,
                                                               C.c_char_p, C.c_int]
+        L.ref_step_error_probe.argtypes = [C.c_double] * 4 + [C.c_int, C.c_int, C.c_char_p, _u64,
+                                                              _u64, _dp, C.c_char_p, C.c_int]
         L.ref_two_way_experiment.argtypes = [C.c_double] * 4 + [
             C.c_char_p, C.c_char_p, C.c_int, C.c_int, C.c_int, _u64, _u64, C.c_int, _dp,
             C.c_char_p, C.c_int]
@@ -482,3 +484,11 @@ class Reference:
                                              approx.encode(), int(kahan), level_min, level_max,
                                              paths, seed, threads, _ptr(out), msg, 256)
         return rc, msg.value.decode(), out[:4 * rows].reshape(rows, 4)
+
+    def step_error_probe(self, *, level, mantissa_bits, approx="exact", n_samples=10000, seed=1,
+                         mu=0.05, sigma=0.2, x0=1.0, horizon=1.0):
+        out = np.zeros(5)
+        msg = C.create_string_buffer(256)
+        rc = self.lib.ref_step_error_probe(mu, sigma, x0, horizon, level, mantissa_bits,
+                                           approx.encode(), n_samples, seed, _ptr(out), msg, 256)
+        return rc, msg.value.decode(), out

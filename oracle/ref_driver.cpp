@@ -388,6 +388,25 @@ int ref_two_way_experiment(double mu, double sigma, double x0, double horizon,
   });
 }
 
+// step_error_probe (sde.hpp:297): out5 = {mean_eta, mean_abs_eta,
+// mean_eta_prime, mean_abs_eta_prime, samples}.
+int ref_step_error_probe(double mu, double sigma, double x0, double horizon, int level,
+                         int mantissa_bits, const char* approx, uint64_t n_samples, uint64_t seed,
+                         double* out5, char* msg, int len) {
+  return guarded(msg, len, [&] {
+    const lpmc::SdeModel model = lpmc::make_gbm(mu, sigma, x0, horizon);
+    const lpmc::InvCdfApprox* t = table_for(approx);
+    lpmc::StepErrorStats r = lpmc::step_error_probe(model, lpmc::LevelSpec{level, horizon},
+                                                    lpmc::PrecisionSpec{mantissa_bits}, t,
+                                                    n_samples, seed);
+    out5[0] = r.mean_eta;
+    out5[1] = r.mean_abs_eta;
+    out5[2] = r.mean_eta_prime;
+    out5[3] = r.mean_abs_eta_prime;
+    out5[4] = static_cast<double>(r.samples);
+  });
+}
+
 int ref_hardware_threads() { return static_cast<int>(std::thread::hardware_concurrency()); }
 
 }  // extern "C"

@@ -122,6 +122,12 @@ class EstimatorResultC(C.Structure):
                 ("secondary", C.POINTER(_u64))]
 
 
+class StepErrorStatsC(C.Structure):
+    _fields_ = [("mean_eta", C.c_double), ("mean_abs_eta", C.c_double),
+                ("mean_eta_prime", C.c_double), ("mean_abs_eta_prime", C.c_double),
+                ("samples", _u64)]
+
+
 # exported symbol -> (restype, argtypes); the CPU test suite checks every
 # symbol include/lpmc_b200.h declares is exported and bound here.
 _P = C.POINTER
@@ -165,6 +171,8 @@ SIGNATURES = {
     "lpmc_run_nested_estimator": (_i32, [_P(Gbm), _i32, _P(Precision), _P(InvCdfTable), _i32,
                                          C.c_double, _u64, _P(CostModelC), _u64, _P(Options),
                                          _P(EstimatorResultC), _P(Error)]),
+    "lpmc_step_error_probe": (_i32, [_P(Gbm), _i32, _P(Precision), _P(InvCdfTable), _u64, _u64,
+                                     _P(Options), _P(StepErrorStatsC), _P(Error)]),
     "lpmc_plan_create": (_i32, [_P(Gbm), _i32, _P(Precision), _P(InvCdfTable), _i32, _u64, _u64,
                                 _u64, _P(Options), _P(C.c_void_p), _P(Error)]),
     "lpmc_plan_create_range": (_i32, [_P(Gbm), _i32, _P(Precision), _P(InvCdfTable), _i32, _u64,

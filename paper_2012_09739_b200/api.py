@@ -25,6 +25,8 @@ SpeedupResult,              mlmc.hpp:215-230
 per_level_speedup
 EstimatorResult,            mlmc.hpp:232-283  (device: lpmc_run_nested_estimator)
 run_nested_estimator
+StepErrorStats,             sde.hpp:289-344   (device: lpmc_step_error_probe)
+step_error_probe
 ==========================  ================================================
 
 Every sampling call runs on the sm_100a kernels through the C-ABI; there is
@@ -737,3 +739,28 @@ def run_nested_estimator(model: SdeModel, max_level: int, spec_low: PrecisionSpe
         allocation=Allocation([int(x) for x in prim], [int(x) for x in sec],
                               bool(res.degenerate)),
         times=PredictedTimes(res.t_hat, res.t_bar), eps=res.eps)
+
+
+# ---------------------------------------- step-error probe (sde.hpp:289-344) --
+@dataclass
+class StepErrorStats:
+    mean_eta: float = 0.0
+    mean_abs_eta: float = 0.0
+    mean_eta_prime: float = 0.0
+    mean_abs_eta_prime: float = 0.0
+    samples: int = 0
+
+
+def step_error_probe(model: SdeModel, level: int, spec: PrecisionSpec,
+                     approx: Optional[InvCdfApprox], n_samples: int, seed: int,
+                     **ext) -> StepErrorStats:
+    """step_error_probe (sde.hpp:297-344) on the device: eta / eta' residual
+    means over n_samples steps of the paths 0, 1, ... of ``seed``."""
+    out = N.StepErrorStatsC()
+    err = N.Error()
+    opts = _options(**ext)
+    N.check(N.load().lpmc_step_error_probe(C.byref(_gbm_c(model)), int(level), C.byref(spec._c()),
+                                           _table_ptr(approx), int(n_samples), int(seed),
+                                           C.byref(opts), C.byref(out), C.byref(err)), err)
+    return StepErrorStats(out.mean_eta, out.mean_abs_eta, out.mean_eta_prime,
+                          out.mean_abs_eta_prime, int(out.samples))

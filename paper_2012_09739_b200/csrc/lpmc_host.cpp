@@ -1274,6 +1274,97 @@ lpmc_status lpmc_level_partials(const lpmc_gbm* model, int32_t level,
   return ok(err);
 }
 
+lpmc_status lpmc_step_error_probe(const lpmc_gbm* model, int32_t level,
+                                  const lpmc_precision* prec, const lpmc_invcdf_table* table,
+                                  uint64_t n_samples, uint64_t seed, const lpmc_options* opts,
+                                  lpmc_step_error_stats* out, lpmc_error* err) {
+  // step_error_probe (sde.hpp:297-344)
+  *out = lpmc_step_error_stats{0.0, 0.0, 0.0, 0.0, 0};
+  if (prec != nullptr && prec->ieee_half)
+    return fail(err, LPMC_INVALID_ARGUMENT, "step-error probe needs an emulated precision");
+  if (level > 40) return fail(err, LPMC_INVALID_ARGUMENT, "level must be <= 40");
+  const double nan = std::nan("");
+  if (n_samples == 0) {  // no step taken: 0 / 0 (sde.hpp:338-342)
+    *out = lpmc_step_error_stats{nan, nan, nan, nan, 0};
+    return ok(err);
+  }
+  const uint64_t n_steps = level >= 0 ? (1ull << level) : 1;
+  const uint64_t n_paths = (n_samples + n_steps - 1) / n_steps;
+  const uint64_t last_steps = n_samples - (n_paths - 1) * n_steps;
+  lpmc_options o;
+  lpmc_default_options(&o);
+  if (opts != nullptr) o = *opts;
+  o.legs = LPMC_LEGS_BAR;
+  RunSpec s;
+  lpmc_status st = build_spec(model, level, prec, table, 0, n_paths, seed, 0, &o, &s, err);
+  if (st != LPMC_OK) return st;
+  DeviceCtx* ctx = nullptr;
+  int dev = -1;
+  st = get_ctx(s.device, &ctx, &dev, err);
+  if (st != LPMC_OK) return st;
+  DeviceGuard guard;
+  cudaError_t e = guard.set(dev);
+  if (e != cudaSuccess) return cuda_fail(err, e, "cudaSetDevice");
+  std::lock_guard<std::mutex> lock(ctx->mu);
+  cudaStream_t stream = o.stream != nullptr ? static_cast<cudaStream_t>(o.stream) : ctx->stream;
+  Buffers& B = ctx->scratch;
+  const uint64_t blocks = (n_paths + 255) / 256;
+  std::vector<double> sums(4 * blocks);
+  for (int attempt = 0; attempt < 2; ++attempt) {
+    LevelArgs A = s.args;
+    if ((e = B.err_key.ensure(1)) != cudaSuccess) break;
+    if ((e = B.range_flag.ensure(1)) != cudaSuccess) break;
+    if ((e = B.batch_acc.ensure(4 * blocks)) != cudaSuccess) break;
+    if ((e = cudaMemsetAsync(B.err_key.ptr, 0xff, sizeof(unsigned long long), stream)) != cudaSuccess) break;
+    if ((e = cudaMemsetAsync(B.range_flag.ptr, 0, sizeof(unsigned int), stream)) != cudaSuccess) break;
+    A.err_key = B.err_key.ptr;
+    A.range_flag = B.range_flag.ptr;
+    A.table = nullptr;
+    if (s.has_table) {
+      if ((e = B.table.ensure(s.table.rows.size())) != cudaSuccess) break;
+      if ((e = cudaMemcpyAsync(B.table.ptr, s.table.rows.data(), s.table.rows.size() * sizeof(double),
+                               cudaMemcpyHostToDevice, stream)) != cudaSuccess)
+        break;
+      A.table = B.table.ptr;
+    }
+    if ((e = launch_step_error(A, s.arith, last_steps, B.batch_acc.ptr, stream)) != cudaSuccess) break;
+    t_launches += 1;
+    unsigned long long key = ~0ull;
+    unsigned int range = 0;
+    e = cudaMemcpyAsync(&key, B.err_key.ptr, sizeof key, cudaMemcpyDeviceToHost, stream);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(&range, B.range_flag.ptr, sizeof range, cudaMemcpyDeviceToHost, stream);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(sums.data(), B.batch_acc.ptr, 4 * blocks * sizeof(double),
+                          cudaMemcpyDeviceToHost, stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
+    if (e != cudaSuccess) break;
+    if (range != 0 && (s.arith == BarArith::kF32 || s.arith == BarArith::kF32Round)) {
+      s.arith = BarArith::kF64Round;  // exact emulation outside the native range
+      continue;
+    }
+    if (key != ~0ull) {
+      const uint64_t path = key >> 24;
+      const int kind = static_cast<int>((key >> 22) & 3u);
+      const uint64_t step = key & ((1ull << 22) - 1);
+      if (kind == LPMC_FAIL_UNIFORM_IS_ONE)
+        return fail(err, LPMC_DOMAIN_ERROR,
+                    table != nullptr ? "approx_inv_cdf requires u in (0, 1)"
+                                     : "exact_inv_cdf requires u in (0, 1)",
+                    kind, path, step);
+      return fail(err, LPMC_DOMAIN_ERROR, "non-finite operand", LPMC_FAIL_NONFINITE, path, step);
+    }
+    double tot[4] = {0.0, 0.0, 0.0, 0.0};
+    for (uint64_t b = 0; b < blocks; ++b)
+      for (int q = 0; q < 4; ++q) tot[q] += sums[4 * b + q];
+    const double count = static_cast<double>(n_samples);
+    *out = lpmc_step_error_stats{tot[0] / count, tot[1] / count, tot[2] / count, tot[3] / count,
+                                 n_samples};
+    return ok(err);
+  }
+  if (e != cudaSuccess) return cuda_fail(err, e, "step-error probe");
+  return fail(err, LPMC_RUNTIME_ERROR, "native range fallback did not converge");
+}
+
 lpmc_status lpmc_simulate_paths(const lpmc_gbm* model, int32_t level, const lpmc_precision* prec,
                                 const lpmc_invcdf_table* table, int32_t kahan, uint64_t n_paths,
                                 uint64_t seed, uint64_t path_base, const lpmc_options* opts,

@@ -100,6 +100,10 @@ cudaError_t configure_level_f32();
 cudaError_t configure_level_f32r();
 cudaError_t configure_level_f64r();
 cudaError_t configure_level_half2();
+cudaError_t configure_probe();
 #endif
+// step_error_probe (lpmc_probe.cu): block_sums = 4 per 256-path block
+cudaError_t launch_step_error(const LevelArgs& A, BarArith arith, uint64_t last_steps,
+                              double* block_sums, void* stream);
 
 }  // namespace lpmc_b200

@@ -171,6 +171,7 @@ int configure_kernels() {
   if (e == cudaSuccess) e = configure_level_f32r();
   if (e == cudaSuccess) e = configure_level_f64r();
   if (e == cudaSuccess) e = configure_level_half2();
+  if (e == cudaSuccess) e = configure_probe();
   return static_cast<int>(e);
 }
 

@@ -11,6 +11,8 @@ FourWayRow / FourWayOutput  experiments.hpp:154-216 (three estimate_level_stats
 run_four_way_experiment       per level: low, low+Kahan, high)
 SpeedupRow /                experiments.hpp:218-246 (per_level_speedup)
 run_speedup_report
+StepErrorRow /              experiments.hpp:297-319 (device step_error_probe)
+run_step_error_report
 ==========================  ================================================
 
 Same path bases, path counts and merge order as the reference, so every row
@@ -26,7 +28,8 @@ from dataclasses import dataclass, field
 from typing import List, Optional
 
 from .api import (CostModel, InvalidArgument, InvCdfApprox, LevelStats, PrecisionSpec,
-                  level_stats_from_moments, make_gbm, per_level_speedup, run_coupled_many)
+                  StepErrorStats, level_stats_from_moments, make_gbm, per_level_speedup,
+                  run_coupled_many, step_error_probe)
 
 
 @dataclass
@@ -187,3 +190,22 @@ def run_speedup_report(high_stats, low_stats, low_kahan_stats) -> List[SpeedupRo
             rows.append(SpeedupRow(low_kahan_stats[i].level, "half_kahan", r.value,
                                    r.cost_ratio_only))
     return rows
+
+
+@dataclass
+class StepErrorRow:
+    level: int
+    stats: StepErrorStats
+
+
+def run_step_error_report(config: ExperimentConfig, samples: int, **ext) -> List[StepErrorRow]:
+    """experiments.hpp:302-319."""
+    config.validate()
+    if samples < 10000:
+        raise InvalidArgument("step-error probe needs >= 1e4 samples")
+    approx = config.build_approx()
+    spec = PrecisionSpec.parse(config.precisions[0])
+    model = config.model()
+    return [StepErrorRow(level, step_error_probe(model, level, spec, approx, samples, config.seed,
+                                                 **ext))
+            for level in range(config.level_min, config.level_max + 1)]

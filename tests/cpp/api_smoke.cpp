@@ -179,6 +179,18 @@ int main(int argc, char** argv) {
     CHECK(report.size() == 12);
   }
 
+  // step-error probe (sde.hpp:297-344) and its report
+  {
+    auto lin = InvCdfApprox::parse("linear:16");
+    auto st = step_error_probe(gbm, LevelSpec{3, 1.0}, PrecisionSpec::fp16(), &lin, 20000, 1);
+    CHECK(st.samples == 20000 && st.mean_abs_eta > 0.0 && st.mean_abs_eta_prime > 0.0);
+    ExperimentConfig cfg;
+    cfg.approx = "linear:16";
+    cfg.level_max = 2;
+    CHECK(run_step_error_report(cfg, 10000).size() == 3);
+    CHECK(throws<std::invalid_argument>([&] { run_step_error_report(cfg, 9999); }));
+  }
+
   // non-GBM models are rejected (no CPU fallback)
   SdeModel custom = gbm;
   custom.gbm.reset();

@@ -232,13 +232,29 @@ def callers():
         nested_errors.append({"max_level": max_level, "eps": eps.hex(), "pilot_paths": pilot,
                               "rc": rc, "msg": msg})
 
+    probe = []
+    for level, m, approx, n_samples, seed in [(0, 10, "linear:16", 100000, 1),
+                                              (3, 23, "linear:16", 100000, 2),
+                                              (6, 7, "cubic:64", 65536 + 123, 3),
+                                              (10, 10, "exact", 50000, 1),
+                                              (2, 52, "linear:16", 10000, 4),
+                                              (4, 23, "exact", 100000, 5),
+                                              (12, 16, "linear:1024", 10000, 6),
+                                              (5, 10, "linear:16", 0, 1)]:
+        rc, msg, out = R.step_error_probe(level=level, mantissa_bits=m, approx=approx,
+                                          n_samples=n_samples, seed=seed)
+        assert rc == 0, msg
+        probe.append({"level": level, "m": m, "approx": approx, "n_samples": n_samples,
+                      "seed": seed, "out": hx(out)})
+
     doc = {"generator": "tests/golden/gen_golden.py callers (reference: "
                         "/root/reference/proj/include, oracle/ref_driver.cpp)",
            "stats_fields": list(Reference.STATS_FIELDS),
            "stats_sets": [[{k: float(v).hex() for k, v in d.items()} for d in st] for st in sets],
            "two_way_paths": two_way_paths, "two_way_rows": two_way_rows,
            "allocation": allocation, "allocation_errors": bad_alloc, "times": times,
-           "speedup": speedup, "nested": nested, "nested_errors": nested_errors}
+           "speedup": speedup, "nested": nested, "nested_errors": nested_errors,
+           "step_error": probe}
     with open(os.path.join(OUT, "callers_vectors.json"), "w") as f:
         json.dump(doc, f, indent=0)
     print("wrote", os.path.join(OUT, "callers_vectors.json"))

@@ -184,3 +184,50 @@ def test_cpp_api_device_part(gpu):
         out = subprocess.run([exe], capture_output=True, text=True, timeout=600)
         assert out.returncode == 0, out.stdout + out.stderr
         assert "device ok" in out.stdout
+
+
+# ------------------------------------------------ step_error_probe (row 3) --
+EPS = 2.0 ** -52
+
+
+@pytest.mark.parametrize("idx", range(8))
+def test_step_error_probe_vs_reference(gpu, cv, idx):
+    c = cv["step_error"][idx]
+    want = unhex(c["out"])
+    r = gpu.step_error_probe(gpu.make_gbm(), c["level"], gpu.PrecisionSpec(c["m"]),
+                             _table(gpu, c["approx"]), c["n_samples"], c["seed"])
+    got = np.array([r.mean_eta, r.mean_abs_eta, r.mean_eta_prime, r.mean_abs_eta_prime,
+                    r.samples], dtype=np.float64)
+    n = c["n_samples"]
+    if n == 0:  # 0 / 0, as the reference
+        assert np.all(np.isnan(got[:4])) and r.samples == 0
+        return
+    assert r.samples == n
+    if c["approx"] != "exact":
+        # identical residuals, different summation order: both sums are within
+        # n eps sum|r| of the exact sum (Higham), so of each other within 2x
+        for k, ak in ((0, 1), (1, 1), (2, 3), (3, 3)):
+            assert abs(got[k] - want[k]) <= 2 * n * EPS * want[ak] + 1e-300, (k, got, want)
+    else:
+        # Gaussians from the device libm: R(z) to m <= 23 bits absorbs nearly
+        # every last-ulp difference; the rare flipped rounding moves a mean
+        # by one residual / n
+        np.testing.assert_allclose(got[[1, 3]], want[[1, 3]], rtol=1e-3)
+        assert abs(got[0] - want[0]) <= 1e-3 * want[1]
+        assert abs(got[2] - want[2]) <= 1e-3 * want[3]
+
+
+def test_step_error_probe_errors_and_report(gpu):
+    from paper_2012_09739_b200.experiments import ExperimentConfig, run_step_error_report
+    with pytest.raises(gpu.InvalidArgument):
+        gpu.step_error_probe(gpu.make_gbm(), 3, gpu.PrecisionSpec.fp16_ieee(), None, 100, 1)
+    bad = gpu.make_gbm(1e30, 0.0, 1e300)
+    with pytest.raises(gpu.DomainError, match="non-finite operand") as ei:
+        gpu.step_error_probe(bad, 2, gpu.PrecisionSpec.carrier(), None, 100, 1)
+    assert ei.value.path_index == 0 and ei.value.step == 0
+    cfg = ExperimentConfig(precisions=["fp16"], approx="linear:16", level_min=0, level_max=4)
+    with pytest.raises(gpu.InvalidArgument, match="1e4 samples"):
+        run_step_error_report(cfg, 9999)
+    rows = run_step_error_report(cfg, 20000)
+    assert [r.level for r in rows] == list(range(5))
+    assert all(r.stats.samples == 20000 and r.stats.mean_abs_eta > 0 for r in rows)
