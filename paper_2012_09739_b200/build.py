@@ -61,6 +61,7 @@ def build(force: bool = False, verbose_ptxas: bool = False) -> str:
         o = os.path.join(BUILD, src + ".o")
         if force or _newer(o, [s] + hdrs):
             extra = ["-Xptxas", "-v"] if verbose_ptxas else []
+            extra += os.environ.get("LPMC_NVCC_EXTRA", "").split()  # experiments only
             jobs.append([NVCC] + NVCC_FLAGS + extra + ["-c", s, "-o", o])
         objs.append(o)
     if jobs:  # one translation unit per bar arithmetic: compile in parallel

@@ -96,12 +96,28 @@ struct TableView {
 //    (c0 + c1 t) + 0 p2 + 0 p3 equals c0 + c1 t including the sign of zero.
 //  * lower: u < 1/2 (the sampler passes the integer test on its draw).
 //  * EXACT_HALF: exactly 0 at u = 1/2; the hot loop replays such draws.
-template <bool EXACT_HALF = true>
+//  * TAB == kTabDyadicLinear: the host proved dyadic && simple && degree 1
+//    (every BASELINE table): the same arithmetic without the run-time kind
+//    tests, so a draw's approximate Gaussian is straight-line code.
+enum : int { kTabNone = 0, kTabDyadicLinear = 1, kTabGeneric = 2 };
+
+template <bool EXACT_HALF = true, int TAB = kTabGeneric>
 __device__ __forceinline__ double approx_inv(const TableView& t, double u, bool lower) {
   const double up = lower ? 1.0 - u : u;  // fl(1-u) for the lower half (:47-49)
   const double v = 1.0 - up;              // exact (Sterbenz)
   double r;
-  if (t.dyadic) {
+  if constexpr (TAB == kTabDyadicLinear) {
+    const uint64_t vb = static_cast<uint64_t>(__double_as_longlong(v));
+    const int e = static_cast<int>(vb >> 52) - 1023;
+    const int fl = (vb & 0xFFFFFFFFFFFFFull) == 0 ? -e : -e - 1;  // floor(-log2 v) >= 1
+    const int j = min(fl - 1, t.K - 1);
+    const double* b = t.base + 6 * j;
+    const math::D2 cw = math::load2(b);
+    const math::D2 c01 = math::load2(b + 2);
+    const double s = __fma_rn(up, cw.b, cw.a);
+    r = __dadd_rn(c01.a, __dmul_rn(c01.b, s));
+    r = fl >= t.K + 1 ? t.tail : r;  // w >= w_max: clamped tail
+  } else if (t.dyadic) {
     const uint64_t vb = static_cast<uint64_t>(__double_as_longlong(v));
     const int e = static_cast<int>(vb >> 52) - 1023;
     const int fl = (vb & 0xFFFFFFFFFFFFFull) == 0 ? -e : -e - 1;  // floor(-log2 v) >= 1
@@ -145,9 +161,9 @@ __device__ __forceinline__ double approx_inv(const TableView& t, double u, bool 
   return r;
 }
 
-template <bool EXACT_HALF = true>
+template <bool EXACT_HALF = true, int TAB = kTabGeneric>
 __device__ __forceinline__ double approx_inv(const TableView& t, double u) {
-  return approx_inv<EXACT_HALF>(t, u, u < 0.5);
+  return approx_inv<EXACT_HALF, TAB>(t, u, u < 0.5);
 }
 
 // u < 1/2 <=> b < 2^52 <=> high word < 2^20

@@ -63,7 +63,7 @@ __device__ __forceinline__ void draw_uniforms(uint64_t (&kc)[NP], Uniforms<H * N
 // the next batch are drawn between the Acklam stage and the Newton stage, so
 // the integer RNG interleaves with FP64 work instead of forming its own
 // phase (software pipelining across batches).
-template <class Arith, bool APPROX, bool NEED_EXACT, bool BAR, bool CHECKED, bool DUMP, int H,
+template <class Arith, int TAB, bool NEED_EXACT, bool BAR, bool CHECKED, bool DUMP, int H,
           bool PREFETCH>
 __device__ __forceinline__ void gen_draws(const LevelArgs& A, const TableView& tab,
                                           const double* s_math, const Arith& ar,
@@ -73,8 +73,8 @@ __device__ __forceinline__ void gen_draws(const LevelArgs& A, const TableView& t
                                           const bool (&valid)[Arith::NP], uint64_t n0,
                                           const Uniforms<H * Arith::NP>& cur,
                                           Uniforms<H * Arith::NP>& next,
-                                          double (&z)[4][Arith::NP],
-                                          typename Arith::T (&zb)[4]) {
+                                          double (&z)[H][Arith::NP],
+                                          typename Arith::T (&zb)[H]) {
   constexpr int NP = Arith::NP;
   constexpr int D = H * NP;
   const double(&u)[D] = cur.u;
@@ -117,8 +117,8 @@ __device__ __forceinline__ void gen_draws(const LevelArgs& A, const TableView& t
         if (A.z_out != nullptr && valid[p])
           A.z_out[local[p] * (1ull << A.level) + n0 + h] = z[h][p];
       }
-      if constexpr (APPROX) {
-        zl[p] = approx_inv<CHECKED>(tab, u[h * NP + p]);
+      if constexpr (TAB != kTabNone) {
+        zl[p] = approx_inv<CHECKED, TAB>(tab, u[h * NP + p]);
       } else {
         zl[p] = z[h][p];
       }
@@ -127,7 +127,7 @@ __device__ __forceinline__ void gen_draws(const LevelArgs& A, const TableView& t
   }
 }
 
-template <class Arith, bool KAHAN, int LEGS, bool APPROX, bool CHECKED, bool DUMP>
+template <class Arith, bool KAHAN, int LEGS, int TAB, bool CHECKED, bool DUMP>
 __device__ __forceinline__ void simulate(const LevelArgs& A, const TableView& tab,
                                          const double* s_math,
                                          const uint64_t (&local)[Arith::NP],
@@ -138,7 +138,7 @@ __device__ __forceinline__ void simulate(const LevelArgs& A, const TableView& ta
   constexpr bool kFineOnly = LEGS == 4;  // simulate_two_way (sde.hpp:162-196)
   constexpr bool kHat = (LEGS & 1) != 0 || kFineOnly;
   constexpr bool kBar = (LEGS & 2) != 0 || kFineOnly;
-  constexpr bool kNeedExact = kHat || !APPROX;
+  constexpr bool kNeedExact = kHat || TAB == kTabNone;
 
   const Arith ar(A);
   typename Arith::Range range;
@@ -237,11 +237,11 @@ __device__ __forceinline__ void simulate(const LevelArgs& A, const TableView& ta
 #endif
   constexpr int G = NP == 1 ? LPMC_COARSE_PER_BATCH : 1;  // coarse steps per batch
   if (A.level == 0) {  // sde.hpp:237-249: one draw, fine legs only, coarse := 0
-    double z[4][NP];
-    T zb[4];
+    double z[1][NP];
+    T zb[1];
     Uniforms<NP> cur, unused;
     draw_uniforms<NP, 1>(kc, cur);
-    gen_draws<Arith, APPROX, kNeedExact, kBar, CHECKED, DUMP, 1, false>(
+    gen_draws<Arith, TAB, kNeedExact, kBar, CHECKED, DUMP, 1, false>(
         A, tab, s_math, ar, kc, u1, fk, local, valid, 0, cur, unused, z, zb);
     if constexpr (kHat) hat_fine(z[0], 0);
     if constexpr (kBar) bar_fine(zb[0], 0);
@@ -253,10 +253,10 @@ __device__ __forceinline__ void simulate(const LevelArgs& A, const TableView& ta
       Uniforms<2 * G * NP> cur;
       draw_uniforms<NP, 2 * G>(kc, cur);
       for (uint64_t m = 0; m < halves; m += G) {
-        double z[4][NP];
-        T zb[4];
+        double z[2 * G][NP];
+        T zb[2 * G];
         Uniforms<2 * G * NP> next;
-        gen_draws<Arith, APPROX, kNeedExact, kBar, CHECKED, DUMP, 2 * G, true>(
+        gen_draws<Arith, TAB, kNeedExact, kBar, CHECKED, DUMP, 2 * G, true>(
             A, tab, s_math, ar, kc, u1, fk, local, valid, 2 * m, cur, next, z, zb);
         cur = next;
 #pragma unroll
@@ -269,18 +269,20 @@ __device__ __forceinline__ void simulate(const LevelArgs& A, const TableView& ta
           coarse(z[2 * g], z[2 * g + 1], zb[2 * g], zb[2 * g + 1], n + 1);
         }
       }
-    } else {  // level 1 with G = 2: a single coarse step
-      double z[4][NP];
-      T zb[4];
-      Uniforms<2 * NP> cur, unused;
-      draw_uniforms<NP, 2>(kc, cur);
-      gen_draws<Arith, APPROX, kNeedExact, kBar, CHECKED, DUMP, 2, false>(
-          A, tab, s_math, ar, kc, u1, fk, local, valid, 0, cur, unused, z, zb);
-      if constexpr (kHat) hat_fine(z[0], 0);
-      if constexpr (kBar) bar_fine(zb[0], 0);
-      if constexpr (kHat) hat_fine(z[1], 1);
-      if constexpr (kBar) bar_fine(zb[1], 1);
-      coarse(z[0], z[1], zb[0], zb[1], 1);
+    } else {  // fewer coarse steps than one batch: one coarse step at a time
+      for (uint64_t m = 0; m < halves; ++m) {
+        double z[2][NP];
+        T zb[2];
+        Uniforms<2 * NP> cur, unused;
+        draw_uniforms<NP, 2>(kc, cur);
+        gen_draws<Arith, TAB, kNeedExact, kBar, CHECKED, DUMP, 2, false>(
+            A, tab, s_math, ar, kc, u1, fk, local, valid, 2 * m, cur, unused, z, zb);
+        if constexpr (kHat) hat_fine(z[0], 2 * m);
+        if constexpr (kBar) bar_fine(zb[0], 2 * m);
+        if constexpr (kHat) hat_fine(z[1], 2 * m + 1);
+        if constexpr (kBar) bar_fine(zb[1], 2 * m + 1);
+        coarse(z[0], z[1], zb[0], zb[1], 2 * m + 1);
+      }
     }
   }
 
@@ -303,13 +305,13 @@ __device__ __forceinline__ void simulate(const LevelArgs& A, const TableView& ta
 // Exact replay of this thread's paths (only for suspects: a u == 1 or
 // u == 1/2 draw, or a non-finite end state): exact transforms and the first
 // failure in the reference's serial order.
-template <class Arith, bool KAHAN, int LEGS, bool APPROX>
+template <class Arith, bool KAHAN, int LEGS, int TAB>
 __device__ __noinline__ void replay_checked(const LevelArgs& A, TableView tab,
                                             const double* s_math,
                                             const uint64_t (&local)[Arith::NP],
                                             const bool (&valid)[Arith::NP],
                                             PathEnd<Arith::NP>& R) {
-  simulate<Arith, KAHAN, LEGS, APPROX, true, false>(A, tab, s_math, local, valid, R);
+  simulate<Arith, KAHAN, LEGS, TAB, true, false>(A, tab, s_math, local, valid, R);
 }
 
 // 256 threads x 4 CTAs per SM (64 registers) for one path per thread; the
@@ -318,20 +320,20 @@ __device__ __noinline__ void replay_checked(const LevelArgs& A, TableView tab,
 #ifndef LPMC_LEVEL_MIN_CTAS
 #define LPMC_LEVEL_MIN_CTAS 4
 #endif
-template <class Arith, bool KAHAN, int LEGS, bool APPROX, bool DUMP>
+template <class Arith, bool KAHAN, int LEGS, int TAB, bool DUMP>
 __global__ void __launch_bounds__(kBatch / Arith::NP, LPMC_LEVEL_MIN_CTAS)
     level_kernel(const __grid_constant__ LevelArgs A) {
   constexpr int NP = Arith::NP;
   constexpr bool kFineOnly = LEGS == 4;
   constexpr bool kHat = (LEGS & 1) != 0 || kFineOnly;
   constexpr bool kBar = (LEGS & 2) != 0 || kFineOnly;
-  constexpr bool kNeedExact = kHat || !APPROX;
+  constexpr bool kNeedExact = kHat || TAB == kTabNone;
 
   extern __shared__ __align__(16) double s_table[];
   __shared__ __align__(16) double s_math[kNeedExact ? kMathWords : 2];
   if constexpr (kNeedExact) stage_math(s_math);
   TableView tab{};
-  if constexpr (APPROX) {
+  if constexpr (TAB != kTabNone) {
     for (int i = threadIdx.x; i < A.table_words; i += blockDim.x) s_table[i] = A.table[i];
     tab = TableView{s_table, A.table_stride, A.K, A.degree, A.dyadic, A.table_simple, A.tail};
   }
@@ -351,14 +353,14 @@ __global__ void __launch_bounds__(kBatch / Arith::NP, LPMC_LEVEL_MIN_CTAS)
   }
 
   PathEnd<NP> R;
-  simulate<Arith, KAHAN, LEGS, APPROX, false, DUMP>(A, tab, s_math, local, valid, R);
+  simulate<Arith, KAHAN, LEGS, TAB, false, DUMP>(A, tab, s_math, local, valid, R);
 
   bool any_suspect = false;
 #pragma unroll
   for (int p = 0; p < NP; ++p) any_suspect |= valid[p] && R.suspect[p];
   if (any_suspect) {  // rare: exact values and first failure (serial order)
     const bool range_bad = R.range_bad;
-    replay_checked<Arith, KAHAN, LEGS, APPROX>(A, tab, s_math, local, valid, R);
+    replay_checked<Arith, KAHAN, LEGS, TAB>(A, tab, s_math, local, valid, R);
     R.range_bad |= range_bad;
 #pragma unroll
     for (int p = 0; p < NP; ++p) {
@@ -413,18 +415,23 @@ __global__ void __launch_bounds__(kBatch / Arith::NP, LPMC_LEVEL_MIN_CTAS)
 constexpr int kMaxTableK = 1024;
 constexpr int kMaxDynSmem = kTableRows * kMaxTableK * 8;
 
-template <class Arith, bool KAHAN, int LEGS, bool APPROX, bool DUMP>
+template <class Arith, bool KAHAN, int LEGS, int TAB, bool DUMP>
 cudaError_t launch_one(const LevelArgs& A, cudaStream_t s) {
-  const size_t smem = APPROX ? static_cast<size_t>(A.table_words) * sizeof(double) : 0;
-  level_kernel<Arith, KAHAN, LEGS, APPROX, DUMP>
+  const size_t smem = TAB != kTabNone ? static_cast<size_t>(A.table_words) * sizeof(double) : 0;
+  level_kernel<Arith, KAHAN, LEGS, TAB, DUMP>
       <<<static_cast<unsigned>(A.n_batches), kBatch / Arith::NP, smem, s>>>(A);
   return cudaGetLastError();
 }
 
+// Table kind: none (exact Gaussians for the bar legs), a dyadic linear table
+// with the signed-zero fix-up proved unnecessary (every BASELINE config; no
+// per-draw branches), or any other table.
 template <class Arith, bool KAHAN, int LEGS, bool DUMP>
 cudaError_t pick_approx(const LevelArgs& A, cudaStream_t s) {
-  return A.table != nullptr ? launch_one<Arith, KAHAN, LEGS, true, DUMP>(A, s)
-                            : launch_one<Arith, KAHAN, LEGS, false, DUMP>(A, s);
+  if (A.table == nullptr) return launch_one<Arith, KAHAN, LEGS, kTabNone, DUMP>(A, s);
+  if (A.dyadic && A.table_simple && A.degree == 1)
+    return launch_one<Arith, KAHAN, LEGS, kTabDyadicLinear, DUMP>(A, s);
+  return launch_one<Arith, KAHAN, LEGS, kTabGeneric, DUMP>(A, s);
 }
 
 template <class Arith, bool KAHAN, bool DUMP>
@@ -443,7 +450,10 @@ cudaError_t launch_level(const LevelArgs& A, bool kahan, bool dump, cudaStream_t
 
 template <class Arith, bool KAHAN, int LEGS, bool DUMP>
 cudaError_t configure_one() {
-  return cudaFuncSetAttribute(level_kernel<Arith, KAHAN, LEGS, true, DUMP>,
+  cudaError_t e = cudaFuncSetAttribute(level_kernel<Arith, KAHAN, LEGS, kTabGeneric, DUMP>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem);
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(level_kernel<Arith, KAHAN, LEGS, kTabDyadicLinear, DUMP>,
                               cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem);
 }
 

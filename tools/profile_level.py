@@ -23,6 +23,8 @@ def main():
     ap.add_argument("--legs", default="all")
     ap.add_argument("--n", type=int, default=1 << 22)
     ap.add_argument("--launches", type=int, default=2)
+    ap.add_argument("--time", action="store_true",
+                    help="also time 5 launches with CUDA events (best of, ms)")
     a = ap.parse_args()
     spec = L.PrecisionSpec.parse(a.prec)
     approx = None if a.approx == "exact" else L.InvCdfApprox.parse(a.approx)
@@ -34,6 +36,21 @@ def main():
     print(f"level {a.level} {a.prec} {a.approx} kahan={a.kahan} legs={a.legs} n={a.n}: "
           f"v_hat={m.d_hat.variance():.6e} v_bar={m.d_bar.variance():.6e} "
           f"V_bar={m.d_four.variance():.6e}")
+    if a.time:
+        import torch
+        st = torch.cuda.Stream()
+        best = None
+        for _ in range(5):
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(st)
+            plan.launch(st.cuda_stream)
+            e1.record(st)
+            torch.cuda.synchronize()
+            plan.collect()
+            ms = e0.elapsed_time(e1)
+            best = ms if best is None else min(best, ms)
+        print(f"time_ms {best:.4f} path_steps_per_s {(a.n << a.level) / (best * 1e-3):.4e}")
     plan.close()
 
 
