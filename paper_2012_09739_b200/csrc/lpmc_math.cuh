@@ -14,8 +14,9 @@
 //  * The correction (Phi(x0) - u) / pdf needs Phi(x0) to ~1 ulp of u, and
 //    1/pdf to ~1e-10 only.  Phi(x0) = erfc(t)/2, t = -x0/sqrt(2), with
 //    erfc(t) = 2^k p(r) G(t): t^2 split exactly by FMA, exp(-t^2) = 2^k p(r)
-//    by a degree-11 minimax polynomial, and G = erfcx by 26 degree-11
-//    piecewise polynomials (tools/fit_math.py, 7e-18 relative).  1/pdf is
+//    from a 64-entry 2^(j/64) hi/lo table and a degree-4 expm1 polynomial,
+//    and G = erfcx by 104 degree-8 piecewise polynomials on intervals of
+//    1/16 with the constant term as hi + lo (tools/fit_math.py).  1/pdf is
 //    sqrt(2 pi) 2^-k / p(r): the same exponential, no second exp, no division.
 //  * t > 6.5 (u < 1e-20; never drawn by the sampler, whose u >= 2^-54) takes
 //    a libdevice slow path.
@@ -152,7 +153,7 @@ constexpr int kErfcxWords = kErfcxRow * kErfcxN;
 constexpr int kExpN = LPMC_EXP_N;
 constexpr int kExpWords = 2 * kExpN;
 constexpr int kMathTableWords = kErfcxWords + kExpWords;  // one shared-memory block
-constexpr double kFastTMax = 6.5;  // 26 intervals of 1/4
+constexpr double kFastTMax = 6.5;  // the erfcx intervals cover [0, 6.5)
 
 // erfcx records, then the 2^(j/64) hi/lo pairs (host copy)
 static const double kMathTableHost[kMathTableWords] = {LPMC_ERFCX_COEF_LIST, LPMC_EXP_TAB_LIST};
@@ -214,26 +215,42 @@ LPMC_HD ExpSplit exp_neg(double th, double tl, const double* tab) {
   return ExpSplit{p, kf >> 6};
 }
 
-// erfcx(t) for t in [0, 6.5): interval record j, highest power first.
+// erfcx(t) for t in [0, 6.5): interval record j (width 1/LPMC_ERFCX_PER_UNIT),
+// highest power first.
 LPMC_HD double erfcx_piecewise(double t, const double* tab) {
-  int j = static_cast<int>(t * 4.0);
+  constexpr int D = LPMC_ERFCX_DEG;
+  constexpr double kPerUnit = LPMC_ERFCX_PER_UNIT;
+  int j = static_cast<int>(t * kPerUnit);
   j = j < kErfcxN - 1 ? j : kErfcxN - 1;
-  const double s = t - (0.25 * j + 0.125);
-  const double* rec = tab + kErfcxRow * j;
+  const double s = t - (j + 0.5) * (1.0 / kPerUnit);  // exact: j < 2^10, power-of-two width
+  const double* rec = tab + kErfcxRow * j;  // c_D, ..., c_1, c0 hi, c0 lo
   D2 c = load2(rec);
-  double q = fmad(c.a, s, c.b);  // c11 s + c10
+  double q = fmad(c.a, s, c.b);  // c_D s + c_{D-1}
+  if constexpr (D % 2 == 0) {
 #ifdef __CUDA_ARCH__
 #pragma unroll
 #endif
-  for (int i = 2; i < 10; i += 2) {  // c9..c2
-    c = load2(rec + i);
+    for (int i = 2; i < D; i += 2) {  // c_{D-2} .. c_1
+      c = load2(rec + i);
+      q = fmad(q, s, c.a);
+      q = fmad(q, s, c.b);
+    }
+    c = load2(rec + D);  // c0 hi, c0 lo
+    return c.a + fmad(q, s, c.b);
+  } else {
+#ifdef __CUDA_ARCH__
+#pragma unroll
+#endif
+    for (int i = 2; i < D - 1; i += 2) {  // c_{D-2} .. c_2
+      c = load2(rec + i);
+      q = fmad(q, s, c.a);
+      q = fmad(q, s, c.b);
+    }
+    c = load2(rec + D - 1);  // c1, c0 hi
     q = fmad(q, s, c.a);
-    q = fmad(q, s, c.b);
+    const D2 lo = load2(rec + D + 1);  // c0 lo, pad
+    return c.b + fmad(q, s, lo.a);
   }
-  c = load2(rec + 10);  // c1, c0 hi
-  q = fmad(q, s, c.a);
-  const D2 lo = load2(rec + 12);  // c0 lo, 0
-  return c.b + fmad(q, s, lo.a);
 }
 
 // 2^k x for |k| <= 1022 and a normal result (the fast path has |k| <= 62).
