@@ -3,7 +3,10 @@ ncu report's SASS page (Instructions Executed per address) with the line
 table of the same kernel in the locally built object (deterministic build of
 the same sources).
 
-    python tools/sass_lines.py rep.ncu-rep obj.o function-regex [--units N] [--top K]
+    python tools/sass_lines.py rep.ncu-rep obj.o function-regex [--units N] [--top K] [--stalls]
+
+--stalls: rank lines by warp-stall samples instead, with each line's
+dominant stall reasons (ncu source-page stall_* columns).
 """
 from __future__ import annotations
 
@@ -28,10 +31,15 @@ out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-so
 rows = list(csv.reader(io.StringIO(out)))
 hdr = rows[1]
 ia, isrc, iex = hdr.index("Address"), hdr.index("Source"), hdr.index("Instructions Executed")
+stall_cols = [(i, k[len("stall_"):]) for i, k in enumerate(hdr)
+              if k.startswith("stall_") and "Not Issued" not in k]
 dyn = []
+stalls = {}
 for r in rows[2:]:
     if len(r) > iex and r[ia].startswith("0x"):
-        dyn.append((int(r[ia], 16), r[isrc].strip(), int(r[iex] or 0)))
+        a = int(r[ia], 16)
+        dyn.append((a, r[isrc].strip(), int(r[iex] or 0)))
+        stalls[a] = {name: int(r[i] or 0) for i, name in stall_cols}
 base = dyn[0][0]
 
 with tempfile.TemporaryDirectory() as d:
@@ -59,6 +67,8 @@ for line in dis.split("\n"):
 
 per = collections.Counter()
 ops = collections.defaultdict(collections.Counter)
+why = collections.defaultdict(collections.Counter)
+samples = collections.Counter()
 miss = 0
 for a, src, n in dyn:
     loc = where.get(a - base)
@@ -66,10 +76,19 @@ for a, src, n in dyn:
         miss += n
         continue
     per[loc] += n
+    for k, v in stalls[a].items():
+        why[loc][k] += v
+        samples[loc] += v
     op = re.sub(r"^@!?U?P\w+\s+", "", src).split()[0] if src else "?"
     ops[loc][op.split(".")[0]] += n
 tot = sum(per.values()) + miss
 print(f"total {tot / units:.2f} per unit (unmapped {miss / units:.2f})")
+if "--stalls" in sys.argv:
+    all_s = sum(samples.values()) or 1
+    for loc, v in samples.most_common(top):
+        reasons = ", ".join(f"{k} {100 * c / v:.0f}%" for k, c in why[loc].most_common(3) if c)
+        print(f"{100 * v / all_s:6.2f}%  {loc:28s} exec {per[loc] / units:7.2f}  {reasons}")
+    sys.exit(0)
 for loc, n in per.most_common(top):
     mix = ", ".join(f"{k} {v / units:.2f}" for k, v in ops[loc].most_common(5))
     print(f"{n / units:8.2f}  {loc:28s} {mix}")
