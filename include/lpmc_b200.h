@@ -30,6 +30,8 @@
  *   lpmc_per_level_speedup      <- per_level_speedup       include/lpmc/mlmc.hpp:223-230
  *   lpmc_run_nested_estimator   <- run_nested_estimator    include/lpmc/mlmc.hpp:244-283
  *   lpmc_step_error_probe       <- step_error_probe        include/lpmc/sde.hpp:297-344
+ *   lpmc_density_histogram      <- the histogram loop of run_density_report
+ *                                  include/lpmc/experiments.hpp:276-285
  *
  * Error contract: every entry point returns an lpmc_status.  The values map
  * one-to-one onto the exception types the reference throws
@@ -361,6 +363,19 @@ lpmc_status lpmc_run_nested_estimator(const lpmc_gbm* model, int32_t max_level,
                                       uint64_t seed, const lpmc_cost_model* cost,
                                       uint64_t pilot_paths, const lpmc_options* opts,
                                       lpmc_estimator_result* out, lpmc_error* err);
+
+/*
+ * The histogram of run_density_report (experiments.hpp:276-285): the draws
+ * 0..n_samples-1 of UniformStream(seed, 0) through the table (NULL = exact
+ * inverse CDF), binned as b = (int)((z + z_max) / bin_width) clamped to
+ * [0, n_bins).  bins: n_bins counts, exact (integer adds).  A draw that
+ * rounds to u == 1 fails as the reference's transform throws (error.step =
+ * the draw index).
+ */
+lpmc_status lpmc_density_histogram(const lpmc_invcdf_table* table, uint64_t seed,
+                                   uint64_t n_samples, double z_max, double bin_width,
+                                   int32_t n_bins, uint64_t* bins, const lpmc_options* opts,
+                                   lpmc_error* err);
 
 /* StepErrorStats (sde.hpp:289-295). */
 typedef struct lpmc_step_error_stats {

@@ -320,6 +320,8 @@ class Reference:
                                                               C.c_char_p, C.c_int]
         L.ref_step_error_probe.argtypes = [C.c_double] * 4 + [C.c_int, C.c_int, C.c_char_p, _u64,
                                                               _u64, _dp, C.c_char_p, C.c_int]
+        L.ref_density_report.argtypes = [C.c_char_p, _u64, C.c_int, _u64, C.c_double, _dp,
+                                         C.c_int, C.POINTER(C.c_int), C.c_char_p, C.c_int]
         L.ref_two_way_experiment.argtypes = [C.c_double] * 4 + [
             C.c_char_p, C.c_char_p, C.c_int, C.c_int, C.c_int, _u64, _u64, C.c_int, _dp,
             C.c_char_p, C.c_int]
@@ -492,3 +494,12 @@ class Reference:
         rc = self.lib.ref_step_error_probe(mu, sigma, x0, horizon, level, mantissa_bits,
                                            approx.encode(), n_samples, seed, _ptr(out), msg, 256)
         return rc, msg.value.decode(), out
+
+    def density_report(self, *, approx, seed=1, curve_points=2048, hist_samples=1000000,
+                       bin_width=0.05, cap=100000):
+        out = np.zeros(3 * cap)
+        n = C.c_int()
+        msg = C.create_string_buffer(256)
+        rc = self.lib.ref_density_report(approx.encode(), seed, curve_points, hist_samples,
+                                         bin_width, _ptr(out), cap, C.byref(n), msg, 256)
+        return rc, msg.value.decode(), out[:3 * n.value].reshape(-1, 3)

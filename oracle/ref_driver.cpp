@@ -407,6 +407,29 @@ int ref_step_error_probe(double mu, double sigma, double x0, double horizon, int
   });
 }
 
+// run_density_report (experiments.hpp:258): rows as {series (0 curve, 1 hist),
+// x, y} triples; returns the row count in *n_rows (cap rows max).
+int ref_density_report(const char* approx, uint64_t seed, int curve_points, uint64_t hist_samples,
+                       double bin_width, double* out3, int cap, int* n_rows, char* msg,
+                       int len) {
+  return guarded(msg, len, [&] {
+    lpmc::ExperimentConfig c;
+    c.approx = approx;
+    c.seed = seed;
+    c.level_min = 0;
+    c.level_max = 0;
+    std::vector<lpmc::DensityRow> rows =
+        lpmc::run_density_report(c, curve_points, hist_samples, bin_width);
+    if (static_cast<int>(rows.size()) > cap) throw std::runtime_error("density rows exceed cap");
+    for (size_t i = 0; i < rows.size(); ++i) {
+      out3[3 * i] = rows[i].series == "curve" ? 0.0 : 1.0;
+      out3[3 * i + 1] = rows[i].x;
+      out3[3 * i + 2] = rows[i].y;
+    }
+    *n_rows = static_cast<int>(rows.size());
+  });
+}
+
 int ref_hardware_threads() { return static_cast<int>(std::thread::hardware_concurrency()); }
 
 }  // extern "C"

@@ -171,6 +171,8 @@ SIGNATURES = {
     "lpmc_run_nested_estimator": (_i32, [_P(Gbm), _i32, _P(Precision), _P(InvCdfTable), _i32,
                                          C.c_double, _u64, _P(CostModelC), _u64, _P(Options),
                                          _P(EstimatorResultC), _P(Error)]),
+    "lpmc_density_histogram": (_i32, [_P(InvCdfTable), _u64, _u64, C.c_double, C.c_double, _i32,
+                                      _P(_u64), _P(Options), _P(Error)]),
     "lpmc_step_error_probe": (_i32, [_P(Gbm), _i32, _P(Precision), _P(InvCdfTable), _u64, _u64,
                                      _P(Options), _P(StepErrorStatsC), _P(Error)]),
     "lpmc_plan_create": (_i32, [_P(Gbm), _i32, _P(Precision), _P(InvCdfTable), _i32, _u64, _u64,

@@ -764,3 +764,19 @@ def step_error_probe(model: SdeModel, level: int, spec: PrecisionSpec,
                                            C.byref(opts), C.byref(out), C.byref(err)), err)
     return StepErrorStats(out.mean_eta, out.mean_abs_eta, out.mean_eta_prime,
                           out.mean_abs_eta_prime, int(out.samples))
+
+
+# ---------------------------------- density histogram (experiments.hpp:276) --
+def density_histogram(approx: Optional[InvCdfApprox], seed: int, n_samples: int, z_max: float,
+                      bin_width: float, n_bins: int, **ext) -> np.ndarray:
+    """Counts of run_density_report's histogram (experiments.hpp:276-285) on
+    the device: draws 0..n-1 of UniformStream(seed, 0) through the table
+    (None = exact inverse CDF), bin (int)((z + z_max) / bin_width) clamped."""
+    bins = np.zeros(int(n_bins), dtype=np.uint64)
+    err = N.Error()
+    opts = _options(**ext)
+    N.check(N.load().lpmc_density_histogram(_table_ptr(approx), int(seed), int(n_samples),
+                                            float(z_max), float(bin_width), int(n_bins),
+                                            bins.ctypes.data_as(C.POINTER(C.c_uint64)),
+                                            C.byref(opts), C.byref(err)), err)
+    return bins

@@ -1478,6 +1478,75 @@ lpmc_status lpmc_device_math(int32_t op, const double* u, uint64_t n,
   return ok(err);
 }
 
+lpmc_status lpmc_density_histogram(const lpmc_invcdf_table* table, uint64_t seed,
+                                   uint64_t n_samples, double z_max, double bin_width,
+                                   int32_t n_bins, uint64_t* bins, const lpmc_options* opts,
+                                   lpmc_error* err) {
+  // the histogram loop of run_density_report (experiments.hpp:276-285)
+  if (n_bins < 1 || bins == nullptr) return fail(err, LPMC_INVALID_ARGUMENT, "need at least one bin");
+  if (!(bin_width > 0.0) || !std::isfinite(z_max))
+    return fail(err, LPMC_INVALID_ARGUMENT, "bad histogram geometry");
+  for (int32_t b = 0; b < n_bins; ++b) bins[b] = 0;
+  if (n_samples == 0) return ok(err);
+  HostTable ht;
+  if (table != nullptr) {
+    lpmc_status st = prepare_table(table, &ht, err);
+    if (st != LPMC_OK) return st;
+  }
+  // UniformStream(seed, 0) (uniform.hpp:23-25): the key of path 0
+  auto mix64 = [](uint64_t z) {
+    z ^= z >> 33;
+    z *= 0xff51afd7ed558ccdull;
+    z ^= z >> 33;
+    z *= 0xc4ceb9fe1a85ec53ull;
+    z ^= z >> 33;
+    return z;
+  };
+  const uint64_t key = mix64(mix64(seed + 0x9e3779b97f4a7c15ull) ^ mix64(0 + 0xbf58476d1ce4e5b9ull));
+  DeviceCtx* ctx = nullptr;
+  int dev = -1;
+  lpmc_status st = get_ctx(opts ? opts->device : -1, &ctx, &dev, err);
+  if (st != LPMC_OK) return st;
+  DeviceGuard guard;
+  cudaError_t e = guard.set(dev);
+  if (e != cudaSuccess) return cuda_fail(err, e, "cudaSetDevice");
+  std::lock_guard<std::mutex> lock(ctx->mu);
+  cudaStream_t stream = ctx->stream;
+  DevBuf<double> dtab;
+  DevBuf<unsigned long long> dbins, dtop;
+  unsigned long long top = ~0ull;
+  if ((e = dbins.ensure(static_cast<size_t>(n_bins))) == cudaSuccess &&
+      (e = dtop.ensure(1)) == cudaSuccess &&
+      (table == nullptr || (e = dtab.ensure(ht.rows.size())) == cudaSuccess)) {
+    cudaMemsetAsync(dbins.ptr, 0, static_cast<size_t>(n_bins) * sizeof(unsigned long long), stream);
+    cudaMemsetAsync(dtop.ptr, 0xff, sizeof(unsigned long long), stream);
+    if (table != nullptr)
+      cudaMemcpyAsync(dtab.ptr, ht.rows.data(), ht.rows.size() * sizeof(double),
+                      cudaMemcpyHostToDevice, stream);
+    LaunchResult r = launch_density(key, n_samples, table ? dtab.ptr : nullptr, ht.K, ht.degree,
+                                    ht.dyadic, ht.stride, ht.simple, ht.tail, z_max, bin_width,
+                                    n_bins, dbins.ptr, dtop.ptr, stream);
+    t_launches += r.kernels;
+    e = static_cast<cudaError_t>(r.cuda_error);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(bins, dbins.ptr, static_cast<size_t>(n_bins) * sizeof(uint64_t),
+                          cudaMemcpyDeviceToHost, stream);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(&top, dtop.ptr, sizeof top, cudaMemcpyDeviceToHost, stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
+  }
+  dtab.release();
+  dbins.release();
+  dtop.release();
+  if (e != cudaSuccess) return cuda_fail(err, e, "density histogram");
+  if (top != ~0ull)  // the reference throws at that draw
+    return fail(err, LPMC_DOMAIN_ERROR,
+                table != nullptr ? "approx_inv_cdf requires u in (0, 1)"
+                                 : "exact_inv_cdf requires u in (0, 1)",
+                LPMC_FAIL_UNIFORM_IS_ONE, 0, top);
+  return ok(err);
+}
+
 lpmc_status lpmc_device_inv_cdf(const double* u, uint64_t n, const lpmc_invcdf_table* table,
                                 double* out, const lpmc_options* opts, lpmc_error* err) {
   return lpmc_device_math(table ? 1 : 0, u, n, table, out, opts, err);

@@ -96,6 +96,61 @@ __global__ void inv_cdf_kernel(const double* __restrict__ u, uint64_t n,
   if (in) out[i] = r;
 }
 
+// The histogram of run_density_report (experiments.hpp:276-285): draws
+// 0..n-1 of UniformStream(seed, 0) (counter-based, so one draw per thread)
+// through the table or the exact transform, bin (int)((z + z_max) / w)
+// clamped to [0, n_bins), counted in a shared-memory histogram per CTA
+// (integer adds: order-independent, so the counts are exact).  Lanes past n
+// evaluate a dummy draw so the warp-collective tail pass stays converged.
+// A draw that rounds to u == 1 (the reference throws) records its index.
+constexpr int kDensitySmemBins = 8192;
+
+__global__ void density_kernel(uint64_t key, uint64_t n, const double* __restrict__ table, int K,
+                               int degree, int dyadic, int stride, int simple, double tail,
+                               double z_max, double width, int n_bins,
+                               unsigned long long* __restrict__ bins,
+                               unsigned long long* __restrict__ top_index) {
+  __shared__ __align__(16) double s_math[kMathWords];
+  __shared__ unsigned int s_bins[kDensitySmemBins];
+  const bool local_bins = n_bins <= kDensitySmemBins;
+  stage_math(s_math);
+  if (local_bins)
+    for (int b = threadIdx.x; b < n_bins; b += blockDim.x) s_bins[b] = 0u;
+  __syncthreads();
+  const TableView t{table, stride, K, degree, dyadic, simple, tail};
+  const uint64_t step = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t base = static_cast<uint64_t>(blockIdx.x) * blockDim.x; base < n; base += step) {
+    const uint64_t i = base + threadIdx.x;
+    const bool in = i < n;
+    uint64_t kc = key + (in ? i : 0) * 0x94d049bb133111ebull;  // counter i (uniform.hpp:38-41)
+    const uint64_t b53 = next_draw(kc);
+    const double u = in ? uniform_of(b53) : 0.25;
+    if (in && b53 == kTopDraw) atomicMin(top_index, static_cast<unsigned long long>(i));
+    double z;
+    if (table != nullptr) {
+      z = approx_inv(t, u);
+    } else {
+      double uu[1] = {u}, zz[1];
+      math::phi_inv_multi<1>(uu, zz, s_math);
+      z = zz[0];
+    }
+    if (in) {
+      int b = static_cast<int>(__ddiv_rn(__dadd_rn(z, z_max), width));
+      b = b < 0 ? 0 : b;
+      b = b >= n_bins ? n_bins - 1 : b;
+      if (local_bins) {
+        atomicAdd(&s_bins[b], 1u);
+      } else {
+        atomicAdd(&bins[b], 1ull);
+      }
+    }
+  }
+  __syncthreads();
+  if (local_bins)
+    for (int b = threadIdx.x; b < n_bins; b += blockDim.x)
+      if (s_bins[b] != 0u) atomicAdd(&bins[b], static_cast<unsigned long long>(s_bins[b]));
+}
+
 // ------------------------------------------------------ pipe peaks ---------
 // Roofline denominators for this non-tensor path: many independent
 // dependency chains per thread so the pipe, not latency, is the limit.
@@ -251,6 +306,22 @@ LaunchResult launch_inv_cdf(const double* u, uint64_t n, const double* table, in
   const unsigned blocks = static_cast<unsigned>((n + 255) / 256);
   inv_cdf_kernel<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(
       u, n, table, K, degree, dyadic, stride, simple, tail, op, out);
+  return {static_cast<int>(cudaGetLastError()), 1};
+}
+
+LaunchResult launch_density(uint64_t key, uint64_t n, const double* table, int K, int degree,
+                            int dyadic, int stride, int simple, double tail, double z_max,
+                            double width, int n_bins, unsigned long long* bins,
+                            unsigned long long* top_index, void* stream) {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const uint64_t need = (n + 255) / 256;
+  const uint64_t cap = static_cast<uint64_t>(sms) * 8;
+  const unsigned blocks = static_cast<unsigned>(need < cap ? (need ? need : 1) : cap);
+  density_kernel<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      key, n, table, K, degree, dyadic, stride, simple, tail, z_max, width, n_bins, bins,
+      top_index);
   return {static_cast<int>(cudaGetLastError()), 1};
 }
 

@@ -13,6 +13,8 @@ SpeedupRow /                experiments.hpp:218-246 (per_level_speedup)
 run_speedup_report
 StepErrorRow /              experiments.hpp:297-319 (device step_error_probe)
 run_step_error_report
+DensityRow /                experiments.hpp:252-295 (device histogram and curve)
+run_density_report
 ==========================  ================================================
 
 Same path bases, path counts and merge order as the reference, so every row
@@ -27,9 +29,13 @@ from __future__ import annotations
 from dataclasses import dataclass, field
 from typing import List, Optional
 
+import math
+
+import numpy as np
+
 from .api import (CostModel, InvalidArgument, InvCdfApprox, LevelStats, PrecisionSpec,
-                  StepErrorStats, level_stats_from_moments, make_gbm, per_level_speedup,
-                  run_coupled_many, step_error_probe)
+                  StepErrorStats, density_histogram, device_inv_cdf, level_stats_from_moments,
+                  make_gbm, per_level_speedup, run_coupled_many, step_error_probe)
 
 
 @dataclass
@@ -209,3 +215,34 @@ def run_step_error_report(config: ExperimentConfig, samples: int, **ext) -> List
     return [StepErrorRow(level, step_error_probe(model, level, spec, approx, samples, config.seed,
                                                  **ext))
             for level in range(config.level_min, config.level_max + 1)]
+
+
+@dataclass
+class DensityRow:
+    series: str  # "curve" or "hist"
+    x: float
+    y: float
+
+
+def run_density_report(config: ExperimentConfig, curve_points: int = 2048,
+                       hist_samples: int = 1000000, bin_width: float = 0.05,
+                       **ext) -> List[DensityRow]:
+    """experiments.hpp:258-295: the inverse-CDF curve at u = i / curve_points
+    and the histogram of hist_samples draws of UniformStream(seed, 0), both
+    evaluated on the device; bin geometry and densities as the reference."""
+    config.validate()
+    approx = config.build_approx()
+    u = np.arange(1, curve_points, dtype=np.float64) / curve_points
+    dev = ext.get("device")
+    curve = device_inv_cdf(u, approx, device=dev) if len(u) else np.zeros(0)
+    rows = [DensityRow("curve", float(a), float(b)) for a, b in zip(u, curve)]
+    if approx is not None:
+        z_max = approx.max_value()
+    else:
+        z_max = float(device_inv_cdf(np.array([1.0 - 2.0 ** -30]), None, device=dev)[0])
+    n_bins = int(math.ceil(2.0 * z_max / bin_width)) + 1
+    bins = density_histogram(approx, config.seed, hist_samples, z_max, bin_width, n_bins, **ext)
+    for b in range(n_bins):
+        center = -z_max + (b + 0.5) * bin_width
+        rows.append(DensityRow("hist", center, float(bins[b]) / (float(hist_samples) * bin_width)))
+    return rows

@@ -191,6 +191,18 @@ int main(int argc, char** argv) {
     CHECK(throws<std::invalid_argument>([&] { run_step_error_report(cfg, 9999); }));
   }
 
+  // density report (experiments.hpp:258-295)
+  {
+    ExperimentConfig cfg;
+    cfg.approx = "linear:16";
+    auto rows = run_density_report(cfg, 64, 20000, 0.1);
+    CHECK(rows.size() == 63 + 88 && rows[0].series == "curve" && rows.back().series == "hist");
+    double mass = 0.0;
+    for (const auto& r : rows)
+      if (r.series == "hist") mass += r.y * 0.1;
+    CHECK(std::fabs(mass - 1.0) < 1e-12);
+  }
+
   // non-GBM models are rejected (no CPU fallback)
   SdeModel custom = gbm;
   custom.gbm.reset();

@@ -247,6 +247,18 @@ def callers():
         probe.append({"level": level, "m": m, "approx": approx, "n_samples": n_samples,
                       "seed": seed, "out": hx(out)})
 
+    density = []
+    for approx, curve_points, hist, width, seed in [("linear:16", 2048, 100000, 0.05, 1),
+                                                    ("cubic:64", 512, 50000, 0.1, 2),
+                                                    ("linear:1024", 256, 100000, 0.05, 3),
+                                                    ("exact", 2048, 100000, 0.05, 1)]:
+        rc, msg, rows = R.density_report(approx=approx, seed=seed, curve_points=curve_points,
+                                         hist_samples=hist, bin_width=width)
+        assert rc == 0, msg
+        density.append({"approx": approx, "seed": seed, "curve_points": curve_points,
+                        "hist_samples": hist, "bin_width": width.hex(),
+                        "rows": [[int(r[0]), float(r[1]).hex(), float(r[2]).hex()] for r in rows]})
+
     doc = {"generator": "tests/golden/gen_golden.py callers (reference: "
                         "/root/reference/proj/include, oracle/ref_driver.cpp)",
            "stats_fields": list(Reference.STATS_FIELDS),
@@ -254,7 +266,7 @@ def callers():
            "two_way_paths": two_way_paths, "two_way_rows": two_way_rows,
            "allocation": allocation, "allocation_errors": bad_alloc, "times": times,
            "speedup": speedup, "nested": nested, "nested_errors": nested_errors,
-           "step_error": probe}
+           "step_error": probe, "density": density}
     with open(os.path.join(OUT, "callers_vectors.json"), "w") as f:
         json.dump(doc, f, indent=0)
     print("wrote", os.path.join(OUT, "callers_vectors.json"))

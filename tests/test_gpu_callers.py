@@ -231,3 +231,31 @@ def test_step_error_probe_errors_and_report(gpu):
     rows = run_step_error_report(cfg, 20000)
     assert [r.level for r in rows] == list(range(5))
     assert all(r.stats.samples == 20000 and r.stats.mean_abs_eta > 0 for r in rows)
+
+
+# ------------------------------------------ density report (row 4, histogram) --
+@pytest.mark.parametrize("idx", range(4))
+def test_density_report_vs_reference(gpu, cv, idx):
+    from paper_2012_09739_b200.experiments import ExperimentConfig, run_density_report
+    c = cv["density"][idx]
+    width = float.fromhex(c["bin_width"])
+    cfg = ExperimentConfig(approx=c["approx"], seed=c["seed"], level_min=0, level_max=0)
+    rows = run_density_report(cfg, c["curve_points"], c["hist_samples"], width)
+    want = c["rows"]
+    assert len(rows) == len(want)
+    got_kind = [0 if r.series == "curve" else 1 for r in rows]
+    assert got_kind == [w[0] for w in want]
+    gx = np.array([r.x for r in rows])
+    gy = np.array([r.y for r in rows])
+    wx = unhex([w[1] for w in want])
+    wy = unhex([w[2] for w in want])
+    assert np.array_equal(bits(gx), bits(wx))  # u grid and bin centres: same arithmetic
+    kind = np.array(got_kind)
+    if c["approx"] != "exact":  # table values and integer counts: bitwise
+        assert np.array_equal(bits(gy), bits(wy))
+    else:  # device exact Gaussians: last-ulp curve; a draw may cross a bin edge
+        cu = kind == 0
+        np.testing.assert_allclose(gy[cu], wy[cu], rtol=1e-13, atol=1e-15)
+        step = 1.0 / (c["hist_samples"] * width)
+        assert np.max(np.abs(gy[~cu] - wy[~cu])) <= 3 * step + 1e-18
+        assert abs(gy[~cu].sum() - wy[~cu].sum()) <= 1e-9
