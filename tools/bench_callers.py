@@ -12,6 +12,8 @@ synchronised by the blocking call itself.
               reference's default path counts (1e4, halved above level 9)
   four_way    run_four_way_experiment, fp16/fp32 linear:16, levels 0..10, 2e4 paths
   probe       step_error_probe, fp16 linear:16, level 10, 1e7 samples
+  density     run_density_report, reference defaults (linear:1024, 2047 curve
+              points, 1e6 histogram samples, bin width 0.05), and exact
   concurrency the nested estimator's pilot pass (11 levels x 1000 paths):
               one run_coupled_many call vs 11 run_coupled_paths calls
 Throughput unit: fine path-steps (paths x 2^level, summed) per second.
@@ -28,7 +30,8 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2012_09739_b200 as L  # noqa: E402
 from oracle.bind import Reference  # noqa: E402
 from paper_2012_09739_b200.experiments import (ExperimentConfig,  # noqa: E402
-                                               run_four_way_experiment, run_two_way_experiment)
+                                               run_density_report, run_four_way_experiment,
+                                               run_two_way_experiment)
 
 
 def best_of(fn, reps=3):
@@ -117,6 +120,18 @@ def main():
                            "gpu_s": t_gpu, "ref_cpu_s": t_cpu, "ref_threads": 1,
                            "speedup": t_cpu / t_gpu, "gpu_steps_per_s": n / t_gpu,
                            "rel_diff_mean_abs_eta": abs(st.mean_abs_eta - out[1]) / out[1]})
+
+    # ---- density report
+    for approx in ("linear:1024", "exact"):
+        cfgd = ExperimentConfig(approx=approx, level_min=0, level_max=0)
+        t_gpu, rows = best_of(lambda: run_density_report(cfgd))
+        t_cpu, (rc, msg, out) = once(lambda: R.density_report(approx=approx))
+        assert rc == 0, msg
+        same = sum(1 for r, w in zip(rows, out) if r.y == w[2])
+        res["results"].append({"row": "density_report", "approx": approx, "samples": 1000000,
+                               "gpu_s": t_gpu, "ref_cpu_s": t_cpu, "ref_threads": 1,
+                               "speedup": t_cpu / t_gpu, "rows": len(rows),
+                               "rows_bitwise_equal": same})
 
     # ---- concurrency of the multi-run entry point
     runs = [(l, L.PrecisionSpec.fp16(), False, 1000, l << 40) for l in range(11)]
