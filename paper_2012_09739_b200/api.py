@@ -156,6 +156,8 @@ class InvCdfApprox:
                                 self._bp.ctypes.data_as(N._dp),
                                 self._coeff.ctypes.data_as(N._dp))
 
+    _built: dict = {}  # (kind, K) -> table: builds are deterministic, tables immutable
+
     @classmethod
     def build(cls, kind: str, interval_count: int) -> "InvCdfApprox":
         if kind not in cls.KINDS:
@@ -163,6 +165,9 @@ class InvCdfApprox:
         K = int(interval_count)
         if K < 2 or (K & (K - 1)) != 0:
             raise InvalidArgument("interval count must be a power of two >= 2")
+        hit = cls._built.get((kind, K))
+        if hit is not None:
+            return hit
         bp = np.zeros(K)
         co = np.zeros(4 * K)
         wm, sw, tl = C.c_double(), C.c_double(), C.c_double()
@@ -170,7 +175,13 @@ class InvCdfApprox:
         N.check(N.load().lpmc_invcdf_build(cls.KINDS[kind], K, bp.ctypes.data_as(N._dp),
                                            co.ctypes.data_as(N._dp), C.byref(wm), C.byref(sw),
                                            C.byref(tl), C.byref(err)), err)
-        return cls(kind, K, wm.value, sw.value, tl.value, bp, co)
+        table = cls(kind, K, wm.value, sw.value, tl.value, bp, co)
+        bp.flags.writeable = False
+        co.flags.writeable = False
+        table._bp.flags.writeable = False
+        table._coeff.flags.writeable = False
+        cls._built[(kind, K)] = table
+        return table
 
     @classmethod
     def parse(cls, name: str) -> "InvCdfApprox":

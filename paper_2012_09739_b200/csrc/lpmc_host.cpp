@@ -476,11 +476,14 @@ struct DevBuf {
 };
 
 struct Buffers {
-  DevBuf<double> table, batch_acc, chunk_acc, path_diff, seq_acc;
-  DevBuf<unsigned long long> err_key;
+  DevBuf<double> table, batch_acc, chunk_acc, path_diff, seq_acc, io_in, io_out;
+  DevBuf<unsigned long long> err_key, counts;
   DevBuf<unsigned int> range_flag;
   std::vector<double> host_parts;
   void release() {
+    io_in.release();
+    io_out.release();
+    counts.release();
     table.release();
     batch_acc.release();
     chunk_acc.release();
@@ -1456,7 +1459,9 @@ lpmc_status lpmc_device_math(int32_t op, const double* u, uint64_t n,
   if (e != cudaSuccess) return cuda_fail(err, e, "cudaSetDevice");
   std::lock_guard<std::mutex> lock(ctx->mu);
   cudaStream_t stream = ctx->stream;
-  DevBuf<double> du, dout, dtab;
+  DevBuf<double>& du = ctx->scratch.io_in;
+  DevBuf<double>& dout = ctx->scratch.io_out;
+  DevBuf<double>& dtab = ctx->scratch.table;
   if ((e = du.ensure(n)) == cudaSuccess && (e = dout.ensure(n)) == cudaSuccess &&
       (table == nullptr || (e = dtab.ensure(ht.rows.size())) == cudaSuccess)) {
     cudaMemcpyAsync(du.ptr, u, n * sizeof(double), cudaMemcpyHostToDevice, stream);
@@ -1471,9 +1476,6 @@ lpmc_status lpmc_device_math(int32_t op, const double* u, uint64_t n,
       e = cudaMemcpyAsync(out, dout.ptr, n * sizeof(double), cudaMemcpyDeviceToHost, stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
   }
-  du.release();
-  dout.release();
-  dtab.release();
   if (e != cudaSuccess) return cuda_fail(err, e, "inv_cdf");
   return ok(err);
 }
@@ -1512,8 +1514,9 @@ lpmc_status lpmc_density_histogram(const lpmc_invcdf_table* table, uint64_t seed
   if (e != cudaSuccess) return cuda_fail(err, e, "cudaSetDevice");
   std::lock_guard<std::mutex> lock(ctx->mu);
   cudaStream_t stream = ctx->stream;
-  DevBuf<double> dtab;
-  DevBuf<unsigned long long> dbins, dtop;
+  DevBuf<double>& dtab = ctx->scratch.table;
+  DevBuf<unsigned long long>& dbins = ctx->scratch.counts;
+  DevBuf<unsigned long long>& dtop = ctx->scratch.err_key;
   unsigned long long top = ~0ull;
   if ((e = dbins.ensure(static_cast<size_t>(n_bins))) == cudaSuccess &&
       (e = dtop.ensure(1)) == cudaSuccess &&
@@ -1523,9 +1526,10 @@ lpmc_status lpmc_density_histogram(const lpmc_invcdf_table* table, uint64_t seed
     if (table != nullptr)
       cudaMemcpyAsync(dtab.ptr, ht.rows.data(), ht.rows.size() * sizeof(double),
                       cudaMemcpyHostToDevice, stream);
-    LaunchResult r = launch_density(key, n_samples, table ? dtab.ptr : nullptr, ht.K, ht.degree,
-                                    ht.dyadic, ht.stride, ht.simple, ht.tail, z_max, bin_width,
-                                    n_bins, dbins.ptr, dtop.ptr, stream);
+    LaunchResult r = launch_density(key, n_samples, table ? dtab.ptr : nullptr,
+                                    static_cast<int>(ht.rows.size()), ht.K, ht.degree, ht.dyadic,
+                                    ht.stride, ht.simple, ht.tail, z_max, bin_width, n_bins,
+                                    dbins.ptr, dtop.ptr, stream);
     t_launches += r.kernels;
     e = static_cast<cudaError_t>(r.cuda_error);
     if (e == cudaSuccess)
@@ -1535,9 +1539,6 @@ lpmc_status lpmc_density_histogram(const lpmc_invcdf_table* table, uint64_t seed
       e = cudaMemcpyAsync(&top, dtop.ptr, sizeof top, cudaMemcpyDeviceToHost, stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
   }
-  dtab.release();
-  dbins.release();
-  dtop.release();
   if (e != cudaSuccess) return cuda_fail(err, e, "density histogram");
   if (top != ~0ull)  // the reference throws at that draw
     return fail(err, LPMC_DOMAIN_ERROR,

@@ -84,9 +84,9 @@ LaunchResult launch_inv_cdf(const double* u, uint64_t n, const double* table, in
                             void* stream);
 // run_density_report's histogram (experiments.hpp:276-285); key = the path
 // key of (seed, path 0); table == nullptr: exact transform.
-LaunchResult launch_density(uint64_t key, uint64_t n, const double* table, int K, int degree,
-                            int dyadic, int stride, int simple, double tail, double z_max,
-                            double width, int n_bins, unsigned long long* bins,
+LaunchResult launch_density(uint64_t key, uint64_t n, const double* table, int table_words,
+                            int K, int degree, int dyadic, int stride, int simple, double tail,
+                            double z_max, double width, int n_bins, unsigned long long* bins,
                             unsigned long long* top_index, void* stream);
 // Upload constants and set kernel attributes on the current device.
 int configure_kernels();

@@ -105,19 +105,21 @@ __global__ void inv_cdf_kernel(const double* __restrict__ u, uint64_t n,
 // A draw that rounds to u == 1 (the reference throws) records its index.
 constexpr int kDensitySmemBins = 8192;
 
-__global__ void density_kernel(uint64_t key, uint64_t n, const double* __restrict__ table, int K,
-                               int degree, int dyadic, int stride, int simple, double tail,
-                               double z_max, double width, int n_bins,
+__global__ void density_kernel(uint64_t key, uint64_t n, const double* __restrict__ table,
+                               int table_words, int K, int degree, int dyadic, int stride,
+                               int simple, double tail, double z_max, double width, int n_bins,
                                unsigned long long* __restrict__ bins,
                                unsigned long long* __restrict__ top_index) {
+  extern __shared__ __align__(16) double s_table[];
   __shared__ __align__(16) double s_math[kMathWords];
   __shared__ unsigned int s_bins[kDensitySmemBins];
   const bool local_bins = n_bins <= kDensitySmemBins;
   stage_math(s_math);
+  for (int i = threadIdx.x; i < table_words; i += blockDim.x) s_table[i] = table[i];
   if (local_bins)
     for (int b = threadIdx.x; b < n_bins; b += blockDim.x) s_bins[b] = 0u;
   __syncthreads();
-  const TableView t{table, stride, K, degree, dyadic, simple, tail};
+  const TableView t{s_table, stride, K, degree, dyadic, simple, tail};
   const uint64_t step = static_cast<uint64_t>(gridDim.x) * blockDim.x;
   for (uint64_t base = static_cast<uint64_t>(blockIdx.x) * blockDim.x; base < n; base += step) {
     const uint64_t i = base + threadIdx.x;
@@ -309,19 +311,26 @@ LaunchResult launch_inv_cdf(const double* u, uint64_t n, const double* table, in
   return {static_cast<int>(cudaGetLastError()), 1};
 }
 
-LaunchResult launch_density(uint64_t key, uint64_t n, const double* table, int K, int degree,
-                            int dyadic, int stride, int simple, double tail, double z_max,
-                            double width, int n_bins, unsigned long long* bins,
+LaunchResult launch_density(uint64_t key, uint64_t n, const double* table, int table_words,
+                            int K, int degree, int dyadic, int stride, int simple, double tail,
+                            double z_max, double width, int n_bins, unsigned long long* bins,
                             unsigned long long* top_index, void* stream) {
+  const size_t smem = table != nullptr ? static_cast<size_t>(table_words) * sizeof(double) : 0;
+  if (smem > 0) {
+    const cudaError_t e = cudaFuncSetAttribute(density_kernel,
+                                               cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               static_cast<int>(smem));
+    if (e != cudaSuccess) return {static_cast<int>(e), 0};
+  }
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const uint64_t need = (n + 255) / 256;
   const uint64_t cap = static_cast<uint64_t>(sms) * 8;
   const unsigned blocks = static_cast<unsigned>(need < cap ? (need ? need : 1) : cap);
-  density_kernel<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(
-      key, n, table, K, degree, dyadic, stride, simple, tail, z_max, width, n_bins, bins,
-      top_index);
+  density_kernel<<<blocks, 256, smem, static_cast<cudaStream_t>(stream)>>>(
+      key, n, table, table != nullptr ? table_words : 0, K, degree, dyadic, stride, simple, tail,
+      z_max, width, n_bins, bins, top_index);
   return {static_cast<int>(cudaGetLastError()), 1};
 }
 
