@@ -219,10 +219,19 @@ def main():
     import paper_2012_09739_b200 as L
     from paper_2012_09739_b200.sharded import allgather_partials, shard_chunks
 
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    # LPMC_BENCH_SHARED_GPU=1: functional test of the multi-rank flow on a
+    # one-GPU box (every rank on cuda:0, gloo collectives on host tensors).
+    # Its numbers are not a scaling measurement and are never reported.
+    shared = os.environ.get("LPMC_BENCH_SHARED_GPU") == "1"
+    gpu_index = 0 if shared else local
+    torch.cuda.set_device(gpu_index)
+    dev = torch.device("cuda", gpu_index)
+    coll_dev = None if shared else dev
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
 
     def barrier():
         if world > 1:
@@ -236,7 +245,7 @@ def main():
     c0, c1 = shard_chunks(n_chunks, rank, world)
     cfgs = [(l, k) for l in LEVELS for k in KAHAN]
     plans = {(l, k): L.LevelPlan(model, l, spec, approx, k, n_total, SEED, path_base(l, k),
-                                 chunks=(c0, c1), device=local) for (l, k) in cfgs}
+                                 chunks=(c0, c1), device=gpu_index) for (l, k) in cfgs}
     # A dedicated stream: torch's legacy default stream has handle 0, which
     # the C-ABI reads as "the plan's own stream".
     stream = torch.cuda.Stream(dev)
@@ -257,7 +266,7 @@ def main():
         out = {}
         for (l, k) in cfgs:
             part = plans[(l, k)].collect_partials()
-            full = allgather_partials(part, n_chunks, None, dev) if world > 1 else part
+            full = allgather_partials(part, n_chunks, None, coll_dev) if world > 1 else part
             out[(l, k)] = L.fold_partials(full)
         return out
 
@@ -267,7 +276,7 @@ def main():
         torch.cuda.synchronize(dev)
         results = gather_all()
 
-    clocks = ClockSampler(local)
+    clocks = ClockSampler(gpu_index)
     if rank == 0:
         clocks.start()
     L.reset_launch_count()
@@ -295,7 +304,7 @@ def main():
     clk = clocks.stop() if rank == 0 else {}
 
     step_ms = sum(per_step_ms) / len(per_step_ms)
-    t = torch.tensor([step_ms], dtype=torch.float64, device=dev)
+    t = torch.tensor([step_ms], dtype=torch.float64, device=coll_dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     step_ms_max = float(t.item())
@@ -311,15 +320,15 @@ def main():
     for _ in range(e2e_steps):
         for (l, k) in cfgs:
             part = L.level_partials(model, l, spec, approx, k, n_total, SEED, path_base(l, k),
-                                    c0, c1, device=local)
-            full = allgather_partials(part, n_total // (1 << 18), None, dev) if world > 1 \
+                                    c0, c1, device=gpu_index)
+            full = allgather_partials(part, n_total // (1 << 18), None, coll_dev) if world > 1 \
                 else part
             m = L.fold_partials(full)
             L.level_stats_from_moments(m, l, spec, k, n_total)
     torch.cuda.synchronize(dev)
     barrier()
     e2e_s = (time.perf_counter() - w0) / e2e_steps
-    te = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+    te = torch.tensor([e2e_s], dtype=torch.float64, device=coll_dev)
     if world > 1:
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
     e2e_value = work_total / float(te.item())
@@ -333,7 +342,7 @@ def main():
         return
 
     # ---- roofline of the dominant kernel (level 10) --------------------------
-    peaks = L.measure_pipe_peaks(local)
+    peaks = L.measure_pipe_peaks(gpu_index)
     dom = [(10, False), (10, True)]
     dom_ms = statistics.mean(statistics.mean(per_cfg_ms[c]) for c in dom)
     dom_steps = fine_steps(10, (c1 - c0) * (1 << 18))
