@@ -886,6 +886,7 @@ void lpmc_default_cost_model(lpmc_cost_model* c) {  // mlmc.hpp:20-28
 }
 
 lpmc_status lpmc_round_to_precision(double x, int32_t m, double* out, lpmc_error* err) {
+  if (out == nullptr) return fail(err, LPMC_INVALID_ARGUMENT, "null argument");
   if (m < 1) return fail(err, LPMC_INVALID_ARGUMENT, "mantissa_bits must be >= 1");
   if (!round_prec(x, m, out)) return fail(err, LPMC_DOMAIN_ERROR, "non-finite operand");
   return ok(err);
@@ -931,6 +932,7 @@ lpmc_status lpmc_invcdf_build(int32_t kind, int32_t K, double* bp, double* coeff
 }
 
 lpmc_status lpmc_invcdf_eval(const lpmc_invcdf_table* t, double u, double* out, lpmc_error* err) {
+  if (t == nullptr || out == nullptr) return fail(err, LPMC_INVALID_ARGUMENT, "null argument");
   // InvCdfApprox::operator() / eval_upper (invcdf_approx.hpp:44-90)
   if (!(u > 0.0 && u < 1.0))
     return fail(err, LPMC_DOMAIN_ERROR, "approx_inv_cdf requires u in (0, 1)");
@@ -1030,6 +1032,7 @@ lpmc_status lpmc_run_coupled_paths(const lpmc_gbm* model, int32_t level,
                                    int32_t kahan, uint64_t n_paths, uint64_t seed,
                                    uint64_t path_base, const lpmc_options* opts,
                                    lpmc_moments* out, lpmc_error* err) {
+  if (out == nullptr) return fail(err, LPMC_INVALID_ARGUMENT, "null argument");
   for (int f = 0; f < 3; ++f) out[f] = lpmc_moments{0, 0.0, 0.0, 0.0, 0.0};
   if (n_paths == 0) return ok(err);  // mlmc.hpp:75: no batches, nothing simulated
   RunSpec s;
@@ -1052,6 +1055,7 @@ lpmc_status lpmc_estimate_level_stats(const lpmc_gbm* model, int32_t level,
                                       const lpmc_cost_model* cost, uint64_t path_base,
                                       const lpmc_options* opts, lpmc_level_stats* out,
                                       lpmc_error* err) {
+  if (out == nullptr) return fail(err, LPMC_INVALID_ARGUMENT, "null argument");
   if (n_paths < 2) return fail(err, LPMC_INVALID_ARGUMENT, "need at least 2 paths");  // mlmc.hpp:121
   lpmc_moments acc[3];
   lpmc_status st = lpmc_run_coupled_paths(model, level, prec, table, kahan, n_paths, seed,
@@ -1101,6 +1105,7 @@ lpmc_status lpmc_run_two_way_paths(const lpmc_gbm* model, int32_t level,
                                    int32_t kahan, uint64_t n_paths, uint64_t seed,
                                    uint64_t path_base, const lpmc_options* opts,
                                    lpmc_moments* out, lpmc_error* err) {
+  if (out == nullptr) return fail(err, LPMC_INVALID_ARGUMENT, "null argument");
   *out = lpmc_moments{0, 0.0, 0.0, 0.0, 0.0};
   lpmc_options o;
   lpmc_default_options(&o);
@@ -1152,6 +1157,7 @@ lpmc_status lpmc_allocate_samples(const lpmc_level_stats* stats, uint64_t n_leve
 
 lpmc_status lpmc_predicted_times(const lpmc_level_stats* stats, uint64_t n_levels, double eps,
                                  double* t_hat, double* t_bar, lpmc_error* err) {
+  if (t_hat == nullptr || t_bar == nullptr) return fail(err, LPMC_INVALID_ARGUMENT, "null argument");
   // predicted_times (mlmc.hpp:202-213)
   if (stats == nullptr || n_levels == 0) return fail(err, LPMC_INVALID_ARGUMENT, "no level stats");
   if (!(eps > 0.0)) return fail(err, LPMC_INVALID_ARGUMENT, "eps must be positive");
@@ -1169,6 +1175,7 @@ lpmc_status lpmc_predicted_times(const lpmc_level_stats* stats, uint64_t n_level
 
 lpmc_status lpmc_per_level_speedup(const lpmc_level_stats* s, double* value,
                                    int32_t* cost_ratio_only, lpmc_error* err) {
+  if (s == nullptr || value == nullptr || cost_ratio_only == nullptr) return fail(err, LPMC_INVALID_ARGUMENT, "null argument");
   // per_level_speedup (mlmc.hpp:223-230)
   if (!(s->v_hat > 0.0) || !(s->c_hat > 0.0))
     return fail(err, LPMC_INVALID_ARGUMENT, "per_level_speedup needs v_hat, c_hat > 0");
@@ -1257,6 +1264,7 @@ lpmc_status lpmc_level_partials(const lpmc_gbm* model, int32_t level,
                                 int32_t kahan, uint64_t n_paths, uint64_t seed,
                                 uint64_t path_base, uint64_t chunk_begin, uint64_t chunk_end,
                                 const lpmc_options* opts, lpmc_moments* out, lpmc_error* err) {
+  if (out == nullptr) return fail(err, LPMC_INVALID_ARGUMENT, "null argument");
   const uint64_t n_chunks = (n_paths + LPMC_CHUNK_PATHS - 1) / LPMC_CHUNK_PATHS;
   if (chunk_end > n_chunks || chunk_begin > chunk_end)
     return fail(err, LPMC_INVALID_ARGUMENT, "chunk range outside the run");
@@ -1281,6 +1289,7 @@ lpmc_status lpmc_step_error_probe(const lpmc_gbm* model, int32_t level,
                                   const lpmc_precision* prec, const lpmc_invcdf_table* table,
                                   uint64_t n_samples, uint64_t seed, const lpmc_options* opts,
                                   lpmc_step_error_stats* out, lpmc_error* err) {
+  if (out == nullptr) return fail(err, LPMC_INVALID_ARGUMENT, "null argument");
   // step_error_probe (sde.hpp:297-344)
   *out = lpmc_step_error_stats{0.0, 0.0, 0.0, 0.0, 0};
   if (prec != nullptr && prec->ieee_half)
@@ -1372,6 +1381,7 @@ lpmc_status lpmc_simulate_paths(const lpmc_gbm* model, int32_t level, const lpmc
                                 const lpmc_invcdf_table* table, int32_t kahan, uint64_t n_paths,
                                 uint64_t seed, uint64_t path_base, const lpmc_options* opts,
                                 double* out4, double* z_out, lpmc_error* err) {
+  if (out4 == nullptr) return fail(err, LPMC_INVALID_ARGUMENT, "null argument");
   if (n_paths == 0) return ok(err);
   if (n_paths > (1ull << 26)) return fail(err, LPMC_INVALID_ARGUMENT, "path dump limited to 2^26 paths");
   RunSpec s;
@@ -1443,6 +1453,7 @@ lpmc_status lpmc_device_math(int32_t op, const double* u, uint64_t n,
                              const lpmc_invcdf_table* table, double* out,
                              const lpmc_options* opts, lpmc_error* err) {
   if (n == 0) return ok(err);
+  if (u == nullptr || out == nullptr) return fail(err, LPMC_INVALID_ARGUMENT, "null argument");
   if (op < 0 || op > 3) return fail(err, LPMC_INVALID_ARGUMENT, "bad math op");
   if (op == 1 && table == nullptr) return fail(err, LPMC_INVALID_ARGUMENT, "op 1 needs a table");
   HostTable ht;
@@ -1559,6 +1570,7 @@ double lpmc_erfc_core(double t) {
 }
 
 lpmc_status lpmc_measure_pipe_peaks(int32_t device, double* out4, lpmc_error* err) {
+  if (out4 == nullptr) return fail(err, LPMC_INVALID_ARGUMENT, "null argument");
   DeviceCtx* ctx = nullptr;
   int dev = -1;
   lpmc_status st = get_ctx(device, &ctx, &dev, err);
@@ -1597,6 +1609,7 @@ lpmc_status lpmc_plan_create_range(const lpmc_gbm* model, int32_t level,
                                    int32_t kahan, uint64_t n_paths, uint64_t seed,
                                    uint64_t path_base, uint64_t chunk_begin, uint64_t chunk_end,
                                    const lpmc_options* opts, lpmc_plan** plan, lpmc_error* err) {
+  if (plan == nullptr) return fail(err, LPMC_INVALID_ARGUMENT, "null argument");
   *plan = nullptr;
   if (n_paths == 0) return fail(err, LPMC_INVALID_ARGUMENT, "plan needs n_paths > 0");
   const uint64_t n_chunks = (n_paths + LPMC_CHUNK_PATHS - 1) / LPMC_CHUNK_PATHS;
@@ -1627,6 +1640,7 @@ lpmc_status lpmc_plan_create_range(const lpmc_gbm* model, int32_t level,
 }
 
 lpmc_status lpmc_plan_launch(lpmc_plan* p, void* stream, lpmc_error* err) {
+  if (p == nullptr) return fail(err, LPMC_INVALID_ARGUMENT, "null argument");
   DeviceGuard guard;
   cudaError_t e = guard.set(p->device);
   if (e != cudaSuccess) return cuda_fail(err, e, "cudaSetDevice");
@@ -1639,6 +1653,7 @@ lpmc_status lpmc_plan_launch(lpmc_plan* p, void* stream, lpmc_error* err) {
 }
 
 lpmc_status lpmc_plan_collect(lpmc_plan* p, lpmc_moments* out, lpmc_error* err) {
+  if (p == nullptr || out == nullptr) return fail(err, LPMC_INVALID_ARGUMENT, "null argument");
   if (!p->launched) return fail(err, LPMC_INVALID_ARGUMENT, "plan was not launched");
   DeviceGuard guard;
   cudaError_t e = guard.set(p->device);
@@ -1663,6 +1678,7 @@ lpmc_status lpmc_plan_collect(lpmc_plan* p, lpmc_moments* out, lpmc_error* err) 
 }
 
 lpmc_status lpmc_plan_collect_partials(lpmc_plan* p, lpmc_moments* out, lpmc_error* err) {
+  if (p == nullptr || out == nullptr) return fail(err, LPMC_INVALID_ARGUMENT, "null argument");
   if (!p->launched) return fail(err, LPMC_INVALID_ARGUMENT, "plan was not launched");
   if (p->spec.reduce != LPMC_REDUCE_TREE)
     return fail(err, LPMC_INVALID_ARGUMENT, "partials need the tree reduction");
