@@ -178,3 +178,18 @@ def test_sampling_without_device_fails_loudly(lib):
     sde = lib.SdeModel()
     with pytest.raises(lib.InvalidArgument):
         lib.run_coupled_paths(sde, 2, lib.PrecisionSpec.fp32(), None, False, 16, 1, 0)
+
+
+def test_null_outputs_are_invalid_argument(lib):
+    """The C-ABI checks its pointers: a null output is invalid_argument, never
+    a crash (host-side entry points; no device needed)."""
+    import ctypes as C
+    from paper_2012_09739_b200 import _native as N
+    so = N.load()
+    err = N.Error()
+    st = (N.LevelStatsC * 1)()
+    assert so.lpmc_predicted_times(st, 1, 0.1, None, None, C.byref(err)) == N.LPMC_INVALID_ARGUMENT
+    assert so.lpmc_per_level_speedup(st, None, None, C.byref(err)) == N.LPMC_INVALID_ARGUMENT
+    assert so.lpmc_round_to_precision(1.0, 10, None, C.byref(err)) == N.LPMC_INVALID_ARGUMENT
+    assert so.lpmc_invcdf_eval(None, 0.3, None, C.byref(err)) == N.LPMC_INVALID_ARGUMENT
+    assert b"null" in err.message
