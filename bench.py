@@ -347,17 +347,22 @@ def main():
     dom_ms = statistics.mean(statistics.mean(per_cfg_ms[c]) for c in dom)
     dom_steps = fine_steps(10, (c1 - c0) * (1 << 18))
     ops_per_step = None
+    traffic = None
     if os.path.exists(PROFILE_CONST):
         with open(PROFILE_CONST) as f:
-            ops_per_step = json.load(f).get("fp64_lane_ops_per_path_step")
+            prof = json.load(f)
+        ops_per_step = prof.get("fp64_lane_ops_per_path_step")
+        traffic = prof.get("dram_bytes_per_launch")
     if ops_per_step:
         achieved = ops_per_step * dom_steps / (dom_ms * 1e-3)
         roof = {"bound": "fp64", "achieved": achieved / 1e12, "peak": peaks["fp64_ops_per_s"] / 1e12,
                 "unit": "Tops/s (fp64 lane-ops)", "frac": achieved / peaks["fp64_ops_per_s"],
-                "traffic": None,
+                "traffic": traffic,
                 "note": "non-tensor FP64-pipe bound (neither HBM nor tensor): per-path state in "
                         "registers, 0 bytes per path-step; ops/step from ncu "
-                        "(profiles/fp64_ops_per_path_step.json), peak = measured FMA lane rate"}
+                        "(profiles/fp64_ops_per_path_step.json), peak = measured FMA lane rate; "
+                        "traffic = DRAM bytes per level-10 launch (ncu --set full), against "
+                        "4.3e9 path-steps"}
     else:
         roof = {"bound": "fp64", "achieved": None, "peak": peaks["fp64_ops_per_s"] / 1e12,
                 "unit": "Tops/s (fp64 lane-ops)", "frac": None, "traffic": None,
