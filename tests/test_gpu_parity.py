@@ -210,6 +210,21 @@ def test_moments_bitexact_on_device_paths(gpu, oracle, level, m, approx, kahan, 
     assert [seq.d_hat.state(), seq.d_bar.state(), seq.d_four.state()] == want_seq
 
 
+@pytest.mark.parametrize("reduce,n", [("tree", 64 * 262144 + 1000),      # > one 64-chunk slice
+                                      ("sequential", 16 * 262144 + 777)])  # > one 16-chunk slice
+def test_launch_slices_bitexact(gpu, oracle, reduce, n):
+    """Runs longer than one launch slice (2^24 paths tree, 2^22 sequential)
+    still reduce bitwise like the restated tree / the reference order."""
+    model = gpu.make_gbm()
+    sp, tb = gpu.PrecisionSpec.fp32(), gpu.InvCdfApprox.parse("linear:16")
+    out = gpu.simulate_paths(model, 0, sp, tb, False, n, 3, 1 << 40)
+    dh, db = out[:, 0].copy(), out[:, 2].copy()
+    del out
+    got = gpu.run_coupled_paths(model, 0, sp, tb, False, n, 3, 1 << 40, reduce=reduce)
+    want = (oracle.tree_from_values if reduce == "tree" else oracle.sequential_from_values)(dh, db)
+    assert [got.d_hat.state(), got.d_bar.state(), got.d_four.state()] == want
+
+
 def test_partials_any_split_bitwise(gpu):
     model = gpu.make_gbm()
     sp, tb = gpu.PrecisionSpec.fp32(), gpu.InvCdfApprox.parse("linear:16")
