@@ -74,7 +74,7 @@ __device__ __forceinline__ void stage_math(double* s_math) {
 // Shared-memory table.  Dyadic layout (K <= 32): one 6-double record per
 // interval {3 - 2^(j+3), 2^(j+3), c0, c1, c2, c3} (128-bit loads).  General
 // layout: kTableRows rows of `stride` = K doubles: a_j, b_j - a_j, c0..c3,
-// v-thresholds.
+// v-thresholds; then one double, 1 / step_w.
 struct TableView {
   const double* base;
   int stride, K, degree, dyadic, simple;
@@ -135,14 +135,19 @@ __device__ __forceinline__ double approx_inv(const TableView& t, double u, bool 
     }
     r = fl >= t.K + 1 ? t.tail : r;  // w >= w_max: clamped tail
   } else {
+    // J(v) = #{k in 1..K : v <= T_k} with the host thresholds T_k = thr[k-1]
+    // (non-increasing); J == K is the tail.  Start from a float estimate of
+    // the reference's floor((-log2 v - 1) / step_w) and walk to the exact J
+    // (the walk alone is correct; the estimate makes it one or two compares).
     const int S = t.stride;
     const double* thr = t.base + 6 * S;
-    int lo = 0, hi = t.K - 1;
-    while (lo < hi) {
-      const int mid = (lo + hi) >> 1;
-      if (v <= thr[mid]) lo = mid + 1; else hi = mid;
-    }
-    const int j = lo;
+    const float inv_step = __double2float_rn(thr[S]);  // 1 / step_w, after T_K
+    const float w = -__log2f(__double2float_rn(v));
+    const float je = floorf((w - 1.0f) * inv_step);
+    int J = je < 0.0f ? 0 : (je > static_cast<float>(t.K) ? t.K : static_cast<int>(je));
+    while (J < t.K && v <= thr[J]) ++J;
+    while (J > 0 && v > thr[J - 1]) --J;
+    const int j = J < t.K ? J : t.K - 1;
     const double* b = t.base + j;
     double s = (2.0 * (up - b[0])) / b[S];
     s = s - 1.0;
@@ -154,7 +159,7 @@ __device__ __forceinline__ double approx_inv(const TableView& t, double u, bool 
       const double p3 = s * (2.5 * s * s - 1.5);
       r = r + b[4 * S] * p2 + b[5 * S] * p3;
     }
-    r = v <= thr[t.K - 1] ? t.tail : r;
+    r = J >= t.K ? t.tail : r;
   }
   r = lower ? -r : r;
   if constexpr (EXACT_HALF) r = u == 0.5 ? 0.0 : r;

@@ -249,7 +249,7 @@ lpmc_status prepare_table(const lpmc_invcdf_table* t, HostTable* out, lpmc_error
       for (int c = 0; c < 4; ++c) r[2 + c] = t->coeff[4 * j + c];
     }
   } else {  // rows of K
-    out->rows.assign(static_cast<size_t>(kTableRows) * K, 0.0);
+    out->rows.assign(static_cast<size_t>(kTableRows) * K + 1, 0.0);  // + 1 / step_w
     for (int j = 0; j < K; ++j) {
       out->rows[j] = left(j);
       out->rows[static_cast<size_t>(K) + j] = t->breakpoints[j] - left(j);
@@ -257,6 +257,7 @@ lpmc_status prepare_table(const lpmc_invcdf_table* t, HostTable* out, lpmc_error
     }
     const std::vector<double> thr = index_thresholds(K, t->w_max, t->step_w);
     std::copy(thr.begin(), thr.end(), out->rows.begin() + 6 * static_cast<size_t>(K));
+    out->rows[static_cast<size_t>(kTableRows) * K] = t->step_w > 0.0 ? 1.0 / t->step_w : 0.0;
   }
   return LPMC_OK;
 }

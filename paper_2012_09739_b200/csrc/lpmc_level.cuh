@@ -413,7 +413,7 @@ __global__ void __launch_bounds__(kBatch / Arith::NP, LPMC_LEVEL_MIN_CTAS)
 
 // ------------------------------------------------------- per-arith glue ----
 constexpr int kMaxTableK = 1024;
-constexpr int kMaxDynSmem = kTableRows * kMaxTableK * 8;
+constexpr int kMaxDynSmem = (kTableRows * kMaxTableK + 1) * 8;  // + 1 / step_w
 
 template <class Arith, bool KAHAN, int LEGS, int TAB, bool DUMP>
 cudaError_t launch_one(const LevelArgs& A, cudaStream_t s) {
