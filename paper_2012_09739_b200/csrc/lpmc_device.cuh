@@ -73,8 +73,9 @@ __device__ __forceinline__ void stage_math(double* s_math) {
 // ------------------------------------------- approximate inverse CDF -------
 // Shared-memory table.  Dyadic layout (K <= 32): one 6-double record per
 // interval {3 - 2^(j+3), 2^(j+3), c0, c1, c2, c3} (128-bit loads).  General
-// layout: kTableRows rows of `stride` = K doubles: a_j, b_j - a_j, c0..c3,
-// v-thresholds; then one double, 1 / step_w.
+// layout: one record of `stride` doubles per interval, {a_j, b_j - a_j, c0,
+// c1} (degree 1) or {.., c2, c3} (degree 3), then the K v-thresholds, then
+// 1 / step_w.
 struct TableView {
   const double* base;
   int stride, K, degree, dyadic, simple;
@@ -139,25 +140,29 @@ __device__ __forceinline__ double approx_inv(const TableView& t, double u, bool 
     // (non-increasing); J == K is the tail.  Start from a float estimate of
     // the reference's floor((-log2 v - 1) / step_w) and walk to the exact J
     // (the walk alone is correct; the estimate makes it one or two compares).
-    const int S = t.stride;
-    const double* thr = t.base + 6 * S;
-    const float inv_step = __double2float_rn(thr[S]);  // 1 / step_w, after T_K
+    const int W = t.stride;  // record width: 4 (degree 1) or 6 (degree 3)
+    const double* thr = t.base + W * t.K;
+    const float inv_step = __double2float_rn(thr[t.K]);  // 1 / step_w, after T_K
     const float w = -__log2f(__double2float_rn(v));
     const float je = floorf((w - 1.0f) * inv_step);
     int J = je < 0.0f ? 0 : (je > static_cast<float>(t.K) ? t.K : static_cast<int>(je));
     while (J < t.K && v <= thr[J]) ++J;
     while (J > 0 && v > thr[J - 1]) --J;
     const int j = J < t.K ? J : t.K - 1;
-    const double* b = t.base + j;
-    double s = (2.0 * (up - b[0])) / b[S];
+    const double* rec = t.base + W * j;
+    const math::D2 ad = math::load2(rec);       // a_j, b_j - a_j
+    const math::D2 c01 = math::load2(rec + 2);  // c0, c1
+    double s = (2.0 * (up - ad.a)) / ad.b;
     s = s - 1.0;
     s = s < -1.0 ? -1.0 : s;
     s = s > 1.0 ? 1.0 : s;
-    r = b[2 * S] + b[3 * S] * s;
+    r = c01.a + c01.b * s;
     if (t.degree == 3 || (!t.simple && r == 0.0)) {
+      // degree-1 tables have c2 = c3 = +0 (invcdf_approx.hpp:124-133)
+      const math::D2 c23 = t.degree == 3 ? math::load2(rec + 4) : math::D2{0.0, 0.0};
       const double p2 = 1.5 * s * s - 0.5;
       const double p3 = s * (2.5 * s * s - 1.5);
-      r = r + b[4 * S] * p2 + b[5 * S] * p3;
+      r = r + c23.a * p2 + c23.b * p3;
     }
     r = J >= t.K ? t.tail : r;
   }

@@ -211,7 +211,7 @@ std::vector<double> index_thresholds(int K, double w_max, double step_w) {
 struct HostTable {
   int K = 0, degree = 1, dyadic = 0, stride = 0, simple = 0;
   double tail = 0.0;
-  std::vector<double> rows;  // kTableRows * stride
+  std::vector<double> rows;  // device layout (lpmc_internal.h)
 };
 
 lpmc_status prepare_table(const lpmc_invcdf_table* t, HostTable* out, lpmc_error* err) {
@@ -248,16 +248,20 @@ lpmc_status prepare_table(const lpmc_invcdf_table* t, HostTable* out, lpmc_error
       r[1] = std::ldexp(1.0, j + 3);
       for (int c = 0; c < 4; ++c) r[2 + c] = t->coeff[4 * j + c];
     }
-  } else {  // rows of K
-    out->rows.assign(static_cast<size_t>(kTableRows) * K + 1, 0.0);  // + 1 / step_w
+  } else {  // records {a, b - a, c0, c1 (, c2, c3)}, thresholds, 1 / step_w
+    const int W = out->degree == 3 ? 6 : 4;
+    out->stride = W;
+    const size_t th = static_cast<size_t>(W) * K;
+    out->rows.assign(th + K + 1, 0.0);
     for (int j = 0; j < K; ++j) {
-      out->rows[j] = left(j);
-      out->rows[static_cast<size_t>(K) + j] = t->breakpoints[j] - left(j);
-      for (int c = 0; c < 4; ++c) out->rows[static_cast<size_t>(2 + c) * K + j] = t->coeff[4 * j + c];
+      double* r = out->rows.data() + static_cast<size_t>(W) * j;
+      r[0] = left(j);
+      r[1] = t->breakpoints[j] - left(j);
+      for (int c = 0; c < W - 2; ++c) r[2 + c] = t->coeff[4 * j + c];
     }
     const std::vector<double> thr = index_thresholds(K, t->w_max, t->step_w);
-    std::copy(thr.begin(), thr.end(), out->rows.begin() + 6 * static_cast<size_t>(K));
-    out->rows[static_cast<size_t>(kTableRows) * K] = t->step_w > 0.0 ? 1.0 / t->step_w : 0.0;
+    std::copy(thr.begin(), thr.end(), out->rows.begin() + th);
+    out->rows[th + K] = t->step_w > 0.0 ? 1.0 / t->step_w : 0.0;
   }
   return LPMC_OK;
 }

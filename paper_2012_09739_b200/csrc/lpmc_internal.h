@@ -21,9 +21,10 @@ enum class BarArith : int {
 };
 
 // Device table layouts (doubles):
-//   dyadic (K <= 32): K records {a_j, 2^(j+2), c0, c1, c2, c3} (kDyadicRecord)
-//   general: kTableRows rows of K: a_j, b_j - a_j, c0, c1, c2, c3,
-//            v-thresholds T_1..T_{K-1}, T_tail
+//   dyadic (K <= 32): K records {3 - 2^(j+3), 2^(j+3), c0, c1, c2, c3} (kDyadicRecord)
+//   general: K records {a_j, b_j - a_j, c0, c1} (degree 1) or {.., c2, c3}
+//            (degree 3), then the v-thresholds T_1..T_{K-1}, T_tail, then
+//            1 / step_w: at most kTableRows * K + 1 doubles
 constexpr int kTableRows = 7;
 constexpr int kDyadicRecord = 6;
 
@@ -45,7 +46,7 @@ struct LevelArgs {
   // approximation table (nullptr = exact inverse CDF for the bar legs)
   const double* table;
   int32_t K, degree, dyadic;
-  int32_t table_stride;  // general layout: K (rows of K doubles)
+  int32_t table_stride;  // general layout: record width (4 or 6 doubles)
   int32_t table_words;   // doubles to stage into shared memory
   int32_t table_simple;  // every c0 != 0 and c2 = c3 = +0: no signed-zero fix-up
   double tail;
