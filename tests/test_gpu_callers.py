@@ -259,3 +259,26 @@ def test_density_report_vs_reference(gpu, cv, idx):
         step = 1.0 / (c["hist_samples"] * width)
         assert np.max(np.abs(gy[~cu] - wy[~cu])) <= 3 * step + 1e-18
         assert abs(gy[~cu].sum() - wy[~cu].sum()) <= 1e-9
+
+
+def test_multi_run_and_probe_range_fallback(gpu, ref):
+    """Runs whose native fp32 legs leave the exact exponent range are re-run
+    in the exact emulation inside a multi-run call and in the probe too."""
+    P = gpu.PrecisionSpec
+    hot = gpu.make_gbm(80.0, 0.2)  # EM growth (1 + 80/16)^16 > 2^33 at level 4
+    tb = gpu.InvCdfApprox.parse("linear:16")
+    runs = [(4, P.fp32(), True, 300, 0), (3, P.fp32(), False, 500, 7)]
+    many = gpu.run_coupled_many(hot, tb, 2, runs)
+    for (level, spec, kahan, n, base), m in zip(runs, many):
+        one = gpu.run_coupled_paths(hot, level, spec, tb, kahan, n, 2, base)
+        assert [m.d_hat.state(), m.d_bar.state(), m.d_four.state()] == \
+               [one.d_hat.state(), one.d_bar.state(), one.d_four.state()]
+    n = 20000
+    got = gpu.step_error_probe(hot, 4, P.fp32(), tb, n, 5)
+    rc, msg, want = ref.step_error_probe(level=4, mantissa_bits=23, approx="linear:16",
+                                         n_samples=n, seed=5, mu=80.0)
+    assert rc == 0, msg
+    eps = 2.0 ** -52
+    g = [got.mean_eta, got.mean_abs_eta, got.mean_eta_prime, got.mean_abs_eta_prime]
+    for k, ak in ((0, 1), (1, 1), (2, 3), (3, 3)):
+        assert abs(g[k] - want[k]) <= 2 * n * eps * want[ak] + 1e-300
