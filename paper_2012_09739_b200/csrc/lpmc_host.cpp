@@ -319,6 +319,21 @@ Moments from_abi(const lpmc_moments& m) {
   return r;
 }
 
+// ------------------------------------------------------------ RNG keys ----
+// detail::mix64 (uniform.hpp:13-19) on the host
+uint64_t host_mix64(uint64_t z) {
+  z ^= z >> 33;
+  z *= 0xff51afd7ed558ccdull;
+  z ^= z >> 33;
+  z *= 0xc4ceb9fe1a85ec53ull;
+  z ^= z >> 33;
+  return z;
+}
+
+// mix64(seed + golden ratio) (uniform.hpp:23): the per-seed half of every
+// path key, hoisted out of the kernels
+uint64_t seed_key_of(uint64_t seed) { return host_mix64(seed + 0x9e3779b97f4a7c15ull); }
+
 // ------------------------------------------------------- run spec ----------
 struct RunSpec {
   LevelArgs args{};
@@ -373,16 +388,7 @@ lpmc_status build_spec(const lpmc_gbm* model, int32_t level, const lpmc_precisio
     s.has_table = true;
   }
   LevelArgs& A = s.args;
-  A.seed_key = 0;
-  {  // mix64(seed + golden) (uniform.hpp:23), hoisted out of every path
-    uint64_t z = seed + 0x9e3779b97f4a7c15ull;
-    z ^= z >> 33;
-    z *= 0xff51afd7ed558ccdull;
-    z ^= z >> 33;
-    z *= 0xc4ceb9fe1a85ec53ull;
-    z ^= z >> 33;
-    A.seed_key = z;
-  }
+  A.seed_key = seed_key_of(seed);  // hoisted out of every path
   A.path_base = path_base;
   A.n_paths = n_paths;
   A.level = level;
@@ -1512,15 +1518,7 @@ lpmc_status lpmc_density_histogram(const lpmc_invcdf_table* table, uint64_t seed
     if (st != LPMC_OK) return st;
   }
   // UniformStream(seed, 0) (uniform.hpp:23-25): the key of path 0
-  auto mix64 = [](uint64_t z) {
-    z ^= z >> 33;
-    z *= 0xff51afd7ed558ccdull;
-    z ^= z >> 33;
-    z *= 0xc4ceb9fe1a85ec53ull;
-    z ^= z >> 33;
-    return z;
-  };
-  const uint64_t key = mix64(mix64(seed + 0x9e3779b97f4a7c15ull) ^ mix64(0 + 0xbf58476d1ce4e5b9ull));
+  const uint64_t key = host_mix64(seed_key_of(seed) ^ host_mix64(0 + 0xbf58476d1ce4e5b9ull));
   DeviceCtx* ctx = nullptr;
   int dev = -1;
   lpmc_status st = get_ctx(opts ? opts->device : -1, &ctx, &dev, err);
