@@ -71,8 +71,11 @@ struct DeviceOptions {
   int reduce = LPMC_REDUCE_TREE;
   int device = -1;
   void* stream = nullptr;
+  int exact_z = LPMC_EXACT_Z_FAST;  // LPMC_EXACT_Z_GLIBC: the reference's Z bit for bit
 
-  lpmc_options c_abi() const { return lpmc_options{legs, payoff, strike, reduce, device, stream}; }
+  lpmc_options c_abi() const {
+    return lpmc_options{legs, payoff, strike, reduce, device, stream, exact_z};
+  }
 };
 
 namespace detail {

@@ -138,6 +138,19 @@ enum {
   LPMC_REDUCE_SEQUENTIAL = 1 /* the reference's own add/merge order, bitwise */
 };
 
+/*
+ * Exact Gaussians (gaussian.hpp:14-65: Acklam + one Newton step on glibc's
+ * erfc/exp/log).  FAST restates the algorithm for the B200 issue budget (own
+ * erfc/exp, MUFU-seeded divisions): Z within a few ulp of the reference's.
+ * GLIBC restates the reference's own operation sequence and glibc 2.39's
+ * erfc/exp/log bit for bit (lpmc_glibc.cuh): Z, hat legs and moments equal
+ * the reference's bitwise, at a lower throughput.
+ */
+enum {
+  LPMC_EXACT_Z_FAST = 0,
+  LPMC_EXACT_Z_GLIBC = 1
+};
+
 typedef struct lpmc_options {
   uint32_t legs;  /* LPMC_LEGS_*; 0 means LPMC_LEGS_ALL */
   int32_t payoff; /* LPMC_PAYOFF_* */
@@ -145,6 +158,7 @@ typedef struct lpmc_options {
   int32_t reduce; /* LPMC_REDUCE_* */
   int32_t device; /* CUDA ordinal; -1 = current device */
   void* stream;   /* cudaStream_t to launch on; NULL = the library's stream */
+  int32_t exact_z; /* LPMC_EXACT_Z_* */
 } lpmc_options;
 
 /* Raw MomentAccumulator state (stats.hpp:84-89). */
@@ -261,7 +275,8 @@ lpmc_status lpmc_simulate_paths(const lpmc_gbm* model, int32_t level, const lpmc
 
 /*
  * Exact Gaussians / approximate Gaussians for host-provided uniforms, on the
- * device (the kernels' own device functions; parity tests of a2/a3).
+ * device (the kernels' own device functions; parity tests of a2/a3); exact
+ * Gaussians in the mode opts->exact_z selects.
  */
 lpmc_status lpmc_device_inv_cdf(const double* u, uint64_t n, const lpmc_invcdf_table* table,
                                 double* out, const lpmc_options* opts, lpmc_error* err);
@@ -277,13 +292,20 @@ lpmc_status lpmc_measure_pipe_peaks(int32_t device, double* out4, lpmc_error* er
  * Diagnostics of the device math on host-given inputs: op 0 = exact inverse
  * CDF (the sampler's), 1 = approximate inverse CDF (table required), 2 = the
  * reference's Acklam+Newton formula on CUDA libdevice, 3 = erfc core on
- * t in [0, 6.5).
+ * t in [0, 6.5), 5 = exact inverse CDF in LPMC_EXACT_Z_GLIBC mode.
  */
 lpmc_status lpmc_device_math(int32_t op, const double* in, uint64_t n,
                              const lpmc_invcdf_table* table, double* out,
                              const lpmc_options* opts, lpmc_error* err);
 /* Host evaluation of the same erfc core (bitwise equal to op 3). */
 double lpmc_erfc_core(double t);
+/*
+ * Host evaluation of the restated glibc routines behind the reference's exact
+ * Gaussian (the LPMC_EXACT_Z_GLIBC device path, same code): op 0 = exp,
+ * 1 = log, 2 = erfc, 3 = exact_inv_cdf (gaussian.hpp:59-65).  *ok = 0 where
+ * the argument is outside the restated ranges.
+ */
+double lpmc_glibc_math(int32_t op, double x, int32_t* ok);
 
 /* ---- callers of the level sampler (mlmc.hpp:151-285) --------------------- */
 /* One run of a multi-run call. */

@@ -28,6 +28,7 @@ LEGS_HAT, LEGS_BAR, LEGS_ALL, LEGS_FINE = 1, 2, 3, 4
 ALLOCATION_STANDARD, ALLOCATION_NESTED = 0, 1
 PAYOFF_TERMINAL, PAYOFF_CALL = 0, 1
 REDUCE_TREE, REDUCE_SEQUENTIAL = 0, 1
+EXACT_Z_FAST, EXACT_Z_GLIBC = 0, 1
 APPROX_LINEAR, APPROX_CUBIC, APPROX_CONSTANT = 0, 1, 2
 BATCH_PATHS = 256
 CHUNK_BATCHES = 1024
@@ -85,7 +86,8 @@ class Precision(C.Structure):
 
 class Options(C.Structure):
     _fields_ = [("legs", C.c_uint32), ("payoff", _i32), ("strike", C.c_double),
-                ("reduce", _i32), ("device", _i32), ("stream", C.c_void_p)]
+                ("reduce", _i32), ("device", _i32), ("stream", C.c_void_p),
+                ("exact_z", _i32)]
 
 
 class Moments(C.Structure):
@@ -160,6 +162,7 @@ SIGNATURES = {
     "lpmc_measure_pipe_peaks": (_i32, [_i32, _dp, _P(Error)]),
     "lpmc_device_math": (_i32, [_i32, _dp, _u64, _P(InvCdfTable), _dp, _P(Options), _P(Error)]),
     "lpmc_erfc_core": (C.c_double, [C.c_double]),
+    "lpmc_glibc_math": (C.c_double, [_i32, C.c_double, _P(_i32)]),
     "lpmc_run_coupled_many": (_i32, [_P(Gbm), _P(InvCdfTable), _u64, _P(RunDesc), _u64,
                                      _P(Options), _P(Moments), _P(Error)]),
     "lpmc_run_two_way_paths": (_i32, [_P(Gbm), _i32, _P(Precision), _P(InvCdfTable), _i32, _u64,

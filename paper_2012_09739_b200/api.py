@@ -55,6 +55,9 @@ from ._native import DomainError, InvalidArgument, SamplerRuntimeError  # noqa: 
 _LEGS = {"hat": N.LEGS_HAT, "bar": N.LEGS_BAR, "all": N.LEGS_ALL, "fine": N.LEGS_FINE}
 _PAYOFF = {"terminal": N.PAYOFF_TERMINAL, "call": N.PAYOFF_CALL}
 _REDUCE = {"tree": N.REDUCE_TREE, "sequential": N.REDUCE_SEQUENTIAL}
+# exact Gaussians: "fast" (B200 restatement, ulp-level) or "glibc" (the
+# reference's Z bit for bit, lpmc_glibc.cuh)
+_EXACT_Z = {"fast": N.EXACT_Z_FAST, "glibc": N.EXACT_Z_GLIBC}
 
 
 # ----------------------------------------------------------- precision -----
@@ -375,12 +378,13 @@ class LevelStats:
 
 # ------------------------------------------------------------ sampling -----
 def _options(legs="all", payoff="terminal", strike=1.0, reduce="tree", device=None,
-             stream=None) -> N.Options:
+             stream=None, exact_z="fast") -> N.Options:
     try:
         return N.default_options(legs=_LEGS[legs], payoff=_PAYOFF[payoff], strike=float(strike),
                                  reduce=_REDUCE[reduce],
                                  device=-1 if device is None else int(device),
-                                 stream=None if stream is None else int(stream))
+                                 stream=None if stream is None else int(stream),
+                                 exact_z=_EXACT_Z[exact_z])
     except KeyError as e:
         raise InvalidArgument(f"bad option value {e}") from None
 
@@ -524,13 +528,14 @@ def simulate_paths(model: SdeModel, level: int, spec_low: PrecisionSpec,
 
 
 def device_inv_cdf(u: np.ndarray, approx: Optional[InvCdfApprox] = None,
-                   device: Optional[int] = None) -> np.ndarray:
+                   device: Optional[int] = None, exact_z: str = "fast") -> np.ndarray:
     """Exact (approx None) or approximate inverse CDF of host uniforms,
-    evaluated by the kernels' device functions."""
+    evaluated by the kernels' device functions (exact Gaussians in the
+    ``exact_z`` mode: "fast" or "glibc")."""
     u = np.ascontiguousarray(u, dtype=np.float64)
     out = np.zeros_like(u)
     err = N.Error()
-    opts = _options(device=device)
+    opts = _options(device=device, exact_z=exact_z)
     N.check(N.load().lpmc_device_inv_cdf(u.ctypes.data_as(N._dp), len(u), _table_ptr(approx),
                                          out.ctypes.data_as(N._dp), C.byref(opts),
                                          C.byref(err)), err)
@@ -539,8 +544,9 @@ def device_inv_cdf(u: np.ndarray, approx: Optional[InvCdfApprox] = None,
 
 def device_math(op: str, x: np.ndarray, approx: Optional[InvCdfApprox] = None,
                 device: Optional[int] = None) -> np.ndarray:
-    """Diagnostics: op in {"exact", "approx", "exact_libdevice", "erfc"}."""
-    ops = {"exact": 0, "approx": 1, "exact_libdevice": 2, "erfc": 3}
+    """Diagnostics: op in {"exact", "approx", "exact_libdevice", "erfc",
+    "exact_glibc"}."""
+    ops = {"exact": 0, "approx": 1, "exact_libdevice": 2, "erfc": 3, "exact_glibc": 5}
     x = np.ascontiguousarray(x, dtype=np.float64)
     out = np.zeros_like(x)
     err = N.Error()
@@ -554,6 +560,16 @@ def device_math(op: str, x: np.ndarray, approx: Optional[InvCdfApprox] = None,
 def erfc_core(t: float) -> float:
     """Host evaluation of the device erfc core (bitwise the device's)."""
     return float(N.load().lpmc_erfc_core(float(t)))
+
+
+def glibc_math(op: str, x: float) -> Optional[float]:
+    """Host evaluation of the restated glibc routine (op in {"exp", "log",
+    "erfc", "inv_cdf"}), bitwise the device's LPMC_EXACT_Z_GLIBC path; None
+    where the argument is outside the restated ranges."""
+    ok = N.C.c_int32(0)
+    r = float(N.load().lpmc_glibc_math({"exp": 0, "log": 1, "erfc": 2, "inv_cdf": 3}[op],
+                                       float(x), N.C.byref(ok)))
+    return r if ok.value else None
 
 
 class LevelPlan:

@@ -24,6 +24,7 @@
 
 #include "../../include/lpmc_b200.h"
 #include "lpmc_internal.h"
+#include "lpmc_glibc.cuh"
 #include "lpmc_math.cuh"
 
 namespace lpmc_b200 {
@@ -374,6 +375,8 @@ lpmc_status build_spec(const lpmc_gbm* model, int32_t level, const lpmc_precisio
     return fail(err, LPMC_INVALID_ARGUMENT, "bad reduction mode");
   if (prec->ieee_half && m != 10)
     return fail(err, LPMC_INVALID_ARGUMENT, "ieee_half requires mantissa_bits == 10");
+  if (o.exact_z != LPMC_EXACT_Z_FAST && o.exact_z != LPMC_EXACT_Z_GLIBC)
+    return fail(err, LPMC_INVALID_ARGUMENT, "bad exact_z mode");
 
   RunSpec& s = *spec;
   s = RunSpec{};
@@ -393,6 +396,7 @@ lpmc_status build_spec(const lpmc_gbm* model, int32_t level, const lpmc_precisio
   A.n_paths = n_paths;
   A.level = level;
   A.legs = static_cast<int32_t>(o.legs);
+  A.exact_z = o.exact_z;
   // per-level constants (sde.hpp:217-224)
   const double dtf = std::ldexp(model->horizon, -level);
   const double sdtf = std::sqrt(dtf);
@@ -886,6 +890,7 @@ void lpmc_default_options(lpmc_options* o) {
   o->reduce = LPMC_REDUCE_TREE;
   o->device = -1;
   o->stream = nullptr;
+  o->exact_z = LPMC_EXACT_Z_FAST;
 }
 
 void lpmc_default_cost_model(lpmc_cost_model* c) {  // mlmc.hpp:20-28
@@ -1465,7 +1470,7 @@ lpmc_status lpmc_device_math(int32_t op, const double* u, uint64_t n,
                              const lpmc_options* opts, lpmc_error* err) {
   if (n == 0) return ok(err);
   if (u == nullptr || out == nullptr) return fail(err, LPMC_INVALID_ARGUMENT, "null argument");
-  if (op < 0 || op > 3) return fail(err, LPMC_INVALID_ARGUMENT, "bad math op");
+  if (op < 0 || op > 5 || op == 4) return fail(err, LPMC_INVALID_ARGUMENT, "bad math op");
   if (op == 1 && table == nullptr) return fail(err, LPMC_INVALID_ARGUMENT, "op 1 needs a table");
   HostTable ht;
   if (table != nullptr) {
@@ -1543,6 +1548,7 @@ lpmc_status lpmc_density_histogram(const lpmc_invcdf_table* table, uint64_t seed
     LaunchResult r = launch_density(key, n_samples, table ? dtab.ptr : nullptr,
                                     static_cast<int>(ht.rows.size()), ht.K, ht.degree, ht.dyadic,
                                     ht.stride, ht.simple, ht.tail, z_max, bin_width, n_bins,
+                                    opts != nullptr ? opts->exact_z : LPMC_EXACT_Z_FAST,
                                     dbins.ptr, dtop.ptr, stream);
     t_launches += r.kernels;
     e = static_cast<cudaError_t>(r.cuda_error);
@@ -1564,12 +1570,30 @@ lpmc_status lpmc_density_histogram(const lpmc_invcdf_table* table, uint64_t seed
 
 lpmc_status lpmc_device_inv_cdf(const double* u, uint64_t n, const lpmc_invcdf_table* table,
                                 double* out, const lpmc_options* opts, lpmc_error* err) {
-  return lpmc_device_math(table ? 1 : 0, u, n, table, out, opts, err);
+  const bool glibc = opts != nullptr && opts->exact_z == LPMC_EXACT_Z_GLIBC;
+  return lpmc_device_math(table ? 1 : (glibc ? 5 : 0), u, n, table, out, opts, err);
 }
 
 double lpmc_erfc_core(double t) {
   if (!(t >= 0.0 && t < math::kFastTMax)) return std::erfc(t);
   return math::erfc_fast(t, math::kMathTableHost);
+}
+
+static_assert(LPMC_EXACT_Z_FAST == 0 && LPMC_EXACT_Z_GLIBC == 1, "dev::kZFast / kZGlibc");
+
+double lpmc_glibc_math(int32_t op, double x, int32_t* ok) {
+  bool good = true;
+  double r = std::nan("");
+  const double* t = math::kMathTableHost;
+  switch (op) {
+    case 0: r = glibc::exp(x, t, &good); break;
+    case 1: r = glibc::log(x, t, &good); break;
+    case 2: r = glibc::erfc(x, t, &good); break;
+    case 3: r = glibc::inv_cdf(x, t, &good); break;
+    default: good = false;
+  }
+  if (ok != nullptr) *ok = good ? 1 : 0;
+  return r;
 }
 
 lpmc_status lpmc_measure_pipe_peaks(int32_t device, double* out4, lpmc_error* err) {

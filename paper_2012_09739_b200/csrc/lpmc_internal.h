@@ -36,6 +36,7 @@ struct LevelArgs {
   uint64_t n_batches;  // batches in this launch
   int32_t level;
   int32_t legs;        // 1 hat, 2 bar, 3 both
+  int32_t exact_z;     // LPMC_EXACT_Z_FAST / _GLIBC
   // carrier legs (sde.hpp:219-221)
   double mu, sigma, x0, dtf, sdtf, dtc;
   // bar-leg constants already rounded into the low precision (sde.hpp:222-224, :232)
@@ -87,8 +88,9 @@ LaunchResult launch_inv_cdf(const double* u, uint64_t n, const double* table, in
 // key of (seed, path 0); table == nullptr: exact transform.
 LaunchResult launch_density(uint64_t key, uint64_t n, const double* table, int table_words,
                             int K, int degree, int dyadic, int stride, int simple, double tail,
-                            double z_max, double width, int n_bins, unsigned long long* bins,
-                            unsigned long long* top_index, void* stream);
+                            double z_max, double width, int n_bins, int exact_z,
+                            unsigned long long* bins, unsigned long long* top_index,
+                            void* stream);
 // Upload constants and set kernel attributes on the current device.
 int configure_kernels();
 // Lane-op rates on the current device: fp64 FMA, fp32 FMA, half2 HFMA2

@@ -12,6 +12,7 @@
 #include <cstdint>
 
 #include "lpmc_device.cuh"
+#include "lpmc_glibc.cuh"
 #include "lpmc_internal.h"
 
 namespace lpmc_b200 {
@@ -68,8 +69,10 @@ __global__ void sequential_batch_kernel(const double* __restrict__ path_diff, ui
 }
 
 // op 0: exact Gaussian (the sampler's path), 1: approximate (table), 2: the
-// reference's formula on libdevice, 3: erfc core on t in [0, 6.5).  Threads
-// past n evaluate a dummy so the warp-collective tail pass stays converged.
+// reference's formula on libdevice, 3: erfc core on t in [0, 6.5), 5: the
+// exact Gaussian in LPMC_EXACT_Z_GLIBC mode (the reference's bit for bit).
+// Threads past n evaluate a dummy so the warp-collective tail pass stays
+// converged.
 __global__ void inv_cdf_kernel(const double* __restrict__ u, uint64_t n,
                                const double* __restrict__ table, int K, int degree, int dyadic,
                                int stride, int simple, double tail, int op,
@@ -90,6 +93,8 @@ __global__ void inv_cdf_kernel(const double* __restrict__ u, uint64_t n,
     r = approx_inv(t, x);
   } else if (op == 2) {
     r = math::phi_inv_libdevice(x);
+  } else if (op == 5) {
+    r = glibc::exact_z(x, s_math);
   } else {
     r = math::erfc_fast(x, s_math);
   }
@@ -104,11 +109,12 @@ __global__ void inv_cdf_kernel(const double* __restrict__ u, uint64_t n,
 // evaluate a dummy draw so the warp-collective tail pass stays converged.
 // A draw that rounds to u == 1 (the reference throws) records its index.
 constexpr int kDensitySmemBins = 8192;
+constexpr int LPMC_DENSITY_GLIBC = 1;    // LPMC_EXACT_Z_GLIBC
 
 __global__ void density_kernel(uint64_t key, uint64_t n, const double* __restrict__ table,
                                int table_words, int K, int degree, int dyadic, int stride,
                                int simple, double tail, double z_max, double width, int n_bins,
-                               unsigned long long* __restrict__ bins,
+                               int exact_z, unsigned long long* __restrict__ bins,
                                unsigned long long* __restrict__ top_index) {
   extern __shared__ __align__(16) double s_table[];
   __shared__ __align__(16) double s_math[kMathWords];
@@ -131,6 +137,8 @@ __global__ void density_kernel(uint64_t key, uint64_t n, const double* __restric
     double z;
     if (table != nullptr) {
       z = approx_inv(t, u);
+    } else if (exact_z == LPMC_DENSITY_GLIBC) {  // the reference's Z bit for bit
+      z = glibc::exact_z(u, s_math);
     } else {
       double uu[1] = {u}, zz[1];
       math::phi_inv_multi<1>(uu, zz, s_math);
@@ -313,8 +321,9 @@ LaunchResult launch_inv_cdf(const double* u, uint64_t n, const double* table, in
 
 LaunchResult launch_density(uint64_t key, uint64_t n, const double* table, int table_words,
                             int K, int degree, int dyadic, int stride, int simple, double tail,
-                            double z_max, double width, int n_bins, unsigned long long* bins,
-                            unsigned long long* top_index, void* stream) {
+                            double z_max, double width, int n_bins, int exact_z,
+                            unsigned long long* bins, unsigned long long* top_index,
+                            void* stream) {
   const size_t smem = table != nullptr ? static_cast<size_t>(table_words) * sizeof(double) : 0;
   if (smem > 0) {
     const cudaError_t e = cudaFuncSetAttribute(density_kernel,
@@ -330,7 +339,7 @@ LaunchResult launch_density(uint64_t key, uint64_t n, const double* table, int t
   const unsigned blocks = static_cast<unsigned>(need < cap ? (need ? need : 1) : cap);
   density_kernel<<<blocks, 256, smem, static_cast<cudaStream_t>(stream)>>>(
       key, n, table, table != nullptr ? table_words : 0, K, degree, dyadic, stride, simple, tail,
-      z_max, width, n_bins, bins, top_index);
+      z_max, width, n_bins, exact_z, bins, top_index);
   return {static_cast<int>(cudaGetLastError()), 1};
 }
 

@@ -14,6 +14,7 @@
 #pragma once
 
 #include "lpmc_device.cuh"
+#include "lpmc_glibc.cuh"
 
 namespace lpmc_b200 {
 namespace dev {
@@ -63,8 +64,11 @@ __device__ __forceinline__ void draw_uniforms(uint64_t (&kc)[NP], Uniforms<H * N
 // the next batch are drawn between the Acklam stage and the Newton stage, so
 // the integer RNG interleaves with FP64 work instead of forming its own
 // phase (software pipelining across batches).
+// Exact-Gaussian mode of a level instance (values of LPMC_EXACT_Z_*).
+enum : int { kZFast = 0, kZGlibc = 1 };
+
 template <class Arith, int TAB, bool NEED_EXACT, bool BAR, bool CHECKED, bool DUMP, int H,
-          bool PREFETCH>
+          bool PREFETCH, int ZM>
 __device__ __forceinline__ void gen_draws(const LevelArgs& A, const TableView& tab,
                                           const double* s_math, const Arith& ar,
                                           uint64_t (&kc)[Arith::NP], bool (&u1)[Arith::NP],
@@ -90,7 +94,11 @@ __device__ __forceinline__ void gen_draws(const LevelArgs& A, const TableView& t
       }
     }
   double zz[D];
-  if constexpr (NEED_EXACT) {
+  if constexpr (NEED_EXACT && ZM == kZGlibc) {
+    if constexpr (PREFETCH) draw_uniforms<NP, H>(kc, next);
+#pragma unroll
+    for (int d = 0; d < D; ++d) zz[d] = glibc::exact_z(u[d], s_math);
+  } else if constexpr (NEED_EXACT) {
     double v[D], x0[D];
     uint32_t neg = 0;
 #pragma unroll
@@ -127,7 +135,7 @@ __device__ __forceinline__ void gen_draws(const LevelArgs& A, const TableView& t
   }
 }
 
-template <class Arith, bool KAHAN, int LEGS, int TAB, bool CHECKED, bool DUMP>
+template <class Arith, bool KAHAN, int LEGS, int TAB, bool CHECKED, bool DUMP, int ZM>
 __device__ __forceinline__ void simulate(const LevelArgs& A, const TableView& tab,
                                          const double* s_math,
                                          const uint64_t (&local)[Arith::NP],
@@ -241,7 +249,7 @@ __device__ __forceinline__ void simulate(const LevelArgs& A, const TableView& ta
     T zb[1];
     Uniforms<NP> cur, unused;
     draw_uniforms<NP, 1>(kc, cur);
-    gen_draws<Arith, TAB, kNeedExact, kBar, CHECKED, DUMP, 1, false>(
+    gen_draws<Arith, TAB, kNeedExact, kBar, CHECKED, DUMP, 1, false, ZM>(
         A, tab, s_math, ar, kc, u1, fk, local, valid, 0, cur, unused, z, zb);
     if constexpr (kHat) hat_fine(z[0], 0);
     if constexpr (kBar) bar_fine(zb[0], 0);
@@ -256,7 +264,7 @@ __device__ __forceinline__ void simulate(const LevelArgs& A, const TableView& ta
         double z[2 * G][NP];
         T zb[2 * G];
         Uniforms<2 * G * NP> next;
-        gen_draws<Arith, TAB, kNeedExact, kBar, CHECKED, DUMP, 2 * G, true>(
+        gen_draws<Arith, TAB, kNeedExact, kBar, CHECKED, DUMP, 2 * G, true, ZM>(
             A, tab, s_math, ar, kc, u1, fk, local, valid, 2 * m, cur, next, z, zb);
         cur = next;
 #pragma unroll
@@ -275,7 +283,7 @@ __device__ __forceinline__ void simulate(const LevelArgs& A, const TableView& ta
         T zb[2];
         Uniforms<2 * NP> cur, unused;
         draw_uniforms<NP, 2>(kc, cur);
-        gen_draws<Arith, TAB, kNeedExact, kBar, CHECKED, DUMP, 2, false>(
+        gen_draws<Arith, TAB, kNeedExact, kBar, CHECKED, DUMP, 2, false, ZM>(
             A, tab, s_math, ar, kc, u1, fk, local, valid, 2 * m, cur, unused, z, zb);
         if constexpr (kHat) hat_fine(z[0], 2 * m);
         if constexpr (kBar) bar_fine(zb[0], 2 * m);
@@ -305,13 +313,13 @@ __device__ __forceinline__ void simulate(const LevelArgs& A, const TableView& ta
 // Exact replay of this thread's paths (only for suspects: a u == 1 or
 // u == 1/2 draw, or a non-finite end state): exact transforms and the first
 // failure in the reference's serial order.
-template <class Arith, bool KAHAN, int LEGS, int TAB>
+template <class Arith, bool KAHAN, int LEGS, int TAB, int ZM>
 __device__ __noinline__ void replay_checked(const LevelArgs& A, TableView tab,
                                             const double* s_math,
                                             const uint64_t (&local)[Arith::NP],
                                             const bool (&valid)[Arith::NP],
                                             PathEnd<Arith::NP>& R) {
-  simulate<Arith, KAHAN, LEGS, TAB, true, false>(A, tab, s_math, local, valid, R);
+  simulate<Arith, KAHAN, LEGS, TAB, true, false, ZM>(A, tab, s_math, local, valid, R);
 }
 
 // 256 threads x 4 CTAs per SM (64 registers) for one path per thread; the
@@ -320,7 +328,7 @@ __device__ __noinline__ void replay_checked(const LevelArgs& A, TableView tab,
 #ifndef LPMC_LEVEL_MIN_CTAS
 #define LPMC_LEVEL_MIN_CTAS 4
 #endif
-template <class Arith, bool KAHAN, int LEGS, int TAB, bool DUMP>
+template <class Arith, bool KAHAN, int LEGS, int TAB, bool DUMP, int ZM>
 __global__ void __launch_bounds__(kBatch / Arith::NP, LPMC_LEVEL_MIN_CTAS)
     level_kernel(const __grid_constant__ LevelArgs A) {
   constexpr int NP = Arith::NP;
@@ -353,14 +361,14 @@ __global__ void __launch_bounds__(kBatch / Arith::NP, LPMC_LEVEL_MIN_CTAS)
   }
 
   PathEnd<NP> R;
-  simulate<Arith, KAHAN, LEGS, TAB, false, DUMP>(A, tab, s_math, local, valid, R);
+  simulate<Arith, KAHAN, LEGS, TAB, false, DUMP, ZM>(A, tab, s_math, local, valid, R);
 
   bool any_suspect = false;
 #pragma unroll
   for (int p = 0; p < NP; ++p) any_suspect |= valid[p] && R.suspect[p];
   if (any_suspect) {  // rare: exact values and first failure (serial order)
     const bool range_bad = R.range_bad;
-    replay_checked<Arith, KAHAN, LEGS, TAB>(A, tab, s_math, local, valid, R);
+    replay_checked<Arith, KAHAN, LEGS, TAB, ZM>(A, tab, s_math, local, valid, R);
     R.range_bad |= range_bad;
 #pragma unroll
     for (int p = 0; p < NP; ++p) {
@@ -415,10 +423,10 @@ __global__ void __launch_bounds__(kBatch / Arith::NP, LPMC_LEVEL_MIN_CTAS)
 constexpr int kMaxTableK = 1024;
 constexpr int kMaxDynSmem = (kTableRows * kMaxTableK + 1) * 8;  // + 1 / step_w
 
-template <class Arith, bool KAHAN, int LEGS, int TAB, bool DUMP>
+template <class Arith, bool KAHAN, int LEGS, int TAB, bool DUMP, int ZM>
 cudaError_t launch_one(const LevelArgs& A, cudaStream_t s) {
   const size_t smem = TAB != kTabNone ? static_cast<size_t>(A.table_words) * sizeof(double) : 0;
-  level_kernel<Arith, KAHAN, LEGS, TAB, DUMP>
+  level_kernel<Arith, KAHAN, LEGS, TAB, DUMP, ZM>
       <<<static_cast<unsigned>(A.n_batches), kBatch / Arith::NP, smem, s>>>(A);
   return cudaGetLastError();
 }
@@ -426,12 +434,24 @@ cudaError_t launch_one(const LevelArgs& A, cudaStream_t s) {
 // Table kind: none (exact Gaussians for the bar legs), a dyadic linear table
 // with the signed-zero fix-up proved unnecessary (every BASELINE config; no
 // per-draw branches), or any other table.
+// Exact-Gaussian mode: glibc instances exist only where exact Gaussians are
+// drawn (hat legs, or bar legs without a table).
 template <class Arith, bool KAHAN, int LEGS, bool DUMP>
 cudaError_t pick_approx(const LevelArgs& A, cudaStream_t s) {
-  if (A.table == nullptr) return launch_one<Arith, KAHAN, LEGS, kTabNone, DUMP>(A, s);
+  const bool glibc = A.exact_z == kZGlibc;  // == LPMC_EXACT_Z_GLIBC
+  if (A.table == nullptr)
+    return glibc ? launch_one<Arith, KAHAN, LEGS, kTabNone, DUMP, kZGlibc>(A, s)
+                 : launch_one<Arith, KAHAN, LEGS, kTabNone, DUMP, kZFast>(A, s);
+  if constexpr (LEGS != 2) {
+    if (glibc) {
+      if (A.dyadic && A.table_simple && A.degree == 1)
+        return launch_one<Arith, KAHAN, LEGS, kTabDyadicLinear, DUMP, kZGlibc>(A, s);
+      return launch_one<Arith, KAHAN, LEGS, kTabGeneric, DUMP, kZGlibc>(A, s);
+    }
+  }
   if (A.dyadic && A.table_simple && A.degree == 1)
-    return launch_one<Arith, KAHAN, LEGS, kTabDyadicLinear, DUMP>(A, s);
-  return launch_one<Arith, KAHAN, LEGS, kTabGeneric, DUMP>(A, s);
+    return launch_one<Arith, KAHAN, LEGS, kTabDyadicLinear, DUMP, kZFast>(A, s);
+  return launch_one<Arith, KAHAN, LEGS, kTabGeneric, DUMP, kZFast>(A, s);
 }
 
 template <class Arith, bool KAHAN, bool DUMP>
@@ -448,13 +468,24 @@ cudaError_t launch_level(const LevelArgs& A, bool kahan, bool dump, cudaStream_t
   return kahan ? pick_legs<Arith, true, false>(A, s) : pick_legs<Arith, false, false>(A, s);
 }
 
-template <class Arith, bool KAHAN, int LEGS, bool DUMP>
-cudaError_t configure_one() {
-  cudaError_t e = cudaFuncSetAttribute(level_kernel<Arith, KAHAN, LEGS, kTabGeneric, DUMP>,
+template <class Arith, bool KAHAN, int LEGS, bool DUMP, int ZM>
+cudaError_t configure_tabs() {
+  cudaError_t e = cudaFuncSetAttribute(level_kernel<Arith, KAHAN, LEGS, kTabGeneric, DUMP, ZM>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem);
   if (e != cudaSuccess) return e;
-  return cudaFuncSetAttribute(level_kernel<Arith, KAHAN, LEGS, kTabDyadicLinear, DUMP>,
+  return cudaFuncSetAttribute(level_kernel<Arith, KAHAN, LEGS, kTabDyadicLinear, DUMP, ZM>,
                               cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem);
+}
+
+template <class Arith, bool KAHAN, int LEGS, bool DUMP>
+cudaError_t configure_one() {
+  const cudaError_t e = configure_tabs<Arith, KAHAN, LEGS, DUMP, kZFast>();
+  if constexpr (LEGS == 2) {
+    return e;  // bar legs with a table draw no exact Gaussians: no glibc instance
+  } else {
+    if (e != cudaSuccess) return e;
+    return configure_tabs<Arith, KAHAN, LEGS, DUMP, kZGlibc>();
+  }
 }
 
 template <class Arith>

@@ -7,8 +7,11 @@ namespace lpmc_b200 {
 cudaError_t launch_level_carrier(const LevelArgs& A, bool kahan, bool dump, void* stream) {
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (A.legs == 1) {  // carrier legs only: precision, Kahan and table do not apply
-    return dump ? dev::launch_one<dev::ArithCarrier, false, 1, dev::kTabNone, true>(A, s)
-                : dev::launch_one<dev::ArithCarrier, false, 1, dev::kTabNone, false>(A, s);
+    if (A.exact_z == dev::kZGlibc)
+      return dump ? dev::launch_one<dev::ArithCarrier, false, 1, dev::kTabNone, true, dev::kZGlibc>(A, s)
+                  : dev::launch_one<dev::ArithCarrier, false, 1, dev::kTabNone, false, dev::kZGlibc>(A, s);
+    return dump ? dev::launch_one<dev::ArithCarrier, false, 1, dev::kTabNone, true, dev::kZFast>(A, s)
+                : dev::launch_one<dev::ArithCarrier, false, 1, dev::kTabNone, false, dev::kZFast>(A, s);
   }
   return dev::launch_level<dev::ArithCarrier>(A, kahan, dump, s);
 }

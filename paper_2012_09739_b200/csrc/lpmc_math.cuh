@@ -30,6 +30,7 @@
 #include <cstring>
 #include <cmath>
 
+#include "lpmc_glibc_coef.h"
 #include "lpmc_math_coef.h"
 
 #ifdef __CUDACC__
@@ -152,18 +153,21 @@ constexpr int kErfcxN = LPMC_ERFCX_INTERVALS;
 constexpr int kErfcxWords = kErfcxRow * kErfcxN;
 constexpr int kExpN = LPMC_EXP_N;
 constexpr int kExpWords = 2 * kExpN;
-constexpr int kMathTableWords = kErfcxWords + kExpWords;  // one shared-memory block
+constexpr int kGlibcOff = kErfcxWords + kExpWords;  // glibc exp and log tables (lpmc_glibc.cuh)
+constexpr int kGlibcWords = 512;
+constexpr int kMathTableWords = kGlibcOff + kGlibcWords;  // one shared-memory block
 constexpr double kFastTMax = 6.5;  // the erfcx intervals cover [0, 6.5)
 
-// erfcx records, then the 2^(j/64) hi/lo pairs (host copy)
-static const double kMathTableHost[kMathTableWords] = {LPMC_ERFCX_COEF_LIST, LPMC_EXP_TAB_LIST};
+// erfcx records, the 2^(j/64) hi/lo pairs, the glibc exp and log tables (host copy)
+static const double kMathTableHost[kMathTableWords] = {LPMC_ERFCX_COEF_LIST, LPMC_EXP_TAB_LIST,
+                                                       LPMC_GLIBC_EXP_TAB, LPMC_GLIBC_LOG_TAB};
 
 #ifdef __CUDACC__
 // TU-local (static): every kernel translation unit has its own copy and
 // uploads it in its configure function (upload_math_constants).
 static __constant__ double kMath[kMathCount];
-static __device__ const double kMathTable[kMathTableWords] = {LPMC_ERFCX_COEF_LIST,
-                                                               LPMC_EXP_TAB_LIST};
+static __device__ const double kMathTable[kMathTableWords] = {
+    LPMC_ERFCX_COEF_LIST, LPMC_EXP_TAB_LIST, LPMC_GLIBC_EXP_TAB, LPMC_GLIBC_LOG_TAB};
 
 static inline cudaError_t upload_math_constants() {
   return cudaMemcpyToSymbol(kMath, kMathHost, sizeof(kMathHost));

@@ -58,6 +58,8 @@ __global__ void __launch_bounds__(kProbeThreads)
     double z;
     if constexpr (APPROX) {
       z = approx_inv<true>(tab, u);
+    } else if (A.exact_z == kZGlibc) {  // the reference's Z bit for bit
+      z = glibc::exact_z(u, s_math);
     } else {
       const double uu[1] = {u};
       double zz[1];

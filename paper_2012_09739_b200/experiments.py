@@ -234,12 +234,14 @@ def run_density_report(config: ExperimentConfig, curve_points: int = 2048,
     approx = config.build_approx()
     u = np.arange(1, curve_points, dtype=np.float64) / curve_points
     dev = ext.get("device")
-    curve = device_inv_cdf(u, approx, device=dev) if len(u) else np.zeros(0)
+    zmode = ext.get("exact_z", "fast")
+    curve = device_inv_cdf(u, approx, device=dev, exact_z=zmode) if len(u) else np.zeros(0)
     rows = [DensityRow("curve", float(a), float(b)) for a, b in zip(u, curve)]
     if approx is not None:
         z_max = approx.max_value()
     else:
-        z_max = float(device_inv_cdf(np.array([1.0 - 2.0 ** -30]), None, device=dev)[0])
+        z_max = float(device_inv_cdf(np.array([1.0 - 2.0 ** -30]), None, device=dev,
+                                     exact_z=zmode)[0])
     n_bins = int(math.ceil(2.0 * z_max / bin_width)) + 1
     bins = density_histogram(approx, config.seed, hist_samples, z_max, bin_width, n_bins, **ext)
     for b in range(n_bins):
