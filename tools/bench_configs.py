@@ -3,7 +3,9 @@
 
     python tools/bench_configs.py [--quick] > profiles/r01_configs.json
 
-C1  level 6, fp64 exact, 2-way hat legs only (and all four legs), 2^20 paths
+C1  level 6, fp64 exact, 2-way hat legs only (and all four legs), 2^20 paths;
+    also in LPMC_EXACT_Z_GLIBC mode (the reference's Z bit for bit), with the
+    C2 level-10 launch
 C3  fp16 bar legs (native IEEE half2 and the emulated m=10 reference
     arithmetic), constant:16 / linear:16, +-Kahan, levels 0..8, 2^24 paths,
     bar legs only
@@ -44,9 +46,10 @@ def timed(plan, stream, reps=3):
     return best
 
 
-def run(name, level, spec, approx, kahan, n, legs="all", payoff="terminal", stream=None):
+def run(name, level, spec, approx, kahan, n, legs="all", payoff="terminal", stream=None,
+        exact_z="fast"):
     plan = L.LevelPlan(L.make_gbm(), level, spec, approx, kahan, n, 1, level << 40, legs=legs,
-                       payoff=payoff, strike=1.0)
+                       payoff=payoff, strike=1.0, exact_z=exact_z)
     ms = timed(plan, stream)
     m = plan.collect() if False else None  # noqa: F841
     plan.launch(stream.cuda_stream)
@@ -56,6 +59,7 @@ def run(name, level, spec, approx, kahan, n, legs="all", payoff="terminal", stre
     return {"config": name, "level": level, "mantissa_bits": spec.mantissa_bits,
             "ieee_half": spec.ieee_half, "approx": None if approx is None else approx.kind + ":" +
             str(approx.interval_count()), "kahan": kahan, "legs": legs, "payoff": payoff,
+            "exact_z": exact_z,
             "paths": n, "ms": ms, "path_steps_per_s": steps / (ms * 1e-3),
             "v_hat": res.d_hat.variance(), "v_bar": res.d_bar.variance(),
             "V_bar": res.d_four.variance()}
@@ -76,6 +80,10 @@ def main():
         n24 = 1 << 22
     out.append(run("C1", 6, P.carrier(), None, False, n20, legs="hat", stream=s))
     out.append(run("C1-all-legs", 6, P.carrier(), None, False, n20, stream=s))
+    # the reference's Z bit for bit (LPMC_EXACT_Z_GLIBC): C1 and the C2 level 10
+    out.append(run("C1-glibc", 6, P.carrier(), None, False, n20, legs="hat", stream=s,
+                   exact_z="glibc"))
+    out.append(run("C2-l10-glibc", 10, P.fp32(), lin, False, 1 << 22, stream=s, exact_z="glibc"))
     for spec, tag in ((P.fp16_ieee(), "C3-ieee-half2"), (P.fp16(), "C3-emulated-m10")):
         for tab in (con, lin):
             for k in (False, True):
