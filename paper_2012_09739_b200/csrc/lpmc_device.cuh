@@ -25,7 +25,8 @@ constexpr int kChunkBatches = 1024;
 constexpr int kChunkThreads = 512;
 constexpr uint64_t kTopDraw = 0x1FFFFFFFFFFFFFull;  // (w >> 11) that rounds u to 1.0
 constexpr uint64_t kNoFail = ~0ull;
-constexpr int kMathWords = math::kMathTableWords;
+constexpr int kMathWords = math::kMathTableWords;  // incl. the glibc-mode tables
+constexpr int kFastMathWords = math::kGlibcOff;     // the fast mode's tables only
 constexpr uint64_t kHalfDraw = 1ull << 52;  // (w >> 11) that rounds u to exactly 1/2
 
 enum : uint32_t { kStageDraw = 0, kStageHatFine = 1, kStageBarFine = 2, kStageHatCoarse = 3,
@@ -66,8 +67,8 @@ __device__ __forceinline__ double uniform_of(uint64_t b) {
 }
 
 // erfcx records + 2^(j/64) pairs into (16-byte aligned) shared memory
-__device__ __forceinline__ void stage_math(double* s_math) {
-  for (int i = threadIdx.x; i < kMathWords; i += blockDim.x) s_math[i] = math::kMathTable[i];
+__device__ __forceinline__ void stage_math(double* s_math, int words = kMathWords) {
+  for (int i = threadIdx.x; i < words; i += blockDim.x) s_math[i] = math::kMathTable[i];
 }
 
 // ------------------------------------------- approximate inverse CDF -------

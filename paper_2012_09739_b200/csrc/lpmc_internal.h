@@ -36,7 +36,6 @@ struct LevelArgs {
   uint64_t n_batches;  // batches in this launch
   int32_t level;
   int32_t legs;        // 1 hat, 2 bar, 3 both
-  int32_t exact_z;     // LPMC_EXACT_Z_FAST / _GLIBC
   // carrier legs (sde.hpp:219-221)
   double mu, sigma, x0, dtf, sdtf, dtc;
   // bar-leg constants already rounded into the low precision (sde.hpp:222-224, :232)
@@ -61,6 +60,9 @@ struct LevelArgs {
   double* z_out;                 // dump: n x 2^level
   unsigned long long* err_key;   // atomicMin: (local path << 24) | (kind << 22) | step
   unsigned int* range_flag;      // native bar legs left the guarded exponent range
+  // exact Gaussians: LPMC_EXACT_Z_FAST / _GLIBC (last: the fields above keep
+  // the offsets the kernels' 128-bit uniform constant loads were tuned for)
+  int32_t exact_z;
 };
 
 struct LaunchResult {

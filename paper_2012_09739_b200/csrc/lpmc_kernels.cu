@@ -94,7 +94,9 @@ __global__ void inv_cdf_kernel(const double* __restrict__ u, uint64_t n,
   } else if (op == 2) {
     r = math::phi_inv_libdevice(x);
   } else if (op == 5) {
-    r = glibc::exact_z(x, s_math);
+    double uu[1] = {x}, zz[1];
+    glibc::inv_cdf_multi<1>(uu, zz, s_math);
+    r = zz[0];
   } else {
     r = math::erfc_fast(x, s_math);
   }
@@ -138,7 +140,9 @@ __global__ void density_kernel(uint64_t key, uint64_t n, const double* __restric
     if (table != nullptr) {
       z = approx_inv(t, u);
     } else if (exact_z == LPMC_DENSITY_GLIBC) {  // the reference's Z bit for bit
-      z = glibc::exact_z(u, s_math);
+      double uu[1] = {u}, zz[1];
+      glibc::inv_cdf_multi<1>(uu, zz, s_math);
+      z = zz[0];
     } else {
       double uu[1] = {u}, zz[1];
       math::phi_inv_multi<1>(uu, zz, s_math);

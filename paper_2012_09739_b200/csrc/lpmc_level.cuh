@@ -96,8 +96,7 @@ __device__ __forceinline__ void gen_draws(const LevelArgs& A, const TableView& t
   double zz[D];
   if constexpr (NEED_EXACT && ZM == kZGlibc) {
     if constexpr (PREFETCH) draw_uniforms<NP, H>(kc, next);
-#pragma unroll
-    for (int d = 0; d < D; ++d) zz[d] = glibc::exact_z(u[d], s_math);
+    glibc::inv_cdf_multi<D>(u, zz, s_math);
   } else if constexpr (NEED_EXACT) {
     double v[D], x0[D];
     uint32_t neg = 0;
@@ -338,8 +337,9 @@ __global__ void __launch_bounds__(kBatch / Arith::NP, LPMC_LEVEL_MIN_CTAS)
   constexpr bool kNeedExact = kHat || TAB == kTabNone;
 
   extern __shared__ __align__(16) double s_table[];
-  __shared__ __align__(16) double s_math[kNeedExact ? kMathWords : 2];
-  if constexpr (kNeedExact) stage_math(s_math);
+  constexpr int kStaged = ZM == kZGlibc ? kMathWords : kFastMathWords;
+  __shared__ __align__(16) double s_math[kNeedExact ? kStaged : 2];
+  if constexpr (kNeedExact) stage_math(s_math, kStaged);
   TableView tab{};
   if constexpr (TAB != kTabNone) {
     for (int i = threadIdx.x; i < A.table_words; i += blockDim.x) s_table[i] = A.table[i];

@@ -59,7 +59,10 @@ __global__ void __launch_bounds__(kProbeThreads)
     if constexpr (APPROX) {
       z = approx_inv<true>(tab, u);
     } else if (A.exact_z == kZGlibc) {  // the reference's Z bit for bit
-      z = glibc::exact_z(u, s_math);
+      const double uu[1] = {u};
+      double zz[1];
+      glibc::inv_cdf_multi<1>(uu, zz, s_math);
+      z = zz[0];
     } else {
       const double uu[1] = {u};
       double zz[1];
