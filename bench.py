@@ -357,12 +357,13 @@ def main():
         achieved = ops_per_step * dom_steps / (dom_ms * 1e-3)
         roof = {"bound": "fp64", "achieved": achieved / 1e12, "peak": peaks["fp64_ops_per_s"] / 1e12,
                 "unit": "Tops/s (fp64 lane-ops)", "frac": achieved / peaks["fp64_ops_per_s"],
-                "traffic": traffic,
+                "traffic": traffic, "co_limits": prof.get("co_limits"),
                 "note": "non-tensor FP64-pipe bound (neither HBM nor tensor): per-path state in "
                         "registers, 0 bytes per path-step; ops/step from ncu "
                         "(profiles/fp64_ops_per_path_step.json), peak = measured FMA lane rate; "
                         "traffic = DRAM bytes per level-10 launch (ncu --set full), against "
-                        "4.3e9 path-steps"}
+                        "4.3e9 path-steps; co_limits = the same launch's issue, FP64-pipe and "
+                        "shared-memory-crossbar utilisation (DESIGN.md section 8)"}
     else:
         roof = {"bound": "fp64", "achieved": None, "peak": peaks["fp64_ops_per_s"] / 1e12,
                 "unit": "Tops/s (fp64 lane-ops)", "frac": None, "traffic": None,

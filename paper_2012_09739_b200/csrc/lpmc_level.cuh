@@ -327,8 +327,12 @@ __device__ __noinline__ void replay_checked(const LevelArgs& A, TableView tab,
 #ifndef LPMC_LEVEL_MIN_CTAS
 #define LPMC_LEVEL_MIN_CTAS 4
 #endif
+#ifndef LPMC_GLIBC_MIN_CTAS
+#define LPMC_GLIBC_MIN_CTAS 4
+#endif
 template <class Arith, bool KAHAN, int LEGS, int TAB, bool DUMP, int ZM>
-__global__ void __launch_bounds__(kBatch / Arith::NP, LPMC_LEVEL_MIN_CTAS)
+__global__ void __launch_bounds__(kBatch / Arith::NP,
+                                  ZM == kZGlibc ? LPMC_GLIBC_MIN_CTAS : LPMC_LEVEL_MIN_CTAS)
     level_kernel(const __grid_constant__ LevelArgs A) {
   constexpr int NP = Arith::NP;
   constexpr bool kFineOnly = LEGS == 4;

@@ -141,6 +141,17 @@ int main(int argc, char** argv) {
   auto c = run_coupled_paths(gbm, 3, PrecisionSpec::carrier(), nullptr, false, 4096, 3, 0);
   CHECK(c.d_four.variance() == 0.0);
 
+  // bit-exact mode: the reference's C1 checkpoint (tests/golden: seed 1,
+  // level 6, fp64, exact Gaussians, 2^20 paths) in the reference's order
+  {
+    DeviceOptions o;
+    o.exact_z = LPMC_EXACT_Z_GLIBC;
+    o.reduce = LPMC_REDUCE_SEQUENTIAL;
+    auto m = run_coupled_paths(gbm, 6, PrecisionSpec::carrier(), nullptr, false, 1u << 20, 1, 0, 1, o);
+    CHECK(m.d_hat.mean() == 0x1.6bc234c2c6020p-16);
+    CHECK(m.d_hat.variance() == 0x1.e0629aa8f5008p+3 / 1048575.0);
+  }
+
   // non-finite operand -> std::domain_error (test_sde.cpp:168-173 shape)
   SdeModel blow = make_gbm(1e30, 0.0, 1e300);
   CHECK(throws<std::domain_error>(
