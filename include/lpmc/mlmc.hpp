@@ -72,9 +72,13 @@ struct DeviceOptions {
   int device = -1;
   void* stream = nullptr;
   int exact_z = LPMC_EXACT_Z_FAST;  // LPMC_EXACT_Z_GLIBC: the reference's Z bit for bit
+  std::vector<int32_t> devices;      // > 1 entries: shard every run over these devices
 
   lpmc_options c_abi() const {
-    return lpmc_options{legs, payoff, strike, reduce, device, stream, exact_z};
+    return lpmc_options{legs,    payoff,         strike,
+                        reduce,  device,         stream,
+                        exact_z, devices.empty() ? nullptr : devices.data(),
+                        static_cast<int32_t>(devices.size())};
   }
 };
 

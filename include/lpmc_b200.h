@@ -50,7 +50,7 @@
 extern "C" {
 #endif
 
-#define LPMC_B200_ABI_VERSION 1
+#define LPMC_B200_ABI_VERSION 2
 
 typedef enum lpmc_status {
   LPMC_OK = 0,
@@ -159,6 +159,16 @@ typedef struct lpmc_options {
   int32_t device; /* CUDA ordinal; -1 = current device */
   void* stream;   /* cudaStream_t to launch on; NULL = the library's stream */
   int32_t exact_z; /* LPMC_EXACT_Z_* */
+  /*
+   * Devices of one process to shard each run over (NULL / n_devices <= 1:
+   * the single device above).  Runs split into contiguous 2^18-path chunk
+   * ranges, one per listed device (a device may repeat), launched
+   * concurrently; the partials are folded in chunk order, so results are
+   * bitwise those of one device.  Multi-device calls are synchronous and
+   * ignore `stream`.
+   */
+  const int32_t* devices;
+  int32_t n_devices;
 } lpmc_options;
 
 /* Raw MomentAccumulator state (stats.hpp:84-89). */

@@ -87,7 +87,7 @@ class Precision(C.Structure):
 class Options(C.Structure):
     _fields_ = [("legs", C.c_uint32), ("payoff", _i32), ("strike", C.c_double),
                 ("reduce", _i32), ("device", _i32), ("stream", C.c_void_p),
-                ("exact_z", _i32)]
+                ("exact_z", _i32), ("devices", C.POINTER(_i32)), ("n_devices", _i32)]
 
 
 class Moments(C.Structure):
@@ -211,7 +211,7 @@ def load(build_if_missing: bool = True) -> C.CDLL:
             fn = getattr(lib, name)
             fn.restype = res
             fn.argtypes = args
-        if lib.lpmc_abi_version() != 1:
+        if lib.lpmc_abi_version() != 2:
             raise ImportError("liblpmc_b200.so ABI version mismatch")
         _lib = lib
         return lib

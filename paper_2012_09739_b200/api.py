@@ -378,15 +378,23 @@ class LevelStats:
 
 # ------------------------------------------------------------ sampling -----
 def _options(legs="all", payoff="terminal", strike=1.0, reduce="tree", device=None,
-             stream=None, exact_z="fast") -> N.Options:
+             stream=None, exact_z="fast", devices=None) -> N.Options:
+    """Per-call options.  ``devices``: several CUDA ordinals of this process
+    to shard each run over (chunk ranges, folded in chunk order: bitwise the
+    single-device result); the call is then synchronous."""
     try:
-        return N.default_options(legs=_LEGS[legs], payoff=_PAYOFF[payoff], strike=float(strike),
-                                 reduce=_REDUCE[reduce],
-                                 device=-1 if device is None else int(device),
-                                 stream=None if stream is None else int(stream),
-                                 exact_z=_EXACT_Z[exact_z])
+        o = N.default_options(legs=_LEGS[legs], payoff=_PAYOFF[payoff], strike=float(strike),
+                              reduce=_REDUCE[reduce],
+                              device=-1 if device is None else int(device),
+                              stream=None if stream is None else int(stream),
+                              exact_z=_EXACT_Z[exact_z])
     except KeyError as e:
         raise InvalidArgument(f"bad option value {e}") from None
+    if devices is not None and len(devices) > 0:
+        o._devices = (C.c_int32 * len(devices))(*[int(d) for d in devices])  # kept alive
+        o.devices = C.cast(o._devices, C.POINTER(C.c_int32))
+        o.n_devices = len(devices)
+    return o
 
 
 def _table_ptr(approx: Optional[InvCdfApprox]):

@@ -346,6 +346,7 @@ struct RunSpec {
   HostTable table;
   bool has_table = false;
   int device = -1;
+  std::vector<int> devices;  // > 1 entries: shard over these devices (run_multi_device)
   bool ieee = false;
 };
 
@@ -377,6 +378,8 @@ lpmc_status build_spec(const lpmc_gbm* model, int32_t level, const lpmc_precisio
     return fail(err, LPMC_INVALID_ARGUMENT, "ieee_half requires mantissa_bits == 10");
   if (o.exact_z != LPMC_EXACT_Z_FAST && o.exact_z != LPMC_EXACT_Z_GLIBC)
     return fail(err, LPMC_INVALID_ARGUMENT, "bad exact_z mode");
+  if (o.n_devices < 0 || (o.n_devices > 0 && o.devices == nullptr) || o.n_devices > 1024)
+    return fail(err, LPMC_INVALID_ARGUMENT, "bad device list");
 
   RunSpec& s = *spec;
   s = RunSpec{};
@@ -384,6 +387,7 @@ lpmc_status build_spec(const lpmc_gbm* model, int32_t level, const lpmc_precisio
   s.kahan = kahan != 0;
   s.reduce = o.reduce;
   s.device = o.device;
+  if (o.n_devices > 1) s.devices.assign(o.devices, o.devices + o.n_devices);
   s.ieee = prec->ieee_half != 0;
   if (table != nullptr) {
     const lpmc_status st = prepare_table(table, &s.table, err);
@@ -743,8 +747,151 @@ void mask_legs(const RunSpec& s, std::vector<Moments>& parts) {
   }
 }
 
+// ------------------------------------------------ several devices -------
+// Runs sharded over the devices of one process: run i's chunk range splits
+// into one contiguous sub-range per listed device (device of sub-range k =
+// list[(k + i) mod n], so one-chunk runs rotate over the devices); each
+// device's sub-runs go round-robin to its stream pool with that slot's
+// buffers; read-backs land in one portable pinned staging area; the host
+// waits once, then interprets runs in list order and sub-runs in chunk
+// order -- the first failure is the serial one, and the concatenated
+// partials are exactly one device's (chunk partials do not depend on where
+// they are computed).  A sub-run whose native legs left their range is
+// re-run alone in the exact emulation (bitwise what a full re-run gives).
+struct MultiStage {
+  std::mutex mu;
+  double* ptr = nullptr;
+  size_t cap = 0;  // doubles
+};
+MultiStage g_multi_stage;
+
+lpmc_status run_multi_device(std::vector<RunSpec>& specs, const std::vector<int>& devs,
+                             std::vector<std::vector<Moments>>* out, lpmc_error* err) {
+  out->assign(specs.size(), {});
+  const size_t nd = devs.size();
+  // contexts of the distinct devices, locked in ascending order
+  std::map<int, DeviceCtx*> ctxs;
+  for (int d : devs) {
+    if (ctxs.count(d)) continue;
+    DeviceCtx* ctx = nullptr;
+    int resolved = -1;
+    const lpmc_status stt = get_ctx(d, &ctx, &resolved, err);
+    if (stt != LPMC_OK) return stt;
+    ctxs[resolved] = ctx;
+  }
+  std::lock_guard<std::mutex> stage_lock(g_multi_stage.mu);
+  std::vector<std::unique_lock<std::mutex>> locks;
+  for (auto& kv : ctxs) locks.emplace_back(kv.second->mu);
+  DeviceGuard guard;  // restores the caller's current device on return
+  cudaError_t e = guard.set(-1);
+  if (e != cudaSuccess) return cuda_fail(err, e, "cudaGetDevice");
+  guard.changed = true;
+
+  struct Sub {
+    size_t run;
+    int dev, slot;
+    RunSpec spec;
+    Enqueued q;
+    size_t off;
+  };
+  std::vector<Sub> subs;
+  std::map<int, int> next_slot;
+  for (size_t i = 0; i < specs.size(); ++i) {
+    const RunSpec& s = specs[i];
+    if (s.n_paths == 0) continue;  // mlmc.hpp:75: nothing simulated
+    const uint64_t b = s.chunk_begin, n = s.chunk_end - s.chunk_begin;
+    for (size_t k = 0; k < nd; ++k) {
+      const uint64_t c0 = b + n * k / nd, c1 = b + n * (k + 1) / nd;
+      if (c0 == c1) continue;
+      int dev = devs[(k + i) % nd];
+      if (dev < 0 && cudaGetDevice(&dev) != cudaSuccess) dev = 0;
+      Sub u{i, dev, next_slot[dev]++ % kPoolStreams, s, Enqueued{}, 0};
+      u.spec.chunk_begin = c0;
+      u.spec.chunk_end = c1;
+      u.spec.devices.clear();
+      subs.push_back(std::move(u));
+    }
+  }
+  size_t total = 0;
+  for (Sub& u : subs) {
+    u.off = total;
+    total += 2 + 15 * acc_count_of(u.spec);
+  }
+  if (total > g_multi_stage.cap) {
+    if (g_multi_stage.ptr != nullptr) cudaFreeHost(g_multi_stage.ptr);
+    g_multi_stage.ptr = nullptr;
+    g_multi_stage.cap = 0;
+    e = cudaHostAlloc(reinterpret_cast<void**>(&g_multi_stage.ptr), total * sizeof(double),
+                      cudaHostAllocPortable);
+    if (e != cudaSuccess) return cuda_fail(err, e, "pinned staging");
+    g_multi_stage.cap = total;
+  }
+  // streams and buffers (each slot reserved for its largest sub-run first)
+  for (Sub& u : subs) {
+    StreamPool& P = ctxs.at(u.dev)->pool;
+    if ((e = cudaSetDevice(u.dev)) != cudaSuccess) break;
+    if (P.streams[u.slot] == nullptr &&
+        (e = cudaStreamCreateWithFlags(&P.streams[u.slot], cudaStreamNonBlocking)) != cudaSuccess)
+      break;
+    if ((e = reserve(u.spec, P.bufs[u.slot])) != cudaSuccess) break;
+  }
+  for (size_t j = 0; j < subs.size() && e == cudaSuccess; ++j) {
+    Sub& u = subs[j];
+    StreamPool& P = ctxs.at(u.dev)->pool;
+    double* stage = g_multi_stage.ptr + u.off;
+    if ((e = cudaSetDevice(u.dev)) != cudaSuccess) break;
+    e = enqueue_run(u.spec, P.bufs[u.slot], P.streams[u.slot], &u.q);
+    if (e == cudaSuccess)
+      e = enqueue_readback(u.q, P.bufs[u.slot], P.streams[u.slot],
+                           reinterpret_cast<unsigned long long*>(stage),
+                           reinterpret_cast<unsigned int*>(stage + 1), stage + 2);
+  }
+  for (auto& kv : ctxs) {
+    if (cudaSetDevice(kv.first) != cudaSuccess) continue;
+    for (int k = 0; k < kPoolStreams; ++k)
+      if (kv.second->pool.streams[k] != nullptr) {
+        const cudaError_t s2 = cudaStreamSynchronize(kv.second->pool.streams[k]);
+        if (e == cudaSuccess) e = s2;
+      }
+  }
+  if (e != cudaSuccess) return cuda_fail(err, e, "level sampler");
+  for (Sub& u : subs) {
+    const double* stage = g_multi_stage.ptr + u.off;
+    unsigned long long key;
+    unsigned int range;
+    std::memcpy(&key, stage, sizeof key);
+    std::memcpy(&range, stage + 1, sizeof range);
+    std::vector<Moments> parts;
+    bool rerun = false;
+    lpmc_status stt = interpret_run(u.spec, acc_count(u.q), key, range, stage + 2, &parts, &rerun,
+                                    err);
+    if (stt != LPMC_OK) return stt;
+    if (rerun) {
+      StreamPool& P = ctxs.at(u.dev)->pool;
+      if ((e = cudaSetDevice(u.dev)) != cudaSuccess) return cuda_fail(err, e, "cudaSetDevice");
+      u.spec.arith = BarArith::kF64Round;
+      Enqueued q2;
+      e = enqueue_run(u.spec, P.bufs[u.slot], P.streams[u.slot], &q2);
+      if (e != cudaSuccess) return cuda_fail(err, e, "fallback launch");
+      stt = collect_run(u.spec, P.bufs[u.slot], P.streams[u.slot], q2, &parts, &rerun, err);
+      if (stt != LPMC_OK) return stt;
+    }
+    auto& dst = (*out)[u.run];
+    dst.insert(dst.end(), parts.begin(), parts.end());
+  }
+  for (size_t i = 0; i < specs.size(); ++i) mask_legs(specs[i], (*out)[i]);
+  return ok(err);
+}
+
 // Full synchronous run on one device: enqueue, collect, fallback re-run.
 lpmc_status run_sync(RunSpec& s, void* user_stream, std::vector<Moments>* parts, lpmc_error* err) {
+  if (s.devices.size() > 1) {
+    std::vector<RunSpec> one(1, s);
+    std::vector<std::vector<Moments>> out;
+    const lpmc_status st = run_multi_device(one, s.devices, &out, err);
+    if (st == LPMC_OK) *parts = std::move(out[0]);
+    return st;
+  }
   DeviceCtx* ctx = nullptr;
   int dev = -1;
   lpmc_status stt = get_ctx(s.device, &ctx, &dev, err);
@@ -780,6 +927,8 @@ lpmc_status run_many(std::vector<RunSpec>& specs, void* user_stream,
                      std::vector<std::vector<Moments>>* out, lpmc_error* err) {
   out->assign(specs.size(), {});
   if (specs.empty()) return ok(err);
+  for (const RunSpec& s : specs)
+    if (s.devices.size() > 1) return run_multi_device(specs, s.devices, out, err);
   DeviceCtx* ctx = nullptr;
   int dev = -1;
   lpmc_status stt = get_ctx(specs[0].device, &ctx, &dev, err);
@@ -891,6 +1040,8 @@ void lpmc_default_options(lpmc_options* o) {
   o->device = -1;
   o->stream = nullptr;
   o->exact_z = LPMC_EXACT_Z_FAST;
+  o->devices = nullptr;
+  o->n_devices = 0;
 }
 
 void lpmc_default_cost_model(lpmc_cost_model* c) {  // mlmc.hpp:20-28

@@ -150,6 +150,9 @@ int main(int argc, char** argv) {
     auto m = run_coupled_paths(gbm, 6, PrecisionSpec::carrier(), nullptr, false, 1u << 20, 1, 0, 1, o);
     CHECK(m.d_hat.mean() == 0x1.6bc234c2c6020p-16);
     CHECK(m.d_hat.variance() == 0x1.e0629aa8f5008p+3 / 1048575.0);
+    o.devices = {0, 0};  // sharded over two sub-ranges of the process's devices: same bits
+    auto m2 = run_coupled_paths(gbm, 6, PrecisionSpec::carrier(), nullptr, false, 1u << 20, 1, 0, 1, o);
+    CHECK(m2.d_hat.mean() == m.d_hat.mean() && m2.d_four.variance() == m.d_four.variance());
   }
 
   // non-finite operand -> std::domain_error (test_sde.cpp:168-173 shape)
