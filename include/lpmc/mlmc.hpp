@@ -73,12 +73,13 @@ struct DeviceOptions {
   void* stream = nullptr;
   int exact_z = LPMC_EXACT_Z_FAST;  // LPMC_EXACT_Z_GLIBC: the reference's Z bit for bit
   std::vector<int32_t> devices;      // > 1 entries: shard every run over these devices
+  int schedule = LPMC_SCHEDULE_AUTO;  // kernel schedule (results identical)
 
   lpmc_options c_abi() const {
     return lpmc_options{legs,    payoff,         strike,
                         reduce,  device,         stream,
                         exact_z, devices.empty() ? nullptr : devices.data(),
-                        static_cast<int32_t>(devices.size())};
+                        static_cast<int32_t>(devices.size()), schedule};
   }
 };
 

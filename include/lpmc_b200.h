@@ -151,6 +151,21 @@ enum {
   LPMC_EXACT_Z_GLIBC = 1
 };
 
+/*
+ * Kernel schedule of a run (results are bitwise the same either way).
+ * FUSED: one thread per path, 256-path CTAs (throughput).  WARP_PER_PATH:
+ * one warp per path, 32 steps' Gaussians drawn in parallel, then the legs
+ * stepped by the warp (latency: runs with too few paths to fill the GPU).
+ * AUTO picks WARP_PER_PATH for runs of at most 6144 paths at levels >= 5
+ * (the fused grid would leave most SMs idle); never for the IEEE half2 legs
+ * (two paths per thread).
+ */
+enum {
+  LPMC_SCHEDULE_AUTO = 0,
+  LPMC_SCHEDULE_FUSED = 1,
+  LPMC_SCHEDULE_WARP_PER_PATH = 2
+};
+
 typedef struct lpmc_options {
   uint32_t legs;  /* LPMC_LEGS_*; 0 means LPMC_LEGS_ALL */
   int32_t payoff; /* LPMC_PAYOFF_* */
@@ -169,6 +184,7 @@ typedef struct lpmc_options {
    */
   const int32_t* devices;
   int32_t n_devices;
+  int32_t schedule; /* LPMC_SCHEDULE_* */
 } lpmc_options;
 
 /* Raw MomentAccumulator state (stats.hpp:84-89). */

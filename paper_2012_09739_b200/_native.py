@@ -29,6 +29,7 @@ ALLOCATION_STANDARD, ALLOCATION_NESTED = 0, 1
 PAYOFF_TERMINAL, PAYOFF_CALL = 0, 1
 REDUCE_TREE, REDUCE_SEQUENTIAL = 0, 1
 EXACT_Z_FAST, EXACT_Z_GLIBC = 0, 1
+SCHEDULE_AUTO, SCHEDULE_FUSED, SCHEDULE_WARP_PER_PATH = 0, 1, 2
 APPROX_LINEAR, APPROX_CUBIC, APPROX_CONSTANT = 0, 1, 2
 BATCH_PATHS = 256
 CHUNK_BATCHES = 1024
@@ -87,7 +88,8 @@ class Precision(C.Structure):
 class Options(C.Structure):
     _fields_ = [("legs", C.c_uint32), ("payoff", _i32), ("strike", C.c_double),
                 ("reduce", _i32), ("device", _i32), ("stream", C.c_void_p),
-                ("exact_z", _i32), ("devices", C.POINTER(_i32)), ("n_devices", _i32)]
+                ("exact_z", _i32), ("devices", C.POINTER(_i32)), ("n_devices", _i32),
+                ("schedule", _i32)]
 
 
 class Moments(C.Structure):

@@ -58,6 +58,8 @@ _REDUCE = {"tree": N.REDUCE_TREE, "sequential": N.REDUCE_SEQUENTIAL}
 # exact Gaussians: "fast" (B200 restatement, ulp-level) or "glibc" (the
 # reference's Z bit for bit, lpmc_glibc.cuh)
 _EXACT_Z = {"fast": N.EXACT_Z_FAST, "glibc": N.EXACT_Z_GLIBC}
+_SCHEDULE = {"auto": N.SCHEDULE_AUTO, "fused": N.SCHEDULE_FUSED,
+             "warp_per_path": N.SCHEDULE_WARP_PER_PATH}
 
 
 # ----------------------------------------------------------- precision -----
@@ -378,16 +380,17 @@ class LevelStats:
 
 # ------------------------------------------------------------ sampling -----
 def _options(legs="all", payoff="terminal", strike=1.0, reduce="tree", device=None,
-             stream=None, exact_z="fast", devices=None) -> N.Options:
+             stream=None, exact_z="fast", devices=None, schedule="auto") -> N.Options:
     """Per-call options.  ``devices``: several CUDA ordinals of this process
     to shard each run over (chunk ranges, folded in chunk order: bitwise the
-    single-device result); the call is then synchronous."""
+    single-device result); the call is then synchronous.  ``schedule``:
+    "auto", "fused" or "warp_per_path" (results identical)."""
     try:
         o = N.default_options(legs=_LEGS[legs], payoff=_PAYOFF[payoff], strike=float(strike),
                               reduce=_REDUCE[reduce],
                               device=-1 if device is None else int(device),
                               stream=None if stream is None else int(stream),
-                              exact_z=_EXACT_Z[exact_z])
+                              exact_z=_EXACT_Z[exact_z], schedule=_SCHEDULE[schedule])
     except KeyError as e:
         raise InvalidArgument(f"bad option value {e}") from None
     if devices is not None and len(devices) > 0:

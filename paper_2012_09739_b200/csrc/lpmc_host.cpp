@@ -348,7 +348,22 @@ struct RunSpec {
   int device = -1;
   std::vector<int> devices;  // > 1 entries: shard over these devices (run_multi_device)
   bool ieee = false;
+  int schedule = LPMC_SCHEDULE_AUTO;
 };
+
+// Warp-per-path when asked, or (AUTO) when the fused grid of this run would
+// leave most of the GPU idle at a level long enough for latency to rule:
+// measured crossover (tools/gpu_schedule_sweep.sh) about
+// 7e3-1e4 paths at levels 8-10; below 6144 paths (24 fused CTAs on 148 SMs)
+// the warp-per-path schedule is 1.6-4.7x faster from level 10 up.
+constexpr uint64_t kWppMaxAutoPaths = 6144;
+constexpr int kWppMinAutoLevel = 5;
+bool use_wpp(const RunSpec& s) {
+  if (s.arith == BarArith::kHalf2 || s.args.level < 1) return false;
+  if (s.schedule == LPMC_SCHEDULE_WARP_PER_PATH) return true;
+  if (s.schedule == LPMC_SCHEDULE_FUSED) return false;
+  return s.args.level >= kWppMinAutoLevel && s.n_paths <= kWppMaxAutoPaths;
+}
 
 bool in_native_range(double c, double lo, double hi) {
   const double a = std::fabs(c);
@@ -380,6 +395,8 @@ lpmc_status build_spec(const lpmc_gbm* model, int32_t level, const lpmc_precisio
     return fail(err, LPMC_INVALID_ARGUMENT, "bad exact_z mode");
   if (o.n_devices < 0 || (o.n_devices > 0 && o.devices == nullptr) || o.n_devices > 1024)
     return fail(err, LPMC_INVALID_ARGUMENT, "bad device list");
+  if (o.schedule < LPMC_SCHEDULE_AUTO || o.schedule > LPMC_SCHEDULE_WARP_PER_PATH)
+    return fail(err, LPMC_INVALID_ARGUMENT, "bad schedule");
 
   RunSpec& s = *spec;
   s = RunSpec{};
@@ -387,6 +404,7 @@ lpmc_status build_spec(const lpmc_gbm* model, int32_t level, const lpmc_precisio
   s.kahan = kahan != 0;
   s.reduce = o.reduce;
   s.device = o.device;
+  s.schedule = o.schedule;
   if (o.n_devices > 1) s.devices.assign(o.devices, o.devices + o.n_devices);
   s.ieee = prec->ieee_half != 0;
   if (table != nullptr) {
@@ -612,6 +630,10 @@ cudaError_t reserve(const RunSpec& s, Buffers& B) {
     return B.path_diff.ensure(2 * std::min(b1 - b0, kSeqSliceChunks * kChunkBatches) * kBatch);
   }
   if ((e = B.chunk_acc.ensure(15 * chunks)) != cudaSuccess) return e;
+  if (use_wpp(s) &&
+      (e = B.path_diff.ensure(2 * std::min(chunks, kSliceChunks) * kChunkBatches * kBatch)) !=
+          cudaSuccess)
+    return e;
   return B.batch_acc.ensure(15 * std::min(chunks, kSliceChunks) * kChunkBatches);
 }
 
@@ -643,6 +665,7 @@ cudaError_t enqueue_run(const RunSpec& s, Buffers& B, cudaStream_t st, Enqueued*
   const uint64_t chunks = s.chunk_end - s.chunk_begin;
   if (chunks == 0) return cudaSuccess;
   const bool seq = s.reduce == LPMC_REDUCE_SEQUENTIAL;
+  const bool wpp = use_wpp(s);
   const uint64_t slice_chunks = seq ? kSeqSliceChunks : kSliceChunks;
   if (seq) {
     q->n_batches_seq = acc_count_of(s);
@@ -660,7 +683,20 @@ cudaError_t enqueue_run(const RunSpec& s, Buffers& B, cudaStream_t st, Enqueued*
     S.path_diff = seq ? B.path_diff.ptr : nullptr;
     S.path_out = nullptr;
     S.z_out = nullptr;
-    LaunchResult r = launch_paths(S, s.arith, s.kahan, false, st);
+    LaunchResult r;
+    if (wpp) {  // per-path differences, then the fused kernel's batch tree over them
+      S.batch_acc = nullptr;
+      S.path_diff = B.path_diff.ptr;
+      r = launch_paths_wpp(S, s.arith, s.kahan, st);
+      q->kernels += r.kernels;
+      if (r.cuda_error != 0) return static_cast<cudaError_t>(r.cuda_error);
+      if (!seq) {
+        const uint64_t paths_slice = std::min(b1 * kBatch, s.n_paths) - b0 * kBatch;
+        r = launch_path_batches(B.path_diff.ptr, paths_slice, B.batch_acc.ptr, st);
+      }
+    } else {
+      r = launch_paths(S, s.arith, s.kahan, false, st);
+    }
     q->kernels += r.kernels;
     if (r.cuda_error != 0) return static_cast<cudaError_t>(r.cuda_error);
     if (seq) {
@@ -1042,6 +1078,7 @@ void lpmc_default_options(lpmc_options* o) {
   o->exact_z = LPMC_EXACT_Z_FAST;
   o->devices = nullptr;
   o->n_devices = 0;
+  o->schedule = LPMC_SCHEDULE_AUTO;
 }
 
 void lpmc_default_cost_model(lpmc_cost_model* c) {  // mlmc.hpp:20-28
@@ -1589,7 +1626,11 @@ lpmc_status lpmc_simulate_paths(const lpmc_gbm* model, int32_t level, const lpmc
     A.path_diff = nullptr;
     A.path_out = d_out.ptr;
     A.z_out = zcount ? d_z.ptr : nullptr;
-    LaunchResult r = launch_paths(A, s.arith, s.kahan, true, stream);
+    // the dump of Gaussians is the fused kernel's; an explicit warp-per-path
+    // request dumps that schedule's terminal values (parity of the schedule)
+    const bool wpp = zcount == 0 && s.schedule == LPMC_SCHEDULE_WARP_PER_PATH && use_wpp(s);
+    LaunchResult r = wpp ? launch_paths_wpp(A, s.arith, s.kahan, stream)
+                         : launch_paths(A, s.arith, s.kahan, true, stream);
     t_launches += r.kernels;
     if (r.cuda_error != 0) {
       e = static_cast<cudaError_t>(r.cuda_error);

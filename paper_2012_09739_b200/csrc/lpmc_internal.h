@@ -93,6 +93,14 @@ LaunchResult launch_density(uint64_t key, uint64_t n, const double* table, int t
                             double z_max, double width, int n_bins, int exact_z,
                             unsigned long long* bins, unsigned long long* top_index,
                             void* stream);
+// The warp-per-path schedule (wpp_kernel, lpmc_level.cuh) for one launch
+// slice: per-path (d_hat, d_bar) into args.path_diff (slice-relative).
+// Not for the IEEE half2 arithmetic (two paths per thread).
+LaunchResult launch_paths_wpp(const LevelArgs& args, BarArith arith, bool kahan, void* stream);
+// The fused kernel's batch tree over per-path differences: batch b of
+// path_diff (n_paths slice paths) -> batch_acc + 15 b.
+LaunchResult launch_path_batches(const double* path_diff, uint64_t n_paths, double* batch_acc,
+                                 void* stream);
 // Upload constants and set kernel attributes on the current device.
 int configure_kernels();
 // Lane-op rates on the current device: fp64 FMA, fp32 FMA, half2 HFMA2
@@ -112,6 +120,15 @@ cudaError_t configure_level_f32r();
 cudaError_t configure_level_f64r();
 cudaError_t configure_level_half2();
 cudaError_t configure_probe();
+// warp-per-path instances (lpmc_wpp_*.cu; NP == 1 arithmetics)
+cudaError_t launch_wpp_carrier(const LevelArgs& A, bool kahan, void* stream);
+cudaError_t launch_wpp_f32(const LevelArgs& A, bool kahan, void* stream);
+cudaError_t launch_wpp_f32r(const LevelArgs& A, bool kahan, void* stream);
+cudaError_t launch_wpp_f64r(const LevelArgs& A, bool kahan, void* stream);
+cudaError_t configure_wpp_carrier();
+cudaError_t configure_wpp_f32();
+cudaError_t configure_wpp_f32r();
+cudaError_t configure_wpp_f64r();
 #endif
 // step_error_probe (lpmc_probe.cu): block_sums = 4 per 256-path block
 cudaError_t launch_step_error(const LevelArgs& A, BarArith arith, uint64_t last_steps,

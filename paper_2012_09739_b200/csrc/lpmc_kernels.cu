@@ -50,6 +50,22 @@ __global__ void __launch_bounds__(kChunkThreads)
   }
 }
 
+// The fused level kernel's batch tree (batch_moments, thread t = slot t) over
+// per-path differences written by the warp-per-path kernel: the same
+// accumulators the fused kernel would have produced.
+__global__ void __launch_bounds__(kBatch)
+    path_batch_kernel(const double* __restrict__ path_diff, uint64_t n_paths,
+                      double* __restrict__ batch_acc) {
+  const uint64_t first = static_cast<uint64_t>(blockIdx.x) * kBatch;
+  const uint64_t left = n_paths - first;
+  const int count = left < kBatch ? static_cast<int>(left) : kBatch;
+  const bool valid[1] = {static_cast<int>(threadIdx.x) < count};
+  const uint64_t i = first + threadIdx.x;
+  const double dh[1] = {valid[0] ? path_diff[2 * i] : 0.0};
+  const double db[1] = {valid[0] ? path_diff[2 * i + 1] : 0.0};
+  batch_moments<1>(dh, db, valid, count, batch_acc + 15 * blockIdx.x);
+}
+
 // Reference order: one thread per (batch, family) adds its <= 256 values in
 // path order, exactly run_batch's loop (mlmc.hpp:78-93).
 __global__ void sequential_batch_kernel(const double* __restrict__ path_diff, uint64_t n_paths,
@@ -241,7 +257,31 @@ int configure_kernels() {
   if (e == cudaSuccess) e = configure_level_f64r();
   if (e == cudaSuccess) e = configure_level_half2();
   if (e == cudaSuccess) e = configure_probe();
+  if (e == cudaSuccess) e = configure_wpp_carrier();
+  if (e == cudaSuccess) e = configure_wpp_f32();
+  if (e == cudaSuccess) e = configure_wpp_f32r();
+  if (e == cudaSuccess) e = configure_wpp_f64r();
   return static_cast<int>(e);
+}
+
+LaunchResult launch_paths_wpp(const LevelArgs& A, BarArith arith, bool kahan, void* stream) {
+  cudaError_t e = cudaErrorInvalidValue;
+  switch (arith) {
+    case BarArith::kCarrier: e = launch_wpp_carrier(A, kahan, stream); break;
+    case BarArith::kF32: e = launch_wpp_f32(A, kahan, stream); break;
+    case BarArith::kF32Round: e = launch_wpp_f32r(A, kahan, stream); break;
+    case BarArith::kF64Round: e = launch_wpp_f64r(A, kahan, stream); break;
+    case BarArith::kHalf2: break;  // two paths per thread: fused schedule only
+  }
+  return {static_cast<int>(e), 1};
+}
+
+LaunchResult launch_path_batches(const double* path_diff, uint64_t n_paths, double* batch_acc,
+                                 void* stream) {
+  const unsigned blocks = static_cast<unsigned>((n_paths + kBatch - 1) / kBatch);
+  path_batch_kernel<<<blocks, kBatch, 0, static_cast<cudaStream_t>(stream)>>>(path_diff, n_paths,
+                                                                              batch_acc);
+  return {static_cast<int>(cudaGetLastError()), 1};
 }
 
 LaunchResult launch_paths(const LevelArgs& A, BarArith arith, bool kahan, bool dump,

@@ -13,6 +13,8 @@
 // its first failing step in the reference's serial order.
 #pragma once
 
+#include <type_traits>
+
 #include "lpmc_device.cuh"
 #include "lpmc_glibc.cuh"
 
@@ -134,6 +136,57 @@ __device__ __forceinline__ void gen_draws(const LevelArgs& A, const TableView& t
   }
 }
 
+// Per-step leg updates in the reference's operation order, shared by the
+// fused level kernel (simulate) and the warp-per-path kernel (wpp_kernel).
+// State lives in the caller's locals (passed by reference: after inlining
+// the same registers as the caller's own code).
+// em_step (sde.hpp:60-68), carrier legs
+template <int NP, bool CHECKED>
+__device__ __forceinline__ void step_hat(const LevelArgs& A, double (&x)[NP], double dt,
+                                         const double (&dw_or_z)[NP], bool fine,
+                                         uint64_t (&fk)[NP], uint64_t n, uint32_t stage) {
+#pragma unroll
+  for (int p = 0; p < NP; ++p) {
+    const double xp = x[p];
+    const double drift = __dmul_rn(__dmul_rn(A.mu, xp), dt);
+    // fine: (b sqrt_dt) z (sde.hpp:65); coarse: b dW (:77)
+    const double diff = fine ? __dmul_rn(__dmul_rn(__dmul_rn(A.sigma, xp), A.sdtf), dw_or_z[p])
+                             : __dmul_rn(__dmul_rn(A.sigma, xp), dw_or_z[p]);
+    x[p] = __dadd_rn(xp, __dadd_rn(drift, diff));
+    if constexpr (CHECKED) note_fail(fk[p], nonfinite64(x[p]), n, stage);
+  }
+}
+
+// em_step / em_step_kahan and the _dw forms (sde.hpp:60-116), bar precision
+template <class Arith, bool KAHAN, bool CHECKED>
+__device__ __forceinline__ void step_bar(const Arith& ar, typename Arith::Range& range,
+                                         typename Arith::T& x, typename Arith::T& cmp,
+                                         typename Arith::T mu_l, typename Arith::T sg_l,
+                                         typename Arith::T dt_l, typename Arith::T sdt_l,
+                                         typename Arith::T zb_or_dw, bool fine,
+                                         uint64_t (&fk)[Arith::NP], uint64_t n, uint32_t stage) {
+  using T = typename Arith::T;
+  const T xp = x;
+  const T drift = ar.mul(ar.mul(mu_l, xp), dt_l);
+  const T diff = fine ? ar.mul(ar.mul(ar.mul(sg_l, xp), sdt_l), zb_or_dw)
+                      : ar.mul(ar.mul(sg_l, xp), zb_or_dw);
+  const T inc = ar.add(drift, diff);
+  if constexpr (KAHAN) {  // kahan_accumulate (sde.hpp:85-92)
+    const T y = ar.sub(inc, cmp);
+    const T s = ar.add(xp, y);
+    cmp = ar.sub(ar.sub(s, xp), y);
+    x = s;
+  } else {
+    x = ar.add(xp, inc);
+  }
+  range.track(x);
+  if constexpr (CHECKED) {
+    const uint32_t m = ar.bad(x);
+#pragma unroll
+    for (int p = 0; p < Arith::NP; ++p) note_fail(fk[p], (m >> p) & 1u, n, stage);
+  }
+}
+
 template <class Arith, bool KAHAN, int LEGS, int TAB, bool CHECKED, bool DUMP, int ZM>
 __device__ __forceinline__ void simulate(const LevelArgs& A, const TableView& tab,
                                          const double* s_math,
@@ -168,71 +221,26 @@ __device__ __forceinline__ void simulate(const LevelArgs& A, const TableView& ta
   T xbc = xbf;
   T cmpf = ar.zero(), cmpc = ar.zero();
 
-  // em_step (sde.hpp:60-68), carrier legs
   auto hat_fine = [&](const double (&z)[NP], uint64_t n) {
-#pragma unroll
-    for (int p = 0; p < NP; ++p) {
-      const double x = xhf[p];
-      const double drift = __dmul_rn(__dmul_rn(A.mu, x), A.dtf);
-      const double diff = __dmul_rn(__dmul_rn(__dmul_rn(A.sigma, x), A.sdtf), z[p]);
-      xhf[p] = __dadd_rn(x, __dadd_rn(drift, diff));
-      if constexpr (CHECKED) note_fail(fk[p], nonfinite64(xhf[p]), n, kStageHatFine);
-    }
+    step_hat<NP, CHECKED>(A, xhf, A.dtf, z, true, fk, n, kStageHatFine);
   };
-  // em_step / em_step_kahan (sde.hpp:60-68, 96-105), bar precision
   auto bar_fine = [&](T zb, uint64_t n) {
-    const T x = xbf;
-    const T drift = ar.mul(ar.mul(mu_l, x), dtf_l);
-    const T diff = ar.mul(ar.mul(ar.mul(sg_l, x), sdtf_l), zb);
-    const T inc = ar.add(drift, diff);
-    if constexpr (KAHAN) {  // kahan_accumulate (sde.hpp:85-92)
-      const T y = ar.sub(inc, cmpf);
-      const T s = ar.add(x, y);
-      cmpf = ar.sub(ar.sub(s, x), y);
-      xbf = s;
-    } else {
-      xbf = ar.add(x, inc);
-    }
-    range.track(xbf);
-    if constexpr (CHECKED) {
-      const uint32_t m = ar.bad(xbf);
-#pragma unroll
-      for (int p = 0; p < NP; ++p) note_fail(fk[p], (m >> p) & 1u, n, kStageBarFine);
-    }
+    step_bar<Arith, KAHAN, CHECKED>(ar, range, xbf, cmpf, mu_l, sg_l, dtf_l, sdtf_l, zb, true, fk,
+                                    n, kStageBarFine);
   };
-  // em_step_dw / em_step_kahan_dw (sde.hpp:72-80, 107-116)
+  // coarse legs: dW = sqrt_dt z0 + sqrt_dt z1 in each precision (sde.hpp:259-264)
   auto coarse = [&](const double (&z0)[NP], const double (&z1)[NP], T zb0, T zb1, uint64_t n) {
     if constexpr (kHat && !kFineOnly) {
+      double dw[NP];
 #pragma unroll
-      for (int p = 0; p < NP; ++p) {
-        const double dw = __dadd_rn(__dmul_rn(A.sdtf, z0[p]), __dmul_rn(A.sdtf, z1[p]));
-        const double x = xhc[p];
-        const double drift = __dmul_rn(__dmul_rn(A.mu, x), A.dtc);
-        const double diff = __dmul_rn(__dmul_rn(A.sigma, x), dw);
-        xhc[p] = __dadd_rn(x, __dadd_rn(drift, diff));
-        if constexpr (CHECKED) note_fail(fk[p], nonfinite64(xhc[p]), n, kStageHatCoarse);
-      }
+      for (int p = 0; p < NP; ++p)
+        dw[p] = __dadd_rn(__dmul_rn(A.sdtf, z0[p]), __dmul_rn(A.sdtf, z1[p]));
+      step_hat<NP, CHECKED>(A, xhc, A.dtc, dw, false, fk, n, kStageHatCoarse);
     }
     if constexpr (kBar && !kFineOnly) {
       const T dw = ar.add(ar.mul(sdtf_l, zb0), ar.mul(sdtf_l, zb1));
-      const T x = xbc;
-      const T drift = ar.mul(ar.mul(mu_l, x), dtc_l);
-      const T diff = ar.mul(ar.mul(sg_l, x), dw);
-      const T inc = ar.add(drift, diff);
-      if constexpr (KAHAN) {
-        const T y = ar.sub(inc, cmpc);
-        const T s = ar.add(x, y);
-        cmpc = ar.sub(ar.sub(s, x), y);
-        xbc = s;
-      } else {
-        xbc = ar.add(x, inc);
-      }
-      range.track(xbc);
-      if constexpr (CHECKED) {
-        const uint32_t m = ar.bad(xbc);
-#pragma unroll
-        for (int p = 0; p < NP; ++p) note_fail(fk[p], (m >> p) & 1u, n, kStageBarCoarse);
-      }
+      step_bar<Arith, KAHAN, CHECKED>(ar, range, xbc, cmpc, mu_l, sg_l, dtc_l, sdtf_l, dw, false,
+                                      fk, n, kStageBarCoarse);
     }
   };
 
@@ -423,6 +431,162 @@ __global__ void __launch_bounds__(kBatch / Arith::NP,
   if (A.batch_acc != nullptr) batch_moments<NP>(dh, db, valid, count, A.batch_acc + 15 * blockIdx.x);
 }
 
+// -------------------------------------------------- warp per path ---------
+// The schedule for runs too small to fill the GPU (few paths of many steps:
+// the deep levels of the two-way experiment, the estimator's pilot pass).
+// The fused kernel then runs one lone warp per SM sub-partition and each
+// path's 2^level steps back to back at dependency latency.  Here one warp
+// owns one path: its 32 lanes draw 32 consecutive fine steps in parallel
+// (counter-based stream: draw n of a path is mix64(mix64(key + n c3)),
+// uniform.hpp:38-41), exact and approximate Gaussians by the fused kernel's
+// own device functions (same values), then every lane steps the legs through
+// those 32 draws (warp-uniform, values broadcast by shuffles), the same
+// step functions as the fused kernel in the reference's order.  A path with
+// a u == 1 or u == 1/2 draw or a non-finite end is replayed exactly
+// (replay_checked, all lanes).  Lane 0 writes the path's (d_hat, d_bar) to
+// path_diff; the batch reduction is the fused kernel's (path_batch_kernel
+// runs batch_moments on them; or the sequential order), so the moments are
+// bitwise the fused schedule's.  NP == 1 arithmetics only.
+constexpr int kWppThreads = 256;  // 8 paths per CTA
+
+template <class Arith, bool KAHAN, int LEGS, int TAB, int ZM>
+__global__ void __launch_bounds__(kWppThreads) wpp_kernel(const __grid_constant__ LevelArgs A) {
+  static_assert(Arith::NP == 1, "warp-per-path runs one path per warp");
+  using T = typename Arith::T;
+  constexpr bool kFineOnly = LEGS == 4;
+  constexpr bool kHat = (LEGS & 1) != 0 || kFineOnly;
+  constexpr bool kBar = (LEGS & 2) != 0 || kFineOnly;
+  constexpr bool kNeedExact = kHat || TAB == kTabNone;
+
+  extern __shared__ __align__(16) double s_table[];
+  constexpr int kStaged = ZM == kZGlibc ? kMathWords : kFastMathWords;
+  __shared__ __align__(16) double s_math[kNeedExact ? kStaged : 2];
+  if constexpr (kNeedExact) stage_math(s_math, kStaged);
+  TableView tab{};
+  if constexpr (TAB != kTabNone) {
+    for (int i = threadIdx.x; i < A.table_words; i += blockDim.x) s_table[i] = A.table[i];
+    tab = TableView{s_table, A.table_stride, A.K, A.degree, A.dyadic, A.table_simple, A.tail};
+  }
+  __syncthreads();
+
+  const int lane = threadIdx.x & 31;
+  const uint64_t local1[1] = {A.batch0 * kBatch + blockIdx.x * (kWppThreads / 32) + (threadIdx.x >> 5)};
+  const uint64_t local = local1[0];
+  if (local >= A.n_paths) return;  // the whole warp
+  const bool valid[1] = {true};
+  const unsigned full = 0xffffffffu;
+
+  const Arith ar(A);
+  typename Arith::Range range;
+  uint64_t fk[1] = {kNoFail};
+  double xhf[1] = {A.x0}, xhc[1] = {A.x0};
+  const T mu_l = ar.c(A.mu_l, A.h_mu), sg_l = ar.c(A.sigma_l, A.h_sigma);
+  const T dtf_l = ar.c(A.dtf_l, A.h_dtf), sdtf_l = ar.c(A.sdtf_l, A.h_sdtf);
+  const T dtc_l = ar.c(A.dtc_l, A.h_dtc);
+  T xbf = ar.c(A.x0_l, A.h_x0);
+  T xbc = xbf;
+  T cmpf = ar.zero(), cmpc = ar.zero();
+
+  const uint64_t key = path_key(A.seed_key, A.path_base + local);
+  const uint64_t n_fine = 1ull << A.level;  // level >= 1 (the host runs level 0 fused)
+  bool special = false;
+  for (uint64_t n0 = 0; n0 < n_fine; n0 += 32) {
+    uint64_t kc = key + (n0 + static_cast<uint64_t>(lane)) * 0x94d049bb133111ebull;
+    const uint64_t b = next_draw(kc);
+    const double u[1] = {uniform_of(b)};
+    const bool live = n0 + lane < n_fine;
+    special |= __any_sync(full, live && (b == kTopDraw || b == kHalfDraw));
+    double z[1] = {0.0};
+    if constexpr (kNeedExact) {
+      if constexpr (ZM == kZGlibc) {
+        glibc::inv_cdf_multi<1>(u, z, s_math);
+      } else {
+        math::phi_inv_multi<1>(u, z, s_math);
+      }
+    }
+    T zb = ar.zero();
+    if constexpr (kBar) {
+      double zl[1];
+      if constexpr (TAB != kTabNone) {
+        zl[0] = approx_inv<false, TAB>(tab, u[0]);
+      } else {
+        zl[0] = z[0];
+      }
+      zb = ar.lift(zl);
+    }
+    const int steps = n_fine - n0 < 32 ? static_cast<int>(n_fine - n0) : 32;
+    for (int s = 0; s < steps; s += 2) {
+      const double z0[1] = {__shfl_sync(full, z[0], s)};
+      const double z1[1] = {__shfl_sync(full, z[0], s + 1)};
+      const T zb0 = __shfl_sync(full, zb, s);
+      const T zb1 = __shfl_sync(full, zb, s + 1);
+      const uint64_t n = n0 + s;
+      if constexpr (kHat) step_hat<1, false>(A, xhf, A.dtf, z0, true, fk, n, kStageHatFine);
+      if constexpr (kBar)
+        step_bar<Arith, KAHAN, false>(ar, range, xbf, cmpf, mu_l, sg_l, dtf_l, sdtf_l, zb0, true,
+                                      fk, n, kStageBarFine);
+      if constexpr (kHat) step_hat<1, false>(A, xhf, A.dtf, z1, true, fk, n + 1, kStageHatFine);
+      if constexpr (kBar)
+        step_bar<Arith, KAHAN, false>(ar, range, xbf, cmpf, mu_l, sg_l, dtf_l, sdtf_l, zb1, true,
+                                      fk, n + 1, kStageBarFine);
+      if constexpr (kHat && !kFineOnly) {  // em_step_dw (sde.hpp:72-80)
+        const double dw[1] = {__dadd_rn(__dmul_rn(A.sdtf, z0[0]), __dmul_rn(A.sdtf, z1[0]))};
+        step_hat<1, false>(A, xhc, A.dtc, dw, false, fk, n + 1, kStageHatCoarse);
+      }
+      if constexpr (kBar && !kFineOnly) {
+        const T dw = ar.add(ar.mul(sdtf_l, zb0), ar.mul(sdtf_l, zb1));
+        step_bar<Arith, KAHAN, false>(ar, range, xbc, cmpc, mu_l, sg_l, dtc_l, sdtf_l, dw, false,
+                                      fk, n + 1, kStageBarCoarse);
+      }
+    }
+  }
+
+  PathEnd<1> R;
+  R.hf[0] = kHat ? xhf[0] : 0.0;
+  R.hc[0] = (kHat && !kFineOnly) ? xhc[0] : 0.0;
+  R.bf[0] = kBar ? ar.get(xbf, 0) : 0.0;
+  R.bc[0] = (kBar && !kFineOnly) ? ar.get(xbc, 0) : 0.0;
+  R.fk[0] = kNoFail;
+  const bool hat_bad = kHat && (nonfinite64(R.hf[0]) || nonfinite64(R.hc[0]));
+  const bool bar_bad = kBar && (ar.bad(xbf) != 0u || (!kFineOnly && ar.bad(xbc) != 0u));
+  R.range_bad = range.bad();
+  if (special || hat_bad || bar_bad) {  // rare: exact values and first failure (all lanes)
+    const bool range_bad = R.range_bad;
+    replay_checked<Arith, KAHAN, LEGS, TAB, ZM>(A, tab, s_math, local1, valid, R);
+    R.range_bad |= range_bad;
+    if (lane == 0 && R.fk[0] != kNoFail) {
+      const uint64_t n = R.fk[0] >> 3;
+      const uint32_t stage = static_cast<uint32_t>(R.fk[0] & 7u);
+      const uint32_t kind = stage == kStageDraw ? kKindU1 : kKindNonFinite;
+      const uint64_t step = n < (1ull << 22) ? n : (1ull << 22) - 1;
+      atomicMin(A.err_key, static_cast<unsigned long long>(
+                               (local << 24) | (static_cast<uint64_t>(kind) << 22) | step));
+    }
+  }
+  if (lane != 0) return;
+  if (R.range_bad) atomicOr(A.range_flag, 1u);
+  if (A.path_out != nullptr) {
+    double* o = A.path_out + 4 * local;
+    o[0] = R.hf[0];
+    o[1] = R.hc[0];
+    o[2] = R.bf[0];
+    o[3] = R.bc[0];
+  }
+  // terminal values -> payoff -> per-path differences (mlmc.hpp:86-90)
+  double pf_h = R.hf[0], pc_h = R.hc[0], pf_b = R.bf[0], pc_b = R.bc[0];
+  if (A.payoff == 1) {
+    pf_h = fmax(__dsub_rn(R.hf[0], A.strike), 0.0);
+    pf_b = fmax(__dsub_rn(R.bf[0], A.strike), 0.0);
+    pc_h = !kFineOnly ? fmax(__dsub_rn(R.hc[0], A.strike), 0.0) : 0.0;
+    pc_b = !kFineOnly ? fmax(__dsub_rn(R.bc[0], A.strike), 0.0) : 0.0;
+  }
+  if (A.path_diff != nullptr) {
+    const uint64_t r = local - A.batch0 * kBatch;  // slice-relative
+    A.path_diff[2 * r + 0] = kHat ? __dsub_rn(pf_h, pc_h) : 0.0;
+    A.path_diff[2 * r + 1] = kBar ? __dsub_rn(pf_b, pc_b) : 0.0;
+  }
+}
+
 // ------------------------------------------------------- per-arith glue ----
 constexpr int kMaxTableK = 1024;
 constexpr int kMaxDynSmem = (kTableRows * kMaxTableK + 1) * 8;  // + 1 / step_w
@@ -510,6 +674,84 @@ cudaError_t configure_level() {
   acc(configure_one<Arith, true, 2, true>());
   acc(configure_one<Arith, false, 3, true>());
   acc(configure_one<Arith, true, 3, true>());
+  return e;
+}
+
+// Warp-per-path dispatch (same table-kind / exact-mode selection).
+template <class Arith, bool KAHAN, int LEGS, int TAB, int ZM>
+cudaError_t launch_wpp_one(const LevelArgs& A, cudaStream_t s) {
+  const size_t smem = TAB != kTabNone ? static_cast<size_t>(A.table_words) * sizeof(double) : 0;
+  const uint64_t paths = (A.batch0 + A.n_batches) * kBatch < A.n_paths
+                             ? A.n_batches * kBatch
+                             : A.n_paths - A.batch0 * kBatch;
+  const unsigned blocks = static_cast<unsigned>((paths + kWppThreads / 32 - 1) / (kWppThreads / 32));
+  wpp_kernel<Arith, KAHAN, LEGS, TAB, ZM><<<blocks, kWppThreads, smem, s>>>(A);
+  return cudaGetLastError();
+}
+
+template <class Arith, bool KAHAN, int LEGS>
+cudaError_t pick_approx_wpp(const LevelArgs& A, cudaStream_t s) {
+  const bool glibc = A.exact_z == kZGlibc;
+  if (A.table == nullptr)
+    return glibc ? launch_wpp_one<Arith, KAHAN, LEGS, kTabNone, kZGlibc>(A, s)
+                 : launch_wpp_one<Arith, KAHAN, LEGS, kTabNone, kZFast>(A, s);
+  if constexpr (LEGS != 2) {
+    if (glibc) {
+      if (A.dyadic && A.table_simple && A.degree == 1)
+        return launch_wpp_one<Arith, KAHAN, LEGS, kTabDyadicLinear, kZGlibc>(A, s);
+      return launch_wpp_one<Arith, KAHAN, LEGS, kTabGeneric, kZGlibc>(A, s);
+    }
+  }
+  if (A.dyadic && A.table_simple && A.degree == 1)
+    return launch_wpp_one<Arith, KAHAN, LEGS, kTabDyadicLinear, kZFast>(A, s);
+  return launch_wpp_one<Arith, KAHAN, LEGS, kTabGeneric, kZFast>(A, s);
+}
+
+template <class Arith>
+cudaError_t launch_level_wpp(const LevelArgs& A, bool kahan, cudaStream_t s) {
+  auto legs = [&](auto k) -> cudaError_t {
+    constexpr bool K = decltype(k)::value;
+    if constexpr (std::is_same_v<Arith, ArithCarrier>) {  // hat-only runs use the carrier
+      if (A.legs == 1) return pick_approx_wpp<Arith, K, 1>(A, s);
+    }
+    if (A.legs == 2) return pick_approx_wpp<Arith, K, 2>(A, s);
+    if (A.legs == 4) return pick_approx_wpp<Arith, K, 4>(A, s);
+    return pick_approx_wpp<Arith, K, 3>(A, s);
+  };
+  return kahan ? legs(std::true_type{}) : legs(std::false_type{});
+}
+
+template <class Arith, bool KAHAN, int LEGS, int ZM>
+cudaError_t configure_wpp_tabs() {
+  cudaError_t e = cudaFuncSetAttribute(wpp_kernel<Arith, KAHAN, LEGS, kTabGeneric, ZM>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem);
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(wpp_kernel<Arith, KAHAN, LEGS, kTabDyadicLinear, ZM>,
+                              cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem);
+}
+
+template <class Arith>
+cudaError_t configure_wpp() {
+  cudaError_t e = cudaSuccess;
+  auto acc = [&](cudaError_t x) {
+    if (e == cudaSuccess) e = x;
+  };
+  if constexpr (std::is_same_v<Arith, ArithCarrier>) {
+    acc(configure_wpp_tabs<Arith, false, 1, kZFast>());
+    acc(configure_wpp_tabs<Arith, true, 1, kZFast>());
+    acc(configure_wpp_tabs<Arith, false, 1, kZGlibc>());
+    acc(configure_wpp_tabs<Arith, true, 1, kZGlibc>());
+  }
+  acc(configure_wpp_tabs<Arith, false, 2, kZFast>());
+  acc(configure_wpp_tabs<Arith, true, 2, kZFast>());
+  acc(configure_wpp_tabs<Arith, false, 3, kZFast>());
+  acc(configure_wpp_tabs<Arith, true, 3, kZFast>());
+  acc(configure_wpp_tabs<Arith, false, 4, kZFast>());
+  acc(configure_wpp_tabs<Arith, true, 4, kZFast>());
+  acc(configure_wpp_tabs<Arith, false, 3, kZGlibc>());
+  acc(configure_wpp_tabs<Arith, true, 3, kZGlibc>());
+  acc(configure_wpp_tabs<Arith, false, 4, kZGlibc>());
+  acc(configure_wpp_tabs<Arith, true, 4, kZGlibc>());
   return e;
 }
 

@@ -24,13 +24,15 @@ def main():
     ap.add_argument("--n", type=int, default=1 << 22)
     ap.add_argument("--launches", type=int, default=2)
     ap.add_argument("--exact-z", default="fast", choices=["fast", "glibc"])
+    ap.add_argument("--schedule", default="auto", choices=["auto", "fused", "warp_per_path"])
     ap.add_argument("--time", action="store_true",
                     help="also time 5 launches with CUDA events (best of, ms)")
     a = ap.parse_args()
     spec = L.PrecisionSpec.parse(a.prec)
     approx = None if a.approx == "exact" else L.InvCdfApprox.parse(a.approx)
     plan = L.LevelPlan(L.make_gbm(), a.level, spec, approx, bool(a.kahan), a.n, 1,
-                       (a.level << 40) | (a.kahan << 36), legs=a.legs, exact_z=a.exact_z)
+                       (a.level << 40) | (a.kahan << 36), legs=a.legs, exact_z=a.exact_z,
+                       schedule=a.schedule)
     for _ in range(a.launches):
         plan.launch()
         m = plan.collect()
