@@ -346,28 +346,47 @@ def main():
     dom = [(10, False), (10, True)]
     dom_ms = statistics.mean(statistics.mean(per_cfg_ms[c]) for c in dom)
     dom_steps = fine_steps(10, (c1 - c0) * (1 << 18))
-    ops_per_step = None
-    traffic = None
+    prof = {}
     if os.path.exists(PROFILE_CONST):
         with open(PROFILE_CONST) as f:
             prof = json.load(f)
-        ops_per_step = prof.get("fp64_lane_ops_per_path_step")
-        traffic = prof.get("dram_bytes_per_launch")
-    if ops_per_step:
-        achieved = ops_per_step * dom_steps / (dom_ms * 1e-3)
-        roof = {"bound": "fp64", "achieved": achieved / 1e12, "peak": peaks["fp64_ops_per_s"] / 1e12,
-                "unit": "Tops/s (fp64 lane-ops)", "frac": achieved / peaks["fp64_ops_per_s"],
-                "traffic": traffic, "co_limits": prof.get("co_limits"),
-                "note": "non-tensor FP64-pipe bound (neither HBM nor tensor): per-path state in "
-                        "registers, 0 bytes per path-step; ops/step from ncu "
-                        "(profiles/fp64_ops_per_path_step.json), peak = measured FMA lane rate; "
-                        "traffic = DRAM bytes per level-10 launch (ncu --set full), against "
-                        "4.3e9 path-steps; co_limits = the same launch's issue, FP64-pipe and "
-                        "shared-memory-crossbar utilisation (DESIGN.md section 8)"}
+    achieved = dom_steps / (dom_ms * 1e-3)  # level-10 path-steps/s, CUDA events
+    sm_hz = (clk.get("sm_mhz") or 1965.0) * 1e6
+    n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
+    # multi-pipe roofline = min over pipes of
+    # peak_p / demand_p per path-step (demands: ncu counts of this kernel)
+    pipes = {}
+    if prof.get("fp64_lane_ops_per_path_step"):
+        pipes["fp64"] = {"demand_per_path_step": prof["fp64_lane_ops_per_path_step"],
+                         "peak_per_s": peaks["fp64_ops_per_s"], "unit": "FP64 lane-ops"}
+    if prof.get("warp_inst_per_path_step"):
+        pipes["issue"] = {"demand_per_path_step": prof["warp_inst_per_path_step"],
+                          "peak_per_s": 4.0 * n_sm * sm_hz, "unit": "warp-instructions"}
+    if prof.get("smem_wavefronts_per_path_step"):
+        pipes["smem"] = {"demand_per_path_step": prof["smem_wavefronts_per_path_step"],
+                         "peak_per_s": 1.0 * n_sm * sm_hz, "unit": "shared-memory wavefronts"}
+    for p in pipes.values():
+        p["ceiling_path_steps_per_s"] = p["peak_per_s"] / p["demand_per_path_step"]
+        p["frac"] = achieved / p["ceiling_path_steps_per_s"]
+    if pipes:
+        bind = min(pipes, key=lambda k: pipes[k]["ceiling_path_steps_per_s"])
+        peak = pipes[bind]["ceiling_path_steps_per_s"]
+        roof = {"bound": f"multi-pipe non-tensor (binding: {bind})", "achieved": achieved,
+                "peak": peak, "unit": "path-steps/s", "frac": achieved / peak,
+                "traffic": prof.get("dram_bytes_per_launch"), "pipes": pipes,
+                "fp64_frac": pipes.get("fp64", {}).get("frac"),
+                "co_limits": prof.get("co_limits"),
+                "note": "neither HBM- nor tensor-bound: per-path state in registers, 0 bytes per "
+                        "path-step (traffic = DRAM bytes of one level-10 launch of 4.3e9 "
+                        "path-steps, ncu). achieved = level-10 path-steps/s (CUDA events); peak = "
+                        "min over pipes of pipe peak / per-path-step demand (ncu counts, "
+                        "profiles/fp64_ops_per_path_step.json; FP64 peak measured live, issue 4 "
+                        "and shared-memory 1 per clock per SM at the sampled clock); fp64_frac = "
+                        "the literal fraction of the FP64 peak (DESIGN.md section 8)"}
     else:
-        roof = {"bound": "fp64", "achieved": None, "peak": peaks["fp64_ops_per_s"] / 1e12,
-                "unit": "Tops/s (fp64 lane-ops)", "frac": None, "traffic": None,
-                "note": "ops per path-step not yet profiled"}
+        roof = {"bound": "multi-pipe non-tensor", "achieved": achieved, "peak": None,
+                "unit": "path-steps/s", "frac": None, "traffic": None,
+                "note": "per-path-step demands not yet profiled"}
 
     cpu = None if args.no_cpu_baseline else cpu_baseline_sample()
     per_level = {}

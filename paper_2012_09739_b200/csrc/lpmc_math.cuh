@@ -9,17 +9,23 @@
 // shared-memory load, and the hot path has one branch (Acklam's tail).
 //
 // Accuracy design:
-//  * Newton squares the initial error, so x0 (Acklam) only needs ~1e-12:
-//    its division/log/sqrt use MUFU seeds + Newton refinement.
-//  * The correction (Phi(x0) - u) / pdf needs Phi(x0) to ~1 ulp of u, and
-//    1/pdf to ~1e-10 only.  Phi(x0) = erfc(t)/2, t = -x0/sqrt(2), with
-//    erfc(t) = 2^k p(r) G(t): t^2 split exactly by FMA, exp(-t^2) = 2^k p(r)
-//    from a 64-entry 2^(j/64) hi/lo table and a degree-4 expm1 polynomial,
-//    and G = erfcx by 104 degree-8 piecewise polynomials on intervals of
-//    1/16 with the constant term as hi + lo (tools/fit_math.py).  1/pdf is
-//    sqrt(2 pi) 2^-k / p(r): the same exponential, no second exp, no division.
+//  * The reference refines Acklam's x0 (1.15e-9) by one Newton step.  Here
+//    x0 comes from an fp32 polynomial in log2(v (1 - v)) (~4e-7 relative,
+//    tools/fit_x0f.py) and one Halley step x0 - r (1 - x0 r / 2),
+//    r = (Phi(x0) - v) / pdf(x0), whose error K e0^3 stays below 1% of an ulp
+//    of Z: the same root, to the same last-ulp noise of the erfc evaluation.
+//  * r needs Phi(x0) to ~1 ulp of v, and 1/pdf to ~1e-12 only.  Phi(x0) =
+//    erfc(t)/2, t = -x0/sqrt(2), with erfc(t) = 2^k p(r) G(t): t^2 split
+//    exactly by FMA, exp(-t^2) = 2^k p(r) from a 64-entry 2^(j/64) hi/lo
+//    table and a degree-4 expm1 polynomial, and G = erfcx by 104 degree-8
+//    piecewise polynomials on intervals of 1/16 with the constant term as
+//    hi + lo (tools/fit_math.py).  1/pdf is sqrt(2 pi) 2^-k / p(r): the same
+//    exponential, no second exp, no division.  Table indices come from the
+//    low words of shifted FMAs (no F2I/I2F conversions).
 //  * t > 6.5 (u < 1e-20; never drawn by the sampler, whose u >= 2^-54) takes
 //    a libdevice slow path.
+//  * -DLPMC_X0_ACKLAM restores Acklam's binary64 x0 + Newton (A/B only,
+//    tools/gpu_ab_x0.sh).
 //
 // All functions are __host__ __device__ so tests/cpp/math_accuracy.cpp can
 // check the erfc core on the CPU against mpmath; the core uses only IEEE
@@ -32,6 +38,7 @@
 
 #include "lpmc_glibc_coef.h"
 #include "lpmc_math_coef.h"
+#include "lpmc_x0f_coef.h"
 
 #ifdef __CUDACC__
 #define LPMC_HD __host__ __device__ __forceinline__
@@ -143,9 +150,9 @@ static const double kMathHost[kMathCount] = {
     3.754408661907416e+00,
     2.0, 2.0 / 3.0, 2.0 / 5.0, 2.0 / 7.0, 2.0 / 9.0, 2.0 / 11.0, 2.0 / 13.0,
     LPMC_EXPM1_COEF_LIST,
-    92.332482616893657,                       // 64 log2(e)
-    6.93147180369123816490e-01 / 64.0,        // exact scaling of the 32-bit ln2 head
-    1.90821492927058770002e-10 / 64.0,
+    92.332482616893657 / 64.0 * LPMC_EXP_N,   // N log2(e) (power-of-two scalings: exact)
+    6.93147180369123816490e-01 / LPMC_EXP_N,  // exact scaling of the 32-bit ln2 head
+    1.90821492927058770002e-10 / LPMC_EXP_N,
     6.93147180559945309417e-01, 0.7071067811865475244, 2.5066282746310002, 0.02425, 0.0};
 
 constexpr int kErfcxRow = LPMC_ERFCX_ROW;
@@ -153,6 +160,8 @@ constexpr int kErfcxN = LPMC_ERFCX_INTERVALS;
 constexpr int kErfcxWords = kErfcxRow * kErfcxN;
 constexpr int kExpN = LPMC_EXP_N;
 constexpr int kExpWords = 2 * kExpN;
+constexpr int kExpShift = kExpN == 64 ? 6 : kExpN == 32 ? 5 : kExpN == 16 ? 4 : 3;
+static_assert(1 << kExpShift == kExpN, "exp table size must be 8, 16, 32 or 64");
 constexpr int kGlibcOff = kErfcxWords + kExpWords;  // glibc exp and log tables (lpmc_glibc.cuh)
 constexpr int kGlibcWords = 512;
 constexpr int kMathTableWords = kGlibcOff + kGlibcWords;  // one shared-memory block
@@ -203,8 +212,9 @@ struct ExpSplit {
 
 LPMC_HD ExpSplit exp_neg(double th, double tl, const double* tab) {
   const double kShift = 6755399441055744.0;  // 1.5 * 2^52 (an encodable immediate)
-  const double kd = fmad(-th, LPMC_K(kLog2eN), kShift) - kShift;
-  const int kf = static_cast<int>(kd);
+  const double ks = fmad(-th, LPMC_K(kLog2eN), kShift);
+  const double kd = ks - kShift;
+  const int kf = static_cast<int>(static_cast<uint32_t>(bits(ks)));  // = (int)kd, no F2I
   double r = fmad(kd, -LPMC_K(kLn2HiN), -th);  // exact
   r = fmad(kd, -LPMC_K(kLn2LoN), r);
   r = r - tl;
@@ -216,7 +226,7 @@ LPMC_HD ExpSplit exp_neg(double th, double tl, const double* tab) {
   q = q * r;  // expm1(r)
   const D2 t2 = load2(tab + kErfcxWords + 2 * (kf & (kExpN - 1)));
   const double p = t2.a + fmad(t2.a, q, t2.b);
-  return ExpSplit{p, kf >> 6};
+  return ExpSplit{p, kf >> kExpShift};
 }
 
 // erfcx(t) for t in [0, 6.5): interval record j (width 1/LPMC_ERFCX_PER_UNIT),
@@ -224,9 +234,19 @@ LPMC_HD ExpSplit exp_neg(double th, double tl, const double* tab) {
 LPMC_HD double erfcx_piecewise(double t, const double* tab) {
   constexpr int D = LPMC_ERFCX_DEG;
   constexpr double kPerUnit = LPMC_ERFCX_PER_UNIT;
+#ifdef __CUDA_ARCH__
+  // j = floor(t kPerUnit) from the low word of a round-down FMA onto 2^52
+  // (no F2I/I2F conversions); s = t - (j + 1/2) / kPerUnit, both steps exact.
+  const double js = __fma_rd(t, kPerUnit, 4503599627370496.0);
+  const double jd = js - 4503599627370496.0;
+  const uint32_t ju = static_cast<uint32_t>(bits(js));
+  const int j = static_cast<int>(ju < kErfcxN - 1 ? ju : kErfcxN - 1);
+  const double s = fmad(jd, -1.0 / kPerUnit, t) - 0.5 / kPerUnit;
+#else
   int j = static_cast<int>(t * kPerUnit);
   j = j < kErfcxN - 1 ? j : kErfcxN - 1;
   const double s = t - (j + 0.5) * (1.0 / kPerUnit);  // exact: j < 2^10, power-of-two width
+#endif
   const double* rec = tab + kErfcxRow * j;  // c_D, ..., c_1, c0 hi, c0 lo
   D2 c = load2(rec);
   double q = fmad(c.a, s, c.b);  // c_D s + c_{D-1}
@@ -367,7 +387,16 @@ __device__ __forceinline__ double newton_fast(double x0, double v, const double*
   // v 2^-k: an exponent add (v is normal: v >= 2^-54, |k| <= 62).
   const double v_k = from_bits(bits(v) - (static_cast<uint64_t>(static_cast<int64_t>(e.k)) << 52));
   const double resid_k = fmad(pg, 0.5, -v_k);
+#ifdef LPMC_X0_ACKLAM
   return x0 - resid_k * (LPMC_K(kSqrt2Pi) * rcp_coarse(e.p));
+#else
+  // Halley: x0 - r (1 - x0 r / 2), r = resid / pdf.  From the fp32 initial
+  // guess (|e0| <= 4.3e-7 |x|) the error K e0^3, K = (x^2 + 2)/12, stays
+  // below 1% of an ulp of Z for |x| <= 5 (Newton alone would leave e0^2 x/2).
+  const double r = resid_k * (LPMC_K(kSqrt2Pi) * rcp_coarse(e.p));
+  const double c = fmad(-0.5 * x0, r, 1.0);
+  return fmad(-r, c, x0);
+#endif
 }
 
 // exact_inv_cdf (gaussian.hpp:59-65) for D independent draws of one thread.
@@ -377,6 +406,57 @@ __device__ __forceinline__ double newton_fast(double x0, double v, const double*
 // one lane active.  Must be called by every active lane of the warp.
 // Stage 1: Acklam x0 of the reflected v = min(u, 1 - u) (gaussian.hpp:63)
 // (central for all, tail pass for the rest).
+#ifndef LPMC_X0_ACKLAM
+// Initial guess in fp32 (tools/fit_x0f.py): x0 = q G(y), q = v - 1/2 exact in
+// binary64, y = log2(v (1 - v)) from one MUFU.LG2, G a degree-8 polynomial
+// with float immediates (v >= 2^-10), or degree 12 in sqrt(-y) in the tail
+// (0.2 % of draws: a warp-uniform pass per draw slot).  ~4e-7 relative, which
+// the Halley step in newton_fast squares and cubes away.  Replaces Acklam's
+// binary64 rational (19 FP64 operations + a reciprocal, and a log/sqrt tail
+// pass for 4.85 % of draws) by 2 FP64 operations and ~12 fp32/MUFU ones.
+__device__ __forceinline__ float x0f_central(float x) {
+  constexpr float c[LPMC_X0F_DEG_C + 1] = {LPMC_X0F_COEF_C};  // immediates after unrolling
+  float p = c[LPMC_X0F_DEG_C];
+#pragma unroll
+  for (int i = LPMC_X0F_DEG_C - 1; i >= 0; --i) p = __fmaf_rn(p, x, c[i]);
+  return p;
+}
+
+__device__ __forceinline__ float x0f_tail(float x) {
+  constexpr float c[LPMC_X0F_DEG_T + 1] = {LPMC_X0F_COEF_T};
+  float p = c[LPMC_X0F_DEG_T];
+#pragma unroll
+  for (int i = LPMC_X0F_DEG_T - 1; i >= 0; --i) p = __fmaf_rn(p, x, c[i]);
+  return p;
+}
+
+template <int D>
+__device__ __forceinline__ void phi_inv_stage1(const double (&v)[D], double (&x0)[D]) {
+  float y[D], g[D];
+  uint32_t pend = 0;
+#pragma unroll
+  for (int d = 0; d < D; ++d) {
+    const float vf = __double2float_rn(v[d]);
+    y[d] = __log2f(__fmaf_rn(-vf, vf, vf));  // log2(v (1 - v))
+    g[d] = x0f_central(__fsub_rn(y[d], LPMC_X0F_Y_MID));
+    if (vf < LPMC_X0F_SPLIT) pend |= 1u << d;
+  }
+  const unsigned mask = __activemask();
+  if (__any_sync(mask, pend != 0)) {
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+      if (__any_sync(mask, (pend >> d) & 1u)) {
+        const float ny = -y[d];
+        const float s = __fmul_rn(ny, rsqrtf(ny));
+        const float gt = x0f_tail(__fsub_rn(s, LPMC_X0F_S_MID));
+        if ((pend >> d) & 1u) g[d] = gt;
+      }
+    }
+  }
+#pragma unroll
+  for (int d = 0; d < D; ++d) x0[d] = (v[d] - 0.5) * static_cast<double>(g[d]);
+}
+#else
 template <int D>
 __device__ __forceinline__ void phi_inv_stage1(const double (&v)[D], double (&x0)[D]) {
   uint32_t pend = 0;
@@ -399,6 +479,7 @@ __device__ __forceinline__ void phi_inv_stage1(const double (&v)[D], double (&x0
     pend &= pend - 1u;
   }
 }
+#endif
 
 // Out of line: keeps the never-taken libdevice path out of the hot loop's
 // instruction footprint (one copy per kernel instead of one per draw).

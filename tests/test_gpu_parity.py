@@ -81,7 +81,11 @@ def test_exact_z_agreement_report(gpu, ref):
     print(f"\nZ == glibc: product path {f_eq:.4f} (max {f_ulp.max()} ulp), "
           f"libdevice formula {l_eq:.4f}")
     assert np.all(np.abs(fast - zr) <= z_tolerance(u, zr))
-    assert f_eq > 0.45  # regression guard; libdevice formula ~0.59, glibc itself is not CR
+    # regression guard (measured 0.386): the fp32 initial guess + Halley step
+    # lands on the root independently of Acklam's x0, so only the erfc rounding
+    # noise of two ~1-ulp libms is shared (Acklam's x0 gave 0.496, the
+    # libdevice formula on Acklam's x0 0.59; glibc itself is not CR)
+    assert f_eq > 0.35
 
 
 @pytest.mark.parametrize("name", ["linear:2", "linear:8", "linear:16", "linear:32", "cubic:16",
