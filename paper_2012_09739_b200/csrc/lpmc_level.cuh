@@ -70,7 +70,7 @@ __device__ __forceinline__ void draw_uniforms(uint64_t (&kc)[NP], Uniforms<H * N
 enum : int { kZFast = 0, kZGlibc = 1 };
 
 template <class Arith, int TAB, bool NEED_EXACT, bool BAR, bool CHECKED, bool DUMP, int H,
-          bool PREFETCH, int ZM>
+          bool PREFETCH, int ZM, class Mid = math::NoMid>
 __device__ __forceinline__ void gen_draws(const LevelArgs& A, const TableView& tab,
                                           const double* s_math, const Arith& ar,
                                           uint64_t (&kc)[Arith::NP], bool (&u1)[Arith::NP],
@@ -80,7 +80,7 @@ __device__ __forceinline__ void gen_draws(const LevelArgs& A, const TableView& t
                                           const Uniforms<H * Arith::NP>& cur,
                                           Uniforms<H * Arith::NP>& next,
                                           double (&z)[H][Arith::NP],
-                                          typename Arith::T (&zb)[H]) {
+                                          typename Arith::T (&zb)[H], Mid&& mid = Mid{}) {
   constexpr int NP = Arith::NP;
   constexpr int D = H * NP;
   const double(&u)[D] = cur.u;
@@ -99,6 +99,7 @@ __device__ __forceinline__ void gen_draws(const LevelArgs& A, const TableView& t
   if constexpr (NEED_EXACT && ZM == kZGlibc) {
     if constexpr (PREFETCH) draw_uniforms<NP, H>(kc, next);
     glibc::inv_cdf_multi<D>(u, zz, s_math);
+    mid();
   } else if constexpr (NEED_EXACT) {
     double v[D], x0[D];
     uint32_t neg = 0;
@@ -110,9 +111,10 @@ __device__ __forceinline__ void gen_draws(const LevelArgs& A, const TableView& t
     }
     math::phi_inv_stage1<D>(v, x0);
     if constexpr (PREFETCH) draw_uniforms<NP, H>(kc, next);
-    math::phi_inv_stage2<D, CHECKED>(v, x0, neg, cur.half, zz, s_math);
+    math::phi_inv_stage2<D, CHECKED>(v, x0, neg, cur.half, zz, s_math, mid);
   } else {
     if constexpr (PREFETCH) draw_uniforms<NP, H>(kc, next);
+    mid();
 #pragma unroll
     for (int d = 0; d < D; ++d) zz[d] = 0.0;
   }
@@ -244,13 +246,25 @@ __device__ __forceinline__ void simulate(const LevelArgs& A, const TableView& ta
     }
   };
 
-  // The draws of G coarse steps are generated together (more independent
-  // chains to hide FP64 latency, one Acklam tail pass per batch); the legs
-  // then consume them in the reference's order (sde.hpp:251-277).
-#ifndef LPMC_COARSE_PER_BATCH
-#define LPMC_COARSE_PER_BATCH 2
+  // The draws of G coarse steps are generated together (independent chains
+  // to hide FP64 latency, one tail pass per batch); the legs consume them in
+  // the reference's order (sde.hpp:251-277), one batch later, inside the
+  // next batch's Newton block (software pipeline below).  G = 1 with the
+  // pipeline at 3 CTAs x 256 threads (85 registers) measured fastest
+  // (32.1 -> 28.9 ms at level 10 against G = 2, no
+  // pipeline, 4 CTAs).
+  // Bar-only and glibc-mode instances keep two coarse steps per batch and no
+  // pipeline (their measured optimum).
+#ifdef LPMC_NO_PIPE_LEGS
+  constexpr bool kPipe = false;
+#else
+  constexpr bool kPipe = kNeedExact && ZM == kZFast;
 #endif
-  constexpr int G = NP == 1 ? LPMC_COARSE_PER_BATCH : 1;  // coarse steps per batch
+#ifdef LPMC_COARSE_PER_BATCH
+  constexpr int G = NP == 1 ? LPMC_COARSE_PER_BATCH : 1;
+#else
+  constexpr int G = NP == 1 ? (kPipe ? 1 : 2) : 1;  // coarse steps per batch
+#endif
   if (A.level == 0) {  // sde.hpp:237-249: one draw, fine legs only, coarse := 0
     double z[1][NP];
     T zb[1];
@@ -267,6 +281,46 @@ __device__ __forceinline__ void simulate(const LevelArgs& A, const TableView& ta
       // bits never recorded): the price of a branch-free pipeline
       Uniforms<2 * G * NP> cur;
       draw_uniforms<NP, 2 * G>(kc, cur);
+      if constexpr (kPipe) {
+      // software pipeline: the legs of batch i run inside the Newton block of
+      // batch i + 1 (one basic block: FP64/shared-load and FP32/integer work
+      // interleave); values and failure ordinals are unchanged.
+      double zp[2 * G][NP];
+      T zbp[2 * G];
+      {
+        Uniforms<2 * G * NP> next;
+        gen_draws<Arith, TAB, kNeedExact, kBar, CHECKED, DUMP, 2 * G, true, ZM>(
+            A, tab, s_math, ar, kc, u1, fk, local, valid, 0, cur, next, zp, zbp);
+        cur = next;
+      }
+      auto legs = [&](const double (&zl)[2 * G][NP], const T (&zbl)[2 * G], uint64_t m0) {
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+          const uint64_t n = 2 * (m0 + g);
+          if constexpr (kHat) hat_fine(zl[2 * g], n);
+          if constexpr (kBar) bar_fine(zbl[2 * g], n);
+          if constexpr (kHat) hat_fine(zl[2 * g + 1], n + 1);
+          if constexpr (kBar) bar_fine(zbl[2 * g + 1], n + 1);
+          coarse(zl[2 * g], zl[2 * g + 1], zbl[2 * g], zbl[2 * g + 1], n + 1);
+        }
+      };
+      for (uint64_t m = G; m < halves; m += G) {
+        double z[2 * G][NP];
+        T zb[2 * G];
+        Uniforms<2 * G * NP> next;
+        gen_draws<Arith, TAB, kNeedExact, kBar, CHECKED, DUMP, 2 * G, true, ZM>(
+            A, tab, s_math, ar, kc, u1, fk, local, valid, 2 * m, cur, next, z, zb,
+            [&]() { legs(zp, zbp, m - G); });
+        cur = next;
+#pragma unroll
+        for (int i = 0; i < 2 * G; ++i) {
+          zbp[i] = zb[i];
+#pragma unroll
+          for (int p = 0; p < NP; ++p) zp[i][p] = z[i][p];
+        }
+      }
+      legs(zp, zbp, halves - G);
+      } else {
       for (uint64_t m = 0; m < halves; m += G) {
         double z[2 * G][NP];
         T zb[2 * G];
@@ -283,6 +337,7 @@ __device__ __forceinline__ void simulate(const LevelArgs& A, const TableView& ta
           if constexpr (kBar) bar_fine(zb[2 * g + 1], n + 1);
           coarse(z[2 * g], z[2 * g + 1], zb[2 * g], zb[2 * g + 1], n + 1);
         }
+      }
       }
     } else {  // fewer coarse steps than one batch: one coarse step at a time
       for (uint64_t m = 0; m < halves; ++m) {
@@ -329,18 +384,27 @@ __device__ __noinline__ void replay_checked(const LevelArgs& A, TableView tab,
   simulate<Arith, KAHAN, LEGS, TAB, true, false, ZM>(A, tab, s_math, local, valid, R);
 }
 
-// 256 threads x 4 CTAs per SM (64 registers) for one path per thread; the
-// half2 instances (two paths, four draws per coarse step) get 128 threads x
-// 4 CTAs (128 registers) so they do not spill.
+// 256 threads x 3 CTAs per SM (85 registers) for one path per thread when
+// the instance computes exact Gaussians in the fast mode (pipelined legs),
+// x 4 CTAs (64 registers) for bar-only and glibc-mode instances; the half2
+// instances (two paths, four draws per coarse step) get 128 threads (170 /
+// 128 registers) so they do not spill.
 #ifndef LPMC_LEVEL_MIN_CTAS
-#define LPMC_LEVEL_MIN_CTAS 4
+#define LPMC_LEVEL_MIN_CTAS 3
+#endif
+#ifndef LPMC_BAR_MIN_CTAS
+#define LPMC_BAR_MIN_CTAS 4
 #endif
 #ifndef LPMC_GLIBC_MIN_CTAS
 #define LPMC_GLIBC_MIN_CTAS 4
 #endif
+template <int LEGS, int TAB, int ZM>
+constexpr int level_min_ctas() {
+  const bool exact = (LEGS & 1) != 0 || LEGS == 4 || TAB == kTabNone;
+  return ZM == kZGlibc ? LPMC_GLIBC_MIN_CTAS : exact ? LPMC_LEVEL_MIN_CTAS : LPMC_BAR_MIN_CTAS;
+}
 template <class Arith, bool KAHAN, int LEGS, int TAB, bool DUMP, int ZM>
-__global__ void __launch_bounds__(kBatch / Arith::NP,
-                                  ZM == kZGlibc ? LPMC_GLIBC_MIN_CTAS : LPMC_LEVEL_MIN_CTAS)
+__global__ void __launch_bounds__(kBatch / Arith::NP, level_min_ctas<LEGS, TAB, ZM>())
     level_kernel(const __grid_constant__ LevelArgs A) {
   constexpr int NP = Arith::NP;
   constexpr bool kFineOnly = LEGS == 4;

@@ -492,16 +492,27 @@ static __device__ __noinline__ double phi_inv_lower_slow(double v) {
 // (u == 1/2, gaussian.hpp:62).  The hot loop instead flags such a draw
 // (probability 2^-53) and has the path replayed with EXACT_HALF, which keeps
 // two selects per draw out of the loop.
-template <int D, bool EXACT_HALF = true>
+struct NoMid {
+  __device__ __forceinline__ void operator()() const {}
+};
+
+// `mid` runs between the Newton block and the slow-path fix-ups, in the
+// same basic block as the Newton steps (the sampler's software pipeline
+// puts the previous batch's legs there, lpmc_level.cuh).
+template <int D, bool EXACT_HALF = true, class Mid = NoMid>
 __device__ __forceinline__ void phi_inv_stage2(const double (&v)[D], const double (&x0)[D],
                                                uint32_t neg, uint32_t half, double (&z)[D],
-                                               const double* mtab) {
+                                               const double* mtab, Mid&& mid = Mid{}) {
   bool slow[D];
 #pragma unroll
   for (int d = 0; d < D; ++d) z[d] = newton_fast(x0[d], v[d], mtab, &slow[d]);
+  mid();
+  bool any_slow = false;
+#pragma unroll
+  for (int d = 0; d < D; ++d) any_slow |= slow[d];
 #pragma unroll
   for (int d = 0; d < D; ++d) {
-    if (slow[d]) z[d] = phi_inv_lower_slow(v[d]);
+    if (any_slow && slow[d]) z[d] = phi_inv_lower_slow(v[d]);
     const double r = (neg >> d) & 1u ? -z[d] : z[d];
     if constexpr (EXACT_HALF) {
       z[d] = (half >> d) & 1u ? 0.0 : r;

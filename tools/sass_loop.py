@@ -18,7 +18,7 @@ import sys
 ROOT = __file__.rsplit("/tools/", 1)[0]
 ARGS = [a for a in sys.argv[1:] if not a.startswith("--")]
 OBJ = ARGS[0] if len(ARGS) > 0 else f"{ROOT}/paper_2012_09739_b200/_build/lpmc_level_f32.cu.o"
-FUN = ARGS[1] if len(ARGS) > 1 else r"level_kernelINS0_8ArithF32ELb0ELi3ELb1ELb0E"
+FUN = ARGS[1] if len(ARGS) > 1 else r"level_kernelINS0_8ArithF32ELb0ELi3ELi1ELb0ELi0E"
 
 sass = subprocess.run(["cuobjdump", "-sass", OBJ], capture_output=True, text=True, check=True).stdout
 funcs = re.split(r"\n\s+Function : ", sass)
