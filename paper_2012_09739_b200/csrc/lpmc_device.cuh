@@ -275,19 +275,35 @@ struct ArithF32Round {  // m <= 10: fp32 op (correctly rounded), then RNE to m+1
   uint32_t d, half_m1, keep;
   uint32_t d64;
   uint64_t half_m1_64, keep64;
+  float split;  // 2^d + 1: Veltkamp's splitter
   __device__ explicit ArithF32Round(const LevelArgs& A) {
     d = 23u - static_cast<uint32_t>(A.mantissa_bits);
     half_m1 = (1u << (d - 1)) - 1u;
     keep = ~((1u << d) - 1u);
+    split = static_cast<float>((1u << d) + 1u);  // exact: d <= 22
     d64 = 52u - static_cast<uint32_t>(A.mantissa_bits);
     half_m1_64 = (1ull << (d64 - 1)) - 1ull;
     keep64 = ~((1ull << d64) - 1ull);
   }
   __device__ T c(double dd, uint16_t) const { return static_cast<float>(dd); }
   __device__ T zero() const { return 0.0f; }
-  __device__ T mul(T a, T b) const { return rne32(__fmul_rn(a, b), d, half_m1, keep); }
-  __device__ T add(T a, T b) const { return rne32(__fadd_rn(a, b), d, half_m1, keep); }
-  __device__ T sub(T a, T b) const { return rne32(__fsub_rn(a, b), d, half_m1, keep); }
+  // RNE of a normal fp32 value to 24 - d = m + 1 significant bits.  Veltkamp's
+  // split c = x (2^d + 1), x - (c - x)... as c - (c - x) in round-to-nearest-
+  // even fp32 is that rounding, ties to even included, for m + 1 >= 2 bits
+  // and no overflow/underflow (the native range guard):
+  // three FMA-pipe operations instead of four integer ones (tests/
+  // test_veltkamp.py checks it against the integer RNE, ties included).
+  __device__ T rn(T x) const {
+#ifdef LPMC_F32R_INT
+    return rne32(x, d, half_m1, keep);
+#else
+    const float c = __fmul_rn(x, split);
+    return __fsub_rn(c, __fsub_rn(c, x));
+#endif
+  }
+  __device__ T mul(T a, T b) const { return rn(__fmul_rn(a, b)); }
+  __device__ T add(T a, T b) const { return rn(__fadd_rn(a, b)); }
+  __device__ T sub(T a, T b) const { return rn(__fsub_rn(a, b)); }
   // R(z) from the full binary64 value: one rounding (softfloat.hpp:69)
   __device__ T lift(const double (&z)[1]) const {
     return __double2float_rn(rne64(z[0], d64, half_m1_64, keep64));
