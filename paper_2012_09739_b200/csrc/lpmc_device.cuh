@@ -275,7 +275,8 @@ struct ArithF32Round {  // m <= 10: fp32 op (correctly rounded), then RNE to m+1
   uint32_t d, half_m1, keep;
   uint32_t d64;
   uint64_t half_m1_64, keep64;
-  float split;  // 2^d + 1: Veltkamp's splitter
+  float split;     // 2^d + 1: Veltkamp's splitter
+  double split64;  // 2^d64 + 1
   __device__ explicit ArithF32Round(const LevelArgs& A) {
     d = 23u - static_cast<uint32_t>(A.mantissa_bits);
     half_m1 = (1u << (d - 1)) - 1u;
@@ -284,6 +285,7 @@ struct ArithF32Round {  // m <= 10: fp32 op (correctly rounded), then RNE to m+1
     d64 = 52u - static_cast<uint32_t>(A.mantissa_bits);
     half_m1_64 = (1ull << (d64 - 1)) - 1ull;
     keep64 = ~((1ull << d64) - 1ull);
+    split64 = static_cast<double>((1ull << d64) + 1ull);  // exact: d64 <= 51
   }
   __device__ T c(double dd, uint16_t) const { return static_cast<float>(dd); }
   __device__ T zero() const { return 0.0f; }
@@ -305,8 +307,14 @@ struct ArithF32Round {  // m <= 10: fp32 op (correctly rounded), then RNE to m+1
   __device__ T add(T a, T b) const { return rn(__fadd_rn(a, b)); }
   __device__ T sub(T a, T b) const { return rn(__fsub_rn(a, b)); }
   // R(z) from the full binary64 value: one rounding (softfloat.hpp:69)
+  // (Veltkamp in binary64: Gaussians are 0 or normal and |z| < 40)
   __device__ T lift(const double (&z)[1]) const {
+#ifdef LPMC_F32R_INT
     return __double2float_rn(rne64(z[0], d64, half_m1_64, keep64));
+#else
+    const double c = __dmul_rn(z[0], split64);
+    return __double2float_rn(__dsub_rn(c, __dsub_rn(c, z[0])));
+#endif
   }
   __device__ double get(T x, int) const { return static_cast<double>(x); }
   __device__ uint32_t bad(T x) const { return nonfinite32(x) ? 1u : 0u; }

@@ -255,15 +255,20 @@ __device__ __forceinline__ void simulate(const LevelArgs& A, const TableView& ta
   // pipeline, 4 CTAs).
   // Bar-only and glibc-mode instances keep two coarse steps per batch and no
   // pipeline (their measured optimum).
-#ifdef LPMC_NO_PIPE_LEGS
+#if defined(LPMC_NO_PIPE_LEGS)
   constexpr bool kPipe = false;
+#elif defined(LPMC_GLIBC_PIPE)
+  constexpr bool kPipe = kNeedExact;
 #else
   constexpr bool kPipe = kNeedExact && ZM == kZFast;
+#endif
+#ifndef LPMC_GLIBC_G
+#define LPMC_GLIBC_G 2
 #endif
 #ifdef LPMC_COARSE_PER_BATCH
   constexpr int G = NP == 1 ? LPMC_COARSE_PER_BATCH : 1;
 #else
-  constexpr int G = NP == 1 ? (kPipe ? 1 : 2) : 1;  // coarse steps per batch
+  constexpr int G = NP == 1 ? (ZM == kZGlibc ? LPMC_GLIBC_G : kPipe ? 1 : 2) : 1;
 #endif
   if (A.level == 0) {  // sde.hpp:237-249: one draw, fine legs only, coarse := 0
     double z[1][NP];

@@ -42,3 +42,27 @@ def test_veltkamp_equals_integer_rne(m):
     with np.errstate(over="raise", under="raise"):
         got = veltkamp(x, d)
     assert np.array_equal(got.view(np.uint32), rne_int(x, d).view(np.uint32))
+
+
+def rne_int64(x: np.ndarray, d: int) -> np.ndarray:
+    b = x.view(np.uint64)
+    b = (b + np.uint64((1 << (d - 1)) - 1) + ((b >> np.uint64(d)) & np.uint64(1))) & \
+        ~np.uint64((1 << d) - 1)
+    return b.view(np.float64)
+
+
+@pytest.mark.parametrize("m", [1, 3, 7, 10])
+def test_veltkamp_binary64_lift(m):
+    """ArithF32Round::lift: R(z) of a binary64 Gaussian (0 or normal, |z| < 40)
+    to m + 1 bits by Veltkamp's split in binary64 (d = 52 - m)."""
+    d = 52 - m
+    rng = np.random.default_rng(100 + m)
+    n = 400_000
+    z = rng.standard_normal(n) * np.exp2(rng.integers(-60, 3, n))
+    b = z.view(np.uint64)
+    tie = rng.random(n) < 0.4
+    b = np.where(tie, (b & ~np.uint64((1 << d) - 1)) | np.uint64(1 << (d - 1)), b)
+    z = np.concatenate([b.view(np.float64), [0.0, -0.0, 4.3153065737391225, -8.3]])
+    c = z * float((1 << d) + 1)
+    got = c - (c - z)
+    assert np.array_equal(got.view(np.uint64), rne_int64(z, d).view(np.uint64))
