@@ -109,9 +109,16 @@ __device__ __forceinline__ void gen_draws(const LevelArgs& A, const TableView& t
       v[d] = ng ? 1.0 - u[d] : u[d];  // exact (gaussian.hpp:63)
       neg |= (ng ? 1u : 0u) << d;
     }
+#ifndef LPMC_MID_LATE  // the previous batch's legs run beside the fp32 initial guesses
+    mid();
+    math::phi_inv_stage1<D>(v, x0);
+    if constexpr (PREFETCH) draw_uniforms<NP, H>(kc, next);
+    math::phi_inv_stage2<D, CHECKED>(v, x0, neg, cur.half, zz, s_math);
+#else
     math::phi_inv_stage1<D>(v, x0);
     if constexpr (PREFETCH) draw_uniforms<NP, H>(kc, next);
     math::phi_inv_stage2<D, CHECKED>(v, x0, neg, cur.half, zz, s_math, mid);
+#endif
   } else {
     if constexpr (PREFETCH) draw_uniforms<NP, H>(kc, next);
     mid();
