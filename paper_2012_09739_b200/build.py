@@ -36,8 +36,8 @@ SOURCES_CU = ["lpmc_kernels.cu", "lpmc_level_carrier.cu", "lpmc_level_f32.cu",
               "lpmc_probe.cu", "lpmc_wpp_carrier.cu", "lpmc_wpp_f32.cu", "lpmc_wpp_f32r.cu",
               "lpmc_wpp_f64r.cu"]
 SOURCES_CXX = ["lpmc_host.cpp"]
-HEADERS = ["lpmc_internal.h", "lpmc_math.cuh", "lpmc_math_coef.h", "lpmc_x0f_coef.h", "lpmc_glibc.cuh",
-           "lpmc_glibc_coef.h", "lpmc_device.cuh",
+HEADERS = ["lpmc_internal.h", "lpmc_math.cuh", "lpmc_math_coef.h", "lpmc_math_coef_w8.h",
+           "lpmc_math_coef_w4.h", "lpmc_x0f_coef.h", "lpmc_glibc.cuh", "lpmc_glibc_coef.h", "lpmc_device.cuh",
            "lpmc_level.cuh", os.path.join("..", "..", "include", "lpmc_b200.h")]
 
 

@@ -44,10 +44,26 @@ struct Uniforms {
   uint32_t top, half;
 };
 
-template <int NP, int H>
+// EXACT = false (the unchecked hot loop, which only needs to know that a
+// path must be replayed): `half` bit p (of draw 0) is set when any of the H
+// draws of path p has a low word of 0 or 0xffffffff, a superset of both
+// special draws (kHalfDraw's low word is 0, kTopDraw's 0xffffffff) that costs
+// two integer operations per draw instead of two 64-bit compares and their
+// selects.  A false positive (probability 2^-31 per draw) only sends the path
+// to the exact replay, which recomputes the same values.  -DLPMC_EXACT_SPECIAL
+// restores the exact tests everywhere (A/B only).
+template <int NP, int H, bool EXACT_ARG = true>
 __device__ __forceinline__ void draw_uniforms(uint64_t (&kc)[NP], Uniforms<H * NP>& U) {
+#ifdef LPMC_EXACT_SPECIAL
+  constexpr bool EXACT = true;
+#else
+  constexpr bool EXACT = EXACT_ARG;
+#endif
   U.top = 0u;
   U.half = 0u;
+  bool rare[NP];
+#pragma unroll
+  for (int p = 0; p < NP; ++p) rare[p] = false;
 #pragma unroll
   for (int h = 0; h < H; ++h)
 #pragma unroll
@@ -55,9 +71,17 @@ __device__ __forceinline__ void draw_uniforms(uint64_t (&kc)[NP], Uniforms<H * N
       const uint64_t b = next_draw(kc[p]);
       const int d = h * NP + p;
       U.u[d] = uniform_of(b);
-      U.top |= (b == kTopDraw ? 1u : 0u) << d;
-      U.half |= (b == kHalfDraw ? 1u : 0u) << d;
+      if constexpr (EXACT) {
+        U.top |= (b == kTopDraw ? 1u : 0u) << d;
+        U.half |= (b == kHalfDraw ? 1u : 0u) << d;
+      } else {
+        rare[p] |= static_cast<uint32_t>(b) + 1u <= 1u;
+      }
     }
+  if constexpr (!EXACT) {
+#pragma unroll
+    for (int p = 0; p < NP; ++p) U.half |= (rare[p] ? 1u : 0u) << p;
+  }
 }
 
 // H draws per path starting at fine index n0 from pre-drawn uniforms `cur`:
@@ -97,7 +121,7 @@ __device__ __forceinline__ void gen_draws(const LevelArgs& A, const TableView& t
     }
   double zz[D];
   if constexpr (NEED_EXACT && ZM == kZGlibc) {
-    if constexpr (PREFETCH) draw_uniforms<NP, H>(kc, next);
+    if constexpr (PREFETCH) draw_uniforms<NP, H, CHECKED>(kc, next);
     glibc::inv_cdf_multi<D>(u, zz, s_math);
     mid();
   } else if constexpr (NEED_EXACT) {
@@ -112,15 +136,15 @@ __device__ __forceinline__ void gen_draws(const LevelArgs& A, const TableView& t
 #ifndef LPMC_MID_LATE  // the previous batch's legs run beside the fp32 initial guesses
     mid();
     math::phi_inv_stage1<D>(v, x0);
-    if constexpr (PREFETCH) draw_uniforms<NP, H>(kc, next);
+    if constexpr (PREFETCH) draw_uniforms<NP, H, CHECKED>(kc, next);
     math::phi_inv_stage2<D, CHECKED>(v, x0, neg, cur.half, zz, s_math);
 #else
     math::phi_inv_stage1<D>(v, x0);
-    if constexpr (PREFETCH) draw_uniforms<NP, H>(kc, next);
+    if constexpr (PREFETCH) draw_uniforms<NP, H, CHECKED>(kc, next);
     math::phi_inv_stage2<D, CHECKED>(v, x0, neg, cur.half, zz, s_math, mid);
 #endif
   } else {
-    if constexpr (PREFETCH) draw_uniforms<NP, H>(kc, next);
+    if constexpr (PREFETCH) draw_uniforms<NP, H, CHECKED>(kc, next);
     mid();
 #pragma unroll
     for (int d = 0; d < D; ++d) zz[d] = 0.0;
@@ -281,7 +305,7 @@ __device__ __forceinline__ void simulate(const LevelArgs& A, const TableView& ta
     double z[1][NP];
     T zb[1];
     Uniforms<NP> cur, unused;
-    draw_uniforms<NP, 1>(kc, cur);
+    draw_uniforms<NP, 1, CHECKED>(kc, cur);
     gen_draws<Arith, TAB, kNeedExact, kBar, CHECKED, DUMP, 1, false, ZM>(
         A, tab, s_math, ar, kc, u1, fk, local, valid, 0, cur, unused, z, zb);
     if constexpr (kHat) hat_fine(z[0], 0);
@@ -292,7 +316,7 @@ __device__ __forceinline__ void simulate(const LevelArgs& A, const TableView& ta
       // the batch after the last is drawn too (never consumed, its u == 1
       // bits never recorded): the price of a branch-free pipeline
       Uniforms<2 * G * NP> cur;
-      draw_uniforms<NP, 2 * G>(kc, cur);
+      draw_uniforms<NP, 2 * G, CHECKED>(kc, cur);
       if constexpr (kPipe) {
       // software pipeline: the legs of batch i run inside the Newton block of
       // batch i + 1 (one basic block: FP64/shared-load and FP32/integer work
@@ -356,7 +380,7 @@ __device__ __forceinline__ void simulate(const LevelArgs& A, const TableView& ta
         double z[2][NP];
         T zb[2];
         Uniforms<2 * NP> cur, unused;
-        draw_uniforms<NP, 2>(kc, cur);
+        draw_uniforms<NP, 2, CHECKED>(kc, cur);
         gen_draws<Arith, TAB, kNeedExact, kBar, CHECKED, DUMP, 2, false, ZM>(
             A, tab, s_math, ar, kc, u1, fk, local, valid, 2 * m, cur, unused, z, zb);
         if constexpr (kHat) hat_fine(z[0], 2 * m);

@@ -37,7 +37,13 @@
 #include <cmath>
 
 #include "lpmc_glibc_coef.h"
+#if defined(LPMC_ERFCX_W8)
+#include "lpmc_math_coef_w8.h"  // erfcx on 1/8 intervals, degree 9 (A/B)
+#elif defined(LPMC_ERFCX_W4)
+#include "lpmc_math_coef_w4.h"  // erfcx on 1/4 intervals, degree 11 (A/B)
+#else
 #include "lpmc_math_coef.h"
+#endif
 #include "lpmc_x0f_coef.h"
 
 #ifdef __CUDACC__
