@@ -396,7 +396,9 @@ def main():
                         "min over pipes of pipe peak / per-path-step demand (ncu counts, "
                         "profiles/fp64_ops_per_path_step.json; FP64 peak measured live, issue 4 "
                         "and shared-memory 1 per clock per SM at the sampled clock); fp64_frac = "
-                        "the literal fraction of the FP64 peak (DESIGN.md section 8)"}
+                        "the literal fraction of the FP64 peak (DESIGN.md section 8). The pipes "
+                        "are co-limits: an erfcx layout that cut the crossbar from 95 % to 70 % "
+                        "of peak ran 4 % slower (more instructions), DESIGN.md section 8"}
     else:
         roof = {"bound": "multi-pipe non-tensor", "achieved": achieved, "peak": None,
                 "unit": "path-steps/s", "frac": None, "traffic": None,
