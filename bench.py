@@ -1,29 +1,37 @@
 """Benchmark of the B200 MLMC level-correction sampler (driver contract).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--scaling weak|strong]
     torchrun --nproc-per-node N bench.py --gpus N ...        (N > 1)
 
-Workload (BASELINE.json configs[1], "C2"): GBM dS = 0.05 S dt + 0.2 S dW,
-S0 = 1, T = 1; levels 0..10; fp32 low-precision legs with the linear:16
-approximate inverse CDF; with and without Kahan; 2^22 paths per level per
-GPU (weak scaling); every path runs all four coupled legs and all three
-moment families -- exactly what the reference's estimate_level_stats /
-run_coupled_paths return (mlmc.hpp:67-149).  One "step" = the whole sweep
-(11 levels x 2 Kahan settings = 22 level launches).  Path bases follow the
-reference's four-way experiment (experiments.hpp:185-194): (l << 40) |
-(kahan << 36).
+Workload (BASELINE.json configs[3], "C4" -- the largest single-GPU config):
+nested-MLMC four-way difference P_f,exact - P_c,exact - P_f,approx + P_c,approx
+for GBM dS = 0.05 S dt + 0.2 S dW, S0 = 1, T = 1, European call payoff
+max(S_T - 1, 0); exact Gaussians in fp64 (hat legs) and approximate ones
+(linear:16 table) in the reference's fp16 (m = 10, emulated) and fp32 (bar
+legs); levels 0..12; 2^24 paths per level per GPU (weak scaling; --scaling
+strong keeps 2^24 paths per level in total).  Every path runs all four
+coupled legs and all three moment families (estimate_level_stats semantics,
+mlmc.hpp:113-149).  Precisions and path bases follow the reference's
+four-way experiment (experiments.hpp:170-213): low = fp16 at l << 40, high =
+fp32 at l << 40 | 2 << 36.  One "step" = 13 levels x 2 precisions = 26 level
+launches (2.75e11 fine path-steps per GPU).
 
 metric: fine path-steps per second (paths x 2^level, summed over the sweep).
 value:  device-timed (CUDA events on the launching stream), parameters and
         tables already resident, max over ranks.
-e2e:    through the public API (lpmc_level_partials + gather + fold +
-        LevelStats per level), host buffers, wall clock with syncs.
+e2e:    through the public multi-run API (lpmc_run_coupled_many_partials on
+        this rank's chunk range of every run, the same call for every N) +
+        all_gather + index-order fold + LevelStats per run, host buffers,
+        wall clock with syncs, max over ranks.
+C2 (BASELINE configs[1]) is measured too and reported under "c2".
 """
 from __future__ import annotations
 
 import argparse
 import json
 import os
+import platform
 import statistics
 import subprocess
 import sys
@@ -35,23 +43,47 @@ sys.path.insert(0, ROOT)
 
 METRIC = "Euler-Maruyama path-steps/sec per MLMC level & precision; % of FP roofline"
 UNIT = "path-steps/s"
-LEVELS = list(range(0, 11))
-KAHAN = (False, True)
-PATHS_PER_GPU = 1 << 22
+LEVELS = list(range(0, 13))
+PRECS = ("fp16", "fp32")  # the four-way experiment's low / high roles
+PATHS_PER_GPU = 1 << 24
 SEED = 1
-WORKLOAD = ("BASELINE config 2: GBM(mu=0.05, sigma=0.2, S0=1, T=1), levels 0..10, fp32 bar legs, "
-            "linear:16 approximate inverse CDF, +-Kahan, 2^22 paths per level per GPU, all four "
-            "coupled legs (fp64 exact + fp32 approx, fine + coarse) -> d_hat, d_bar, d_four "
-            "moments (estimate_level_stats semantics)")
-PROFILE_CONST = os.path.join(ROOT, "profiles", "fp64_ops_per_path_step.json")
+STRIKE = 1.0
+APPROX = "linear:16"
+WORKLOAD = ("BASELINE config 4: nested-MLMC 4-way difference, GBM(mu=0.05, sigma=0.2, S0=1, T=1), "
+            "European call payoff max(S_T-1,0), exact fp64 Gaussians + linear:16 approximate "
+            "Gaussians in fp16 (reference m=10 emulation) and fp32, no Kahan, levels 0..12, "
+            "2^24 paths per level, all four coupled legs -> d_hat, d_bar, d_four moments")
+DEMANDS = os.path.join(ROOT, "profiles", "r02_c4_l12_demands.json")
+CPU_SAMPLE = 1 << 15  # >= 256 paths x threads x 8 at 16 threads
+
+C2_LEVELS = list(range(0, 11))
+C2_PATHS = 1 << 22
 
 
-def path_base(level: int, kahan: bool) -> int:
-    return (level << 40) | (int(kahan) << 36)
+def path_base(level: int, prec: str) -> int:
+    return (level << 40) | ((2 << 36) if prec == "fp32" else 0)
+
+
+def mbits(prec: str) -> int:
+    return 10 if prec == "fp16" else 23
 
 
 def fine_steps(level: int, n: int) -> int:
     return n << level
+
+
+def host_info() -> dict:
+    model = platform.processor() or ""
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"cpu_model": model, "host_threads": os.cpu_count(),
+            "glibc": " ".join(platform.libc_ver())}
 
 
 # --------------------------------------------------------------- clocks -----
@@ -109,89 +141,141 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------ reference -----
-def run_reference(args, rank: int) -> None:
-    """--impl reference: the reference's own CPU run_coupled_paths (oracle/_ref,
-    compiled from /root/reference's headers) on all host cores, on a bounded
-    sample of the same workload; the oracle restatement if _ref is absent."""
-    if rank != 0:
-        return
+def _cpu_runner():
+    """The reference's own CPU run_coupled_paths (oracle/_ref, the unmodified
+    /root/reference headers compiled by oracle/Makefile); the oracle port if
+    _ref is absent.  The reference has no payoff option: it runs the terminal
+    payoff, a free post-step on the same four legs (mlmc.hpp:86-90)."""
     from oracle.bind import Oracle, Reference
     threads = os.cpu_count() or 1
-    sample = 1 << 13  # paths per (level, kahan) per step
     if Reference.available():
         R = Reference()
-        kind = "reference"
 
-        def one(level, kahan):
-            rc, msg, _ = R.run_coupled_paths(level=level, mantissa_bits=23, approx="linear:16",
-                                             kahan=kahan, n=sample, seed=SEED,
-                                             path_base=path_base(level, kahan), threads=threads)
+        def one(level, prec, n):
+            rc, msg, _ = R.run_coupled_paths(level=level, mantissa_bits=mbits(prec), approx=APPROX,
+                                             kahan=False, n=n, seed=SEED,
+                                             path_base=path_base(level, prec), threads=threads)
             assert rc == 0, msg
-    else:
-        O = Oracle()
-        kind = "port"
+        return one, "reference", threads
+    O = Oracle()
 
-        def one(level, kahan):
-            cfg = O.config(level=level, mantissa_bits=23, approx="linear:16", kahan=kahan,
-                           seed=SEED)
-            rc, _, _ = O.run_sequential(cfg, sample, path_base(level, kahan), threads=threads)
-            assert rc == 0
+    def one(level, prec, n):
+        cfg = O.config(level=level, mantissa_bits=mbits(prec), approx=APPROX, kahan=False,
+                       seed=SEED)
+        rc, _, _ = O.run_sequential(cfg, n, path_base(level, prec), threads=threads)
+        assert rc == 0
+    return one, "port", threads
 
-    work = sum(fine_steps(l, sample) for l in LEVELS for _ in KAHAN)
-    for _ in range(args.warmup):
+
+def run_reference(args, rank: int) -> None:
+    """--impl reference: the reference's CPU path on all host cores, on a
+    bounded sample of the same workload: step i runs precision PRECS[i % 2]
+    over levels 0..12 at 2^15 paths per level (both precisions alternate, so
+    any two consecutive steps cover the C4 mix)."""
+    if rank != 0:
+        return
+    one, kind, threads = _cpu_runner()
+
+    def step(i):
+        prec = PRECS[i % 2]
         for l in LEVELS:
-            for k in KAHAN:
-                one(l, k)
+            one(l, prec, CPU_SAMPLE)
+        return sum(fine_steps(l, CPU_SAMPLE) for l in LEVELS)
+
+    for i in range(args.warmup):
+        step(i)
+    work = 0
     t0 = time.perf_counter()
-    for _ in range(args.steps):
-        for l in LEVELS:
-            for k in KAHAN:
-                one(l, k)
+    for i in range(args.steps):
+        work += step(args.warmup + i)
     dt = time.perf_counter() - t0
-    value = work * args.steps / dt
-    desc = (f"{sample} paths per (level, kahan) per step, levels 0..10, +-Kahan, fp32 linear:16, "
-            f"all four legs; {threads} threads")
+    value = work / dt
+    desc = (f"{CPU_SAMPLE} paths per (level 0..12, precision); step i runs one precision "
+            f"(fp16, fp32 alternating), all four legs, terminal payoff (the reference has no call "
+            f"payoff: a free post-step); {threads} threads")
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f64+f32", "data": "synthetic (seeded counter RNG)",
-            "impl": "reference",
-            "config": {"workload": WORKLOAD, "sample_paths_per_level": sample},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind,
-                             "sample": desc},
+            "vs_baseline": None, "dtype": "f64+f32+f16(m=10)",
+            "data": "synthetic (seeded counter RNG)", "impl": "reference",
+            "config": {"workload": WORKLOAD, "sample_paths_per_level": CPU_SAMPLE},
+            "cpu_baseline": dict({"value": value, "unit": UNIT, "cores": threads, "kind": kind,
+                                  "sample": desc}, **host_info()),
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
 def cpu_baseline_sample() -> dict:
-    """The reference timed on this host on a bounded sample (~10-30 core-s)."""
-    from oracle.bind import Oracle, Reference
-    threads = os.cpu_count() or 1
-    sample = 1 << 14
-    work = sum(fine_steps(l, sample) for l in LEVELS for _ in KAHAN)
+    """The reference timed on this host on a bounded sample (~10-30 s)."""
+    one, kind, threads = _cpu_runner()
+    work = sum(fine_steps(l, CPU_SAMPLE) for l in LEVELS) * len(PRECS)
     t0 = time.perf_counter()
-    if Reference.available():
-        R = Reference()
-        kind = "reference"
+    for prec in PRECS:
         for l in LEVELS:
-            for k in KAHAN:
-                rc, msg, _ = R.run_coupled_paths(level=l, mantissa_bits=23, approx="linear:16",
-                                                 kahan=k, n=sample, seed=SEED,
-                                                 path_base=path_base(l, k), threads=threads)
-                assert rc == 0, msg
-    else:
-        O = Oracle()
-        kind = "port"
-        for l in LEVELS:
-            for k in KAHAN:
-                cfg = O.config(level=l, mantissa_bits=23, approx="linear:16", kahan=k, seed=SEED)
-                rc, _, _ = O.run_sequential(cfg, sample, path_base(l, k), threads=threads)
-                assert rc == 0
+            one(l, prec, CPU_SAMPLE)
     dt = time.perf_counter() - t0
-    return {"value": work / dt, "unit": UNIT, "cores": threads, "kind": kind,
-            "sample": f"{sample} paths per (level 0..10, +-Kahan) = {work:.3e} fine path-steps, "
-                      f"all four legs, {dt:.2f} s wall on {threads} threads"}
+    return dict({"value": work / dt, "unit": UNIT, "cores": threads, "kind": kind,
+                 "sample": f"{CPU_SAMPLE} paths per (level 0..12, fp16/fp32) = {work:.3e} fine "
+                           f"path-steps, all four legs, terminal payoff, {dt:.2f} s wall on "
+                           f"{threads} threads"}, **host_info())
+
+
+# ------------------------------------------------------------- roofline -----
+def roofline(L, per_cfg_ms, cfgs, n_local, clk, peaks, n_sm):
+    """North-star roofline of the dominant kernel: FP64 lane-ops/s achieved
+    (ncu-counted FP64 lane-ops per fine path-step x live path-steps/s) against
+    the measured FP64 peak; the multi-pipe view (FP64, issue, shared-memory
+    crossbar) is kept under multi_pipe."""
+    from paper_2012_09739_b200.build import kernel_source_hash
+    dom = max(cfgs, key=lambda c: statistics.mean(per_cfg_ms[c]))
+    dom_ms = statistics.mean(per_cfg_ms[dom])
+    rate = fine_steps(dom[0], n_local) / (dom_ms * 1e-3)  # path-steps/s, CUDA events
+    prof = {}
+    if os.path.exists(DEMANDS):
+        with open(DEMANDS) as f:
+            prof = json.load(f)
+    src_hash = kernel_source_hash()
+    stale = prof.get("kernel_source_hash") != src_hash
+    sm_hz = (clk.get("sm_mhz") or 1965.0) * 1e6
+    pipes = {}
+    if prof.get("fp64_lane_ops_per_path_step"):
+        pipes["fp64"] = {"demand_per_path_step": prof["fp64_lane_ops_per_path_step"],
+                         "peak_per_s": peaks["fp64_ops_per_s"], "unit": "FP64 lane-ops"}
+    if prof.get("warp_inst_per_path_step"):
+        pipes["issue"] = {"demand_per_path_step": prof["warp_inst_per_path_step"],
+                          "peak_per_s": 4.0 * n_sm * sm_hz, "unit": "warp-instructions"}
+    if prof.get("smem_wavefronts_per_path_step"):
+        pipes["smem"] = {"demand_per_path_step": prof["smem_wavefronts_per_path_step"],
+                         "peak_per_s": 1.0 * n_sm * sm_hz, "unit": "shared-memory wavefronts"}
+    for p in pipes.values():
+        p["ceiling_path_steps_per_s"] = p["peak_per_s"] / p["demand_per_path_step"]
+        p["frac"] = rate / p["ceiling_path_steps_per_s"]
+    kernel = f"level_kernel level {dom[0]} {dom[1]} (all legs, call payoff, linear:16)"
+    if "fp64" not in pipes:
+        return {"bound": "fp64", "achieved": None, "peak": peaks["fp64_ops_per_s"] / 1e12,
+                "unit": "TFLOP/s", "frac": None, "traffic": None, "kernel": kernel,
+                "path_steps_per_s": rate, "note": "per-path-step demands not profiled"}
+    achieved = pipes["fp64"]["demand_per_path_step"] * rate  # FP64 lane-ops/s
+    bind = min(pipes, key=lambda k: pipes[k]["ceiling_path_steps_per_s"])
+    return {
+        "bound": "fp64", "achieved": achieved / 1e12, "peak": peaks["fp64_ops_per_s"] / 1e12,
+        "unit": "TFLOP/s", "frac": achieved / peaks["fp64_ops_per_s"],
+        "traffic": prof.get("dram_bytes_per_launch"), "kernel": kernel,
+        "path_steps_per_s": rate, "launch_ms": dom_ms,
+        "fp64_lane_ops_per_path_step": pipes["fp64"]["demand_per_path_step"],
+        "demands": os.path.relpath(DEMANDS, ROOT), "demands_stale": stale,
+        "kernel_source_hash": src_hash,
+        "multi_pipe": {"binding": bind, "frac": pipes[bind]["frac"],
+                       "ceiling_path_steps_per_s": pipes[bind]["ceiling_path_steps_per_s"],
+                       "pipes": pipes, "co_limits": prof.get("co_limits")},
+        "note": "no HBM or tensor bound: per-path state lives in registers (traffic = DRAM bytes "
+                "of one launch, ncu). achieved = FP64 lane-ops per fine path-step (ncu "
+                "sm__sass_thread_inst_executed_op_{dadd,dmul,dfma}, one lane-op per DFMA as the "
+                "pipe issues it) x the dominant launch's path-steps/s from CUDA events; peak = "
+                "FP64 lane-op rate measured live on this GPU (lpmc_measure_pipe_peaks; "
+                "MEASURED_PEAKS.json has no FP64 figure), in 1e12 lane-ops/s. demands_stale = "
+                "the profiled kernel sources differ from this build."}
 
 
 # ------------------------------------------------------------------ ours ----
@@ -201,7 +285,9 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-c2", action="store_true")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -212,7 +298,6 @@ def main():
         run_reference(args, rank)
         return
 
-    import numpy as np
     import torch
     import torch.distributed as dist
 
@@ -238,14 +323,16 @@ def main():
             dist.barrier()
 
     model = L.make_gbm(0.05, 0.2, 1.0, 1.0)
-    spec = L.PrecisionSpec.fp32()
-    approx = L.InvCdfApprox.parse("linear:16")
-    n_total = PATHS_PER_GPU * world  # weak scaling
+    specs = {"fp16": L.PrecisionSpec.fp16(), "fp32": L.PrecisionSpec.fp32()}
+    approx = L.InvCdfApprox.parse(APPROX)
+    n_total = PATHS_PER_GPU * (world if args.scaling == "weak" else 1)
     n_chunks = n_total // (1 << 18)
     c0, c1 = shard_chunks(n_chunks, rank, world)
-    cfgs = [(l, k) for l in LEVELS for k in KAHAN]
-    plans = {(l, k): L.LevelPlan(model, l, spec, approx, k, n_total, SEED, path_base(l, k),
-                                 chunks=(c0, c1), device=gpu_index) for (l, k) in cfgs}
+    n_local = (c1 - c0) * (1 << 18)
+    cfgs = [(l, p) for l in LEVELS for p in PRECS]
+    ext = dict(payoff="call", strike=STRIKE)
+    plans = {(l, p): L.LevelPlan(model, l, specs[p], approx, False, n_total, SEED, path_base(l, p),
+                                 chunks=(c0, c1), device=gpu_index, **ext) for (l, p) in cfgs}
     # A dedicated stream: torch's legacy default stream has handle 0, which
     # the C-ABI reads as "the plan's own stream".
     stream = torch.cuda.Stream(dev)
@@ -254,84 +341,80 @@ def main():
     assert sptr != 0
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 
-    def sweep(events=None):
-        for (l, k) in cfgs:
+    def sweep(pl, keys, events=None):
+        for c in keys:
             if events is not None:
-                events[(l, k)][0].record(stream)
-            plans[(l, k)].launch(sptr)
+                events[c][0].record(stream)
+            pl[c].launch(sptr)
             if events is not None:
-                events[(l, k)][1].record(stream)
+                events[c][1].record(stream)
 
-    def gather_all():
+    def gather_all(pl, keys, nck):
         out = {}
-        for (l, k) in cfgs:
-            part = plans[(l, k)].collect_partials()
-            full = allgather_partials(part, n_chunks, None, coll_dev) if world > 1 else part
-            out[(l, k)] = L.fold_partials(full)
+        for c in keys:
+            part = pl[c].collect_partials()
+            full = allgather_partials(part, nck, None, coll_dev) if world > 1 else part
+            out[c] = L.fold_partials(full)
         return out
+
+    def timed(pl, keys, steps, nck):
+        per_step, per_cfg = [], {c: [] for c in keys}
+        res = None
+        barrier()
+        torch.cuda.synchronize(dev)
+        for _ in range(steps):
+            flush.zero_()  # L2 flush (256 MiB > 126 MB L2), outside the events
+            ev = {c: (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                  for c in keys}
+            t0 = torch.cuda.Event(enable_timing=True)
+            t1 = torch.cuda.Event(enable_timing=True)
+            t0.record(stream)
+            sweep(pl, keys, ev)
+            t1.record(stream)
+            torch.cuda.synchronize(dev)
+            per_step.append(t0.elapsed_time(t1))
+            for c in keys:
+                per_cfg[c].append(ev[c][0].elapsed_time(ev[c][1]))
+            res = gather_all(pl, keys, nck)  # results of every timed step are produced
+        barrier()
+        torch.cuda.synchronize(dev)
+        return per_step, per_cfg, res
 
     # warm-up (also a correctness pass of the collective path)
     for _ in range(max(args.warmup, 1)):
-        sweep()
+        sweep(plans, cfgs)
         torch.cuda.synchronize(dev)
-        results = gather_all()
+        results = gather_all(plans, cfgs, n_chunks)
 
     clocks = ClockSampler(gpu_index)
     if rank == 0:
         clocks.start()
     L.reset_launch_count()
-    per_step_ms = []
-    per_cfg_ms = {c: [] for c in cfgs}
-    barrier()
-    torch.cuda.synchronize(dev)
-    for _ in range(args.steps):
-        flush.zero_()  # L2 flush (256 MiB > 126 MB L2), outside the events
-        ev = {c: (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-              for c in cfgs}
-        t0 = torch.cuda.Event(enable_timing=True)
-        t1 = torch.cuda.Event(enable_timing=True)
-        t0.record(stream)
-        sweep(ev)
-        t1.record(stream)
-        torch.cuda.synchronize(dev)
-        per_step_ms.append(t0.elapsed_time(t1))
-        for c in cfgs:
-            per_cfg_ms[c].append(ev[c][0].elapsed_time(ev[c][1]))
-        results = gather_all()  # results of every timed step are produced
-    barrier()
-    torch.cuda.synchronize(dev)
+    per_step_ms, per_cfg_ms, results = timed(plans, cfgs, args.steps, n_chunks)
     launches = L.launch_count()
     clk = clocks.stop() if rank == 0 else {}
 
-    step_ms = sum(per_step_ms) / len(per_step_ms)
-    t = torch.tensor([step_ms], dtype=torch.float64, device=coll_dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    step_ms_max = float(t.item())
-    work_total = sum(fine_steps(l, n_total) for (l, k) in cfgs)
+    def max_over_ranks(x: float) -> float:
+        t = torch.tensor([x], dtype=torch.float64, device=coll_dev)
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    step_ms_max = max_over_ranks(sum(per_step_ms) / len(per_step_ms))
+    work_total = sum(fine_steps(l, n_total) for (l, p) in cfgs)
     value = work_total / (step_ms_max * 1e-3)
 
-    # ---- e2e through the public API (host buffers, syncs, gather, fold) ----
-    lib = L.api.N.load()
+    # ---- e2e through the public multi-run API (the same call for every N) ----
     e2e_steps = max(1, min(args.steps, 3))
-    barrier()
-    torch.cuda.synchronize(dev)
+    runs = [(l, specs[p], False, n_total, path_base(l, p)) for (l, p) in cfgs]
+    ranges = [(c0, c1)] * len(runs)
+
     def e2e_step():
-        if world == 1:
-            # one multi-run call (lpmc_run_coupled_many, the drop-in for the
-            # reference callers' per-level loop): levels run concurrently on the
-            # device's stream pool, results land in host memory, one wait
-            runs = [(l, spec, k, n_total, path_base(l, k)) for (l, k) in cfgs]
-            for (l, k), m in zip(cfgs, L.run_coupled_many(model, approx, SEED, runs,
-                                                          device=gpu_index)):
-                L.level_stats_from_moments(m, l, spec, k, n_total)
-        else:  # rank-sharded chunk partials, gathered and folded in chunk order
-            for (l, k) in cfgs:
-                part = L.level_partials(model, l, spec, approx, k, n_total, SEED,
-                                        path_base(l, k), c0, c1, device=gpu_index)
-                full = allgather_partials(part, n_total // (1 << 18), None, coll_dev)
-                m = L.fold_partials(full)
-                L.level_stats_from_moments(m, l, spec, k, n_total)
+        parts = L.run_coupled_many_partials(model, approx, SEED, runs, ranges,
+                                            device=gpu_index, **ext)
+        for (l, p), part in zip(cfgs, parts):
+            full = allgather_partials(part, n_chunks, None, coll_dev) if world > 1 else part
+            L.level_stats_from_moments(L.fold_partials(full), l, specs[p], False, n_total)
 
     e2e_step()  # untimed warm-up: stream pool, pinned staging and buffers are created once
     torch.cuda.synchronize(dev)
@@ -341,83 +424,59 @@ def main():
         e2e_step()
     torch.cuda.synchronize(dev)
     barrier()
-    e2e_s = (time.perf_counter() - w0) / e2e_steps
-    te = torch.tensor([e2e_s], dtype=torch.float64, device=coll_dev)
-    if world > 1:
-        dist.all_reduce(te, op=dist.ReduceOp.MAX)
-    e2e_value = work_total / float(te.item())
-    table_bytes = 7 * 16 * 8
-    h2d = len(cfgs) * (table_bytes + 12)  # table + failure-word/flag init
-    d2h = len(cfgs) * ((c1 - c0) * 15 * 8 + 12)
+    e2e_value = work_total / max_over_ranks((time.perf_counter() - w0) / e2e_steps)
+    table_bytes = 7 * 16 * 8  # linear:16 breakpoints, coefficients and scalars
+    h2d = len(cfgs) * (table_bytes + 12)  # table + failure-word/flag init per run
+    d2h = len(cfgs) * ((c1 - c0) * 15 * 8 + 12)  # chunk partials + failure word/flag per run
+
+    # ---- C2 (BASELINE configs[1]) as a secondary line ------------------------
+    c2 = None
+    if not args.no_c2:
+        c2_total = C2_PATHS * (world if args.scaling == "weak" else 1)
+        c2_chunks = c2_total // (1 << 18)
+        d0, d1 = shard_chunks(c2_chunks, rank, world)
+        c2_cfgs = [(l, k) for l in C2_LEVELS for k in (False, True)]
+        fp32 = specs["fp32"]
+        c2_plans = {(l, k): L.LevelPlan(model, l, fp32, approx, k, c2_total, SEED,
+                                        (l << 40) | (int(k) << 36), chunks=(d0, d1),
+                                        device=gpu_index) for (l, k) in c2_cfgs}
+        sweep(c2_plans, c2_cfgs)
+        torch.cuda.synchronize(dev)
+        gather_all(c2_plans, c2_cfgs, c2_chunks)
+        c2_steps, _, _ = timed(c2_plans, c2_cfgs, max(3, min(args.steps, 10)), c2_chunks)
+        c2_ms = max_over_ranks(statistics.mean(c2_steps))
+        c2 = {"workload": "BASELINE config 2: levels 0..10, fp32 linear:16, +-Kahan, 2^22 paths per "
+                          "level per GPU, terminal payoff, all four legs",
+              "value": sum(fine_steps(l, c2_total) for (l, k) in c2_cfgs) / (c2_ms * 1e-3),
+              "unit": UNIT, "ms_per_step": c2_ms}
+        for p in c2_plans.values():
+            p.close()
 
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
         return
 
-    # ---- roofline of the dominant kernel (level 10) --------------------------
     peaks = L.measure_pipe_peaks(gpu_index)
-    dom = [(10, False), (10, True)]
-    dom_ms = statistics.mean(statistics.mean(per_cfg_ms[c]) for c in dom)
-    dom_steps = fine_steps(10, (c1 - c0) * (1 << 18))
-    prof = {}
-    if os.path.exists(PROFILE_CONST):
-        with open(PROFILE_CONST) as f:
-            prof = json.load(f)
-    achieved = dom_steps / (dom_ms * 1e-3)  # level-10 path-steps/s, CUDA events
-    sm_hz = (clk.get("sm_mhz") or 1965.0) * 1e6
     n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
-    # multi-pipe roofline = min over pipes of
-    # peak_p / demand_p per path-step (demands: ncu counts of this kernel)
-    pipes = {}
-    if prof.get("fp64_lane_ops_per_path_step"):
-        pipes["fp64"] = {"demand_per_path_step": prof["fp64_lane_ops_per_path_step"],
-                         "peak_per_s": peaks["fp64_ops_per_s"], "unit": "FP64 lane-ops"}
-    if prof.get("warp_inst_per_path_step"):
-        pipes["issue"] = {"demand_per_path_step": prof["warp_inst_per_path_step"],
-                          "peak_per_s": 4.0 * n_sm * sm_hz, "unit": "warp-instructions"}
-    if prof.get("smem_wavefronts_per_path_step"):
-        pipes["smem"] = {"demand_per_path_step": prof["smem_wavefronts_per_path_step"],
-                         "peak_per_s": 1.0 * n_sm * sm_hz, "unit": "shared-memory wavefronts"}
-    for p in pipes.values():
-        p["ceiling_path_steps_per_s"] = p["peak_per_s"] / p["demand_per_path_step"]
-        p["frac"] = achieved / p["ceiling_path_steps_per_s"]
-    if pipes:
-        bind = min(pipes, key=lambda k: pipes[k]["ceiling_path_steps_per_s"])
-        peak = pipes[bind]["ceiling_path_steps_per_s"]
-        roof = {"bound": f"multi-pipe non-tensor (binding: {bind})", "achieved": achieved,
-                "peak": peak, "unit": "path-steps/s", "frac": achieved / peak,
-                "traffic": prof.get("dram_bytes_per_launch"), "pipes": pipes,
-                "fp64_frac": pipes.get("fp64", {}).get("frac"),
-                "co_limits": prof.get("co_limits"),
-                "note": "neither HBM- nor tensor-bound: per-path state in registers, 0 bytes per "
-                        "path-step (traffic = DRAM bytes of one level-10 launch of 4.3e9 "
-                        "path-steps, ncu). achieved = level-10 path-steps/s (CUDA events); peak = "
-                        "min over pipes of pipe peak / per-path-step demand (ncu counts, "
-                        "profiles/fp64_ops_per_path_step.json; FP64 peak measured live, issue 4 "
-                        "and shared-memory 1 per clock per SM at the sampled clock); fp64_frac = "
-                        "the literal fraction of the FP64 peak (DESIGN.md section 8). The pipes "
-                        "are co-limits: an erfcx layout that cut the crossbar from 95 % to 70 % "
-                        "of peak ran 4 % slower (more instructions), DESIGN.md section 8"}
-    else:
-        roof = {"bound": "multi-pipe non-tensor", "achieved": achieved, "peak": None,
-                "unit": "path-steps/s", "frac": None, "traffic": None,
-                "note": "per-path-step demands not yet profiled"}
-
+    roof = roofline(L, per_cfg_ms, cfgs, n_local, clk, peaks, n_sm)
     cpu = None if args.no_cpu_baseline else cpu_baseline_sample()
-    per_level = {}
-    for l in LEVELS:
-        ms = sum(statistics.mean(per_cfg_ms[(l, k)]) for k in KAHAN)
-        per_level[str(l)] = fine_steps(l, (c1 - c0) * (1 << 18)) * 2 / (ms * 1e-3)
+    per_level = {p: {} for p in PRECS}
+    for (l, p) in cfgs:
+        per_level[p][str(l)] = fine_steps(l, n_local) / (statistics.mean(per_cfg_ms[(l, p)]) * 1e-3)
+    top = results[(12, "fp16")], results[(12, "fp32")]
     out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": step_ms_max, "higher_is_better": True,
-           "scaling": "weak", "vs_baseline": None, "dtype": "f64+f32",
+           "scaling": args.scaling, "vs_baseline": None, "dtype": "f64+f32+f16(m=10)",
            "data": "synthetic (seeded counter-based RNG; no dataset)",
-           "config": {"workload": WORKLOAD, "paths_per_level_per_gpu": PATHS_PER_GPU,
-                      "levels": "0..10", "kahan": [False, True], "precision": "fp32",
-                      "approx": "linear:16", "legs": "all", "reduce": "tree",
+           "config": {"workload": WORKLOAD,
+                      "paths_per_level": n_total, "paths_per_level_per_gpu": n_local,
+                      "levels": "0..12", "precisions": ["fp16 (m=10, reference emulation)", "fp32"],
+                      "kahan": False, "approx": APPROX, "payoff": "call, strike 1",
+                      "legs": "all", "reduce": "tree",
+                      "path_bases": "fp16: l<<40, fp32: l<<40 | 2<<36 (experiments.hpp:185-194)",
                       "parallelism": f"paths sharded by 2^18-path chunks over {world} GPU(s); "
-                                     "one all_gather of chunk moments",
+                                     "one all_gather of chunk moments per run",
                       "l2": "flushed between timed steps (256 MiB write); kernels read no "
                             "input tensors"},
            "gpu_launches": int(launches),
@@ -426,12 +485,16 @@ def main():
            "pipe_peaks_measured": peaks,
            "per_level_path_steps_per_s_per_gpu": per_level,
            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
-                   "d2h_bytes_per_step": d2h},
+                   "d2h_bytes_per_step": d2h,
+                   "method": "lpmc_run_coupled_many_partials over the rank's chunk range of all "
+                             "26 runs (concurrent on the device's stream pool), all_gather, fold, "
+                             "LevelStats; wall clock, max over ranks"},
            "cpu_baseline": cpu,
-           "check": {"v_hat_l10": results[(10, False)].d_hat.variance(),
-                     "v_bar_l10": results[(10, False)].d_bar.variance(),
-                     "V_bar_l10": results[(10, False)].d_four.variance(),
-                     "V_bar_l10_kahan": results[(10, True)].d_four.variance()}}
+           "c2": c2,
+           "check": {"v_hat_l12": top[0].d_hat.variance(),
+                     "v_bar_l12_fp16": top[0].d_bar.variance(),
+                     "V_bar_l12_fp16": top[0].d_four.variance(),
+                     "V_bar_l12_fp32": top[1].d_four.variance()}}
     print(json.dumps(out), flush=True)
     if world > 1:
         dist.destroy_process_group()

@@ -357,6 +357,22 @@ lpmc_status lpmc_run_coupled_many(const lpmc_gbm* model, const lpmc_invcdf_table
                                   const lpmc_options* opts, lpmc_moments* out, lpmc_error* err);
 
 /*
+ * The multi-run call restricted to one chunk range per run (one process per
+ * GPU: rank r passes its contiguous chunk shard of every run).  Chunks are
+ * LPMC_CHUNK_PATHS paths; run i covers chunks [chunk_begin[i], chunk_end[i]).
+ * out: the raw chunk accumulators, run-major, 3 per chunk (d_hat, d_bar,
+ * d_four), i.e. sum_i 3 (chunk_end[i] - chunk_begin[i]) entries; fold the
+ * gathered ranges of all ranks with lpmc_fold_partials.  Always the tree
+ * reduction.  Same concurrency, failure order and blocking as
+ * lpmc_run_coupled_many.
+ */
+lpmc_status lpmc_run_coupled_many_partials(const lpmc_gbm* model, const lpmc_invcdf_table* table,
+                                           uint64_t seed, const lpmc_run_desc* runs,
+                                           uint64_t n_runs, const uint64_t* chunk_begin,
+                                           const uint64_t* chunk_end, const lpmc_options* opts,
+                                           lpmc_moments* out, lpmc_error* err);
+
+/*
  * The two-way sampler: MomentAccumulator of x_hat - x_bar over n_paths
  * simulate_two_way paths (sde.hpp:162-196), batched and merged like
  * run_batched (experiments.hpp:89-112).  out: 1 accumulator.

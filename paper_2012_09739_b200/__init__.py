@@ -13,12 +13,14 @@ from .api import (Allocation, AllocationKind, CostModel, CoupledMoments,  # noqa
                   device_inv_cdf, estimate_level_stats, fold_partials, launch_count,
                   level_partials, level_stats_from_moments, make_gbm, measure_pipe_peaks,
                   per_level_speedup, predicted_times, reset_launch_count, round_to_precision,
-                  run_coupled_many, run_coupled_paths, run_nested_estimator, run_two_way_paths,
+                  run_coupled_many, run_coupled_many_partials, run_coupled_paths,
+                  run_nested_estimator, run_two_way_paths,
                   simulate_paths, StepErrorStats, step_error_probe, density_histogram)
 
 __all__ = [
     "Allocation", "AllocationKind", "EstimatorResult", "PredictedTimes", "SpeedupResult",
     "allocate_samples", "per_level_speedup", "predicted_times", "run_coupled_many",
+    "run_coupled_many_partials",
     "run_nested_estimator", "run_two_way_paths", "StepErrorStats", "step_error_probe", "density_histogram",
     "CostModel", "CoupledMoments", "DomainError", "InvalidArgument", "InvCdfApprox", "LevelPlan",
     "LevelStats", "MomentAccumulator", "PrecisionSpec", "SamplerRuntimeError", "SdeModel",

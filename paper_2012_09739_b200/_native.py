@@ -167,6 +167,9 @@ SIGNATURES = {
     "lpmc_glibc_math": (C.c_double, [_i32, C.c_double, _P(_i32)]),
     "lpmc_run_coupled_many": (_i32, [_P(Gbm), _P(InvCdfTable), _u64, _P(RunDesc), _u64,
                                      _P(Options), _P(Moments), _P(Error)]),
+    "lpmc_run_coupled_many_partials": (_i32, [_P(Gbm), _P(InvCdfTable), _u64, _P(RunDesc), _u64,
+                                              _P(_u64), _P(_u64), _P(Options), _P(Moments),
+                                              _P(Error)]),
     "lpmc_run_two_way_paths": (_i32, [_P(Gbm), _i32, _P(Precision), _P(InvCdfTable), _i32, _u64,
                                       _u64, _u64, _P(Options), _P(Moments), _P(Error)]),
     "lpmc_allocate_samples": (_i32, [_P(LevelStatsC), _u64, C.c_double, _i32, _P(_u64),

@@ -457,6 +457,40 @@ def run_coupled_many(model: SdeModel, approx: Optional[InvCdfApprox], seed: int,
     return [CoupledMoments.from_c3(acc[3 * i:3 * i + 3]) for i in range(len(runs))]
 
 
+def run_coupled_many_partials(model: SdeModel, approx: Optional[InvCdfApprox], seed: int, runs,
+                              chunk_ranges, **ext) -> list:
+    """run_coupled_many over one chunk range per run (this rank's shard):
+    ``chunk_ranges`` holds (chunk_begin, chunk_end) per run.  Returns one
+    (k_i, 3, 5) array of raw chunk accumulators per run (fold the gathered
+    shards of all ranks with fold_partials)."""
+    runs = list(runs)
+    ranges = [(int(a), int(b)) for a, b in chunk_ranges]
+    if len(ranges) != len(runs):
+        raise InvalidArgument("one chunk range per run")
+    n = max(1, len(runs))
+    descs = (N.RunDesc * n)()
+    cb = (C.c_uint64 * n)()
+    ce = (C.c_uint64 * n)()
+    for i, (level, spec, kahan, npaths, base) in enumerate(runs):
+        descs[i] = N.RunDesc(int(level), spec._c(), int(bool(kahan)), int(npaths), int(base))
+        cb[i], ce[i] = ranges[i]
+    total = sum(max(b - a, 0) for a, b in ranges)
+    acc = (N.Moments * max(1, 3 * total))()
+    err = N.Error()
+    opts = _options(**ext)
+    N.check(N.load().lpmc_run_coupled_many_partials(C.byref(_gbm_c(model)), _table_ptr(approx),
+                                                    int(seed), descs, len(runs), cb, ce,
+                                                    C.byref(opts), acc, C.byref(err)), err)
+    flat = np.array([acc[i].as_tuple() for i in range(3 * total)],
+                    dtype=np.float64).reshape(-1, 3, 5)
+    out, o = [], 0
+    for a, b in ranges:
+        k = max(b - a, 0)
+        out.append(flat[o:o + k])
+        o += k
+    return out
+
+
 def run_two_way_paths(model: SdeModel, level: int, spec_low: PrecisionSpec,
                       approx: Optional[InvCdfApprox], kahan: bool, n_paths: int, seed: int,
                       path_base: int, threads: int = 1, **ext) -> MomentAccumulator:

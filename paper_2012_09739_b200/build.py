@@ -53,6 +53,18 @@ def _run(cmd: list[str]) -> None:
     subprocess.check_call(cmd)
 
 
+def kernel_source_hash() -> str:
+    """sha256 (16 hex digits) over the device sources and nvcc flags: ties a
+    profile's ncu-counted per-path-step demands to the kernels that produced
+    them (bench.py flags a mismatch as stale)."""
+    import hashlib
+    h = hashlib.sha256(" ".join(NVCC_FLAGS).encode())
+    for name in sorted(SOURCES_CU) + sorted(x for x in HEADERS if not x.startswith("..")):
+        with open(os.path.join(CSRC, name), "rb") as f:
+            h.update(name.encode() + b"\0" + f.read())
+    return h.hexdigest()[:16]
+
+
 def build(force: bool = False, verbose_ptxas: bool = False) -> str:
     os.makedirs(BUILD, exist_ok=True)
     hdrs = [os.path.join(CSRC, h) for h in HEADERS]

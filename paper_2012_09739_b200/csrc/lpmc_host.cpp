@@ -1304,6 +1304,56 @@ lpmc_status lpmc_run_coupled_many(const lpmc_gbm* model, const lpmc_invcdf_table
   return ok(err);
 }
 
+lpmc_status lpmc_run_coupled_many_partials(const lpmc_gbm* model, const lpmc_invcdf_table* table,
+                                           uint64_t seed, const lpmc_run_desc* runs,
+                                           uint64_t n_runs, const uint64_t* chunk_begin,
+                                           const uint64_t* chunk_end, const lpmc_options* opts,
+                                           lpmc_moments* out, lpmc_error* err) {
+  if (n_runs == 0) return ok(err);
+  if (runs == nullptr || out == nullptr || chunk_begin == nullptr || chunk_end == nullptr)
+    return fail(err, LPMC_INVALID_ARGUMENT, "null run list, chunk range or output");
+  lpmc_options o;
+  lpmc_default_options(&o);
+  if (opts != nullptr) o = *opts;
+  o.reduce = LPMC_REDUCE_TREE;  // chunk partials are defined by the tree
+  std::vector<RunSpec> specs;
+  specs.reserve(n_runs);
+  std::vector<uint64_t> off(n_runs + 1, 0);
+  for (uint64_t i = 0; i < n_runs; ++i) {
+    const uint64_t n_chunks = (runs[i].n_paths + LPMC_CHUNK_PATHS - 1) / LPMC_CHUNK_PATHS;
+    if (chunk_end[i] > n_chunks || chunk_begin[i] > chunk_end[i])
+      return fail(err, LPMC_INVALID_ARGUMENT, "chunk range outside the run");
+    off[i + 1] = off[i] + 3 * (chunk_end[i] - chunk_begin[i]);
+  }
+  for (uint64_t i = 0; i < off[n_runs]; ++i) out[i] = lpmc_moments{0, 0.0, 0.0, 0.0, 0.0};
+  lpmc_status setup = LPMC_OK;
+  lpmc_error setup_err{};
+  for (uint64_t i = 0; i < n_runs; ++i) {
+    RunSpec s;
+    if (runs[i].n_paths == 0 || chunk_begin[i] == chunk_end[i]) {
+      s.device = o.device;  // nothing simulated on this rank
+    } else {
+      setup = build_spec(model, runs[i].level, &runs[i].prec, table, runs[i].kahan,
+                         runs[i].n_paths, seed, runs[i].path_base, &o, &s, &setup_err);
+      if (setup != LPMC_OK) break;
+      s.chunk_begin = chunk_begin[i];
+      s.chunk_end = chunk_end[i];
+    }
+    specs.push_back(std::move(s));
+  }
+  std::vector<std::vector<Moments>> parts;
+  lpmc_status st = run_many(specs, o.stream, &parts, err);
+  if (st != LPMC_OK) return st;
+  if (setup != LPMC_OK) {
+    if (err != nullptr) *err = setup_err;
+    return setup;
+  }
+  for (size_t i = 0; i < specs.size(); ++i)
+    for (size_t k = 0; k < parts[i].size() && off[i] + k < off[i + 1]; ++k)
+      out[off[i] + k] = to_abi(parts[i][k]);
+  return ok(err);
+}
+
 lpmc_status lpmc_run_two_way_paths(const lpmc_gbm* model, int32_t level,
                                    const lpmc_precision* prec, const lpmc_invcdf_table* table,
                                    int32_t kahan, uint64_t n_paths, uint64_t seed,

@@ -75,3 +75,30 @@ def sharded_run_coupled_paths(model, level, spec_low, approx, kahan, n_paths, se
         local = np.zeros((0, 3, 5))
     full = allgather_partials(np.asarray(local).reshape(-1, 3, 5), n_chunks, group, device)
     return fold_partials(full)
+
+
+def _many_partials(model, approx, seed, runs, ranges, **ext):
+    from .api import run_coupled_many_partials
+    return run_coupled_many_partials(model, approx, seed, runs, ranges, **ext)
+
+
+def sharded_run_coupled_many(model, approx, seed, runs, group=None, device: Optional[str] = None,
+                             partials_fn: Callable = _many_partials, **ext) -> list:
+    """run_coupled_many with every run sharded over the ranks: rank r runs its
+    contiguous chunk range of each run in ONE concurrent multi-run call
+    (lpmc_run_coupled_many_partials), then one all_gather per run and an
+    index-order fold.  Every rank returns the same (bitwise) list of
+    CoupledMoments, equal to run_coupled_many's on one device."""
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    runs = list(runs)
+    nck = [n_chunks_for(r[3]) for r in runs]
+    ranges = [shard_chunks(k, rank, world) for k in nck]
+    parts = partials_fn(model, approx, seed, runs, ranges, **ext)
+    out = []
+    for k, part in zip(nck, parts):
+        full = allgather_partials(np.asarray(part).reshape(-1, 3, 5), k, group, device)
+        out.append(fold_partials(full))
+    return out

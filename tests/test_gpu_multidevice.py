@@ -63,3 +63,32 @@ def test_sharded_failures_and_range_fallback(gpu):
     assert _state(gpu.run_coupled_paths(*args, devices=[0, 0])) == _state(gpu.run_coupled_paths(*args))
     with pytest.raises(gpu.InvalidArgument):
         gpu.run_coupled_paths(gpu.make_gbm(), 2, P.fp32(), tb, False, 100, 1, 0, devices=[0, 99])
+
+
+def test_many_partials_equal_level_partials(gpu):
+    """lpmc_run_coupled_many_partials (bench.py's e2e call for every N): each
+    run's chunk range equals lpmc_level_partials of that range bitwise, and
+    folding the ranges of all 'ranks' equals run_coupled_many."""
+    import numpy as np
+
+    from paper_2012_09739_b200.sharded import n_chunks_for, shard_chunks
+    model = gpu.make_gbm()
+    P = gpu.PrecisionSpec
+    tb = gpu.InvCdfApprox.parse("linear:16")
+    runs = [(l, P.fp16() if l % 2 else P.fp32(), False, 2 * 262144 + 1000 * l, l << 40)
+            for l in (0, 3, 7)]
+    ext = dict(payoff="call", strike=1.0)
+    whole = gpu.run_coupled_many(model, tb, 1, runs, **ext)
+    for world in (1, 2, 4):
+        shards = []
+        for rank in range(world):
+            ranges = [shard_chunks(n_chunks_for(r[3]), rank, world) for r in runs]
+            parts = gpu.run_coupled_many_partials(model, tb, 1, runs, ranges, **ext)
+            for (l, spec, k, n, base), (c0, c1), part in zip(runs, ranges, parts):
+                if c1 > c0:
+                    one = gpu.level_partials(model, l, spec, tb, k, n, 1, base, c0, c1, **ext)
+                    assert np.array_equal(part.view(np.uint64), one.view(np.uint64))
+            shards.append(parts)
+        for i, m in enumerate(whole):
+            full = np.concatenate([s[i] for s in shards], axis=0)
+            assert _state(gpu.fold_partials(full)) == _state(m)

@@ -23,6 +23,8 @@ def main():
     ap.add_argument("--legs", default="all")
     ap.add_argument("--n", type=int, default=1 << 22)
     ap.add_argument("--launches", type=int, default=2)
+    ap.add_argument("--payoff", default="terminal", choices=["terminal", "call"])
+    ap.add_argument("--base", type=int, default=None, help="path base (default level<<40 | kahan<<36)")
     ap.add_argument("--exact-z", default="fast", choices=["fast", "glibc"])
     ap.add_argument("--schedule", default="auto", choices=["auto", "fused", "warp_per_path"])
     ap.add_argument("--time", action="store_true",
@@ -31,8 +33,9 @@ def main():
     spec = L.PrecisionSpec.parse(a.prec)
     approx = None if a.approx == "exact" else L.InvCdfApprox.parse(a.approx)
     plan = L.LevelPlan(L.make_gbm(), a.level, spec, approx, bool(a.kahan), a.n, 1,
-                       (a.level << 40) | (a.kahan << 36), legs=a.legs, exact_z=a.exact_z,
-                       schedule=a.schedule)
+                       (a.level << 40) | (a.kahan << 36) if a.base is None else a.base,
+                       legs=a.legs, exact_z=a.exact_z, schedule=a.schedule, payoff=a.payoff,
+                       strike=1.0)
     for _ in range(a.launches):
         plan.launch()
         m = plan.collect()

@@ -54,7 +54,81 @@ WANT = [
     "smsp__thread_inst_executed_per_inst_executed.ratio", "dram__bytes_read.sum",
     "dram__bytes_write.sum", "sm__cycles_elapsed.avg.per_second",
     "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum",
+    "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum",
+    "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed",
+    "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active",
+    "sm__pipe_fp16_cycles_active.avg.pct_of_peak_sustained_active",
+    "sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active",
+    "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active",
+    "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active",
+    "sm__sass_thread_inst_executed_op_fadd_pred_on.sum",
+    "sm__sass_thread_inst_executed_op_fmul_pred_on.sum",
+    "sm__sass_thread_inst_executed_op_ffma_pred_on.sum",
+    "sm__sass_thread_inst_executed_op_hadd_pred_on.sum",
+    "sm__sass_thread_inst_executed_op_hmul_pred_on.sum",
+    "sm__sass_thread_inst_executed_op_hfma_pred_on.sum",
+    "sm__sass_thread_inst_executed_op_integer_pred_on.sum",
+    "launch__occupancy_limit_shared_mem", "launch__shared_mem_per_block_static",
 ]
+
+
+def raw_values(path: str) -> tuple[str, dict, dict]:
+    """(kernel name, metric -> float, metric -> unit) of the first kernel."""
+    raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True,
+                         text=True).stdout
+    rows = list(csv.reader(io.StringIO(raw)))
+    h, units, v = rows[0], rows[1], rows[2]
+    vals, us = {}, {}
+    for i, name in enumerate(h):
+        try:
+            vals[name] = float(v[i].replace(",", ""))
+            us[name] = units[i]
+        except ValueError:
+            pass
+    return v[h.index("Kernel Name")], vals, us
+
+
+def demands(path: str, path_steps: float, note: str) -> str:
+    """Per-fine-path-step demands of one profiled launch, the JSON bench.py
+    reads (profiles/r02_c4_l12_demands.json); tied to the kernel sources by
+    their hash."""
+    import json
+    import os
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    from paper_2012_09739_b200.build import kernel_source_hash
+    name, v, u = raw_values(path)
+    fp64 = sum(v.get(f"sm__sass_thread_inst_executed_op_{o}_pred_on.sum", 0.0)
+               for o in ("dadd", "dmul", "dfma"))
+    dur = v["gpu__time_duration.sum"] * {"ns": 1e-6, "us": 1e-3, "usecond": 1e-3,
+                                         "nsecond": 1e-6, "ms": 1.0, "msecond": 1.0}.get(
+        u["gpu__time_duration.sum"], 1.0)
+    out = {
+        "kernel": kernel_key(name), "note": note, "path_steps_per_launch": path_steps,
+        "ncu_duration_ms": dur,
+        "fp64_lane_ops_per_path_step": round(fp64 / path_steps, 3),
+        "warp_inst_per_path_step": round(v["smsp__inst_executed.sum"] / path_steps, 4),
+        "smem_wavefronts_per_path_step": round(
+            v.get("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", 0.0) / path_steps, 4),
+        "dram_bytes_per_launch": v.get("dram__bytes_read.sum", 0.0) + v.get("dram__bytes_write.sum", 0.0),
+        "registers_per_thread": v.get("launch__registers_per_thread"),
+        "co_limits": {
+            "issue_active_pct": v.get("smsp__issue_active.avg.pct_of_peak_sustained_active"),
+            "fp64_pipe_active_pct": v.get("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"),
+            "smem_wavefronts_pct_of_peak": v.get(
+                "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed"),
+            "fma_pipe_inst_pct": v.get("sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active"),
+            "alu_pipe_inst_pct": v.get("sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active"),
+            "xu_pipe_pct": v.get("sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active"),
+            "bank_conflicts": v.get("l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum"),
+        },
+        "definition": "ncu --set full of one launch: FP64 lane-ops = sm__sass_thread_inst_executed_"
+                      "op_{dadd,dmul,dfma}_pred_on.sum, warp-instructions = smsp__inst_executed.sum, "
+                      "shared-memory wavefronts = l1tex__data_pipe_lsu_wavefronts_mem_shared.sum, "
+                      "each / fine path-steps of the launch; DRAM = dram__bytes_read.sum + "
+                      "dram__bytes_write.sum",
+        "kernel_source_hash": kernel_source_hash(),
+    }
+    return json.dumps(out, indent=1)
 
 
 def full(path: str, path_steps: float | None) -> str:
@@ -120,5 +194,7 @@ def full(path: str, path_steps: float | None) -> str:
 if __name__ == "__main__":
     if sys.argv[1] == "launches":
         print(launches(sys.argv[2]))
+    elif sys.argv[1] == "demands":
+        print(demands(sys.argv[2], float(sys.argv[3]), sys.argv[4] if len(sys.argv) > 4 else ""))
     else:
         print(full(sys.argv[2], float(sys.argv[3]) if len(sys.argv) > 3 else None))
