@@ -12,6 +12,8 @@ import threading
 
 PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(PKG, "liblpmc_b200.so")
+if os.environ.get("LPMC_LIB"):  # A/B experiments only (build.py --variant=NAME)
+    LIB_PATH = os.path.abspath(os.environ["LPMC_LIB"])
 
 _u64 = C.c_uint64
 _i32 = C.c_int32

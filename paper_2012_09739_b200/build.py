@@ -65,7 +65,14 @@ def kernel_source_hash() -> str:
     return h.hexdigest()[:16]
 
 
-def build(force: bool = False, verbose_ptxas: bool = False) -> str:
+def build(force: bool = False, verbose_ptxas: bool = False, variant: str = "") -> str:
+    """variant (experiments only): build with LPMC_NVCC_EXTRA into
+    _build_<variant>/ and liblpmc_b200_<variant>.so, selected at load time by
+    LPMC_LIB=<that path> (A/B timing on one GPU box without rebuilding there)."""
+    global BUILD, LIB
+    if variant:
+        BUILD = os.path.join(PKG, f"_build_{variant}")
+        LIB = os.path.join(PKG, f"liblpmc_b200_{variant}.so")
     os.makedirs(BUILD, exist_ok=True)
     hdrs = [os.path.join(CSRC, h) for h in HEADERS]
     objs = []
@@ -99,4 +106,5 @@ def build(force: bool = False, verbose_ptxas: bool = False) -> str:
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose_ptxas="-v" in sys.argv)
+    var = next((a.split("=", 1)[1] for a in sys.argv if a.startswith("--variant=")), "")
+    build(force="--force" in sys.argv, verbose_ptxas="-v" in sys.argv, variant=var)

@@ -71,6 +71,13 @@ __device__ __forceinline__ void stage_math(double* s_math, int words = kMathWord
   for (int i = threadIdx.x; i < words; i += blockDim.x) s_math[i] = math::kMathTable[i];
 }
 
+// the fast mode's tables in the lane-private layout (math::LaneTab)
+constexpr int kLaneWords = math::kLaneWords;
+__device__ __forceinline__ void stage_lane(double* s_lane) {
+  for (int i = threadIdx.x; i < kLaneWords; i += blockDim.x)
+    s_lane[i] = math::kMathTable[math::lane_source(i)];
+}
+
 // ------------------------------------------- approximate inverse CDF -------
 // Shared-memory table.  Dyadic layout (K <= 32): one 6-double record per
 // interval {3 - 2^(j+3), 2^(j+3), c0, c1, c2, c3} (128-bit loads).  General
@@ -211,6 +218,37 @@ __device__ __forceinline__ bool nonfinite32(float x) {
   return (__float_as_uint(x) & 0x7f800000u) == 0x7f800000u;
 }
 
+// ------------------------------------------------- packed fp32 pairs ------
+// sm_100 executes two fp32 lanes per instruction (FFMA2).  Every packed op is
+// an fma.rn.f32x2 whose addend/multiplier constants come from the launch
+// parameters (LevelArgs::f2_neg0 / f2_neg1), never immediates: with known
+// constants ptxas fuses a multiply and a following add into one FFMA2 even
+// though each is written with .rn, which would change the rounding.
+// a * b + (-0) is the correctly rounded product (the sign of a zero product
+// is kept); c + (-1) x is the correctly rounded difference c - x.
+__device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ uint64_t pack2(float lo, float hi) {
+  uint64_t d;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(d) : "f"(lo), "f"(hi));
+  return d;
+}
+__device__ __forceinline__ float lo2(uint64_t v) {
+  float a, b;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
+  (void)b;
+  return a;
+}
+__device__ __forceinline__ float hi2(uint64_t v) {
+  float a, b;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
+  (void)a;
+  return b;
+}
+
 // ------------------------------------------------------ bar arithmetic -----
 // Policies: T (state type), NP (paths per thread), mul/add/sub in the target
 // precision, lift(z[NP]) = R(z) packed, get(x, p) -> double, bad(x) ->
@@ -240,6 +278,7 @@ struct ArithCarrier {  // m >= 52
   using Range = RangeNone;
   static constexpr int NP = 1;
   static constexpr bool kIeee = false;
+  static constexpr bool kPair = false;  // no packed fp32 pairs (see ArithF32)
   __device__ explicit ArithCarrier(const LevelArgs&) {}
   __device__ T c(double d, uint16_t) const { return d; }
   __device__ T zero() const { return 0.0; }
@@ -256,7 +295,20 @@ struct ArithF32 {  // m == 23, native
   using Range = RangeF32;
   static constexpr int NP = 1;
   static constexpr bool kIeee = false;
-  __device__ explicit ArithF32(const LevelArgs&) {}
+  // mul2: two independent products of one leg step in one FFMA2 (bitwise
+  // the two scalar products)
+#ifdef LPMC_NO_PAIR  // A/B only
+  static constexpr bool kPair = false;
+#else
+  static constexpr bool kPair = true;
+#endif
+  uint64_t n0, n1, p1;
+  __device__ explicit ArithF32(const LevelArgs& A)
+      : n0(A.f2_neg0), n1(A.f2_neg1), p1(A.f2_neg1 & 0x7fffffff7fffffffull) {}
+  __device__ uint64_t mul2(uint64_t a, uint64_t b) const { return ffma2(a, b, n0); }
+  __device__ uint64_t add2(uint64_t a, uint64_t b) const { return ffma2(a, p1, b); }
+  __device__ uint64_t sub2(uint64_t a, uint64_t b) const { return ffma2(b, n1, a); }
+  __device__ float one() const { return lo2(p1); }  // +1.0f the compiler cannot fold
   __device__ T c(double d, uint16_t) const { return static_cast<float>(d); }  // exact
   __device__ T zero() const { return 0.0f; }
   __device__ T mul(T a, T b) const { return __fmul_rn(a, b); }
@@ -277,7 +329,14 @@ struct ArithF32Round {  // m <= 10: fp32 op (correctly rounded), then RNE to m+1
   uint64_t half_m1_64, keep64;
   float split;     // 2^d + 1: Veltkamp's splitter
   double split64;  // 2^d64 + 1
-  __device__ explicit ArithF32Round(const LevelArgs& A) {
+#if defined(LPMC_F32R_INT) || defined(LPMC_NO_PAIR)
+  static constexpr bool kPair = false;
+#else
+  static constexpr bool kPair = true;  // mul2: packed product + packed Veltkamp split
+#endif
+  uint64_t n0, n1, p1, split2;
+  __device__ explicit ArithF32Round(const LevelArgs& A)
+      : n0(A.f2_neg0), n1(A.f2_neg1), p1(A.f2_neg1 & 0x7fffffff7fffffffull) {
     d = 23u - static_cast<uint32_t>(A.mantissa_bits);
     half_m1 = (1u << (d - 1)) - 1u;
     keep = ~((1u << d) - 1u);
@@ -286,6 +345,7 @@ struct ArithF32Round {  // m <= 10: fp32 op (correctly rounded), then RNE to m+1
     half_m1_64 = (1ull << (d64 - 1)) - 1ull;
     keep64 = ~((1ull << d64) - 1ull);
     split64 = static_cast<double>((1ull << d64) + 1ull);  // exact: d64 <= 51
+    split2 = pack2(split, split);
   }
   __device__ T c(double dd, uint16_t) const { return static_cast<float>(dd); }
   __device__ T zero() const { return 0.0f; }
@@ -306,6 +366,15 @@ struct ArithF32Round {  // m <= 10: fp32 op (correctly rounded), then RNE to m+1
   __device__ T mul(T a, T b) const { return rn(__fmul_rn(a, b)); }
   __device__ T add(T a, T b) const { return rn(__fadd_rn(a, b)); }
   __device__ T sub(T a, T b) const { return rn(__fsub_rn(a, b)); }
+  // rn of both halves: c = x s, c - (c - x) as packed FFMA2s (see ffma2)
+  __device__ uint64_t rn2(uint64_t x) const {
+    const uint64_t c = ffma2(x, split2, n0);
+    return ffma2(ffma2(x, n1, c), n1, c);
+  }
+  __device__ uint64_t mul2(uint64_t a, uint64_t b) const { return rn2(ffma2(a, b, n0)); }
+  __device__ uint64_t add2(uint64_t a, uint64_t b) const { return rn2(ffma2(a, p1, b)); }
+  __device__ uint64_t sub2(uint64_t a, uint64_t b) const { return rn2(ffma2(b, n1, a)); }
+  __device__ float one() const { return lo2(p1); }
   // R(z) from the full binary64 value: one rounding (softfloat.hpp:69)
   // (Veltkamp in binary64: Gaussians are 0 or normal and |z| < 40)
   __device__ T lift(const double (&z)[1]) const {
@@ -325,6 +394,7 @@ struct ArithF64Round {  // any m < 52: binary64 op, then integer RNE (exact emul
   using Range = RangeNone;
   static constexpr int NP = 1;
   static constexpr bool kIeee = false;
+  static constexpr bool kPair = false;
   uint32_t d;
   uint64_t half_m1, keep;
   __device__ explicit ArithF64Round(const LevelArgs& A) {
@@ -347,6 +417,7 @@ struct ArithHalf2 {  // native IEEE binary16, two paths per thread
   using Range = RangeNone;
   static constexpr int NP = 2;
   static constexpr bool kIeee = true;
+  static constexpr bool kPair = false;  // already two paths per half2 op
   __device__ explicit ArithHalf2(const LevelArgs&) {}
   __device__ T c(double, uint16_t bits) const {
     const __half h = __ushort_as_half(bits);

@@ -419,6 +419,10 @@ lpmc_status build_spec(const lpmc_gbm* model, int32_t level, const lpmc_precisio
   A.level = level;
   A.legs = static_cast<int32_t>(o.legs);
   A.exact_z = o.exact_z;
+  A.err_step_bits = err_step_bits_for(level);
+  if (n_paths > (1ull << (62 - A.err_step_bits)))  // failure key layout (lpmc_internal.h)
+    return fail(err, LPMC_INVALID_ARGUMENT,
+                "n_paths too large for the failure record: at most 2^(62 - max(22, level))");
   // per-level constants (sde.hpp:217-224)
   const double dtf = std::ldexp(model->horizon, -level);
   const double sdtf = std::sqrt(dtf);
@@ -717,9 +721,10 @@ cudaError_t enqueue_run(const RunSpec& s, Buffers& B, cudaStream_t st, Enqueued*
 // Map the device failure word to the reference's exception (first failing
 // path in path order, as the serial reference would throw).
 lpmc_status failure_from_key(const RunSpec& s, unsigned long long key, lpmc_error* err) {
-  const uint64_t local = key >> 24;
-  const int kind = static_cast<int>((key >> 22) & 3u);
-  const uint64_t step = key & ((1ull << 22) - 1);
+  const int bits = s.args.err_step_bits;
+  const uint64_t local = key >> (bits + 2);
+  const int kind = static_cast<int>((key >> bits) & 3u);
+  const uint64_t step = key & ((1ull << bits) - 1);
   const uint64_t path = s.args.path_base + local;
   if (kind == LPMC_FAIL_UNIFORM_IS_ONE)
     return fail(err, LPMC_DOMAIN_ERROR, "exact_inv_cdf requires u in (0, 1)", kind, path, step);
@@ -1609,9 +1614,10 @@ lpmc_status lpmc_step_error_probe(const lpmc_gbm* model, int32_t level,
       continue;
     }
     if (key != ~0ull) {
-      const uint64_t path = key >> 24;
-      const int kind = static_cast<int>((key >> 22) & 3u);
-      const uint64_t step = key & ((1ull << 22) - 1);
+      const int bits = s.args.err_step_bits;
+      const uint64_t path = key >> (bits + 2);
+      const int kind = static_cast<int>((key >> bits) & 3u);
+      const uint64_t step = key & ((1ull << bits) - 1);
       if (kind == LPMC_FAIL_UNIFORM_IS_ONE)
         return fail(err, LPMC_DOMAIN_ERROR,
                     table != nullptr ? "approx_inv_cdf requires u in (0, 1)"
@@ -1650,6 +1656,8 @@ lpmc_status lpmc_simulate_paths(const lpmc_gbm* model, int32_t level, const lpmc
   if (e != cudaSuccess) return cuda_fail(err, e, "cudaSetDevice");
   std::lock_guard<std::mutex> lock(ctx->mu);
   cudaStream_t stream = (opts && opts->stream) ? static_cast<cudaStream_t>(opts->stream) : ctx->stream;
+  if (z_out != nullptr && (level > 32 || (n_paths << level) > (1ull << 32)))
+    return fail(err, LPMC_INVALID_ARGUMENT, "Gaussian dump limited to 2^32 draws");
   const uint64_t zcount = z_out ? n_paths << level : 0;
   DevBuf<double> d_out, d_z;
   Buffers& B = ctx->scratch;
@@ -1658,16 +1666,19 @@ lpmc_status lpmc_simulate_paths(const lpmc_gbm* model, int32_t level, const lpmc
     if (zcount && (e = d_z.ensure(zcount)) != cudaSuccess) break;
     if ((e = B.err_key.ensure(1)) != cudaSuccess) break;
     if ((e = B.range_flag.ensure(1)) != cudaSuccess) break;
-    cudaMemsetAsync(B.err_key.ptr, 0xff, sizeof(unsigned long long), stream);
-    cudaMemsetAsync(B.range_flag.ptr, 0, sizeof(unsigned int), stream);
+    if ((e = cudaMemsetAsync(B.err_key.ptr, 0xff, sizeof(unsigned long long), stream)) != cudaSuccess)
+      break;
+    if ((e = cudaMemsetAsync(B.range_flag.ptr, 0, sizeof(unsigned int), stream)) != cudaSuccess) break;
     LevelArgs A = s.args;
     A.err_key = B.err_key.ptr;
     A.range_flag = B.range_flag.ptr;
     A.table = nullptr;
     if (s.has_table) {
       if ((e = B.table.ensure(s.table.rows.size())) != cudaSuccess) break;
-      cudaMemcpyAsync(B.table.ptr, s.table.rows.data(), s.table.rows.size() * sizeof(double),
-                      cudaMemcpyHostToDevice, stream);
+      if ((e = cudaMemcpyAsync(B.table.ptr, s.table.rows.data(),
+                               s.table.rows.size() * sizeof(double), cudaMemcpyHostToDevice,
+                               stream)) != cudaSuccess)
+        break;
       A.table = B.table.ptr;
     }
     A.batch0 = 0;
@@ -1688,11 +1699,16 @@ lpmc_status lpmc_simulate_paths(const lpmc_gbm* model, int32_t level, const lpmc
     }
     unsigned long long key = ~0ull;
     unsigned int range = 0;
-    cudaMemcpyAsync(&key, B.err_key.ptr, sizeof key, cudaMemcpyDeviceToHost, stream);
-    cudaMemcpyAsync(&range, B.range_flag.ptr, sizeof range, cudaMemcpyDeviceToHost, stream);
-    cudaMemcpyAsync(out4, d_out.ptr, 4 * n_paths * sizeof(double), cudaMemcpyDeviceToHost, stream);
-    if (zcount) cudaMemcpyAsync(z_out, d_z.ptr, zcount * sizeof(double), cudaMemcpyDeviceToHost, stream);
-    if ((e = cudaStreamSynchronize(stream)) != cudaSuccess) break;
+    e = cudaMemcpyAsync(&key, B.err_key.ptr, sizeof key, cudaMemcpyDeviceToHost, stream);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(&range, B.range_flag.ptr, sizeof range, cudaMemcpyDeviceToHost, stream);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(out4, d_out.ptr, 4 * n_paths * sizeof(double), cudaMemcpyDeviceToHost,
+                          stream);
+    if (e == cudaSuccess && zcount)
+      e = cudaMemcpyAsync(z_out, d_z.ptr, zcount * sizeof(double), cudaMemcpyDeviceToHost, stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
+    if (e != cudaSuccess) break;
     if (range != 0 && (s.arith == BarArith::kF32 || s.arith == BarArith::kF32Round)) {
       s.arith = BarArith::kF64Round;
       continue;
@@ -1733,10 +1749,11 @@ lpmc_status lpmc_device_math(int32_t op, const double* u, uint64_t n,
   DevBuf<double>& dtab = ctx->scratch.table;
   if ((e = du.ensure(n)) == cudaSuccess && (e = dout.ensure(n)) == cudaSuccess &&
       (table == nullptr || (e = dtab.ensure(ht.rows.size())) == cudaSuccess)) {
-    cudaMemcpyAsync(du.ptr, u, n * sizeof(double), cudaMemcpyHostToDevice, stream);
-    if (table != nullptr)
-      cudaMemcpyAsync(dtab.ptr, ht.rows.data(), ht.rows.size() * sizeof(double),
-                      cudaMemcpyHostToDevice, stream);
+    e = cudaMemcpyAsync(du.ptr, u, n * sizeof(double), cudaMemcpyHostToDevice, stream);
+    if (e == cudaSuccess && table != nullptr)
+      e = cudaMemcpyAsync(dtab.ptr, ht.rows.data(), ht.rows.size() * sizeof(double),
+                          cudaMemcpyHostToDevice, stream);
+    if (e != cudaSuccess) return cuda_fail(err, e, "inverse-CDF upload");
     LaunchResult r = launch_inv_cdf(du.ptr, n, table ? dtab.ptr : nullptr, ht.K, ht.degree,
                                     ht.dyadic, ht.stride, ht.simple, ht.tail, op, dout.ptr, stream);
     t_launches += r.kernels;
@@ -1782,11 +1799,13 @@ lpmc_status lpmc_density_histogram(const lpmc_invcdf_table* table, uint64_t seed
   if ((e = dbins.ensure(static_cast<size_t>(n_bins))) == cudaSuccess &&
       (e = dtop.ensure(1)) == cudaSuccess &&
       (table == nullptr || (e = dtab.ensure(ht.rows.size())) == cudaSuccess)) {
-    cudaMemsetAsync(dbins.ptr, 0, static_cast<size_t>(n_bins) * sizeof(unsigned long long), stream);
-    cudaMemsetAsync(dtop.ptr, 0xff, sizeof(unsigned long long), stream);
-    if (table != nullptr)
-      cudaMemcpyAsync(dtab.ptr, ht.rows.data(), ht.rows.size() * sizeof(double),
-                      cudaMemcpyHostToDevice, stream);
+    e = cudaMemsetAsync(dbins.ptr, 0, static_cast<size_t>(n_bins) * sizeof(unsigned long long),
+                        stream);
+    if (e == cudaSuccess) e = cudaMemsetAsync(dtop.ptr, 0xff, sizeof(unsigned long long), stream);
+    if (e == cudaSuccess && table != nullptr)
+      e = cudaMemcpyAsync(dtab.ptr, ht.rows.data(), ht.rows.size() * sizeof(double),
+                          cudaMemcpyHostToDevice, stream);
+    if (e != cudaSuccess) return cuda_fail(err, e, "density upload");
     LaunchResult r = launch_density(key, n_samples, table ? dtab.ptr : nullptr,
                                     static_cast<int>(ht.rows.size()), ht.K, ht.degree, ht.dyadic,
                                     ht.stride, ht.simple, ht.tail, z_max, bin_width, n_bins,

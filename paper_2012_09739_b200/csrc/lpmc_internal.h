@@ -28,6 +28,12 @@ enum class BarArith : int {
 constexpr int kTableRows = 7;
 constexpr int kDyadicRecord = 6;
 
+#ifdef __CUDACC__
+#define LPMC_KEY_HD __host__ __device__
+#else
+#define LPMC_KEY_HD
+#endif
+
 struct LevelArgs {
   uint64_t seed_key;   // mix64(seed + 0x9e37...) (uniform.hpp:23), hoisted per launch
   uint64_t path_base;  // global path index of local path 0
@@ -58,12 +64,31 @@ struct LevelArgs {
   double* path_diff;             // sequential mode: slice paths x 2 (d_hat, d_bar)
   double* path_out;              // dump: n x 4
   double* z_out;                 // dump: n x 2^level
-  unsigned long long* err_key;   // atomicMin: (local path << 24) | (kind << 22) | step
+  unsigned long long* err_key;   // atomicMin: err_key_of(local path, kind, step, err_step_bits)
   unsigned int* range_flag;      // native bar legs left the guarded exponent range
   // exact Gaussians: LPMC_EXACT_Z_FAST / _GLIBC (last: the fields above keep
   // the offsets the kernels' 128-bit uniform constant loads were tuned for)
   int32_t exact_z;
+  // packed-fp32 operands (-0, -0) and (-1, -1) as f32x2 bit patterns, passed
+  // as parameters so that the kernels cannot see them as constants: ptxas
+  // folds an f32x2 multiply and add with known constant operands into one
+  // fused FFMA2, which would change the rounding (dev::ffma2).
+  uint64_t f2_neg0 = 0x8000000080000000ull;
+  uint64_t f2_neg1 = 0xbf800000bf800000ull;
+  // bits of the step field of the failure key (err_step_bits_for(level))
+  int32_t err_step_bits = 22;
 };
+
+// Failure key: the path in the high bits (atomicMin finds the lowest failing
+// path, the reference's serial order), then the failure kind (2 bits), then
+// the step.  The step field has max(22, level) bits, so every step of a
+// path fits; the host rejects runs whose path indices would not fit the rest
+// (n_paths >= 2^(62 - bits): n_paths 2^level >= 2^62 fine steps).
+constexpr int err_step_bits_for(int level) { return level > 22 ? level : 22; }
+inline LPMC_KEY_HD unsigned long long err_key_of(uint64_t path, uint32_t kind, uint64_t step,
+                                                 int bits) {
+  return (path << (bits + 2)) | (static_cast<uint64_t>(kind) << bits) | step;
+}
 
 struct LaunchResult {
   int cuda_error;  // cudaError_t

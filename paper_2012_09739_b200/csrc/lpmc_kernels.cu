@@ -102,7 +102,7 @@ __global__ void inv_cdf_kernel(const double* __restrict__ u, uint64_t n,
   double r = 0.0;
   if (op == 0) {
     double uu[1] = {x}, zz[1];
-    math::phi_inv_multi<1>(uu, zz, s_math);
+    math::phi_inv_multi<1>(uu, zz, math::FlatTab{s_math});
     r = zz[0];
   } else if (op == 1) {
     const TableView t{table, stride, K, degree, dyadic, simple, tail};
@@ -161,7 +161,7 @@ __global__ void density_kernel(uint64_t key, uint64_t n, const double* __restric
       z = zz[0];
     } else {
       double uu[1] = {u}, zz[1];
-      math::phi_inv_multi<1>(uu, zz, s_math);
+      math::phi_inv_multi<1>(uu, zz, math::FlatTab{s_math});
       z = zz[0];
     }
     if (in) {

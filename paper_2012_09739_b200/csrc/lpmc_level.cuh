@@ -90,6 +90,20 @@ __device__ __forceinline__ void draw_uniforms(uint64_t (&kc)[NP], Uniforms<H * N
 // the next batch are drawn between the Acklam stage and the Newton stage, so
 // the integer RNG interleaves with FP64 work instead of forming its own
 // phase (software pipelining across batches).
+// The fast mode's staged tables: the lane-private layout (math::LaneTab);
+// -DLPMC_FLAT_TABLES restores the flat layout (A/B only; same values).
+#ifdef LPMC_FLAT_TABLES
+using FastTab = math::FlatTab;
+constexpr int kFastWords = kFastMathWords;
+__device__ __forceinline__ void stage_fast(double* s) { stage_math(s, kFastMathWords); }
+__device__ __forceinline__ FastTab fast_tab(const double* s) { return FastTab{s}; }
+#else
+using FastTab = math::LaneTab;
+constexpr int kFastWords = kLaneWords;
+__device__ __forceinline__ void stage_fast(double* s) { stage_lane(s); }
+__device__ __forceinline__ FastTab fast_tab(const double* s) { return math::lane_tab(s); }
+#endif
+
 // Exact-Gaussian mode of a level instance (values of LPMC_EXACT_Z_*).
 enum : int { kZFast = 0, kZGlibc = 1 };
 
@@ -133,15 +147,16 @@ __device__ __forceinline__ void gen_draws(const LevelArgs& A, const TableView& t
       v[d] = ng ? 1.0 - u[d] : u[d];  // exact (gaussian.hpp:63)
       neg |= (ng ? 1u : 0u) << d;
     }
+    const FastTab lt = fast_tab(s_math);  // staged by stage_fast
 #ifndef LPMC_MID_LATE  // the previous batch's legs run beside the fp32 initial guesses
     mid();
     math::phi_inv_stage1<D>(v, x0);
     if constexpr (PREFETCH) draw_uniforms<NP, H, CHECKED>(kc, next);
-    math::phi_inv_stage2<D, CHECKED>(v, x0, neg, cur.half, zz, s_math);
+    math::phi_inv_stage2<D, CHECKED>(v, x0, neg, cur.half, zz, lt);
 #else
     math::phi_inv_stage1<D>(v, x0);
     if constexpr (PREFETCH) draw_uniforms<NP, H, CHECKED>(kc, next);
-    math::phi_inv_stage2<D, CHECKED>(v, x0, neg, cur.half, zz, s_math, mid);
+    math::phi_inv_stage2<D, CHECKED>(v, x0, neg, cur.half, zz, lt, mid);
 #endif
   } else {
     if constexpr (PREFETCH) draw_uniforms<NP, H, CHECKED>(kc, next);
@@ -200,9 +215,25 @@ __device__ __forceinline__ void step_bar(const Arith& ar, typename Arith::Range&
                                          uint64_t (&fk)[Arith::NP], uint64_t n, uint32_t stage) {
   using T = typename Arith::T;
   const T xp = x;
-  const T drift = ar.mul(ar.mul(mu_l, xp), dt_l);
-  const T diff = fine ? ar.mul(ar.mul(ar.mul(sg_l, xp), sdt_l), zb_or_dw)
-                      : ar.mul(ar.mul(sg_l, xp), zb_or_dw);
+  T drift, diff;
+  if constexpr (Arith::kPair) {
+    // the same products pairwise: (mu x, sigma x), then (. dt, . sqrt_dt)
+    // (fine) or (. 2dt, . dW) (coarse); bitwise the scalar form below
+    const uint64_t ab = ar.mul2(pack2(mu_l, sg_l), pack2(xp, xp));
+    if (fine) {
+      const uint64_t cd = ar.mul2(ab, pack2(dt_l, sdt_l));
+      drift = lo2(cd);
+      diff = ar.mul(hi2(cd), zb_or_dw);
+    } else {
+      const uint64_t cd = ar.mul2(ab, pack2(dt_l, zb_or_dw));
+      drift = lo2(cd);
+      diff = hi2(cd);
+    }
+  } else {
+    drift = ar.mul(ar.mul(mu_l, xp), dt_l);
+    diff = fine ? ar.mul(ar.mul(ar.mul(sg_l, xp), sdt_l), zb_or_dw)
+                : ar.mul(ar.mul(sg_l, xp), zb_or_dw);
+  }
   const T inc = ar.add(drift, diff);
   if constexpr (KAHAN) {  // kahan_accumulate (sde.hpp:85-92)
     const T y = ar.sub(inc, cmp);
@@ -218,6 +249,46 @@ __device__ __forceinline__ void step_bar(const Arith& ar, typename Arith::Range&
 #pragma unroll
     for (int p = 0; p < Arith::NP; ++p) note_fail(fk[p], (m >> p) & 1u, n, stage);
   }
+}
+
+// One coarse step of both bar legs with packed fp32 pairs (Arith::kPair):
+// fine step n (zb0) and the coarse step (dW = sqrt_dt zb0 + sqrt_dt zb1) as
+// (fine, coarse) pairs -- the two legs are independent, so evaluating them
+// side by side changes no value -- then fine step n + 1 (zb1) alone.  Every
+// pair operation is the reference's operation on each half (sde.hpp:60-116):
+// fine diff (b sqrt_dt) z, coarse diff b dW, the coarse half multiplied by
+// an exact 1 where the fine half takes its z.
+template <class Arith, bool KAHAN>
+__device__ __forceinline__ void step_bar_joint(const Arith& ar, typename Arith::Range& range,
+                                               float& xf, float& xc, float& cf, float& cc,
+                                               float mu_l, float sg_l, float dtf_l, float sdt_l,
+                                               float dtc_l, float zb0, float zb1,
+                                               uint64_t (&fk)[1], uint64_t n) {
+  const uint64_t p = ar.mul2(pack2(zb0, zb1), pack2(sdt_l, sdt_l));
+  const float dw = ar.add(lo2(p), hi2(p));  // sde.hpp:261-264
+  const uint64_t X = pack2(xf, xc);
+  const uint64_t a = ar.mul2(pack2(mu_l, mu_l), X);
+  const uint64_t b = ar.mul2(pack2(sg_l, sg_l), X);
+  const uint64_t drift = ar.mul2(a, pack2(dtf_l, dtc_l));
+  const uint64_t e = ar.mul2(b, pack2(sdt_l, dw));
+  const uint64_t diff = ar.mul2(e, pack2(zb0, ar.one()));
+  const uint64_t inc = ar.add2(drift, diff);
+  uint64_t Xn;
+  if constexpr (KAHAN) {  // kahan_accumulate (sde.hpp:85-92) on both legs
+    const uint64_t y = ar.sub2(inc, pack2(cf, cc));
+    Xn = ar.add2(X, y);
+    const uint64_t c = ar.sub2(ar.sub2(Xn, X), y);
+    cf = lo2(c);
+    cc = hi2(c);
+  } else {
+    Xn = ar.add2(X, inc);
+  }
+  xf = lo2(Xn);
+  xc = hi2(Xn);
+  range.track(xf);
+  range.track(xc);
+  step_bar<Arith, KAHAN, false>(ar, range, xf, cf, mu_l, sg_l, dtf_l, sdt_l, zb1, true, fk, n + 1,
+                                kStageBarFine);
 }
 
 template <class Arith, bool KAHAN, int LEGS, int TAB, bool CHECKED, bool DUMP, int ZM>
@@ -254,6 +325,7 @@ __device__ __forceinline__ void simulate(const LevelArgs& A, const TableView& ta
   T xbc = xbf;
   T cmpf = ar.zero(), cmpc = ar.zero();
 
+  constexpr bool kJoint = Arith::kPair && kBar && !kFineOnly && !CHECKED;
   auto hat_fine = [&](const double (&z)[NP], uint64_t n) {
     step_hat<NP, CHECKED>(A, xhf, A.dtf, z, true, fk, n, kStageHatFine);
   };
@@ -270,10 +342,38 @@ __device__ __forceinline__ void simulate(const LevelArgs& A, const TableView& ta
         dw[p] = __dadd_rn(__dmul_rn(A.sdtf, z0[p]), __dmul_rn(A.sdtf, z1[p]));
       step_hat<NP, CHECKED>(A, xhc, A.dtc, dw, false, fk, n, kStageHatCoarse);
     }
-    if constexpr (kBar && !kFineOnly) {
-      const T dw = ar.add(ar.mul(sdtf_l, zb0), ar.mul(sdtf_l, zb1));
+    if constexpr (kBar && !kFineOnly && !kJoint) {
+      T dw;
+      if constexpr (Arith::kPair) {
+        const uint64_t p = ar.mul2(pack2(zb0, zb1), pack2(sdtf_l, sdtf_l));
+        dw = ar.add(lo2(p), hi2(p));
+      } else {
+        dw = ar.add(ar.mul(sdtf_l, zb0), ar.mul(sdtf_l, zb1));
+      }
       step_bar<Arith, KAHAN, CHECKED>(ar, range, xbc, cmpc, mu_l, sg_l, dtc_l, sdtf_l, dw, false,
                                       fk, n, kStageBarCoarse);
+    }
+  };
+
+  // all legs of one coarse step (fine n, fine n + 1, coarse) in the
+  // reference's order; the unchecked instances with packed fp32 pairs step
+  // the two bar legs side by side (step_bar_joint; the same values)
+  auto coarse_step = [&](const double (&z0)[NP], const double (&z1)[NP], T zb0, T zb1,
+                         uint64_t n) {
+    if constexpr (kJoint) {
+      if constexpr (kHat) {
+        hat_fine(z0, n);
+        hat_fine(z1, n + 1);
+        coarse(z0, z1, zb0, zb1, n + 1);  // the hat leg only (kJoint: bar below)
+      }
+      step_bar_joint<Arith, KAHAN>(ar, range, xbf, xbc, cmpf, cmpc, mu_l, sg_l, dtf_l, sdtf_l,
+                                   dtc_l, zb0, zb1, fk, n);
+    } else {
+      if constexpr (kHat) hat_fine(z0, n);
+      if constexpr (kBar) bar_fine(zb0, n);
+      if constexpr (kHat) hat_fine(z1, n + 1);
+      if constexpr (kBar) bar_fine(zb1, n + 1);
+      coarse(z0, z1, zb0, zb1, n + 1);
     }
   };
 
@@ -333,11 +433,7 @@ __device__ __forceinline__ void simulate(const LevelArgs& A, const TableView& ta
 #pragma unroll
         for (int g = 0; g < G; ++g) {
           const uint64_t n = 2 * (m0 + g);
-          if constexpr (kHat) hat_fine(zl[2 * g], n);
-          if constexpr (kBar) bar_fine(zbl[2 * g], n);
-          if constexpr (kHat) hat_fine(zl[2 * g + 1], n + 1);
-          if constexpr (kBar) bar_fine(zbl[2 * g + 1], n + 1);
-          coarse(zl[2 * g], zl[2 * g + 1], zbl[2 * g], zbl[2 * g + 1], n + 1);
+          coarse_step(zl[2 * g], zl[2 * g + 1], zbl[2 * g], zbl[2 * g + 1], n);
         }
       };
       for (uint64_t m = G; m < halves; m += G) {
@@ -367,11 +463,7 @@ __device__ __forceinline__ void simulate(const LevelArgs& A, const TableView& ta
 #pragma unroll
         for (int g = 0; g < G; ++g) {
           const uint64_t n = 2 * (m + g);
-          if constexpr (kHat) hat_fine(z[2 * g], n);
-          if constexpr (kBar) bar_fine(zb[2 * g], n);
-          if constexpr (kHat) hat_fine(z[2 * g + 1], n + 1);
-          if constexpr (kBar) bar_fine(zb[2 * g + 1], n + 1);
-          coarse(z[2 * g], z[2 * g + 1], zb[2 * g], zb[2 * g + 1], n + 1);
+          coarse_step(z[2 * g], z[2 * g + 1], zb[2 * g], zb[2 * g + 1], n);
         }
       }
       }
@@ -383,11 +475,7 @@ __device__ __forceinline__ void simulate(const LevelArgs& A, const TableView& ta
         draw_uniforms<NP, 2, CHECKED>(kc, cur);
         gen_draws<Arith, TAB, kNeedExact, kBar, CHECKED, DUMP, 2, false, ZM>(
             A, tab, s_math, ar, kc, u1, fk, local, valid, 2 * m, cur, unused, z, zb);
-        if constexpr (kHat) hat_fine(z[0], 2 * m);
-        if constexpr (kBar) bar_fine(zb[0], 2 * m);
-        if constexpr (kHat) hat_fine(z[1], 2 * m + 1);
-        if constexpr (kBar) bar_fine(zb[1], 2 * m + 1);
-        coarse(z[0], z[1], zb[0], zb[1], 2 * m + 1);
+        coarse_step(z[0], z[1], zb[0], zb[1], 2 * m);
       }
     }
   }
@@ -449,9 +537,16 @@ __global__ void __launch_bounds__(kBatch / Arith::NP, level_min_ctas<LEGS, TAB, 
   constexpr bool kNeedExact = kHat || TAB == kTabNone;
 
   extern __shared__ __align__(16) double s_table[];
-  constexpr int kStaged = ZM == kZGlibc ? kMathWords : kFastMathWords;
+  // glibc mode: the flat tables incl. glibc's; fast mode: the lane layout
+  constexpr int kStaged = ZM == kZGlibc ? kMathWords : kFastWords;
   __shared__ __align__(16) double s_math[kNeedExact ? kStaged : 2];
-  if constexpr (kNeedExact) stage_math(s_math, kStaged);
+  if constexpr (kNeedExact) {
+    if constexpr (ZM == kZGlibc) {
+      stage_math(s_math, kStaged);
+    } else {
+      stage_fast(s_math);
+    }
+  }
   TableView tab{};
   if constexpr (TAB != kTabNone) {
     for (int i = threadIdx.x; i < A.table_words; i += blockDim.x) s_table[i] = A.table[i];
@@ -489,9 +584,7 @@ __global__ void __launch_bounds__(kBatch / Arith::NP, level_min_ctas<LEGS, TAB, 
       const uint32_t stage = static_cast<uint32_t>(R.fk[p] & 7u);
       uint32_t kind = stage == kStageDraw ? kKindU1 : kKindNonFinite;
       if (Arith::kIeee && (stage == kStageBarFine || stage == kStageBarCoarse)) kind = kKindState;
-      const uint64_t step = n < (1ull << 22) ? n : (1ull << 22) - 1;
-      atomicMin(A.err_key, static_cast<unsigned long long>(
-                               (local[p] << 24) | (static_cast<uint64_t>(kind) << 22) | step));
+      atomicMin(A.err_key, err_key_of(local[p], kind, n, A.err_step_bits));
     }
   }
   if (R.range_bad) atomicOr(A.range_flag, 1u);
@@ -559,9 +652,16 @@ __global__ void __launch_bounds__(kWppThreads) wpp_kernel(const __grid_constant_
   constexpr bool kNeedExact = kHat || TAB == kTabNone;
 
   extern __shared__ __align__(16) double s_table[];
-  constexpr int kStaged = ZM == kZGlibc ? kMathWords : kFastMathWords;
+  // glibc mode: the flat tables incl. glibc's; fast mode: the lane layout
+  constexpr int kStaged = ZM == kZGlibc ? kMathWords : kFastWords;
   __shared__ __align__(16) double s_math[kNeedExact ? kStaged : 2];
-  if constexpr (kNeedExact) stage_math(s_math, kStaged);
+  if constexpr (kNeedExact) {
+    if constexpr (ZM == kZGlibc) {
+      stage_math(s_math, kStaged);
+    } else {
+      stage_fast(s_math);
+    }
+  }
   TableView tab{};
   if constexpr (TAB != kTabNone) {
     for (int i = threadIdx.x; i < A.table_words; i += blockDim.x) s_table[i] = A.table[i];
@@ -601,7 +701,7 @@ __global__ void __launch_bounds__(kWppThreads) wpp_kernel(const __grid_constant_
       if constexpr (ZM == kZGlibc) {
         glibc::inv_cdf_multi<1>(u, z, s_math);
       } else {
-        math::phi_inv_multi<1>(u, z, s_math);
+        math::phi_inv_multi<1>(u, z, fast_tab(s_math));
       }
     }
     T zb = ar.zero();
@@ -658,9 +758,7 @@ __global__ void __launch_bounds__(kWppThreads) wpp_kernel(const __grid_constant_
       const uint64_t n = R.fk[0] >> 3;
       const uint32_t stage = static_cast<uint32_t>(R.fk[0] & 7u);
       const uint32_t kind = stage == kStageDraw ? kKindU1 : kKindNonFinite;
-      const uint64_t step = n < (1ull << 22) ? n : (1ull << 22) - 1;
-      atomicMin(A.err_key, static_cast<unsigned long long>(
-                               (local << 24) | (static_cast<uint64_t>(kind) << 22) | step));
+      atomicMin(A.err_key, err_key_of(local, kind, n, A.err_step_bits));
     }
   }
   if (lane != 0) return;

@@ -22,8 +22,9 @@
 //    hi + lo (tools/fit_math.py).  1/pdf is sqrt(2 pi) 2^-k / p(r): the same
 //    exponential, no second exp, no division.  Table indices come from the
 //    low words of shifted FMAs (no F2I/I2F conversions).
-//  * t > 6.5 (u < 1e-20; never drawn by the sampler, whose u >= 2^-54) takes
-//    a libdevice slow path.
+//  * t >= 3 (|x0| > 4.24, u < 1.1e-5: 2.2e-5 of the draws) takes a
+//    libdevice slow path out of line; the records for t < 3 are staged in
+//    a conflict-free lane-private layout (LaneTab below).
 //  * -DLPMC_X0_ACKLAM restores Acklam's binary64 x0 + Newton (A/B only,
 //    tools/gpu_ab_x0.sh).
 //
@@ -171,7 +172,7 @@ static_assert(1 << kExpShift == kExpN, "exp table size must be 8, 16, 32 or 64")
 constexpr int kGlibcOff = kErfcxWords + kExpWords;  // glibc exp and log tables (lpmc_glibc.cuh)
 constexpr int kGlibcWords = 512;
 constexpr int kMathTableWords = kGlibcOff + kGlibcWords;  // one shared-memory block
-constexpr double kFastTMax = 6.5;  // the erfcx intervals cover [0, 6.5)
+constexpr double kFastTMax = 6.5;  // the erfcx intervals cover [0, 6.5) (host core)
 
 // erfcx records, the 2^(j/64) hi/lo pairs, the glibc exp and log tables (host copy)
 static const double kMathTableHost[kMathTableWords] = {LPMC_ERFCX_COEF_LIST, LPMC_EXP_TAB_LIST,
@@ -208,6 +209,57 @@ LPMC_HD D2 load2(const double* p) {
 #endif
 }
 
+// Table layouts of the erfcx records and the 2^(j/64) pairs.
+//  * FlatTab: the records one after another (host, the erfc-core diagnostic
+//    and the small kernels: inverse-CDF diagnostics, step-error probe,
+//    density histogram).
+//  * LaneTab (device, the level and warp-per-path kernels): eight
+//    lane-private copies, transposed so that quad q of record j of copy c
+//    sits at 16-byte index (j Q + q) 8 + c (Q quads per record) and every
+//    lane reads copy c = lane % 8.  The eight lanes of each quarter-warp
+//    phase of a 128-bit shared load then hit eight different bank quads
+//    whatever records they gather: conflict-free by construction, with no
+//    extra instruction (the copy offset is hoisted into the per-thread base
+//    pointer; the record stride and the quad offsets are immediates).  Only
+//    the records for t < kDevTMax = 3 are staged (99.998 % of the sampler's
+//    draws); a draw with t >= 3 takes the out-of-line libdevice path that
+//    already served t >= 6.5 (newton_fast's `slow`).  kDevTMax applies to
+//    both layouts on the device, so every kernel computes the same Z.
+struct FlatTab {
+  const double* t;
+  static constexpr int kRec = kErfcxRow;  // doubles between records
+  static constexpr int kStep = 1;         // in-record offset multiplier
+  static constexpr int kExpStride = 2;    // doubles between exp entries
+  static constexpr int kNRec = kErfcxN;
+  LPMC_HD const double* erfcx() const { return t; }
+  LPMC_HD const double* expt() const { return t + kErfcxWords; }
+};
+
+constexpr int kLaneCopies = 8;
+constexpr double kDevTMax = 3.0;  // device fast path: erfcx records for t < 3
+constexpr int kHotRec = static_cast<int>(kDevTMax * LPMC_ERFCX_PER_UNIT);
+static_assert(kErfcxRow % 2 == 0 && kHotRec <= kErfcxN, "lane layout needs whole quads");
+constexpr int kLaneErfcxWords = kHotRec * kErfcxRow * kLaneCopies;
+constexpr int kLaneWords = kLaneErfcxWords + kExpWords * kLaneCopies;
+
+struct LaneTab {
+  const double* e;  // copy c of the erfcx records (base + 2c)
+  const double* x;  // copy c of the exp pairs
+  static constexpr int kRec = kErfcxRow * kLaneCopies;
+  static constexpr int kStep = kLaneCopies;
+  static constexpr int kExpStride = 2 * kLaneCopies;
+  static constexpr int kNRec = kHotRec;
+  LPMC_HD const double* erfcx() const { return e; }
+  LPMC_HD const double* expt() const { return x; }
+};
+
+// source word of lane-layout word i (staging; host tests use it too)
+LPMC_HD int lane_source(int i) {
+  const int half = i & 1, quad = i >> 4;  // 16 doubles = 8 copies of one quad
+  if (i < kLaneErfcxWords) return 2 * quad + half;
+  return kErfcxWords + 2 * ((i - kLaneErfcxWords) >> 4) + half;
+}
+
 // exp(-(th + tl)) = 2^k p, p in [2^-1/2, 2^1/2], th in [0, 700]:
 // kf = round(-64 th log2 e) = 64 k + j, r = -th - kf ln2/64 (exact head),
 // p = 2^(j/64) (1 + r P(r)) with the table value as hi + lo.
@@ -216,7 +268,8 @@ struct ExpSplit {
   int k;
 };
 
-LPMC_HD ExpSplit exp_neg(double th, double tl, const double* tab) {
+template <class V>
+LPMC_HD ExpSplit exp_neg(double th, double tl, const V& tab) {
   const double kShift = 6755399441055744.0;  // 1.5 * 2^52 (an encodable immediate)
   const double ks = fmad(-th, LPMC_K(kLog2eN), kShift);
   const double kd = ks - kShift;
@@ -230,30 +283,32 @@ LPMC_HD ExpSplit exp_neg(double th, double tl, const double* tab) {
 #endif
   for (int i = LPMC_EXPM1_DEG - 1; i >= 0; --i) q = fmad(q, r, LPMC_K(kOffExpm1 + i));
   q = q * r;  // expm1(r)
-  const D2 t2 = load2(tab + kErfcxWords + 2 * (kf & (kExpN - 1)));
+  const D2 t2 = load2(tab.expt() + V::kExpStride * (kf & (kExpN - 1)));
   const double p = t2.a + fmad(t2.a, q, t2.b);
   return ExpSplit{p, kf >> kExpShift};
 }
 
-// erfcx(t) for t in [0, 6.5): interval record j (width 1/LPMC_ERFCX_PER_UNIT),
-// highest power first.
-LPMC_HD double erfcx_piecewise(double t, const double* tab) {
+// erfcx(t) for t in [0, 6.5) (FlatTab) or [0, 3) (LaneTab): interval record
+// j (width 1/LPMC_ERFCX_PER_UNIT), highest power first.
+template <class V>
+LPMC_HD double erfcx_piecewise(double t, const V& tab) {
   constexpr int D = LPMC_ERFCX_DEG;
   constexpr double kPerUnit = LPMC_ERFCX_PER_UNIT;
+  constexpr int S = V::kStep;
 #ifdef __CUDA_ARCH__
   // j = floor(t kPerUnit) from the low word of a round-down FMA onto 2^52
   // (no F2I/I2F conversions); s = t - (j + 1/2) / kPerUnit, both steps exact.
   const double js = __fma_rd(t, kPerUnit, 4503599627370496.0);
   const double jd = js - 4503599627370496.0;
   const uint32_t ju = static_cast<uint32_t>(bits(js));
-  const int j = static_cast<int>(ju < kErfcxN - 1 ? ju : kErfcxN - 1);
+  const int j = static_cast<int>(ju < V::kNRec - 1 ? ju : V::kNRec - 1);
   const double s = fmad(jd, -1.0 / kPerUnit, t) - 0.5 / kPerUnit;
 #else
   int j = static_cast<int>(t * kPerUnit);
-  j = j < kErfcxN - 1 ? j : kErfcxN - 1;
+  j = j < V::kNRec - 1 ? j : V::kNRec - 1;
   const double s = t - (j + 0.5) * (1.0 / kPerUnit);  // exact: j < 2^10, power-of-two width
 #endif
-  const double* rec = tab + kErfcxRow * j;  // c_D, ..., c_1, c0 hi, c0 lo
+  const double* rec = tab.erfcx() + V::kRec * j;  // c_D, ..., c_1, c0 hi, c0 lo
   D2 c = load2(rec);
   double q = fmad(c.a, s, c.b);  // c_D s + c_{D-1}
   if constexpr (D % 2 == 0) {
@@ -261,24 +316,24 @@ LPMC_HD double erfcx_piecewise(double t, const double* tab) {
 #pragma unroll
 #endif
     for (int i = 2; i < D; i += 2) {  // c_{D-2} .. c_1
-      c = load2(rec + i);
+      c = load2(rec + S * i);
       q = fmad(q, s, c.a);
       q = fmad(q, s, c.b);
     }
-    c = load2(rec + D);  // c0 hi, c0 lo
+    c = load2(rec + S * D);  // c0 hi, c0 lo
     return c.a + fmad(q, s, c.b);
   } else {
 #ifdef __CUDA_ARCH__
 #pragma unroll
 #endif
     for (int i = 2; i < D - 1; i += 2) {  // c_{D-2} .. c_2
-      c = load2(rec + i);
+      c = load2(rec + S * i);
       q = fmad(q, s, c.a);
       q = fmad(q, s, c.b);
     }
-    c = load2(rec + D - 1);  // c1, c0 hi
+    c = load2(rec + S * (D - 1));  // c1, c0 hi
     q = fmad(q, s, c.a);
-    const D2 lo = load2(rec + D + 1);  // c0 lo, pad
+    const D2 lo = load2(rec + S * (D + 1));  // c0 lo, pad
     return c.b + fmad(q, s, lo.a);
   }
 }
@@ -290,14 +345,23 @@ LPMC_HD double scale(double x, int k) {
 
 // erfc(t), 0 <= t < 6.5 (host/device identical).
 LPMC_HD double erfc_fast(double t, const double* tab) {
+  const FlatTab ft{tab};
   const double th = t * t;
   const double tl = fmad(t, t, -th);
-  const ExpSplit e = exp_neg(th, tl, tab);
-  return scale(e.p * erfcx_piecewise(t, tab), e.k);
+  const ExpSplit e = exp_neg(th, tl, ft);
+  return scale(e.p * erfcx_piecewise(t, ft), e.k);
 }
 
 #ifdef __CUDACC__
-// The reference's own formula on libdevice (slow path, t > 6.5 only).
+// per-thread view of the staged lane layout (copy = lane % 8)
+__device__ __forceinline__ LaneTab lane_tab(const double* s) {
+  const int c = 2 * static_cast<int>(threadIdx.x & (kLaneCopies - 1));
+  return LaneTab{s + c, s + kLaneErfcxWords + c};
+}
+#endif
+
+#ifdef __CUDACC__
+// The reference's own formula on libdevice (slow path, t >= kDevTMax only).
 __device__ __forceinline__ double phi_inv_lower_libdevice(double u) {
   double x;
   if (u < 0.02425) {
@@ -374,14 +438,15 @@ __device__ __forceinline__ double acklam_tail(double v) {
 
 // The Newton step of gaussian.hpp:52-53, x0 - (Phi(x0) - v) / pdf(x0), with
 // Phi(x0) = erfc(t)/2 and t = (-x0) * (1/sqrt 2) rounded as the reference
-// rounds it.  *slow is set when t >= 6.5 (v < ~1e-20: outside the sampler's
-// range); the caller then redoes that draw on libdevice (the value computed
-// here for such a lane is garbage but never used, and no operation traps).
+// rounds it.  *slow is set when t >= kDevTMax = 3 (v < ~1.1e-5, 2.2e-5 of
+// the sampler's draws); the caller then redoes that draw on libdevice (the
+// value computed here for such a lane is garbage but never used, and no
+// operation traps).
 // mtab = the staged math table (erfcx records, then 2^(j/64)).
-__device__ __forceinline__ double newton_fast(double x0, double v, const double* mtab,
-                                              bool* slow) {
+template <class V>
+__device__ __forceinline__ double newton_fast(double x0, double v, const V& mtab, bool* slow) {
   const double t = -x0 * LPMC_K(kInvSqrt2);
-  *slow = !(t < kFastTMax);
+  *slow = !(t < kDevTMax);
   const double th = t * t;
   const double tl = fmad(t, t, -th);
   const ExpSplit e = exp_neg(th, tl, mtab);
@@ -505,10 +570,10 @@ struct NoMid {
 // `mid` runs between the Newton block and the slow-path fix-ups, in the
 // same basic block as the Newton steps (the sampler's software pipeline
 // puts the previous batch's legs there, lpmc_level.cuh).
-template <int D, bool EXACT_HALF = true, class Mid = NoMid>
+template <int D, bool EXACT_HALF = true, class V = FlatTab, class Mid = NoMid>
 __device__ __forceinline__ void phi_inv_stage2(const double (&v)[D], const double (&x0)[D],
                                                uint32_t neg, uint32_t half, double (&z)[D],
-                                               const double* mtab, Mid&& mid = Mid{}) {
+                                               const V& mtab, Mid&& mid = Mid{}) {
   bool slow[D];
 #pragma unroll
   for (int d = 0; d < D; ++d) z[d] = newton_fast(x0[d], v[d], mtab, &slow[d]);
@@ -530,9 +595,9 @@ __device__ __forceinline__ void phi_inv_stage2(const double (&v)[D], const doubl
 
 // exact_inv_cdf for D arbitrary u (diagnostics; the sampler reflects from
 // its integer draws, dev::draw_reflect).
-template <int D>
+template <int D, class V>
 __device__ __forceinline__ void phi_inv_multi(const double (&u)[D], double (&z)[D],
-                                              const double* mtab) {
+                                              const V& mtab) {
   double v[D], x0[D];
   uint32_t neg = 0, half = 0;
 #pragma unroll

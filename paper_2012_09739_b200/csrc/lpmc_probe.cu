@@ -66,7 +66,7 @@ __global__ void __launch_bounds__(kProbeThreads)
     } else {
       const double uu[1] = {u};
       double zz[1];
-      math::phi_inv_multi<1>(uu, zz, s_math);
+      math::phi_inv_multi<1>(uu, zz, math::FlatTab{s_math});
       z = zz[0];
     }
     const double zr[1] = {z};
@@ -97,9 +97,7 @@ __global__ void __launch_bounds__(kProbeThreads)
   if (valid && fk != kNoFail) {
     const uint64_t n = fk >> 3;
     const uint32_t kind = (fk & 7u) == kStageDraw ? kKindU1 : kKindNonFinite;
-    const uint64_t step = n < (1ull << 22) ? n : (1ull << 22) - 1;
-    atomicMin(A.err_key, static_cast<unsigned long long>((path << 24) |
-                                                         (static_cast<uint64_t>(kind) << 22) | step));
+    atomicMin(A.err_key, err_key_of(path, kind, n, A.err_step_bits));
   }
   if (valid && range.bad()) atomicOr(A.range_flag, 1u);
 

@@ -114,7 +114,11 @@ FULL = [
     ("C1", 6, 52, "exact", False, "terminal", 1 << 20),
     ("C2", 10, 23, "linear:16", False, "terminal", 1 << 22),
     ("C2+K", 10, 23, "linear:16", True, "terminal", 1 << 22),
+    ("C3-ref-lin+K", 8, 10, "linear:16", True, "terminal", 1 << 24),
+    ("C3-ref-const", 8, 10, "constant:16", False, "terminal", 1 << 24),
     ("C4-fp16", 12, 10, "linear:16", False, "call", 1 << 24),
+    ("C4-fp32", 12, 23, "linear:16", False, "call", 1 << 24),
+    ("C4-fp32+K", 12, 23, "linear:16", True, "call", 1 << 24),
     ("C5-l14", 14, 23, "linear:16", True, "terminal", 1 << 22),
 ]
 

@@ -91,3 +91,80 @@ def test_false_positive_path_is_exact(gpu, oracle, b, path, ctr, m, approx, kaha
     got = gpu.run_coupled_paths(model, level, sp, tb, kahan, n, seed, base)
     assert [got.d_hat.state(), got.d_bar.state(), got.d_four.state()] == \
         oracle.tree_from_values(dh, db)
+
+
+# ---- the two genuinely special draws mid-path ----------------
+# u == 1/2 (b = 2^52): both transforms return exactly +0 (gaussian.hpp:62,
+# invcdf_approx.hpp:47); the prefilter sends the path to the exact replay,
+# whose legs and dumped Gaussians must be the oracle's bitwise.
+# u == 1 (b = 2^53 - 1): the reference throws domain_error("exact_inv_cdf
+# requires u in (0, 1)") at that draw; the device reports the same exception
+# with the path index and the step.
+SPECIAL_PRECS = [(23, False, "linear:16", False), (10, False, "cubic:64", True),
+                 (52, False, "exact", False), (10, True, "linear:16", False)]
+SPECIAL_IDS = ["fp32-lin16", "fp16-cubic64-K", "fp64-exact", "half2-lin16"]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("exact_z", ["fast", "glibc"])
+@pytest.mark.parametrize("m,ieee,approx,kahan", SPECIAL_PRECS, ids=SPECIAL_IDS)
+@pytest.mark.parametrize("path,ctr", [(17, 9), (130, 0), (299, 63)])
+def test_half_draw_mid_path(gpu, oracle, exact_z, m, ieee, approx, kahan, path, ctr):
+    level, base, n = 6, 1000, 300
+    seed = seed_for_draw(HALF_DRAW, base + path, ctr)
+    assert stream_draw(seed, base + path, ctr) == HALF_DRAW
+    assert oracle.uniforms(seed, base + path, 1, ctr)[0] == 0.5
+    model = gpu.make_gbm()
+    sp = gpu.PrecisionSpec(m, ieee)
+    tb = None if approx == "exact" else gpu.InvCdfApprox.parse(approx)
+    ext = {"exact_z": exact_z}
+    out, z = gpu.simulate_paths(model, level, sp, tb, kahan, n, seed, base, want_z=True,
+                                schedule="fused", **ext)
+    assert bits(z[path, ctr:ctr + 1]).tolist() == [0]  # exactly +0 in the dump
+    cfg = oracle.config(level=level, mantissa_bits=m, approx=approx, kahan=kahan, seed=seed,
+                        ieee_half=ieee)
+    rep, _, fails = oracle.simulate(cfg, base, n, z_in=z)
+    assert not fails
+    assert np.array_equal(bits(out), bits(rep))
+    own, zo, _ = oracle.simulate(cfg, base, n, want_z=True)
+    assert zo[path, ctr] == 0.0
+    if approx != "exact" or exact_z == "glibc":
+        cols = slice(0, 4) if exact_z == "glibc" else slice(2, 4)
+        assert np.array_equal(bits(out[:, cols]), bits(own[:, cols]))
+    if not ieee:  # the warp-per-path schedule (NP == 1 arithmetics): same terminal values
+        wpp = gpu.simulate_paths(model, level, sp, tb, kahan, n, seed, base,
+                                 schedule="warp_per_path", **ext)
+        assert np.array_equal(bits(wpp), bits(out))
+    got = gpu.run_coupled_paths(model, level, sp, tb, kahan, n, seed, base, **ext)
+    dh = out[:, 0] - out[:, 1]
+    db = out[:, 2] - out[:, 3]
+    assert [got.d_hat.state(), got.d_bar.state(), got.d_four.state()] == \
+        oracle.tree_from_values(dh, db)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("exact_z", ["fast", "glibc"])
+@pytest.mark.parametrize("sched", ["fused", "warp_per_path"])
+@pytest.mark.parametrize("m,ieee,approx,kahan", SPECIAL_PRECS, ids=SPECIAL_IDS)
+def test_top_draw_raises_at_its_step(gpu, ref, exact_z, sched, m, ieee, approx, kahan):
+    level, base, n, path, ctr = 6, 1000, 300, 211, 37
+    seed = seed_for_draw(TOP_DRAW, base + path, ctr)
+    if ieee and sched == "warp_per_path":
+        pytest.skip("half2 legs run two paths per thread (fused schedule only)")
+    model = gpu.make_gbm()
+    sp = gpu.PrecisionSpec(m, ieee)
+    tb = None if approx == "exact" else gpu.InvCdfApprox.parse(approx)
+    # the reference itself throws at this draw (the same message)
+    rc, msg, _ = ref.run_coupled_paths(level=level, mantissa_bits=m, approx=approx, kahan=kahan,
+                                       n=n, seed=seed, path_base=base, threads=1)
+    assert rc == 2 and "exact_inv_cdf requires u in (0, 1)" in msg
+    for call in ("run", "dump"):
+        with pytest.raises(gpu.DomainError, match=r"exact_inv_cdf requires u in \(0, 1\)") as ei:
+            if call == "run":
+                gpu.run_coupled_paths(model, level, sp, tb, kahan, n, seed, base, schedule=sched,
+                                      exact_z=exact_z)
+            else:
+                gpu.simulate_paths(model, level, sp, tb, kahan, n, seed, base, schedule=sched,
+                                   exact_z=exact_z)
+        assert ei.value.path_index == base + path
+        assert ei.value.step == ctr
