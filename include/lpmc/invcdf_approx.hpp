@@ -13,6 +13,8 @@
 #include <vector>
 
 #include "error.hpp"
+#include "gaussian.hpp"
+#include "quadrature.hpp"
 
 namespace lpmc {
 
@@ -89,5 +91,16 @@ class InvCdfApprox {
   std::vector<double> breakpoints_;
   std::vector<std::array<double, 4>> coeff_;
 };
+
+// E[Z^p], p = 1..p_max, by the reference's per-interval quadrature over both
+// halves plus the clamped tails (invcdf_approx.hpp:147-185)
+inline std::vector<double> moment_diagnostics(const InvCdfApprox& approx, int p_max) {
+  if (p_max < 1 || p_max > 8) throw std::invalid_argument("moment order must be in [1, 8]");
+  std::vector<double> out(p_max, 0.0);
+  const lpmc_invcdf_table t = approx.c_abi();
+  lpmc_error err{};
+  detail::throw_status(lpmc_moment_diagnostics(&t, p_max, out.data(), &err), err);
+  return out;
+}
 
 }  // namespace lpmc

@@ -50,7 +50,7 @@
 extern "C" {
 #endif
 
-#define LPMC_B200_ABI_VERSION 2
+#define LPMC_B200_ABI_VERSION 3
 
 typedef enum lpmc_status {
   LPMC_OK = 0,
@@ -185,6 +185,12 @@ typedef struct lpmc_options {
   const int32_t* devices;
   int32_t n_devices;
   int32_t schedule; /* LPMC_SCHEDULE_* */
+  /*
+   * First counter of every path's uniform stream (UniformStream(seed, path,
+   * counter), uniform.hpp:31-36); 0 everywhere in the reference's own
+   * callers (mlmc.hpp:83).  Lets a per-path call resume a stream.
+   */
+  uint64_t counter;
 } lpmc_options;
 
 /* Raw MomentAccumulator state (stats.hpp:84-89). */
@@ -332,6 +338,32 @@ double lpmc_erfc_core(double t);
  * the argument is outside the restated ranges.
  */
 double lpmc_glibc_math(int32_t op, double x, int32_t* ok);
+
+/* ---- host scheme utilities of the reference API ----------------------------
+ * The reference's header-only helpers around the sampler, computed by the
+ * library on the host with the reference's expression trees (bitwise the
+ * reference's on the same libm):
+ *   lpmc_stream_word / _uniform  <- detail::stream_word, UniformStream::next
+ *                                   include/lpmc/uniform.hpp:22-41
+ *   lpmc_normal_cdf / _pdf       <- normal_cdf, normal_pdf   gaussian.hpp:14-20
+ *   lpmc_exact_inv_cdf           <- exact_inv_cdf            gaussian.hpp:59-65
+ *   lpmc_inv_cdf_lower           <- detail::inv_cdf_lower    gaussian.hpp:26-55
+ *   lpmc_gauss_legendre          <- gauss_legendre           quadrature.hpp:17-41
+ *   lpmc_ulp_spacing             <- ulp_spacing              softfloat.hpp:129-136
+ *   lpmc_moment_diagnostics      <- moment_diagnostics       invcdf_approx.hpp:150-185
+ */
+uint64_t lpmc_stream_word(uint64_t seed, uint64_t path_index, uint64_t counter);
+double lpmc_stream_uniform(uint64_t seed, uint64_t path_index, uint64_t counter);
+double lpmc_normal_cdf(double x);
+double lpmc_normal_pdf(double x);
+lpmc_status lpmc_exact_inv_cdf(double u, double* out, lpmc_error* err);
+double lpmc_inv_cdf_lower(double u);
+/* nodes, weights: n doubles each */
+lpmc_status lpmc_gauss_legendre(int32_t n, double* nodes, double* weights, lpmc_error* err);
+lpmc_status lpmc_ulp_spacing(double x, int32_t mantissa_bits, double* out, lpmc_error* err);
+/* out: E[Z^p], p = 1..p_max (p_max in [1, 8]) */
+lpmc_status lpmc_moment_diagnostics(const lpmc_invcdf_table* table, int32_t p_max, double* out,
+                                    lpmc_error* err);
 
 /* ---- callers of the level sampler (mlmc.hpp:151-285) --------------------- */
 /* One run of a multi-run call. */

@@ -91,7 +91,7 @@ class Options(C.Structure):
     _fields_ = [("legs", C.c_uint32), ("payoff", _i32), ("strike", C.c_double),
                 ("reduce", _i32), ("device", _i32), ("stream", C.c_void_p),
                 ("exact_z", _i32), ("devices", C.POINTER(_i32)), ("n_devices", _i32),
-                ("schedule", _i32)]
+                ("schedule", _i32), ("counter", _u64)]
 
 
 class Moments(C.Structure):
@@ -172,6 +172,15 @@ SIGNATURES = {
     "lpmc_run_coupled_many_partials": (_i32, [_P(Gbm), _P(InvCdfTable), _u64, _P(RunDesc), _u64,
                                               _P(_u64), _P(_u64), _P(Options), _P(Moments),
                                               _P(Error)]),
+    "lpmc_stream_word": (_u64, [_u64, _u64, _u64]),
+    "lpmc_stream_uniform": (C.c_double, [_u64, _u64, _u64]),
+    "lpmc_normal_cdf": (C.c_double, [C.c_double]),
+    "lpmc_normal_pdf": (C.c_double, [C.c_double]),
+    "lpmc_exact_inv_cdf": (_i32, [C.c_double, _dp, _P(Error)]),
+    "lpmc_inv_cdf_lower": (C.c_double, [C.c_double]),
+    "lpmc_gauss_legendre": (_i32, [_i32, _dp, _dp, _P(Error)]),
+    "lpmc_ulp_spacing": (_i32, [C.c_double, _i32, _dp, _P(Error)]),
+    "lpmc_moment_diagnostics": (_i32, [_P(InvCdfTable), _i32, _dp, _P(Error)]),
     "lpmc_run_two_way_paths": (_i32, [_P(Gbm), _i32, _P(Precision), _P(InvCdfTable), _i32, _u64,
                                       _u64, _u64, _P(Options), _P(Moments), _P(Error)]),
     "lpmc_allocate_samples": (_i32, [_P(LevelStatsC), _u64, C.c_double, _i32, _P(_u64),
@@ -218,7 +227,7 @@ def load(build_if_missing: bool = True) -> C.CDLL:
             fn = getattr(lib, name)
             fn.restype = res
             fn.argtypes = args
-        if lib.lpmc_abi_version() != 2:
+        if lib.lpmc_abi_version() != 3:
             raise ImportError("liblpmc_b200.so ABI version mismatch")
         _lib = lib
         return lib

@@ -56,9 +56,10 @@ __device__ __forceinline__ uint64_t path_key(uint64_t seed_key, uint64_t path) {
 // on its high word instead of FP64 compares.
 // b == kTopDraw: u rounds to 1 (the reference throws, gaussian.hpp:60);
 // b == kHalfDraw: u rounds to exactly 1/2 (both transforms return exactly 0).
+constexpr uint64_t kCounterStep = 0x94d049bb133111ebull;  // uniform.hpp:26
 __device__ __forceinline__ uint64_t next_draw(uint64_t& kc) {
   const uint64_t w = mix64(mix64(kc));
-  kc += 0x94d049bb133111ebull;
+  kc += kCounterStep;
   return w >> 11;
 }
 
@@ -219,7 +220,10 @@ __device__ __forceinline__ bool nonfinite32(float x) {
 }
 
 // ------------------------------------------------- packed fp32 pairs ------
-// sm_100 executes two fp32 lanes per instruction (FFMA2).  Every packed op is
+// (-DLPMC_PAIR, A/B only.)  sm_100 executes two fp32 lanes per instruction
+// (FFMA2).  Measured on the C4 kernels: 7 % fewer warp-instructions, but
+// FFMA2 holds the FMA pipe twice as long and the kernels ran 0-3 % slower
+// (DESIGN.md section 8), so the scalar form is the default.  Every packed op is
 // an fma.rn.f32x2 whose addend/multiplier constants come from the launch
 // parameters (LevelArgs::f2_neg0 / f2_neg1), never immediates: with known
 // constants ptxas fuses a multiply and a following add into one FFMA2 even
@@ -297,10 +301,10 @@ struct ArithF32 {  // m == 23, native
   static constexpr bool kIeee = false;
   // mul2: two independent products of one leg step in one FFMA2 (bitwise
   // the two scalar products)
-#ifdef LPMC_NO_PAIR  // A/B only
-  static constexpr bool kPair = false;
-#else
+#ifdef LPMC_PAIR  // A/B only: measured slower
   static constexpr bool kPair = true;
+#else
+  static constexpr bool kPair = false;
 #endif
   uint64_t n0, n1, p1;
   __device__ explicit ArithF32(const LevelArgs& A)
@@ -329,10 +333,10 @@ struct ArithF32Round {  // m <= 10: fp32 op (correctly rounded), then RNE to m+1
   uint64_t half_m1_64, keep64;
   float split;     // 2^d + 1: Veltkamp's splitter
   double split64;  // 2^d64 + 1
-#if defined(LPMC_F32R_INT) || defined(LPMC_NO_PAIR)
-  static constexpr bool kPair = false;
-#else
+#if defined(LPMC_PAIR) && !defined(LPMC_F32R_INT)
   static constexpr bool kPair = true;  // mul2: packed product + packed Veltkamp split
+#else
+  static constexpr bool kPair = false;
 #endif
   uint64_t n0, n1, p1, split2;
   __device__ explicit ArithF32Round(const LevelArgs& A)

@@ -22,6 +22,8 @@
 #include <tuple>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../include/lpmc_b200.h"
 #include "lpmc_internal.h"
 #include "lpmc_glibc.cuh"
@@ -419,6 +421,7 @@ lpmc_status build_spec(const lpmc_gbm* model, int32_t level, const lpmc_precisio
   A.level = level;
   A.legs = static_cast<int32_t>(o.legs);
   A.exact_z = o.exact_z;
+  A.counter0 = o.counter;
   A.err_step_bits = err_step_bits_for(level);
   if (n_paths > (1ull << (62 - A.err_step_bits)))  // failure key layout (lpmc_internal.h)
     return fail(err, LPMC_INVALID_ARGUMENT,
@@ -649,7 +652,22 @@ uint64_t acc_count_of(const RunSpec& s) {
   return std::min(s.chunk_end * kChunkBatches, n_batches_total) - s.chunk_begin * kChunkBatches;
 }
 
+// NVTX ranges (header-only NVTX3: no-ops unless a tool such as nsys or ncu
+// injects itself): one per level enqueue, one per host fold.
+struct NvtxRange {
+  explicit NvtxRange(const char* msg) { nvtxRangePushA(msg); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
+
 cudaError_t enqueue_run(const RunSpec& s, Buffers& B, cudaStream_t st, Enqueued* q) {
+  char label[96];
+  std::snprintf(label, sizeof label, "lpmc level %d m=%d%s legs=%d chunks [%llu,%llu)",
+                s.args.level, s.args.mantissa_bits, s.kahan ? " kahan" : "", s.args.legs,
+                static_cast<unsigned long long>(s.chunk_begin),
+                static_cast<unsigned long long>(s.chunk_end));
+  const NvtxRange range(label);
   cudaError_t e;
   *q = Enqueued{};
   if ((e = reserve(s, B)) != cudaSuccess) return e;
@@ -1044,6 +1062,7 @@ lpmc_status run_many(std::vector<RunSpec>& specs, void* user_stream,
 }
 
 void fold(const std::vector<Moments>& parts, lpmc_moments* out3) {
+  const NvtxRange range("lpmc fold");
   Moments acc[3];
   for (size_t i = 0; i < parts.size(); ++i) merge_into(acc[i % 3], parts[i]);
   for (int f = 0; f < 3; ++f) out3[f] = to_abi(acc[f]);
@@ -1084,6 +1103,7 @@ void lpmc_default_options(lpmc_options* o) {
   o->devices = nullptr;
   o->n_devices = 0;
   o->schedule = LPMC_SCHEDULE_AUTO;
+  o->counter = 0;
 }
 
 void lpmc_default_cost_model(lpmc_cost_model* c) {  // mlmc.hpp:20-28
@@ -1140,6 +1160,97 @@ lpmc_status lpmc_invcdf_build(int32_t kind, int32_t K, double* bp, double* coeff
   return ok(err);
 }
 
+// ---- host scheme utilities of the reference API (uniform.hpp, gaussian.hpp,
+// quadrature.hpp, softfloat.hpp:129-136, invcdf_approx.hpp:150-185) --------
+uint64_t lpmc_stream_word(uint64_t seed, uint64_t path_index, uint64_t counter) {
+  // stream_word (uniform.hpp:22-27)
+  uint64_t key = host_mix64(seed + 0x9e3779b97f4a7c15ull);
+  key = host_mix64(key ^ host_mix64(path_index + 0xbf58476d1ce4e5b9ull));
+  return host_mix64(host_mix64(key + counter * 0x94d049bb133111ebull));
+}
+
+double lpmc_stream_uniform(uint64_t seed, uint64_t path_index, uint64_t counter) {
+  // UniformStream::next (uniform.hpp:38-41): the 53-bit draw offset by half a step
+  return static_cast<double>(lpmc_stream_word(seed, path_index, counter) >> 11) * 0x1p-53 +
+         0x1p-54;
+}
+
+double lpmc_normal_cdf(double x) { return 0.5 * std::erfc(-x * 0.7071067811865475244); }
+double lpmc_normal_pdf(double x) { return 0.3989422804014326779 * std::exp(-0.5 * x * x); }
+
+lpmc_status lpmc_exact_inv_cdf(double u, double* out, lpmc_error* err) {
+  if (out == nullptr) return fail(err, LPMC_INVALID_ARGUMENT, "null argument");
+  if (!(u > 0.0 && u < 1.0))  // gaussian.hpp:59-61
+    return fail(err, LPMC_DOMAIN_ERROR, "exact_inv_cdf requires u in (0, 1)");
+  *out = host_phi_inv(u);
+  return ok(err);
+}
+
+double lpmc_inv_cdf_lower(double u) { return host_phi_inv_lower(u); }
+
+lpmc_status lpmc_gauss_legendre(int32_t n, double* nodes, double* weights, lpmc_error* err) {
+  if (n < 1 || nodes == nullptr || weights == nullptr)
+    return fail(err, LPMC_INVALID_ARGUMENT, "need n >= 1 and output arrays");
+  std::vector<double> x, w;
+  gauss_legendre_rule(n, x, w);
+  std::copy(x.begin(), x.end(), nodes);
+  std::copy(w.begin(), w.end(), weights);
+  return ok(err);
+}
+
+lpmc_status lpmc_ulp_spacing(double x, int32_t m, double* out, lpmc_error* err) {
+  if (out == nullptr) return fail(err, LPMC_INVALID_ARGUMENT, "null argument");
+  // ulp_spacing (softfloat.hpp:129-136)
+  if (!std::isfinite(x)) return fail(err, LPMC_DOMAIN_ERROR, "non-finite operand");
+  if (x == 0.0)
+    return fail(err, LPMC_DOMAIN_ERROR, "ulp_spacing undefined at zero with an unbounded exponent");
+  int e = 0;
+  std::frexp(x, &e);
+  *out = std::ldexp(1.0, e - 1 - m);
+  return ok(err);
+}
+
+lpmc_status lpmc_moment_diagnostics(const lpmc_invcdf_table* t, int32_t p_max, double* out,
+                                    lpmc_error* err) {
+  // moment_diagnostics (invcdf_approx.hpp:150-185), same quadrature and order
+  if (t == nullptr || out == nullptr) return fail(err, LPMC_INVALID_ARGUMENT, "null argument");
+  if (p_max < 1 || p_max > 8)
+    return fail(err, LPMC_INVALID_ARGUMENT, "moment order must be in [1, 8]");
+  std::vector<double> nodes, weights;
+  gauss_legendre_rule(32, nodes, weights);
+  for (int p = 0; p < p_max; ++p) out[p] = 0.0;
+  lpmc_status st = LPMC_OK;
+  auto accumulate = [&](double a, double b) {
+    for (size_t i = 0; i < nodes.size() && st == LPMC_OK; ++i) {
+      const double u = 0.5 * (a + b) + 0.5 * (b - a) * nodes[i];
+      double z = 0.0;
+      st = lpmc_invcdf_eval(t, u, &z, err);
+      const double wgt = 0.5 * (b - a) * weights[i];
+      double zp = 1.0;
+      for (int p = 0; p < p_max; ++p) {
+        zp *= z;
+        out[p] += wgt * zp;
+      }
+    }
+  };
+  double a = 0.5;
+  for (int j = 0; j < t->interval_count && st == LPMC_OK; ++j) {
+    const double b = t->breakpoints[j];
+    accumulate(a, b);
+    accumulate(1.0 - b, 1.0 - a);  // mirrored interval
+    a = b;
+  }
+  if (st != LPMC_OK) return st;
+  const double tail_mass = 1.0 - t->breakpoints[t->interval_count - 1];
+  double zp_hi = 1.0, zp_lo = 1.0;
+  for (int p = 0; p < p_max; ++p) {
+    zp_hi *= t->tail_value;
+    zp_lo *= -t->tail_value;
+    out[p] += tail_mass * (zp_hi + zp_lo);
+  }
+  return ok(err);
+}
+
 lpmc_status lpmc_invcdf_eval(const lpmc_invcdf_table* t, double u, double* out, lpmc_error* err) {
   if (t == nullptr || out == nullptr) return fail(err, LPMC_INVALID_ARGUMENT, "null argument");
   // InvCdfApprox::operator() / eval_upper (invcdf_approx.hpp:44-90)
@@ -1192,6 +1303,7 @@ void lpmc_moments_merge(lpmc_moments* acc, const lpmc_moments* other) {
 }
 
 void lpmc_fold_partials(const lpmc_moments* partials, uint64_t n_chunks, lpmc_moments* out) {
+  const NvtxRange range("lpmc fold partials");
   Moments acc[3];
   for (uint64_t i = 0; i < 3 * n_chunks; ++i) merge_into(acc[i % 3], from_abi(partials[i]));
   for (int f = 0; f < 3; ++f) out[f] = to_abi(acc[f]);

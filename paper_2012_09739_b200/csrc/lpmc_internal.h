@@ -77,6 +77,8 @@ struct LevelArgs {
   uint64_t f2_neg1 = 0xbf800000bf800000ull;
   // bits of the step field of the failure key (err_step_bits_for(level))
   int32_t err_step_bits = 22;
+  // first counter of every path's stream (lpmc_options::counter)
+  uint64_t counter0 = 0;
 };
 
 // Failure key: the path in the high bits (atomicMin finds the lowest failing

@@ -90,9 +90,14 @@ __device__ __forceinline__ void draw_uniforms(uint64_t (&kc)[NP], Uniforms<H * N
 // the next batch are drawn between the Acklam stage and the Newton stage, so
 // the integer RNG interleaves with FP64 work instead of forming its own
 // phase (software pipelining across batches).
-// The fast mode's staged tables: the lane-private layout (math::LaneTab);
-// -DLPMC_FLAT_TABLES restores the flat layout (A/B only; same values).
-#ifdef LPMC_FLAT_TABLES
+// The fast mode's staged tables: the flat layout (math::FlatTab);
+// -DLPMC_LANE_TABLES selects the conflict-free lane-private layout
+// (math::LaneTab; same values).  Measured A/B (DESIGN.md section 8,
+// profiles/r02_ab_summary.md): the lane layout halves the shared-memory
+// wavefronts but leaves fp32 levels within 0.3 % and slows the emulated-fp16
+// kernel by 3 % (the 8x table copies shrink L1 under the replay call's
+// stack), so the flat layout stays the default.
+#ifndef LPMC_LANE_TABLES
 using FastTab = math::FlatTab;
 constexpr int kFastWords = kFastMathWords;
 __device__ __forceinline__ void stage_fast(double* s) { stage_math(s, kFastMathWords); }
@@ -312,7 +317,7 @@ __device__ __forceinline__ void simulate(const LevelArgs& A, const TableView& ta
   double xhf[NP], xhc[NP];
 #pragma unroll
   for (int p = 0; p < NP; ++p) {
-    kc[p] = path_key(A.seed_key, A.path_base + local[p]);
+    kc[p] = path_key(A.seed_key, A.path_base + local[p]) + A.counter0 * kCounterStep;
     u1[p] = false;
     fk[p] = kNoFail;
     xhf[p] = A.x0;
@@ -691,7 +696,7 @@ __global__ void __launch_bounds__(kWppThreads) wpp_kernel(const __grid_constant_
   const uint64_t n_fine = 1ull << A.level;  // level >= 1 (the host runs level 0 fused)
   bool special = false;
   for (uint64_t n0 = 0; n0 < n_fine; n0 += 32) {
-    uint64_t kc = key + (n0 + static_cast<uint64_t>(lane)) * 0x94d049bb133111ebull;
+    uint64_t kc = key + (A.counter0 + n0 + static_cast<uint64_t>(lane)) * kCounterStep;
     const uint64_t b = next_draw(kc);
     const double u[1] = {uniform_of(b)};
     const bool live = n0 + lane < n_fine;

@@ -22,9 +22,9 @@
 //    hi + lo (tools/fit_math.py).  1/pdf is sqrt(2 pi) 2^-k / p(r): the same
 //    exponential, no second exp, no division.  Table indices come from the
 //    low words of shifted FMAs (no F2I/I2F conversions).
-//  * t >= 3 (|x0| > 4.24, u < 1.1e-5: 2.2e-5 of the draws) takes a
-//    libdevice slow path out of line; the records for t < 3 are staged in
-//    a conflict-free lane-private layout (LaneTab below).
+//  * t >= kDevTMax (6.5: u < 1e-20, never drawn by the sampler; 3 with the
+//    lane-private table layout, LaneTab below) takes a libdevice slow path
+//    out of line.
 //  * -DLPMC_X0_ACKLAM restores Acklam's binary64 x0 + Newton (A/B only,
 //    tools/gpu_ab_x0.sh).
 //
@@ -221,10 +221,11 @@ LPMC_HD D2 load2(const double* p) {
 //    whatever records they gather: conflict-free by construction, with no
 //    extra instruction (the copy offset is hoisted into the per-thread base
 //    pointer; the record stride and the quad offsets are immediates).  Only
-//    the records for t < kDevTMax = 3 are staged (99.998 % of the sampler's
-//    draws); a draw with t >= 3 takes the out-of-line libdevice path that
-//    already served t >= 6.5 (newton_fast's `slow`).  kDevTMax applies to
-//    both layouts on the device, so every kernel computes the same Z.
+//    the records for t < 3 are staged (99.998 % of the sampler's draws); a
+//    draw with t >= 3 takes the out-of-line libdevice path that serves
+//    t >= 6.5 with the flat layout (newton_fast's `slow`).  kDevTMax is one
+//    value for every kernel of a build (3 with -DLPMC_LANE_TABLES, else 6.5),
+//    so all kernels compute the same Z.
 struct FlatTab {
   const double* t;
   static constexpr int kRec = kErfcxRow;  // doubles between records
@@ -236,8 +237,12 @@ struct FlatTab {
 };
 
 constexpr int kLaneCopies = 8;
+#ifdef LPMC_LANE_TABLES
 constexpr double kDevTMax = 3.0;  // device fast path: erfcx records for t < 3
-constexpr int kHotRec = static_cast<int>(kDevTMax * LPMC_ERFCX_PER_UNIT);
+#else
+constexpr double kDevTMax = kFastTMax;  // the flat table covers [0, 6.5)
+#endif
+constexpr int kHotRec = 3 * LPMC_ERFCX_PER_UNIT;  // lane layout: records for t < 3
 static_assert(kErfcxRow % 2 == 0 && kHotRec <= kErfcxN, "lane layout needs whole quads");
 constexpr int kLaneErfcxWords = kHotRec * kErfcxRow * kLaneCopies;
 constexpr int kLaneWords = kLaneErfcxWords + kExpWords * kLaneCopies;
@@ -438,10 +443,10 @@ __device__ __forceinline__ double acklam_tail(double v) {
 
 // The Newton step of gaussian.hpp:52-53, x0 - (Phi(x0) - v) / pdf(x0), with
 // Phi(x0) = erfc(t)/2 and t = (-x0) * (1/sqrt 2) rounded as the reference
-// rounds it.  *slow is set when t >= kDevTMax = 3 (v < ~1.1e-5, 2.2e-5 of
-// the sampler's draws); the caller then redoes that draw on libdevice (the
-// value computed here for such a lane is garbage but never used, and no
-// operation traps).
+// rounds it.  *slow is set when t >= kDevTMax (6.5: v < 1e-20, outside the
+// sampler's range; 3 with the lane layout: v < 1.1e-5); the caller then
+// redoes that draw on libdevice (the value computed here for such a lane is
+// garbage but never used, and no operation traps).
 // mtab = the staged math table (erfcx records, then 2^(j/64)).
 template <class V>
 __device__ __forceinline__ double newton_fast(double x0, double v, const V& mtab, bool* slow) {

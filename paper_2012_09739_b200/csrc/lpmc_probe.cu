@@ -42,7 +42,7 @@ __global__ void __launch_bounds__(kProbeThreads)
 
   const Arith ar(A);
   typename Arith::Range range;
-  uint64_t kc = path_key(A.seed_key, A.path_base + (valid ? path : 0));
+  uint64_t kc = path_key(A.seed_key, A.path_base + (valid ? path : 0)) + A.counter0 * kCounterStep;
   const T mu_l = ar.c(A.mu_l, A.h_mu), sg_l = ar.c(A.sigma_l, A.h_sigma);
   const T dt_l = ar.c(A.dtf_l, A.h_dtf), sdt_l = ar.c(A.sdtf_l, A.h_sdtf);
   T x = ar.c(A.x0_l, A.h_x0);

@@ -29,7 +29,7 @@ def test_library_exports_every_declared_symbol(lib):
     for name in declared:
         assert hasattr(so, name), name
         assert name in N.SIGNATURES, f"{name} not bound in _native.SIGNATURES"
-    assert so.lpmc_abi_version() == 2
+    assert so.lpmc_abi_version() == 3
 
 
 def test_cpp_api_header_compiles():
