@@ -10,7 +10,7 @@ for GBM dS = 0.05 S dt + 0.2 S dW, S0 = 1, T = 1, European call payoff
 max(S_T - 1, 0); exact Gaussians in fp64 (hat legs) and approximate ones
 (linear:16 table) in the reference's fp16 (m = 10, emulated) and fp32 (bar
 legs); levels 0..12; 2^24 paths per level per GPU (weak scaling; --scaling
-strong keeps 2^24 paths per level in total).  Every path runs all four
+strong keeps 2^24 paths per level in total; --paths changes either).  Every path runs all four
 coupled legs and all three moment families (estimate_level_stats semantics,
 mlmc.hpp:113-149).  Precisions and path bases follow the reference's
 four-way experiment (experiments.hpp:170-213): low = fp16 at l << 40, high =
@@ -286,6 +286,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
+    ap.add_argument("--paths", type=int, default=PATHS_PER_GPU,
+                    help="paths per level: per GPU (weak) or in total (strong); a multiple of "
+                         "2^18 (e.g. 2^30 for the C5 strong-scaling total)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-c2", action="store_true")
     args = ap.parse_args()
@@ -325,7 +328,9 @@ def main():
     model = L.make_gbm(0.05, 0.2, 1.0, 1.0)
     specs = {"fp16": L.PrecisionSpec.fp16(), "fp32": L.PrecisionSpec.fp32()}
     approx = L.InvCdfApprox.parse(APPROX)
-    n_total = PATHS_PER_GPU * (world if args.scaling == "weak" else 1)
+    if args.paths % (1 << 18):
+        raise SystemExit("--paths must be a multiple of 2^18 (one chunk)")
+    n_total = args.paths * (world if args.scaling == "weak" else 1)
     n_chunks = n_total // (1 << 18)
     c0, c1 = shard_chunks(n_chunks, rank, world)
     n_local = (c1 - c0) * (1 << 18)

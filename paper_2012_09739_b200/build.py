@@ -58,10 +58,16 @@ def kernel_source_hash() -> str:
     profile's ncu-counted per-path-step demands to the kernels that produced
     them (bench.py flags a mismatch as stale)."""
     import hashlib
+    import re
     h = hashlib.sha256(" ".join(NVCC_FLAGS).encode())
     for name in sorted(SOURCES_CU) + sorted(x for x in HEADERS if not x.startswith("..")):
-        with open(os.path.join(CSRC, name), "rb") as f:
-            h.update(name.encode() + b"\0" + f.read())
+        with open(os.path.join(CSRC, name)) as f:
+            text = f.read()
+        # code only: comments and blank-line/space changes do not change the kernels
+        text = re.sub(r"/\*.*?\*/", " ", text, flags=re.S)
+        text = re.sub(r"//[^\n]*", "", text)
+        text = "\n".join(" ".join(line.split()) for line in text.splitlines() if line.strip())
+        h.update(name.encode() + b"\0" + text.encode())
     return h.hexdigest()[:16]
 
 

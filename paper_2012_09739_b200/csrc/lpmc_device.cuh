@@ -121,6 +121,7 @@ __device__ __forceinline__ double approx_inv(const TableView& t, double u, bool 
     const int e = static_cast<int>(vb >> 52) - 1023;
     const int fl = (vb & 0xFFFFFFFFFFFFFull) == 0 ? -e : -e - 1;  // floor(-log2 v) >= 1
     const int j = min(fl - 1, t.K - 1);
+    LPMC_DCHECK(j >= 0 && j < t.K);
     const double* b = t.base + 6 * j;
     const math::D2 cw = math::load2(b);
     const math::D2 c01 = math::load2(b + 2);
@@ -132,6 +133,7 @@ __device__ __forceinline__ double approx_inv(const TableView& t, double u, bool 
     const int e = static_cast<int>(vb >> 52) - 1023;
     const int fl = (vb & 0xFFFFFFFFFFFFFull) == 0 ? -e : -e - 1;  // floor(-log2 v) >= 1
     const int j = min(fl - 1, t.K - 1);
+    LPMC_DCHECK(j >= 0 && j < t.K);
     const double* b = t.base + 6 * j;
     const math::D2 cw = math::load2(b);
     const math::D2 c01 = math::load2(b + 2);
@@ -158,6 +160,7 @@ __device__ __forceinline__ double approx_inv(const TableView& t, double u, bool 
     while (J < t.K && v <= thr[J]) ++J;
     while (J > 0 && v > thr[J - 1]) --J;
     const int j = J < t.K ? J : t.K - 1;
+    LPMC_DCHECK(J >= 0 && J <= t.K && j >= 0 && j < t.K);
     const double* rec = t.base + W * j;
     const math::D2 ad = math::load2(rec);       // a_j, b_j - a_j
     const math::D2 c01 = math::load2(rec + 2);  // c0, c1
@@ -283,6 +286,7 @@ struct ArithCarrier {  // m >= 52
   static constexpr int NP = 1;
   static constexpr bool kIeee = false;
   static constexpr bool kPair = false;  // no packed fp32 pairs (see ArithF32)
+  static constexpr bool kPow2 = false;  // no power-of-two step folding (see step_bar_pw)
   __device__ explicit ArithCarrier(const LevelArgs&) {}
   __device__ T c(double d, uint16_t) const { return d; }
   __device__ T zero() const { return 0.0; }
@@ -306,6 +310,7 @@ struct ArithF32 {  // m == 23, native
 #else
   static constexpr bool kPair = false;
 #endif
+  static constexpr bool kPow2 = true;  // native range guard: step_bar_pw is exact
   uint64_t n0, n1, p1;
   __device__ explicit ArithF32(const LevelArgs& A)
       : n0(A.f2_neg0), n1(A.f2_neg1), p1(A.f2_neg1 & 0x7fffffff7fffffffull) {}
@@ -338,6 +343,7 @@ struct ArithF32Round {  // m <= 10: fp32 op (correctly rounded), then RNE to m+1
 #else
   static constexpr bool kPair = false;
 #endif
+  static constexpr bool kPow2 = true;  // native range guard: step_bar_pw is exact
   uint64_t n0, n1, p1, split2;
   __device__ explicit ArithF32Round(const LevelArgs& A)
       : n0(A.f2_neg0), n1(A.f2_neg1), p1(A.f2_neg1 & 0x7fffffff7fffffffull) {
@@ -399,6 +405,7 @@ struct ArithF64Round {  // any m < 52: binary64 op, then integer RNE (exact emul
   static constexpr int NP = 1;
   static constexpr bool kIeee = false;
   static constexpr bool kPair = false;
+  static constexpr bool kPow2 = false;
   uint32_t d;
   uint64_t half_m1, keep;
   __device__ explicit ArithF64Round(const LevelArgs& A) {
@@ -422,6 +429,7 @@ struct ArithHalf2 {  // native IEEE binary16, two paths per thread
   static constexpr int NP = 2;
   static constexpr bool kIeee = true;
   static constexpr bool kPair = false;  // already two paths per half2 op
+  static constexpr bool kPow2 = false;
   __device__ explicit ArithHalf2(const LevelArgs&) {}
   __device__ T c(double, uint16_t bits) const {
     const __half h = __ushort_as_half(bits);
@@ -473,6 +481,7 @@ __device__ void batch_moments(const double (&vh)[NP], const double (&vb)[NP],
 #pragma unroll
     for (int p = 0; p < NP; ++p) {
       const double s = warp_sum(v[f][p], 16);
+      LPMC_DCHECK(warp + p * kWarps < 8);
       if (lane == 0) s_grp[f][warp + p * kWarps] = s;
     }
   __syncthreads();

@@ -18,6 +18,21 @@
 // -fmad=false and IEEE division/sqrt, on the host with -ffp-contract=off, so
 // each operator is one correctly rounded operation on both; the contracted
 // glibc builds are reproduced with explicit fmad().
+//
+// Upstream notices of the restated algorithms:
+//  * erfc -- Sun fdlibm s_erf.c:
+//      Copyright (C) 1993 by Sun Microsystems, Inc. All rights reserved.
+//      Developed at SunPro, a Sun Microsystems, Inc. business.
+//      Permission to use, copy, modify, and distribute this
+//      software is freely granted, provided that this notice
+//      is preserved.
+//    (as distributed in the GNU C Library, sysdeps/ieee754/dbl-64/s_erf.c,
+//    GNU LGPL 2.1 or later)
+//  * exp, log -- ARM optimized-routines (Copyright (c) 2018 Arm Limited;
+//    upstream licence MIT OR Apache-2.0 WITH LLVM-exception), as contributed
+//    to the GNU C Library (sysdeps/ieee754/dbl-64/e_exp.c, e_log.c,
+//    e_exp_data.c, e_log_data.c; Copyright (C) 2018-2024 Free Software
+//    Foundation, Inc., GNU LGPL 2.1 or later).
 #pragma once
 
 #include "lpmc_glibc_coef.h"

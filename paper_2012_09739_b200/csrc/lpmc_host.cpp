@@ -491,6 +491,21 @@ lpmc_status build_spec(const lpmc_gbm* model, int32_t level, const lpmc_precisio
   } else {
     s.arith = BarArith::kF64Round;
   }
+  // Power-of-two steps (T = 1 and an even level: dt, 2dt and sqrt(dt) are
+  // powers of two): the native fp32 bar legs may fold them into the model
+  // constants, R(R(mu x) dt) = R(x (mu dt)) etc., bitwise within the native
+  // range guard (every intermediate stays normal; lpmc_level.cuh, step_bar_pw).
+  auto pow2 = [](double v) {
+    int e = 0;
+    return v > 0.0 && std::frexp(v, &e) == 0.5;
+  };
+  if ((s.arith == BarArith::kF32 || s.arith == BarArith::kF32Round) && pow2(low[3]) &&
+      pow2(low[4]) && pow2(low[5])) {
+    A.bar_pow2 = 1;
+    A.mu_dtf_l = low[0] * low[3];  // exact: a power-of-two scaling
+    A.mu_dtc_l = low[0] * low[5];
+    A.sg_sdt_l = low[1] * low[4];
+  }
   const uint64_t n_chunks = (n_paths + kChunkPaths - 1) / kChunkPaths;
   s.chunk_begin = 0;
   s.chunk_end = n_chunks;

@@ -79,6 +79,10 @@ struct LevelArgs {
   int32_t err_step_bits = 22;
   // first counter of every path's stream (lpmc_options::counter)
   uint64_t counter0 = 0;
+  // native fp32 bar legs with power-of-two dt, 2dt, sqrt(dt) (host-proved):
+  // the products mu dt, mu 2dt, sigma sqrt(dt), exact
+  int32_t bar_pow2 = 0;
+  double mu_dtf_l = 0.0, mu_dtc_l = 0.0, sg_sdt_l = 0.0;
 };
 
 // Failure key: the path in the high bits (atomicMin finds the lowest failing

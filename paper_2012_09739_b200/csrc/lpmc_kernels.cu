@@ -168,6 +168,7 @@ __global__ void density_kernel(uint64_t key, uint64_t n, const double* __restric
       int b = static_cast<int>(__ddiv_rn(__dadd_rn(z, z_max), width));
       b = b < 0 ? 0 : b;
       b = b >= n_bins ? n_bins - 1 : b;
+      LPMC_DCHECK(b >= 0 && b < n_bins);
       if (local_bins) {
         atomicAdd(&s_bins[b], 1u);
       } else {

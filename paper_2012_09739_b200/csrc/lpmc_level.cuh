@@ -176,8 +176,10 @@ __device__ __forceinline__ void gen_draws(const LevelArgs& A, const TableView& t
     for (int p = 0; p < NP; ++p) {
       z[h][p] = zz[h * NP + p];
       if constexpr (DUMP) {
-        if (A.z_out != nullptr && valid[p])
+        if (A.z_out != nullptr && valid[p]) {
+          LPMC_DCHECK(local[p] < A.n_paths && n0 + h < (1ull << A.level));
           A.z_out[local[p] * (1ull << A.level) + n0 + h] = z[h][p];
+        }
       }
       if constexpr (TAB != kTabNone) {
         zl[p] = approx_inv<CHECKED, TAB>(tab, u[h * NP + p]);
@@ -256,6 +258,41 @@ __device__ __forceinline__ void step_bar(const Arith& ar, typename Arith::Range&
   }
 }
 
+// The bar-leg step with power-of-two steps folded into the model constants
+// (LevelArgs::bar_pow2; native fp32 arithmetics only).  With dt = 2^-l,
+// sqrt(dt) = 2^(-l/2) and mu, sigma, x, z already on the target grid:
+//   drift  R(R(mu x) dt)          = R(x (mu dt))
+//   fine   R(R(R(sigma x) s) z)   = R(R(x (sigma s)) z)
+//   coarse dW = R(s z0 + s z1)    = s R(z0 + z1),
+//          R(R(sigma x) dW)       = R(R(x (sigma s)) R(z0 + z1))
+// because scaling by a power of two commutes with rounding while every
+// intermediate stays normal -- which the native range guard guarantees (states
+// in [2^-32, 2^33), constants in [2^-20, 2^20], dt >= 2^-40; a run that leaves
+// the range is re-run in the exact binary64 emulation).  Two fewer roundings
+// per fine step and 1.5 per coarse step; no failure can occur inside the
+// guard, so the failure semantics are unchanged (the checked replay keeps the
+// reference's own form).  zs = z (fine) or R(z0 + z1) (coarse).
+template <class Arith, bool KAHAN>
+__device__ __forceinline__ void step_bar_pw(const Arith& ar, typename Arith::Range& range,
+                                            typename Arith::T& x, typename Arith::T& cmp,
+                                            typename Arith::T mu_dt, typename Arith::T sg_sdt,
+                                            typename Arith::T zs) {
+  using T = typename Arith::T;
+  const T xp = x;
+  const T drift = ar.mul(xp, mu_dt);
+  const T diff = ar.mul(ar.mul(xp, sg_sdt), zs);
+  const T inc = ar.add(drift, diff);
+  if constexpr (KAHAN) {  // kahan_accumulate (sde.hpp:85-92)
+    const T y = ar.sub(inc, cmp);
+    const T s = ar.add(xp, y);
+    cmp = ar.sub(ar.sub(s, xp), y);
+    x = s;
+  } else {
+    x = ar.add(xp, inc);
+  }
+  range.track(x);
+}
+
 // One coarse step of both bar legs with packed fp32 pairs (Arith::kPair):
 // fine step n (zb0) and the coarse step (dW = sqrt_dt zb0 + sqrt_dt zb1) as
 // (fine, coarse) pairs -- the two legs are independent, so evaluating them
@@ -296,7 +333,8 @@ __device__ __forceinline__ void step_bar_joint(const Arith& ar, typename Arith::
                                 kStageBarFine);
 }
 
-template <class Arith, bool KAHAN, int LEGS, int TAB, bool CHECKED, bool DUMP, int ZM>
+template <class Arith, bool KAHAN, int LEGS, int TAB, bool CHECKED, bool DUMP, int ZM,
+          bool PW = false>
 __device__ __forceinline__ void simulate(const LevelArgs& A, const TableView& tab,
                                          const double* s_math,
                                          const uint64_t (&local)[Arith::NP],
@@ -330,13 +368,21 @@ __device__ __forceinline__ void simulate(const LevelArgs& A, const TableView& ta
   T xbc = xbf;
   T cmpf = ar.zero(), cmpc = ar.zero();
 
-  constexpr bool kJoint = Arith::kPair && kBar && !kFineOnly && !CHECKED;
+  constexpr bool kJoint = Arith::kPair && kBar && !kFineOnly && !CHECKED && !PW;
+  constexpr bool kPw = PW && Arith::kPow2 && !CHECKED;
+  const T mu_dtf = kPw ? ar.c(A.mu_dtf_l, 0) : T{};
+  const T mu_dtc = kPw ? ar.c(A.mu_dtc_l, 0) : T{};
+  const T sg_sdt = kPw ? ar.c(A.sg_sdt_l, 0) : T{};
   auto hat_fine = [&](const double (&z)[NP], uint64_t n) {
     step_hat<NP, CHECKED>(A, xhf, A.dtf, z, true, fk, n, kStageHatFine);
   };
   auto bar_fine = [&](T zb, uint64_t n) {
-    step_bar<Arith, KAHAN, CHECKED>(ar, range, xbf, cmpf, mu_l, sg_l, dtf_l, sdtf_l, zb, true, fk,
-                                    n, kStageBarFine);
+    if constexpr (kPw) {
+      step_bar_pw<Arith, KAHAN>(ar, range, xbf, cmpf, mu_dtf, sg_sdt, zb);
+    } else {
+      step_bar<Arith, KAHAN, CHECKED>(ar, range, xbf, cmpf, mu_l, sg_l, dtf_l, sdtf_l, zb, true,
+                                      fk, n, kStageBarFine);
+    }
   };
   // coarse legs: dW = sqrt_dt z0 + sqrt_dt z1 in each precision (sde.hpp:259-264)
   auto coarse = [&](const double (&z0)[NP], const double (&z1)[NP], T zb0, T zb1, uint64_t n) {
@@ -347,7 +393,9 @@ __device__ __forceinline__ void simulate(const LevelArgs& A, const TableView& ta
         dw[p] = __dadd_rn(__dmul_rn(A.sdtf, z0[p]), __dmul_rn(A.sdtf, z1[p]));
       step_hat<NP, CHECKED>(A, xhc, A.dtc, dw, false, fk, n, kStageHatCoarse);
     }
-    if constexpr (kBar && !kFineOnly && !kJoint) {
+    if constexpr (kBar && !kFineOnly && kPw) {
+      step_bar_pw<Arith, KAHAN>(ar, range, xbc, cmpc, mu_dtc, sg_sdt, ar.add(zb0, zb1));
+    } else if constexpr (kBar && !kFineOnly && !kJoint) {
       T dw;
       if constexpr (Arith::kPair) {
         const uint64_t p = ar.mul2(pack2(zb0, zb1), pack2(sdtf_l, sdtf_l));
@@ -532,7 +580,7 @@ constexpr int level_min_ctas() {
   const bool exact = (LEGS & 1) != 0 || LEGS == 4 || TAB == kTabNone;
   return ZM == kZGlibc ? LPMC_GLIBC_MIN_CTAS : exact ? LPMC_LEVEL_MIN_CTAS : LPMC_BAR_MIN_CTAS;
 }
-template <class Arith, bool KAHAN, int LEGS, int TAB, bool DUMP, int ZM>
+template <class Arith, bool KAHAN, int LEGS, int TAB, bool DUMP, int ZM, bool PW = false>
 __global__ void __launch_bounds__(kBatch / Arith::NP, level_min_ctas<LEGS, TAB, ZM>())
     level_kernel(const __grid_constant__ LevelArgs A) {
   constexpr int NP = Arith::NP;
@@ -573,7 +621,7 @@ __global__ void __launch_bounds__(kBatch / Arith::NP, level_min_ctas<LEGS, TAB, 
   }
 
   PathEnd<NP> R;
-  simulate<Arith, KAHAN, LEGS, TAB, false, DUMP, ZM>(A, tab, s_math, local, valid, R);
+  simulate<Arith, KAHAN, LEGS, TAB, false, DUMP, ZM, PW>(A, tab, s_math, local, valid, R);
 
   bool any_suspect = false;
 #pragma unroll
@@ -600,6 +648,7 @@ __global__ void __launch_bounds__(kBatch / Arith::NP, level_min_ctas<LEGS, TAB, 
   for (int p = 0; p < NP; ++p) {
     if constexpr (DUMP) {
       if (A.path_out != nullptr && valid[p]) {
+        LPMC_DCHECK(local[p] < A.n_paths);
         double* o = A.path_out + 4 * local[p];
         o[0] = R.hf[p];
         o[1] = R.hc[p];
@@ -622,10 +671,12 @@ __global__ void __launch_bounds__(kBatch / Arith::NP, level_min_ctas<LEGS, TAB, 
     for (int p = 0; p < NP; ++p)
       if (valid[p]) {
         const uint64_t r = local[p] - A.batch0 * kBatch;  // slice-relative
+        LPMC_DCHECK(local[p] < A.n_paths && r < A.n_batches * kBatch);
         A.path_diff[2 * r + 0] = dh[p];
         A.path_diff[2 * r + 1] = db[p];
       }
   }
+  LPMC_DCHECK(blockIdx.x < A.n_batches && count >= 1 && count <= kBatch);
   if (A.batch_acc != nullptr) batch_moments<NP>(dh, db, valid, count, A.batch_acc + 15 * blockIdx.x);
 }
 
@@ -794,11 +845,24 @@ __global__ void __launch_bounds__(kWppThreads) wpp_kernel(const __grid_constant_
 constexpr int kMaxTableK = 1024;
 constexpr int kMaxDynSmem = (kTableRows * kMaxTableK + 1) * 8;  // + 1 / step_w
 
+// Instances with power-of-two step folding (step_bar_pw): production
+// (non-dump) fast-mode launches of the native fp32 arithmetics with bar legs.
+template <class Arith, int LEGS, bool DUMP, int ZM>
+constexpr bool has_pw() {
+  return Arith::kPow2 && !DUMP && ZM == kZFast && LEGS != 1;
+}
+
 template <class Arith, bool KAHAN, int LEGS, int TAB, bool DUMP, int ZM>
 cudaError_t launch_one(const LevelArgs& A, cudaStream_t s) {
   const size_t smem = TAB != kTabNone ? static_cast<size_t>(A.table_words) * sizeof(double) : 0;
-  level_kernel<Arith, KAHAN, LEGS, TAB, DUMP, ZM>
-      <<<static_cast<unsigned>(A.n_batches), kBatch / Arith::NP, smem, s>>>(A);
+  const unsigned grid = static_cast<unsigned>(A.n_batches);
+  if constexpr (has_pw<Arith, LEGS, DUMP, ZM>()) {
+    if (A.bar_pow2) {
+      level_kernel<Arith, KAHAN, LEGS, TAB, DUMP, ZM, true><<<grid, kBatch / Arith::NP, smem, s>>>(A);
+      return cudaGetLastError();
+    }
+  }
+  level_kernel<Arith, KAHAN, LEGS, TAB, DUMP, ZM><<<grid, kBatch / Arith::NP, smem, s>>>(A);
   return cudaGetLastError();
 }
 
@@ -844,8 +908,17 @@ cudaError_t configure_tabs() {
   cudaError_t e = cudaFuncSetAttribute(level_kernel<Arith, KAHAN, LEGS, kTabGeneric, DUMP, ZM>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem);
   if (e != cudaSuccess) return e;
-  return cudaFuncSetAttribute(level_kernel<Arith, KAHAN, LEGS, kTabDyadicLinear, DUMP, ZM>,
-                              cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem);
+  e = cudaFuncSetAttribute(level_kernel<Arith, KAHAN, LEGS, kTabDyadicLinear, DUMP, ZM>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem);
+  if constexpr (has_pw<Arith, LEGS, DUMP, ZM>()) {
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(level_kernel<Arith, KAHAN, LEGS, kTabGeneric, DUMP, ZM, true>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(level_kernel<Arith, KAHAN, LEGS, kTabDyadicLinear, DUMP, ZM, true>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem);
+  }
+  return e;
 }
 
 template <class Arith, bool KAHAN, int LEGS, bool DUMP>

@@ -53,6 +53,25 @@
 #define LPMC_HD inline
 #endif
 
+// -DLPMC_DEVICE_CHECKS (test builds only -- compute-sanitizer is not
+// available on the B200 pool): bounds checks on every table, shared-memory
+// and output index; a failed check prints the condition and traps the kernel,
+// so the calling test fails loudly (tools/gpu_checks.sh).
+#if defined(LPMC_DEVICE_CHECKS) && defined(__CUDA_ARCH__)
+#define LPMC_DCHECK(c)                                                                 \
+  do {                                                                                 \
+    if (!(c)) {                                                                        \
+      printf("LPMC_DCHECK failed %s:%d: %s (block %d thread %d)\n", __FILE__, __LINE__, #c, \
+             static_cast<int>(blockIdx.x), static_cast<int>(threadIdx.x));             \
+      __trap();                                                                        \
+    }                                                                                  \
+  } while (0)
+#else
+#define LPMC_DCHECK(c) \
+  do {                 \
+  } while (0)
+#endif
+
 namespace lpmc_b200 {
 namespace math {
 
@@ -313,6 +332,7 @@ LPMC_HD double erfcx_piecewise(double t, const V& tab) {
   j = j < V::kNRec - 1 ? j : V::kNRec - 1;
   const double s = t - (j + 0.5) * (1.0 / kPerUnit);  // exact: j < 2^10, power-of-two width
 #endif
+  LPMC_DCHECK(j >= 0 && j < V::kNRec);
   const double* rec = tab.erfcx() + V::kRec * j;  // c_D, ..., c_1, c0 hi, c0 lo
   D2 c = load2(rec);
   double q = fmad(c.a, s, c.b);  // c_D s + c_{D-1}

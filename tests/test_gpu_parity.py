@@ -113,9 +113,10 @@ def test_z_tolerance_rejects_8_ulp(gpu, ref):
     zr = ref.exact_inv_cdf(u)
     fast = gpu.device_inv_cdf(u)
     assert np.all(np.abs(fast - zr) <= z_tolerance(u, zr))
-    bumped = np.array([np.nextafter(z, np.inf) for z in fast])
-    for _ in range(7):
-        bumped = np.nextafter(bumped, np.inf)  # fast + 8 ulp
+    away = np.where(fast >= zr, np.inf, -np.inf)  # perturb away from the reference's Z
+    bumped = fast.copy()
+    for _ in range(8):
+        bumped = np.nextafter(bumped, away)  # 8 ulp
     caught = np.abs(bumped - zr) > z_tolerance(u, zr)
     assert caught[np.abs(zr) > 0.5].all()
     assert caught.mean() > 0.55
@@ -248,6 +249,42 @@ def test_moments_bitexact_on_device_paths(gpu, oracle, level, m, approx, kahan, 
     want_seq = oracle.sequential_from_values(dh, db)
     assert [tree.d_hat.state(), tree.d_bar.state(), tree.d_four.state()] == want_tree
     assert [seq.d_hat.state(), seq.d_bar.state(), seq.d_four.state()] == want_seq
+
+
+@pytest.mark.parametrize("level", [2, 4, 6, 12])
+@pytest.mark.parametrize("m,approx,kahan", [(23, "linear:16", False), (23, "linear:16", True),
+                                             (10, "linear:16", False), (10, "cubic:64", True),
+                                             (10, "exact", False), (23, "exact", True)])
+@pytest.mark.parametrize("legs,payoff", [("all", "call"), ("bar", "terminal"),
+                                         ("fine", "terminal")])
+def test_pow2_step_folding_bitexact(gpu, oracle, level, m, approx, kahan, legs, payoff):
+    """Even levels with T = 1 run the native fp32 bar legs with dt, 2dt and
+    sqrt(dt) folded into the model constants (step_bar_pw, lpmc_level.cuh):
+    the production run's moments must equal the restated reductions of the
+    per-path values of the unfolded dump kernel (which test_paths_vs_reference
+    pins to the reference), bitwise; a horizon of 0.75 (no power-of-two
+    steps) takes the unfolded kernels as a control."""
+    n = 3000 if level < 12 else 600
+    for horizon in (1.0, 0.75):
+        model = gpu.make_gbm(0.05, 0.2, 1.0, horizon)
+        sp, tb = spec(gpu, m), table(gpu, approx)
+        ext = {"legs": legs, "payoff": payoff, "strike": 1.0}
+        out = gpu.simulate_paths(model, level, sp, tb, kahan, n, 5, level << 40, **ext)
+        if tb is not None:  # the unfolded bar legs are the oracle's (the reference's) own
+            cfg = oracle.config(level=level, mantissa_bits=m, approx=approx, kahan=kahan, seed=5,
+                                horizon=horizon)
+            own, _, _ = oracle.simulate(cfg, level << 40, n)
+            cols = slice(2, 3) if legs == "fine" else slice(2, 4)
+            assert np.array_equal(bits(out[:, cols]), bits(own[:, cols]))
+        pay = (lambda x: np.maximum(x - 1.0, 0.0)) if payoff == "call" else (lambda x: x)
+        coarse = level > 0 and legs != "fine"
+        dh = pay(out[:, 0]) - (pay(out[:, 1]) if coarse else 0.0)
+        db = pay(out[:, 2]) - (pay(out[:, 3]) if coarse else 0.0)
+        if legs == "bar":
+            dh = np.zeros_like(db)
+        got = gpu.run_coupled_paths(model, level, sp, tb, kahan, n, 5, level << 40, **ext)
+        want = oracle.tree_from_values(dh, db, legs={"all": 3, "bar": 2, "fine": 3}[legs])
+        assert [got.d_hat.state(), got.d_bar.state(), got.d_four.state()] == want, horizon
 
 
 @pytest.mark.parametrize("reduce,n", [("tree", 64 * 262144 + 1000),      # > one 64-chunk slice
