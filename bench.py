@@ -266,6 +266,11 @@ def roofline(L, per_cfg_ms, cfgs, n_local, clk, peaks, n_sm):
         "fp64_lane_ops_per_path_step": pipes["fp64"]["demand_per_path_step"],
         "demands": os.path.relpath(DEMANDS, ROOT), "demands_stale": stale,
         "kernel_source_hash": src_hash,
+        # the FP64 pipe takes a warp-instruction every 2 cycles per SMSP, issue 1 per cycle:
+        # with this instruction mix the FP64 fraction cannot exceed 2 x its issue share
+        "fp64_frac_at_full_issue": min(1.0, 2.0 * pipes["fp64"]["demand_per_path_step"] /
+                                       (32.0 * pipes["issue"]["demand_per_path_step"]))
+        if "issue" in pipes else None,
         "multi_pipe": {"binding": bind, "frac": pipes[bind]["frac"],
                        "ceiling_path_steps_per_s": pipes[bind]["ceiling_path_steps_per_s"],
                        "pipes": pipes, "co_limits": prof.get("co_limits")},
@@ -274,8 +279,10 @@ def roofline(L, per_cfg_ms, cfgs, n_local, clk, peaks, n_sm):
                 "sm__sass_thread_inst_executed_op_{dadd,dmul,dfma}, one lane-op per DFMA as the "
                 "pipe issues it) x the dominant launch's path-steps/s from CUDA events; peak = "
                 "FP64 lane-op rate measured live on this GPU (lpmc_measure_pipe_peaks; "
-                "MEASURED_PEAKS.json has no FP64 figure), in 1e12 lane-ops/s. demands_stale = "
-                "the profiled kernel sources differ from this build."}
+                "MEASURED_PEAKS.json has no FP64 figure), in 1e12 lane-ops/s. "
+                "fp64_frac_at_full_issue = the FP64 fraction this instruction mix would reach "
+                "at 100 % issue (FP64 pipe: one warp-instruction per 2 cycles per SMSP). "
+                "demands_stale = the profiled kernel sources differ from this build."}
 
 
 # ------------------------------------------------------------------ ours ----

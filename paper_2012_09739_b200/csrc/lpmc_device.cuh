@@ -63,8 +63,11 @@ __device__ __forceinline__ uint64_t next_draw(uint64_t& kc) {
   return w >> 11;
 }
 
+// (double)b 2^-53 + 2^-54 (uniform.hpp:40): b < 2^53 converts exactly and the
+// product by 2^-53 is exact, so the reference's one rounding (of the sum) is
+// the FMA's one rounding -- bitwise, one FP64 operation fewer.
 __device__ __forceinline__ double uniform_of(uint64_t b) {
-  return __dadd_rn(__dmul_rn(__ull2double_rn(b), 0x1p-53), 0x1p-54);
+  return __fma_rn(__ull2double_rn(b), 0x1p-53, 0x1p-54);
 }
 
 // erfcx records + 2^(j/64) pairs into (16-byte aligned) shared memory

@@ -26,8 +26,12 @@ top = int(sys.argv[sys.argv.index("--top") + 1]) if "--top" in sys.argv else 60
 args = [a for a in args if a not in (str(units), str(top)) and not re.fullmatch(r"[0-9.e+]+", a)]
 rep, obj, fun = args[:3]
 
-out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
-                     capture_output=True, text=True).stdout
+if rep.endswith(".csv"):  # the source page exported on the GPU box (tools/ncu_capture.sh)
+    with open(rep) as f:
+        out = f.read()
+else:
+    out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
+                         capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(out)))
 hdr = rows[1]
 ia, isrc, iex = hdr.index("Address"), hdr.index("Source"), hdr.index("Instructions Executed")
