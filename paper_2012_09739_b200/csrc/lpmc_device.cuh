@@ -120,17 +120,19 @@ __device__ __forceinline__ double approx_inv(const TableView& t, double u, bool 
   const double v = 1.0 - up;              // exact (Sterbenz)
   double r;
   if constexpr (TAB == kTabDyadicLinear) {
+    // floor(-log2 v) = 1022 - e', e' the biased exponent of the next double
+    // below v (v = 2^k drops a binade, anything else stays): j = fl - 1 =
+    // 1021 - e' from one 64-bit decrement and a shift.  Records j >= K are
+    // the host's tail records (c0 = tail, c1 = 0: tail + 0 * 0 = tail), so
+    // neither the reference's clamp nor its tail test needs an instruction.
     const uint64_t vb = static_cast<uint64_t>(__double_as_longlong(v));
-    const int e = static_cast<int>(vb >> 52) - 1023;
-    const int fl = (vb & 0xFFFFFFFFFFFFFull) == 0 ? -e : -e - 1;  // floor(-log2 v) >= 1
-    const int j = min(fl - 1, t.K - 1);
-    LPMC_DCHECK(j >= 0 && j < t.K);
-    const double* b = t.base + 6 * j;
+    const int eb = static_cast<int>((vb - 1) >> 52);
+    LPMC_DCHECK(1021 - eb >= 0 && 1021 - eb < kDyadicRecords);
+    const double* b = t.base + 6 * (1021 - eb);
     const math::D2 cw = math::load2(b);
     const math::D2 c01 = math::load2(b + 2);
     const double s = __fma_rn(up, cw.b, cw.a);
     r = __dadd_rn(c01.a, __dmul_rn(c01.b, s));
-    r = fl >= t.K + 1 ? t.tail : r;  // w >= w_max: clamped tail
   } else if (t.dyadic) {
     const uint64_t vb = static_cast<uint64_t>(__double_as_longlong(v));
     const int e = static_cast<int>(vb >> 52) - 1023;

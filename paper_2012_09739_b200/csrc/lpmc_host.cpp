@@ -244,12 +244,20 @@ lpmc_status prepare_table(const lpmc_invcdf_table* t, HostTable* out, lpmc_error
   out->simple = simple ? 1 : 0;
   auto left = [&](int j) { return j == 0 ? 0.5 : t->breakpoints[j - 1]; };
   if (dyadic) {  // records {3 - 2^(j+3), 2^(j+3), c0, c1, c2, c3} (dev::approx_inv)
-    out->rows.assign(static_cast<size_t>(kDyadicRecord) * K, 0.0);
-    for (int j = 0; j < K; ++j) {
+    // K interval records, then tail records {0, 0, tail, 0, 0, 0} up to
+    // j = 52 (v = 1 - u' >= 2^-53): the straight-line dyadic-linear
+    // evaluation indexes j = floor(-log2 v) - 1 without a clamp or a tail
+    // select, and a tail record gives tail + 0 * 0 = tail exactly.
+    out->rows.assign(static_cast<size_t>(kDyadicRecord) * kDyadicRecords, 0.0);
+    for (int j = 0; j < kDyadicRecords; ++j) {
       double* r = out->rows.data() + kDyadicRecord * j;
-      r[0] = 3.0 - std::ldexp(1.0, j + 3);
-      r[1] = std::ldexp(1.0, j + 3);
-      for (int c = 0; c < 4; ++c) r[2 + c] = t->coeff[4 * j + c];
+      if (j < K) {
+        r[0] = 3.0 - std::ldexp(1.0, j + 3);
+        r[1] = std::ldexp(1.0, j + 3);
+        for (int c = 0; c < 4; ++c) r[2 + c] = t->coeff[4 * j + c];
+      } else {
+        r[2] = t->tail_value;
+      }
     }
   } else {  // records {a, b - a, c0, c1 (, c2, c3)}, thresholds, 1 / step_w
     const int W = out->degree == 3 ? 6 : 4;

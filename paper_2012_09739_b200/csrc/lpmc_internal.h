@@ -21,12 +21,16 @@ enum class BarArith : int {
 };
 
 // Device table layouts (doubles):
-//   dyadic (K <= 32): K records {3 - 2^(j+3), 2^(j+3), c0, c1, c2, c3} (kDyadicRecord)
+//   dyadic (K <= 32): K records {3 - 2^(j+3), 2^(j+3), c0, c1, c2, c3} (kDyadicRecord),
+//            then tail records {0, 0, tail, 0, 0, 0} up to kDyadicRecords
 //   general: K records {a_j, b_j - a_j, c0, c1} (degree 1) or {.., c2, c3}
 //            (degree 3), then the v-thresholds T_1..T_{K-1}, T_tail, then
 //            1 / step_w: at most kTableRows * K + 1 doubles
 constexpr int kTableRows = 7;
 constexpr int kDyadicRecord = 6;
+// dyadic tables carry records j = 0..52 (K interval records, then tail
+// records): j = floor(-log2 v) - 1 for every v = 1 - u' in [2^-53, 1/2]
+constexpr int kDyadicRecords = 53;
 
 #ifdef __CUDACC__
 #define LPMC_KEY_HD __host__ __device__

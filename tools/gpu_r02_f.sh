@@ -2,7 +2,7 @@
 # ncu captures, the C4 demands -> bench (the driver's own command lines),
 # the reference arm, the launch list, the Z ratio.
 cd $GRAFT_REPO_ROOT
-O=gpurun_out/r02f; mkdir -p $O
+O=gpurun_out/${RUN:-r02f}; mkdir -p $O
 timeout 1500 python -m pytest tests -m gpu -q -p no:cacheprovider > $O/pytest_gpu.log 2>&1; echo "pytest exit $?" >> $O/pytest_gpu.log
 t() { echo "$1 $(timeout 300 python tools/profile_level.py --time "${@:2}" | tail -1)" >> $O/timing.log; }
 t c4-l12-fp16 --level 12 --prec fp16 --payoff call --n 4194304 --base $((12<<40))
