@@ -332,6 +332,14 @@ lpmc_status lpmc_device_math(int32_t op, const double* in, uint64_t n,
 /* Host evaluation of the same erfc core (bitwise equal to op 3). */
 double lpmc_erfc_core(double t);
 /*
+ * Host evaluation of the direct table behind op 0 (the default exact inverse
+ * CDF, gaussian.hpp:59-65 to 0.42 eps (v / pdf(z) + |z|)): Phi^-1(v) for
+ * v = min(u, 1 - u) in [2^-15, 1/2], bitwise the device's value.
+ * *in_table = 0 (and NaN returned) for v outside that range, where the device
+ * takes the Halley step on the erfc core instead.
+ */
+double lpmc_phi_inv_direct_core(double v, int32_t* in_table);
+/*
  * Host evaluation of the restated glibc routines behind the reference's exact
  * Gaussian (the LPMC_EXACT_Z_GLIBC device path, same code): op 0 = exp,
  * 1 = log, 2 = erfc, 3 = exact_inv_cdf (gaussian.hpp:59-65).  *ok = 0 where

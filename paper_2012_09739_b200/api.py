@@ -607,6 +607,15 @@ def erfc_core(t: float) -> float:
     return float(N.load().lpmc_erfc_core(float(t)))
 
 
+def phi_inv_direct_core(v: float) -> Optional[float]:
+    """Host evaluation of the direct table of the default exact inverse CDF
+    (bitwise the device's value) for v = min(u, 1 - u) in [2^-15, 1/2]; None
+    outside the table."""
+    ok = C.c_int32(0)
+    z = float(N.load().lpmc_phi_inv_direct_core(float(v), C.byref(ok)))
+    return z if ok.value else None
+
+
 def glibc_math(op: str, x: float) -> Optional[float]:
     """Host evaluation of the restated glibc routine (op in {"exp", "log",
     "erfc", "inv_cdf"}), bitwise the device's LPMC_EXACT_Z_GLIBC path; None

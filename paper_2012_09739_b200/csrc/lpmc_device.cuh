@@ -125,10 +125,14 @@ __device__ __forceinline__ double approx_inv(const TableView& t, double u, bool 
     // 1021 - e' from one 64-bit decrement and a shift.  Records j >= K are
     // the host's tail records (c0 = tail, c1 = 0: tail + 0 * 0 = tail), so
     // neither the reference's clamp nor its tail test needs an instruction.
+    // v == 0 (u == 1, where the reference throws and the path is replayed
+    // checked; or the smallest draw u = 2^-54, whose 1 - u rounds to 1 and
+    // which the reference maps to the tail value): vb - 1 wraps, the
+    // unsigned min sends it to the last tail record.
     const uint64_t vb = static_cast<uint64_t>(__double_as_longlong(v));
-    const int eb = static_cast<int>((vb - 1) >> 52);
-    LPMC_DCHECK(1021 - eb >= 0 && 1021 - eb < kDyadicRecords);
-    const double* b = t.base + 6 * (1021 - eb);
+    const uint32_t eb = static_cast<uint32_t>((vb - 1) >> 52);
+    const uint32_t j = min(1021u - eb, static_cast<uint32_t>(kDyadicRecords - 1));
+    const double* b = t.base + 6 * j;
     const math::D2 cw = math::load2(b);
     const math::D2 c01 = math::load2(b + 2);
     const double s = __fma_rn(up, cw.b, cw.a);
@@ -466,14 +470,30 @@ __device__ __forceinline__ double warp_sum(double x, int first) {
   return x;
 }
 
-template <int NP>
+// GROUPS > 1 (the persistent level kernel): GROUPS independent batches per
+// CTA, one per group of kBatch / NP threads; `tid` is the thread's index in
+// its group, `grp` the group; the groups synchronise on their own named
+// barriers (1 + grp) and use their own scratch rows.
+template <int GROUPS>
+__device__ __forceinline__ void group_sync(int grp) {
+  if constexpr (GROUPS == 1) {
+    __syncthreads();
+  } else {
+    asm volatile("bar.sync %0, %1;" ::"r"(1 + grp), "r"(static_cast<int>(blockDim.x) / GROUPS) : "memory");
+  }
+}
+
+template <int NP, int GROUPS = 1>
 __device__ void batch_moments(const double (&vh)[NP], const double (&vb)[NP],
-                              const bool (&valid)[NP], int count, double* out15) {
-  __shared__ double s_grp[9][8];
-  __shared__ double s_mean[3];
+                              const bool (&valid)[NP], int count, double* out15,
+                              int tid = static_cast<int>(threadIdx.x), int grp = 0) {
+  __shared__ double s_grp_all[GROUPS][9][8];
+  __shared__ double s_mean_all[GROUPS][3];
+  double(&s_grp)[9][8] = s_grp_all[grp];
+  double(&s_mean)[3] = s_mean_all[grp];
   constexpr int kWarps = kBatch / NP / 32;
-  const int lane = threadIdx.x & 31;
-  const int warp = threadIdx.x >> 5;
+  const int lane = tid & 31;
+  const int warp = tid >> 5;
   double v[3][NP];
 #pragma unroll
   for (int p = 0; p < NP; ++p) {
@@ -489,7 +509,7 @@ __device__ void batch_moments(const double (&vh)[NP], const double (&vb)[NP],
       LPMC_DCHECK(warp + p * kWarps < 8);
       if (lane == 0) s_grp[f][warp + p * kWarps] = s;
     }
-  __syncthreads();
+  group_sync<GROUPS>(grp);
   if (warp == 0) {
 #pragma unroll
     for (int f = 0; f < 3; ++f) {
@@ -497,7 +517,7 @@ __device__ void batch_moments(const double (&vh)[NP], const double (&vb)[NP],
       if (lane == 0) s_mean[f] = __ddiv_rn(g, static_cast<double>(count));
     }
   }
-  __syncthreads();
+  group_sync<GROUPS>(grp);
   const double mean[3] = {s_mean[0], s_mean[1], s_mean[2]};
 #pragma unroll
   for (int f = 0; f < 3; ++f)
@@ -516,7 +536,7 @@ __device__ void batch_moments(const double (&vh)[NP], const double (&vb)[NP],
         s_grp[3 * f + 2][warp + p * kWarps] = s4;
       }
     }
-  __syncthreads();
+  group_sync<GROUPS>(grp);
   if (warp == 0) {
 #pragma unroll
     for (int q = 0; q < 9; ++q) {
@@ -531,6 +551,11 @@ __device__ void batch_moments(const double (&vh)[NP], const double (&vb)[NP],
       }
     }
   }
+  // persistent callers: the next batch's first pass rewrites s_grp rows 0..2
+  // only after its own first barrier, which every thread of the group reaches
+  // after reading s_mean and the final rows above -- except warp 0's reads of
+  // rows 0..8 just above, hence one more barrier.
+  if constexpr (GROUPS > 1) group_sync<GROUPS>(grp);
 }
 
 // ----------------------------------------------------------- moments -------

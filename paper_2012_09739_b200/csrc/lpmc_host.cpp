@@ -1975,6 +1975,14 @@ double lpmc_erfc_core(double t) {
   return math::erfc_fast(t, math::kMathTableHost);
 }
 
+double lpmc_phi_inv_direct_core(double v, int32_t* in_table) {
+  bool tail = true;
+  double z = std::nan("");
+  if (v > 0.0 && v <= 0.5) z = math::phi_inv_direct(v, math::DirectTab{math::kDirectHost}, &tail);
+  if (in_table != nullptr) *in_table = tail ? 0 : 1;
+  return tail ? std::nan("") : z;
+}
+
 static_assert(LPMC_EXACT_Z_FAST == 0 && LPMC_EXACT_Z_GLIBC == 1, "dev::kZFast / kZGlibc");
 
 double lpmc_glibc_math(int32_t op, double x, int32_t* ok) {

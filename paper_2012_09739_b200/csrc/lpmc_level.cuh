@@ -97,7 +97,43 @@ __device__ __forceinline__ void draw_uniforms(uint64_t (&kc)[NP], Uniforms<H * N
 // wavefronts but leaves fp32 levels within 0.3 % and slows the emulated-fp16
 // kernel by 3 % (the 8x table copies shrink L1 under the replay call's
 // stack), so the flat layout stays the default.
-#ifndef LPMC_LANE_TABLES
+#if !defined(LPMC_HALLEY_Z)
+// The direct table (math::phi_inv_direct).  The fused level kernel is
+// persistent where it draws exact Gaussians in the fast mode: one CTA per SM,
+// kGroups groups of kBatch / NP threads, each group looping over batches, and
+// eight lane-private copies of the table (144 KB) staged once per CTA -- the
+// gathers are then free of bank conflicts (math::LaneDirectTab).  With one
+// flat copy per 256-thread CTA the shared-memory crossbar bound the kernel:
+// fp16 and fp32 legs ran at the same 1.68e11 path-steps/s
+// (gpurun_out/r02g), 55 wavefronts per warp-step against 37 issue cycles.
+// -DLPMC_FLAT_DIRECT keeps that one-batch-per-CTA form (A/B).  The
+// warp-per-path kernel stages the flat table.
+#ifndef LPMC_FLAT_DIRECT
+#define LPMC_PERSISTENT 1
+using FastTab = math::LaneDirectTab;
+constexpr int kFastWords = math::kLaneDirectWords;
+__device__ __forceinline__ void stage_fast(double* s) {
+  for (int i = threadIdx.x; i < kFastWords; i += blockDim.x)
+    s[i] = math::kDirectTable[math::lane_direct_source(i)];
+}
+__device__ __forceinline__ FastTab fast_tab(const double* s) {
+  return FastTab{s + 2 * static_cast<int>(threadIdx.x & (math::kLaneCopies - 1))};
+}
+#else
+using FastTab = math::DirectTab;
+constexpr int kFastWords = math::kDirectWords;
+__device__ __forceinline__ void stage_fast(double* s) {
+  for (int i = threadIdx.x; i < kFastWords; i += blockDim.x) s[i] = math::kDirectTable[i];
+}
+__device__ __forceinline__ FastTab fast_tab(const double* s) { return FastTab{s}; }
+#endif
+using WppTab = math::DirectTab;
+constexpr int kWppFastWords = math::kDirectWords;
+__device__ __forceinline__ void stage_wpp(double* s) {
+  for (int i = threadIdx.x; i < kWppFastWords; i += blockDim.x) s[i] = math::kDirectTable[i];
+}
+__device__ __forceinline__ WppTab wpp_tab(const double* s) { return WppTab{s}; }
+#elif !defined(LPMC_LANE_TABLES)
 using FastTab = math::FlatTab;
 constexpr int kFastWords = kFastMathWords;
 __device__ __forceinline__ void stage_fast(double* s) { stage_math(s, kFastMathWords); }
@@ -107,6 +143,12 @@ using FastTab = math::LaneTab;
 constexpr int kFastWords = kLaneWords;
 __device__ __forceinline__ void stage_fast(double* s) { stage_lane(s); }
 __device__ __forceinline__ FastTab fast_tab(const double* s) { return math::lane_tab(s); }
+#endif
+#ifdef LPMC_HALLEY_Z
+using WppTab = FastTab;
+constexpr int kWppFastWords = kFastWords;
+__device__ __forceinline__ void stage_wpp(double* s) { stage_fast(s); }
+__device__ __forceinline__ WppTab wpp_tab(const double* s) { return fast_tab(s); }
 #endif
 
 // Exact-Gaussian mode of a level instance (values of LPMC_EXACT_Z_*).
@@ -152,13 +194,33 @@ __device__ __forceinline__ void gen_draws(const LevelArgs& A, const TableView& t
       v[d] = ng ? 1.0 - u[d] : u[d];  // exact (gaussian.hpp:63)
       neg |= (ng ? 1u : 0u) << d;
     }
+#if !defined(LPMC_HALLEY_Z)
+    (void)x0;
+    if constexpr (CHECKED) {
+      // the rare exact replay (also the warp-per-path kernel's, which stages
+      // the flat layout): the same table straight from global memory
+      const math::DirectTab gt{math::kDirectTable};
+      if constexpr (PREFETCH) draw_uniforms<NP, H, CHECKED>(kc, next);
+      math::phi_inv_direct_multi<D>(v, neg, zz, gt, mid);
+    } else {
+      const FastTab lt = fast_tab(s_math);  // staged by stage_fast
+#if defined(LPMC_DIRECT_MID_FIRST)  // legs, then the RNG, then the polynomials
+      mid();
+      if constexpr (PREFETCH) draw_uniforms<NP, H, CHECKED>(kc, next);
+      math::phi_inv_direct_multi<D>(v, neg, zz, lt);
+#else  // the previous batch's legs in the polynomials' basic block
+      if constexpr (PREFETCH) draw_uniforms<NP, H, CHECKED>(kc, next);
+      math::phi_inv_direct_multi<D>(v, neg, zz, lt, mid);
+#endif
+    }
+#elif !defined(LPMC_MID_LATE)  // the previous batch's legs run beside the fp32 initial guesses
     const FastTab lt = fast_tab(s_math);  // staged by stage_fast
-#ifndef LPMC_MID_LATE  // the previous batch's legs run beside the fp32 initial guesses
     mid();
     math::phi_inv_stage1<D>(v, x0);
     if constexpr (PREFETCH) draw_uniforms<NP, H, CHECKED>(kc, next);
     math::phi_inv_stage2<D, CHECKED>(v, x0, neg, cur.half, zz, lt);
 #else
+    const FastTab lt = fast_tab(s_math);  // staged by stage_fast
     math::phi_inv_stage1<D>(v, x0);
     if constexpr (PREFETCH) draw_uniforms<NP, H, CHECKED>(kc, next);
     math::phi_inv_stage2<D, CHECKED>(v, x0, neg, cur.half, zz, lt, mid);
@@ -576,28 +638,58 @@ __device__ __noinline__ void replay_checked(const LevelArgs& A, TableView tab,
 #define LPMC_GLIBC_MIN_CTAS 4
 #endif
 template <int LEGS, int TAB, int ZM>
-constexpr int level_min_ctas() {
+__host__ __device__ constexpr int level_min_ctas() {
   const bool exact = (LEGS & 1) != 0 || LEGS == 4 || TAB == kTabNone;
   return ZM == kZGlibc ? LPMC_GLIBC_MIN_CTAS : exact ? LPMC_LEVEL_MIN_CTAS : LPMC_BAR_MIN_CTAS;
 }
+
+// Persistent instances: those that draw exact Gaussians in the fast mode.
+// kGroups batches in flight per CTA, one CTA per SM (the lane-private table
+// fills most of its shared memory); group g of CTA c runs batches
+// c + g gridDim.x, then every kGroups gridDim.x-th.
+constexpr int kGroups = 3;
+template <int LEGS, int TAB, int ZM>
+__host__ __device__ constexpr bool level_persistent() {
+#ifdef LPMC_PERSISTENT
+  return ZM == kZFast && ((LEGS & 1) != 0 || LEGS == 4 || TAB == kTabNone);
+#else
+  return false;
+#endif
+}
+template <class Arith, int LEGS, int TAB, int ZM>
+__host__ __device__ constexpr int level_threads() {
+  return (level_persistent<LEGS, TAB, ZM>() ? kGroups : 1) * (kBatch / Arith::NP);
+}
+template <int LEGS, int TAB, int ZM>
+__host__ __device__ constexpr int level_ctas() {
+  return level_persistent<LEGS, TAB, ZM>() ? 1 : level_min_ctas<LEGS, TAB, ZM>();
+}
+
 template <class Arith, bool KAHAN, int LEGS, int TAB, bool DUMP, int ZM, bool PW = false>
-__global__ void __launch_bounds__(kBatch / Arith::NP, level_min_ctas<LEGS, TAB, ZM>())
+__global__ void __launch_bounds__(level_threads<Arith, LEGS, TAB, ZM>(), level_ctas<LEGS, TAB, ZM>())
     level_kernel(const __grid_constant__ LevelArgs A) {
   constexpr int NP = Arith::NP;
   constexpr bool kFineOnly = LEGS == 4;
   constexpr bool kHat = (LEGS & 1) != 0 || kFineOnly;
   constexpr bool kBar = (LEGS & 2) != 0 || kFineOnly;
   constexpr bool kNeedExact = kHat || TAB == kTabNone;
+  constexpr bool kPersist = level_persistent<LEGS, TAB, ZM>();
+  constexpr int kG = kPersist ? kGroups : 1;
+  constexpr int kGroupThreads = kBatch / NP;
 
-  extern __shared__ __align__(16) double s_table[];
-  // glibc mode: the flat tables incl. glibc's; fast mode: the lane layout
+  // dynamic shared memory: [the lane-private direct table (persistent
+  // instances)] [the approximation table]; static: the flat fast-mode or
+  // glibc-mode tables of the one-batch-per-CTA instances
+  extern __shared__ __align__(16) double s_dyn[];
   constexpr int kStaged = ZM == kZGlibc ? kMathWords : kFastWords;
-  __shared__ __align__(16) double s_math[kNeedExact ? kStaged : 2];
+  __shared__ __align__(16) double s_static[(kNeedExact && !kPersist) ? kStaged : 2];
+  const double* s_math = kPersist ? s_dyn : s_static;
+  double* s_table = s_dyn + (kPersist ? kFastWords : 0);
   if constexpr (kNeedExact) {
     if constexpr (ZM == kZGlibc) {
-      stage_math(s_math, kStaged);
+      stage_math(s_static, kStaged);
     } else {
-      stage_fast(s_math);
+      stage_fast(kPersist ? s_dyn : s_static);
     }
   }
   TableView tab{};
@@ -607,7 +699,13 @@ __global__ void __launch_bounds__(kBatch / Arith::NP, level_min_ctas<LEGS, TAB, 
   }
   __syncthreads();
 
-  const uint64_t batch = A.batch0 + blockIdx.x;
+  const int grp = kPersist ? static_cast<int>(threadIdx.x) / kGroupThreads : 0;
+  const int tid = kPersist ? static_cast<int>(threadIdx.x) - grp * kGroupThreads
+                           : static_cast<int>(threadIdx.x);
+  const uint64_t stride = kPersist ? static_cast<uint64_t>(kG) * gridDim.x : A.n_batches;
+  for (uint64_t slot_b = blockIdx.x + static_cast<uint64_t>(grp) * gridDim.x; slot_b < A.n_batches;
+       slot_b += stride) {
+  const uint64_t batch = A.batch0 + slot_b;
   const uint64_t first = batch * kBatch;
   const uint64_t left = A.n_paths - first;
   const int count = left < kBatch ? static_cast<int>(left) : kBatch;
@@ -615,7 +713,7 @@ __global__ void __launch_bounds__(kBatch / Arith::NP, level_min_ctas<LEGS, TAB, 
   bool valid[NP];
 #pragma unroll
   for (int p = 0; p < NP; ++p) {
-    const int slot = threadIdx.x + p * blockDim.x;
+    const int slot = tid + p * kGroupThreads;
     local[p] = first + slot;
     valid[p] = slot < count;
   }
@@ -676,8 +774,10 @@ __global__ void __launch_bounds__(kBatch / Arith::NP, level_min_ctas<LEGS, TAB, 
         A.path_diff[2 * r + 1] = db[p];
       }
   }
-  LPMC_DCHECK(blockIdx.x < A.n_batches && count >= 1 && count <= kBatch);
-  if (A.batch_acc != nullptr) batch_moments<NP>(dh, db, valid, count, A.batch_acc + 15 * blockIdx.x);
+  LPMC_DCHECK(slot_b < A.n_batches && count >= 1 && count <= kBatch);
+  if (A.batch_acc != nullptr)
+    batch_moments<NP, kG>(dh, db, valid, count, A.batch_acc + 15 * slot_b, tid, grp);
+  }
 }
 
 // -------------------------------------------------- warp per path ---------
@@ -709,13 +809,13 @@ __global__ void __launch_bounds__(kWppThreads) wpp_kernel(const __grid_constant_
 
   extern __shared__ __align__(16) double s_table[];
   // glibc mode: the flat tables incl. glibc's; fast mode: the lane layout
-  constexpr int kStaged = ZM == kZGlibc ? kMathWords : kFastWords;
+  constexpr int kStaged = ZM == kZGlibc ? kMathWords : kWppFastWords;
   __shared__ __align__(16) double s_math[kNeedExact ? kStaged : 2];
   if constexpr (kNeedExact) {
     if constexpr (ZM == kZGlibc) {
       stage_math(s_math, kStaged);
     } else {
-      stage_fast(s_math);
+      stage_wpp(s_math);
     }
   }
   TableView tab{};
@@ -757,7 +857,7 @@ __global__ void __launch_bounds__(kWppThreads) wpp_kernel(const __grid_constant_
       if constexpr (ZM == kZGlibc) {
         glibc::inv_cdf_multi<1>(u, z, s_math);
       } else {
-        math::phi_inv_multi<1>(u, z, fast_tab(s_math));
+        math::phi_inv_multi<1>(u, z, wpp_tab(s_math));
       }
     }
     T zb = ar.zero();
@@ -852,17 +952,41 @@ constexpr bool has_pw() {
   return Arith::kPow2 && !DUMP && ZM == kZFast && LEGS != 1;
 }
 
+// SMs of the current device (cached per device ordinal).
+inline cudaError_t sm_count(int* out) {
+  static int cache[64] = {};
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev >= 0 && dev < 64 && cache[dev] > 0) {
+    *out = cache[dev];
+    return cudaSuccess;
+  }
+  e = cudaDeviceGetAttribute(out, cudaDevAttrMultiProcessorCount, dev);
+  if (e == cudaSuccess && dev >= 0 && dev < 64) cache[dev] = *out;
+  return e;
+}
+
 template <class Arith, bool KAHAN, int LEGS, int TAB, bool DUMP, int ZM>
 cudaError_t launch_one(const LevelArgs& A, cudaStream_t s) {
-  const size_t smem = TAB != kTabNone ? static_cast<size_t>(A.table_words) * sizeof(double) : 0;
-  const unsigned grid = static_cast<unsigned>(A.n_batches);
+  constexpr bool kPersist = level_persistent<LEGS, TAB, ZM>();
+  constexpr int kThreads = level_threads<Arith, LEGS, TAB, ZM>();
+  const size_t smem = (TAB != kTabNone ? static_cast<size_t>(A.table_words) * sizeof(double) : 0) +
+                      (kPersist ? static_cast<size_t>(kFastWords) * sizeof(double) : 0);
+  unsigned grid = static_cast<unsigned>(A.n_batches);
+  if constexpr (kPersist) {  // one CTA per SM, each group looping over batches
+    int sms = 0;
+    const cudaError_t e = sm_count(&sms);
+    if (e != cudaSuccess) return e;
+    grid = A.n_batches < static_cast<uint64_t>(sms) ? grid : static_cast<unsigned>(sms);
+  }
   if constexpr (has_pw<Arith, LEGS, DUMP, ZM>()) {
     if (A.bar_pow2) {
-      level_kernel<Arith, KAHAN, LEGS, TAB, DUMP, ZM, true><<<grid, kBatch / Arith::NP, smem, s>>>(A);
+      level_kernel<Arith, KAHAN, LEGS, TAB, DUMP, ZM, true><<<grid, kThreads, smem, s>>>(A);
       return cudaGetLastError();
     }
   }
-  level_kernel<Arith, KAHAN, LEGS, TAB, DUMP, ZM><<<grid, kBatch / Arith::NP, smem, s>>>(A);
+  level_kernel<Arith, KAHAN, LEGS, TAB, DUMP, ZM><<<grid, kThreads, smem, s>>>(A);
   return cudaGetLastError();
 }
 
@@ -905,18 +1029,31 @@ cudaError_t launch_level(const LevelArgs& A, bool kahan, bool dump, cudaStream_t
 
 template <class Arith, bool KAHAN, int LEGS, bool DUMP, int ZM>
 cudaError_t configure_tabs() {
+  // persistent instances add the lane-private direct table
+  constexpr int kGen = kMaxDynSmem + (level_persistent<LEGS, kTabGeneric, ZM>() ? kFastWords * 8 : 0);
+  constexpr int kDyn = kMaxDynSmem + (level_persistent<LEGS, kTabDyadicLinear, ZM>() ? kFastWords * 8 : 0);
   cudaError_t e = cudaFuncSetAttribute(level_kernel<Arith, KAHAN, LEGS, kTabGeneric, DUMP, ZM>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem);
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, kGen);
   if (e != cudaSuccess) return e;
+  if constexpr (level_persistent<LEGS, kTabNone, ZM>()) {  // no table: the direct table alone
+    e = cudaFuncSetAttribute(level_kernel<Arith, KAHAN, LEGS, kTabNone, DUMP, ZM>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, kFastWords * 8);
+    if (e != cudaSuccess) return e;
+    if constexpr (has_pw<Arith, LEGS, DUMP, ZM>()) {
+      e = cudaFuncSetAttribute(level_kernel<Arith, KAHAN, LEGS, kTabNone, DUMP, ZM, true>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, kFastWords * 8);
+      if (e != cudaSuccess) return e;
+    }
+  }
   e = cudaFuncSetAttribute(level_kernel<Arith, KAHAN, LEGS, kTabDyadicLinear, DUMP, ZM>,
-                           cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem);
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, kDyn);
   if constexpr (has_pw<Arith, LEGS, DUMP, ZM>()) {
     if (e != cudaSuccess) return e;
     e = cudaFuncSetAttribute(level_kernel<Arith, KAHAN, LEGS, kTabGeneric, DUMP, ZM, true>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem);
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, kGen);
     if (e != cudaSuccess) return e;
     e = cudaFuncSetAttribute(level_kernel<Arith, KAHAN, LEGS, kTabDyadicLinear, DUMP, ZM, true>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem);
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, kDyn);
   }
   return e;
 }
@@ -929,6 +1066,17 @@ cudaError_t configure_one() {
   } else {
     if (e != cudaSuccess) return e;
     return configure_tabs<Arith, KAHAN, LEGS, DUMP, kZGlibc>();
+  }
+}
+
+// The carrier's hat-only instances (LEGS == 1, no table).
+template <class Arith, bool DUMP>
+cudaError_t configure_hat_only() {
+  if constexpr (level_persistent<1, kTabNone, kZFast>()) {
+    return cudaFuncSetAttribute(level_kernel<Arith, false, 1, kTabNone, DUMP, kZFast>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, kFastWords * 8);
+  } else {
+    return cudaSuccess;
   }
 }
 

@@ -19,6 +19,9 @@ cudaError_t launch_level_carrier(const LevelArgs& A, bool kahan, bool dump, void
 cudaError_t configure_level_carrier() {
   cudaError_t e = math::upload_math_constants();
   if (e == cudaSuccess) e = dev::configure_level<dev::ArithCarrier>();
+  // the hat-only instances (LEGS == 1, launched above)
+  if (e == cudaSuccess) e = dev::configure_hat_only<dev::ArithCarrier, false>();
+  if (e == cudaSuccess) e = dev::configure_hat_only<dev::ArithCarrier, true>();
   return e;
 }
 

@@ -46,6 +46,7 @@
 #include "lpmc_math_coef.h"
 #endif
 #include "lpmc_x0f_coef.h"
+#include "lpmc_direct_coef.h"
 
 #ifdef __CUDACC__
 #define LPMC_HD __host__ __device__ __forceinline__
@@ -193,7 +194,18 @@ constexpr int kGlibcWords = 512;
 constexpr int kMathTableWords = kGlibcOff + kGlibcWords;  // one shared-memory block
 constexpr double kFastTMax = 6.5;  // the erfcx intervals cover [0, 6.5) (host core)
 
+// The direct table of the fast exact Gaussian (tools/fit_direct.py):
+// Phi^-1 on [2^-(B+1), 1/2] as degree-8 polynomials on 16 sub-intervals per
+// binade, the record index read off v's high word.
+constexpr int kDirectRow = LPMC_DIRECT_ROW;
+constexpr int kDirectN = LPMC_DIRECT_N;
+constexpr int kDirectWords = kDirectRow * kDirectN;
+constexpr int kDirectShift = 20 - LPMC_DIRECT_S;  // high-word bits below the index
+constexpr uint32_t kDirectBase = static_cast<uint32_t>(1023 - (LPMC_DIRECT_B + 1)) << LPMC_DIRECT_S;
+static_assert(LPMC_DIRECT_DEG == 8 && LPMC_DIRECT_ROW == 10, "phi_inv_direct reads c8..c1, c0_lo, c0_hi as five quads");
+
 // erfcx records, the 2^(j/64) hi/lo pairs, the glibc exp and log tables (host copy)
+alignas(16) static const double kDirectHost[kDirectWords] = {LPMC_DIRECT_COEF_LIST};
 static const double kMathTableHost[kMathTableWords] = {LPMC_ERFCX_COEF_LIST, LPMC_EXP_TAB_LIST,
                                                        LPMC_GLIBC_EXP_TAB, LPMC_GLIBC_LOG_TAB};
 
@@ -201,8 +213,10 @@ static const double kMathTableHost[kMathTableWords] = {LPMC_ERFCX_COEF_LIST, LPM
 // TU-local (static): every kernel translation unit has its own copy and
 // uploads it in its configure function (upload_math_constants).
 static __constant__ double kMath[kMathCount];
-static __device__ const double kMathTable[kMathTableWords] = {
+static __device__ __align__(16) const double kMathTable[kMathTableWords] = {
     LPMC_ERFCX_COEF_LIST, LPMC_EXP_TAB_LIST, LPMC_GLIBC_EXP_TAB, LPMC_GLIBC_LOG_TAB};
+
+static __device__ __align__(16) const double kDirectTable[kDirectWords] = {LPMC_DIRECT_COEF_LIST};
 
 static inline cudaError_t upload_math_constants() {
   return cudaMemcpyToSymbol(kMath, kMathHost, sizeof(kMathHost));
@@ -276,6 +290,60 @@ struct LaneTab {
   LPMC_HD const double* erfcx() const { return e; }
   LPMC_HD const double* expt() const { return x; }
 };
+
+// The direct table: flat (kDirectHost / kDirectTable or a shared-memory copy:
+// the small kernels, the warp-per-path kernel, the host) or eight
+// lane-private copies in shared memory (the persistent level kernel): quad q
+// of record j of copy c at 16-byte index (5 j + q) 8 + c, every lane reads
+// copy c = lane % 8, so the eight lanes of each quarter-warp phase of a
+// 128-bit load hit eight different bank quads whatever records they gather
+// -- conflict-free by construction, no extra instruction (the copy offset
+// sits in the per-thread base pointer, record stride and quad offsets are
+// immediates).  225 records x 80 B x 8 = 144 KB: one table per SM.
+struct DirectTab {
+  const double* t;
+  static constexpr int kRec = kDirectRow;  // doubles between records
+  static constexpr int kStep = 1;          // in-record offset multiplier
+};
+struct LaneDirectTab {
+  const double* t;  // copy c (base + 2 c)
+  static constexpr int kRec = kDirectRow * kLaneCopies;
+  static constexpr int kStep = kLaneCopies;
+};
+constexpr int kLaneDirectWords = kDirectWords * kLaneCopies;
+// source word of lane-layout word i: 16 doubles = 8 copies of one quad
+LPMC_HD int lane_direct_source(int i) { return 2 * (i >> 4) + (i & 1); }
+
+// Phi^-1(v) for v in [2^-(B+1), 1/2] (v == 1/2: the all-zero record, +0
+// exactly, gaussian.hpp:62).  Record index = exponent and top S mantissa
+// bits of v; t = v - midpoint is exact (both in one binade; the midpoint is
+// v's bit pattern with the low mantissa bits replaced by 100...0).
+// *tail: v below the table (probability 2^-B per draw); the value returned
+// for such a lane comes from the zero record and is never used.
+// Error: <= 0.42 eps (v/phi(z) + |z|) (tools/fit_direct.py --check): the
+// final addition's half ulp; the interpolation error is ~1 % of it.
+template <class V>
+LPMC_HD double phi_inv_direct(double v, const V& tab, bool* tail) {
+  const uint32_t hi = static_cast<uint32_t>(bits(v) >> 32);
+  const uint32_t idx = (hi >> kDirectShift) - kDirectBase;
+  *tail = idx >= static_cast<uint32_t>(kDirectN);  // below the table: idx wrapped
+  const uint32_t j = idx < static_cast<uint32_t>(kDirectN - 1) ? idx : static_cast<uint32_t>(kDirectN - 1);
+  const double* r = tab.t + j * V::kRec;
+  const uint32_t hc = (hi & ~((1u << kDirectShift) - 1u)) | (1u << (kDirectShift - 1));
+  const double t = v - from_bits(static_cast<uint64_t>(hc) << 32);
+  constexpr int S = V::kStep;
+  const D2 a = load2(r), b = load2(r + 2 * S), c = load2(r + 4 * S), d = load2(r + 6 * S);
+  const D2 e = load2(r + 8 * S);  // c0_lo, c0_hi
+  double p = fmad(a.a, t, a.b);
+  p = fmad(p, t, b.a);
+  p = fmad(p, t, b.b);
+  p = fmad(p, t, c.a);
+  p = fmad(p, t, c.b);
+  p = fmad(p, t, d.a);
+  p = fmad(p, t, d.b);
+  p = fmad(p, t, e.a);  // + c0_lo
+  return p + e.b;       // + c0_hi
+}
 
 // source word of lane-layout word i (staging; host tests use it too)
 LPMC_HD int lane_source(int i) {
@@ -583,6 +651,18 @@ static __device__ __noinline__ double phi_inv_lower_slow(double v) {
   return phi_inv_lower_libdevice(v);
 }
 
+// The draws below the direct table (v < 2^-(B+1), 2^-B of all draws): the
+// fp32 initial guess + Halley step on the erfc, tables read from global
+// memory (L1/L2 hits).  Out of line, one copy per kernel.
+static __device__ __noinline__ double phi_inv_lower_tail(double v) {
+  const double vv[1] = {v};
+  double x0[1];
+  phi_inv_stage1<1>(vv, x0);
+  bool slow;
+  const double z = newton_fast(x0[0], v, FlatTab{kMathTable}, &slow);
+  return slow ? phi_inv_lower_libdevice(v) : z;
+}
+
 // Stage 2: the Newton step, libdevice fix-up of out-of-range draws, sign
 // (bit d of `neg`: u > 1/2).  EXACT_HALF: exactly 0 where bit d of `half`
 // (u == 1/2, gaussian.hpp:62).  The hot loop instead flags such a draw
@@ -591,6 +671,28 @@ static __device__ __noinline__ double phi_inv_lower_slow(double v) {
 struct NoMid {
   __device__ __forceinline__ void operator()() const {}
 };
+
+// exact_inv_cdf for D reflected draws from the direct table: polynomial
+// evaluation for all, the tail fix-up behind one combined branch, sign (bit d
+// of `neg`: u > 1/2).  u == 1/2 needs no special case (the zero record).
+// `mid` runs in the same basic block as the polynomial evaluations.
+template <int D, class V, class Mid = NoMid>
+__device__ __forceinline__ void phi_inv_direct_multi(const double (&v)[D], uint32_t neg,
+                                                     double (&z)[D], const V& tab,
+                                                     Mid&& mid = Mid{}) {
+  bool tail[D];
+#pragma unroll
+  for (int d = 0; d < D; ++d) z[d] = phi_inv_direct(v[d], tab, &tail[d]);
+  mid();
+  bool any_tail = false;
+#pragma unroll
+  for (int d = 0; d < D; ++d) any_tail |= tail[d];
+#pragma unroll
+  for (int d = 0; d < D; ++d) {
+    if (any_tail && tail[d]) z[d] = phi_inv_lower_tail(v[d]);
+    z[d] = (neg >> d) & 1u ? -z[d] : z[d];
+  }
+}
 
 // `mid` runs between the Newton block and the slow-path fix-ups, in the
 // same basic block as the Newton steps (the sampler's software pipeline
@@ -620,9 +722,38 @@ __device__ __forceinline__ void phi_inv_stage2(const double (&v)[D], const doubl
 
 // exact_inv_cdf for D arbitrary u (diagnostics; the sampler reflects from
 // its integer draws, dev::draw_reflect).
+// -DLPMC_HALLEY_Z (A/B only): the round-1 fast mode (fp32 guess + Halley step
+// on the erfc) instead of the direct table, in every kernel of the build.
 template <int D, class V>
+__device__ __forceinline__ void phi_inv_multi_direct(const double (&u)[D], double (&z)[D],
+                                                     const V& tab) {
+  double v[D];
+  uint32_t neg = 0;
+#pragma unroll
+  for (int d = 0; d < D; ++d) {
+    v[d] = u[d] > 0.5 ? 1.0 - u[d] : u[d];  // exact (gaussian.hpp:63)
+    neg |= (u[d] > 0.5 ? 1u : 0u) << d;
+  }
+  phi_inv_direct_multi<D>(v, neg, z, tab);
+}
+template <int D>
 __device__ __forceinline__ void phi_inv_multi(const double (&u)[D], double (&z)[D],
-                                              const V& mtab) {
+                                              const DirectTab& tab) {
+  phi_inv_multi_direct<D>(u, z, tab);
+}
+template <int D>
+__device__ __forceinline__ void phi_inv_multi(const double (&u)[D], double (&z)[D],
+                                              const LaneDirectTab& tab) {
+  phi_inv_multi_direct<D>(u, z, tab);
+}
+
+template <int D>
+__device__ __forceinline__ void phi_inv_multi(const double (&u)[D], double (&z)[D],
+                                              const FlatTab& mtab) {
+#ifndef LPMC_HALLEY_Z
+  (void)mtab;  // small kernels: the direct table straight from global memory
+  phi_inv_multi_direct<D>(u, z, DirectTab{kDirectTable});
+#else
   double v[D], x0[D];
   uint32_t neg = 0, half = 0;
 #pragma unroll
@@ -633,6 +764,7 @@ __device__ __forceinline__ void phi_inv_multi(const double (&u)[D], double (&z)[
   }
   phi_inv_stage1<D>(v, x0);
   phi_inv_stage2<D, true>(v, x0, neg, half, z, mtab);
+#endif
 }
 
 // The same with the reference's formula on libdevice (diagnostics only).

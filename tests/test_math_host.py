@@ -51,3 +51,59 @@ def test_erfc_core_domain_edges(lib):
     # outside the fast range the host hook falls back to libm; never NaN
     for t in (6.5, 10.0, 27.0):
         assert math.isfinite(lib.api.erfc_core(t))
+
+
+# ---- the direct table of the default exact inverse CDF ----------------------
+def _ndtri_lower(v):
+    return -mp.sqrt(2) * mp.erfinv(1 - 2 * mp.mpf(v))
+
+
+def _unit(v, z):
+    """eps (v / pdf(z) + |z|): the conditioning of Z on a 1-ulp error of u
+    plus one ulp of Z (the unit of tests/test_gpu_parity.py's Z bound)."""
+    pdf = mp.exp(-z * z / 2) / mp.sqrt(2 * mp.pi)
+    return mp.mpf(2) ** -52 * (mp.mpf(v) / pdf + abs(z))
+
+
+def test_direct_table_accuracy(lib):
+    """Phi^-1 from the direct table (bitwise the device's evaluation) against
+    mpmath: at most 0.6 units (measured 0.41: the final addition's half ulp),
+    on the sampler's grid, at every sub-interval edge and one grid step either
+    side of it."""
+    rng = np.random.default_rng(11)
+    b = rng.integers(0, 1 << 52, 4000, dtype=np.uint64)  # u < 1/2: v = u
+    v = [(float(x) + 0.5) * 2.0 ** -53 for x in b]
+    for e in range(1, 15):  # binades [2^-(e+1), 2^-e): 32 sub-intervals each
+        lo = 2.0 ** -(e + 1)
+        for sub in range(32):
+            a = lo * (1 + sub / 32)
+            v += [a, np.nextafter(a, 1.0), np.nextafter(a, 0.0)]
+    worst = 0.0
+    n = 0
+    for x in v:
+        z = lib.api.phi_inv_direct_core(float(x))
+        if z is None:
+            assert x < 2.0 ** -15
+            continue
+        zt = _ndtri_lower(x)
+        worst = max(worst, float(abs(mp.mpf(z) - zt) / _unit(x, zt)))
+        n += 1
+    print(f"\ndirect table: max normalised error {worst:.3f} over {n} points")
+    assert n > 5000 and worst <= 0.6
+
+
+def test_direct_table_edges(lib):
+    z = lib.api.phi_inv_direct_core(0.5)
+    assert z == 0.0 and math.copysign(1.0, z) == 1.0  # gaussian.hpp:62: exactly +0
+    assert lib.api.phi_inv_direct_core(2.0 ** -15) is not None
+    assert lib.api.phi_inv_direct_core(np.nextafter(2.0 ** -15, 0.0)) is None
+    for bad in (0.0, -1.0, 0.75, float("nan")):
+        assert lib.api.phi_inv_direct_core(bad) is None
+    # monotone across sub-interval and binade edges
+    for e in range(1, 15):
+        for sub in range(32):
+            a = 2.0 ** -(e + 1) * (1 + sub / 32)
+            below = np.nextafter(a, 0.0)
+            if below < 2.0 ** -15:
+                continue
+            assert lib.api.phi_inv_direct_core(below) <= lib.api.phi_inv_direct_core(a)
