@@ -187,7 +187,7 @@ __device__ __forceinline__ double approx_inv(const TableView& t, double u, bool 
     }
     r = J >= t.K ? t.tail : r;
   }
-  r = lower ? -r : r;
+  r = math::flip_sign(r, lower);
   if constexpr (EXACT_HALF) r = u == 0.5 ? 0.0 : r;
   return r;
 }
@@ -279,14 +279,16 @@ struct RangeNone {
   __device__ void track(__half2) {}
   __device__ bool bad() const { return false; }
 };
+// |x| in [2^-32, 2^33) <=> (bits(|x|) - bits(2^-32)) < bits(2^33) - bits(2^-32)
+// unsigned (a smaller |x| wraps to a huge value): one running maximum
+// (LOP3 + VIADDMNMX per state update).
 struct RangeF32 {
-  uint32_t lo = 0xffffffffu, hi = 0u;
+  static constexpr uint32_t kLo = 0x2f800000u, kHi = 0x50000000u;
+  uint32_t worst = 0u;
   __device__ void track(float x) {
-    const uint32_t b = __float_as_uint(x) & 0x7fffffffu;
-    lo = min(lo, b);
-    hi = max(hi, b);
+    worst = max(worst, (__float_as_uint(x) & 0x7fffffffu) - kLo);
   }
-  __device__ bool bad() const { return hi >= 0x50000000u || lo < 0x2f800000u; }
+  __device__ bool bad() const { return worst >= kHi - kLo; }
 };
 
 struct ArithCarrier {  // m >= 52

@@ -45,15 +45,19 @@ struct Uniforms {
 };
 
 // EXACT = false (the unchecked hot loop, which only needs to know that a
-// path must be replayed): `half` bit p (of draw 0) is set when any of the H
-// draws of path p has a low word of 0 or 0xffffffff, a superset of both
+// path must be replayed): the path is flagged (lomin, below) when any of its
+// draws has a low word of 0 or 0xffffffff, a superset of both
 // special draws (kHalfDraw's low word is 0, kTopDraw's 0xffffffff) that costs
 // two integer operations per draw instead of two 64-bit compares and their
 // selects.  A false positive (probability 2^-31 per draw) only sends the path
 // to the exact replay, which recomputes the same values.  -DLPMC_EXACT_SPECIAL
 // restores the exact tests everywhere (A/B only).
+// lomin[p] (EXACT = false): the running minimum over all draws of path p of
+// (low word + 1) mod 2^32 -- <= 1 at the end of the path iff some draw's low
+// word was 0xffffffff or 0: one fused add-min per draw.
 template <int NP, int H, bool EXACT_ARG = true>
-__device__ __forceinline__ void draw_uniforms(uint64_t (&kc)[NP], Uniforms<H * NP>& U) {
+__device__ __forceinline__ void draw_uniforms(uint64_t (&kc)[NP], Uniforms<H * NP>& U,
+                                              uint32_t (&lomin)[NP]) {
 #ifdef LPMC_EXACT_SPECIAL
   constexpr bool EXACT = true;
 #else
@@ -61,9 +65,6 @@ __device__ __forceinline__ void draw_uniforms(uint64_t (&kc)[NP], Uniforms<H * N
 #endif
   U.top = 0u;
   U.half = 0u;
-  bool rare[NP];
-#pragma unroll
-  for (int p = 0; p < NP; ++p) rare[p] = false;
 #pragma unroll
   for (int h = 0; h < H; ++h)
 #pragma unroll
@@ -75,13 +76,9 @@ __device__ __forceinline__ void draw_uniforms(uint64_t (&kc)[NP], Uniforms<H * N
         U.top |= (b == kTopDraw ? 1u : 0u) << d;
         U.half |= (b == kHalfDraw ? 1u : 0u) << d;
       } else {
-        rare[p] |= static_cast<uint32_t>(b) + 1u <= 1u;
+        lomin[p] = min(lomin[p], static_cast<uint32_t>(b) + 1u);
       }
     }
-  if constexpr (!EXACT) {
-#pragma unroll
-    for (int p = 0; p < NP; ++p) U.half |= (rare[p] ? 1u : 0u) << p;
-  }
 }
 
 // H draws per path starting at fine index n0 from pre-drawn uniforms `cur`:
@@ -159,6 +156,7 @@ template <class Arith, int TAB, bool NEED_EXACT, bool BAR, bool CHECKED, bool DU
 __device__ __forceinline__ void gen_draws(const LevelArgs& A, const TableView& tab,
                                           const double* s_math, const Arith& ar,
                                           uint64_t (&kc)[Arith::NP], bool (&u1)[Arith::NP],
+                                          uint32_t (&lomin)[Arith::NP],
                                           uint64_t (&fk)[Arith::NP],
                                           const uint64_t (&local)[Arith::NP],
                                           const bool (&valid)[Arith::NP], uint64_t n0,
@@ -177,12 +175,16 @@ __device__ __forceinline__ void gen_draws(const LevelArgs& A, const TableView& t
       if constexpr (CHECKED) {
         note_fail(fk[p], (cur.top & bit) != 0u, n0 + h, kStageDraw);
       } else {  // u == 1 or u == 1/2: the path is replayed exactly
+#ifdef LPMC_EXACT_SPECIAL
         u1[p] |= ((cur.top | cur.half) & bit) != 0u;
+#else
+        (void)bit;  // flagged through lomin (draw_uniforms)
+#endif
       }
     }
   double zz[D];
   if constexpr (NEED_EXACT && ZM == kZGlibc) {
-    if constexpr (PREFETCH) draw_uniforms<NP, H, CHECKED>(kc, next);
+    if constexpr (PREFETCH) draw_uniforms<NP, H, CHECKED>(kc, next, lomin);
     glibc::inv_cdf_multi<D>(u, zz, s_math);
     mid();
   } else if constexpr (NEED_EXACT) {
@@ -200,16 +202,16 @@ __device__ __forceinline__ void gen_draws(const LevelArgs& A, const TableView& t
       // the rare exact replay (also the warp-per-path kernel's, which stages
       // the flat layout): the same table straight from global memory
       const math::DirectTab gt{math::kDirectTable};
-      if constexpr (PREFETCH) draw_uniforms<NP, H, CHECKED>(kc, next);
+      if constexpr (PREFETCH) draw_uniforms<NP, H, CHECKED>(kc, next, lomin);
       math::phi_inv_direct_multi<D>(v, neg, zz, gt, mid);
     } else {
       const FastTab lt = fast_tab(s_math);  // staged by stage_fast
 #if defined(LPMC_DIRECT_MID_FIRST)  // legs, then the RNG, then the polynomials
       mid();
-      if constexpr (PREFETCH) draw_uniforms<NP, H, CHECKED>(kc, next);
+      if constexpr (PREFETCH) draw_uniforms<NP, H, CHECKED>(kc, next, lomin);
       math::phi_inv_direct_multi<D>(v, neg, zz, lt);
 #else  // the previous batch's legs in the polynomials' basic block
-      if constexpr (PREFETCH) draw_uniforms<NP, H, CHECKED>(kc, next);
+      if constexpr (PREFETCH) draw_uniforms<NP, H, CHECKED>(kc, next, lomin);
       math::phi_inv_direct_multi<D>(v, neg, zz, lt, mid);
 #endif
     }
@@ -217,16 +219,16 @@ __device__ __forceinline__ void gen_draws(const LevelArgs& A, const TableView& t
     const FastTab lt = fast_tab(s_math);  // staged by stage_fast
     mid();
     math::phi_inv_stage1<D>(v, x0);
-    if constexpr (PREFETCH) draw_uniforms<NP, H, CHECKED>(kc, next);
+    if constexpr (PREFETCH) draw_uniforms<NP, H, CHECKED>(kc, next, lomin);
     math::phi_inv_stage2<D, CHECKED>(v, x0, neg, cur.half, zz, lt);
 #else
     const FastTab lt = fast_tab(s_math);  // staged by stage_fast
     math::phi_inv_stage1<D>(v, x0);
-    if constexpr (PREFETCH) draw_uniforms<NP, H, CHECKED>(kc, next);
+    if constexpr (PREFETCH) draw_uniforms<NP, H, CHECKED>(kc, next, lomin);
     math::phi_inv_stage2<D, CHECKED>(v, x0, neg, cur.half, zz, lt, mid);
 #endif
   } else {
-    if constexpr (PREFETCH) draw_uniforms<NP, H, CHECKED>(kc, next);
+    if constexpr (PREFETCH) draw_uniforms<NP, H, CHECKED>(kc, next, lomin);
     mid();
 #pragma unroll
     for (int d = 0; d < D; ++d) zz[d] = 0.0;
@@ -244,7 +246,10 @@ __device__ __forceinline__ void gen_draws(const LevelArgs& A, const TableView& t
         }
       }
       if constexpr (TAB != kTabNone) {
-        zl[p] = approx_inv<CHECKED, TAB>(tab, u[h * NP + p]);
+        // lower = !(u > 1/2): one half-plane test for both transforms (at
+        // u == 1/2 both selections of 1 - u and u coincide and the result is
+        // the exact 0 of EXACT_HALF / the replay)
+        zl[p] = approx_inv<CHECKED, TAB>(tab, u[h * NP + p], !(u[h * NP + p] > 0.5));
       } else {
         zl[p] = z[h][p];
       }
@@ -395,6 +400,13 @@ __device__ __forceinline__ void step_bar_joint(const Arith& ar, typename Arith::
                                 kStageBarFine);
 }
 
+// iterations of a loop over `left` coarse steps, `g` per iteration, capped
+// so that they fit 32 bits (the caller loops again)
+__device__ __forceinline__ uint32_t trip_count(uint64_t left, int g) {
+  const uint64_t t = (left + static_cast<uint64_t>(g - 1)) / static_cast<uint64_t>(g);
+  return t > 0x40000000ull ? 0x40000000u : static_cast<uint32_t>(t);
+}
+
 template <class Arith, bool KAHAN, int LEGS, int TAB, bool CHECKED, bool DUMP, int ZM,
           bool PW = false>
 __device__ __forceinline__ void simulate(const LevelArgs& A, const TableView& tab,
@@ -413,12 +425,14 @@ __device__ __forceinline__ void simulate(const LevelArgs& A, const TableView& ta
   typename Arith::Range range;
   uint64_t kc[NP];
   bool u1[NP];
+  uint32_t lomin[NP];
   uint64_t fk[NP];
   double xhf[NP], xhc[NP];
 #pragma unroll
   for (int p = 0; p < NP; ++p) {
     kc[p] = path_key(A.seed_key, A.path_base + local[p]) + A.counter0 * kCounterStep;
     u1[p] = false;
+    lomin[p] = 0xffffffffu;
     fk[p] = kNoFail;
     xhf[p] = A.x0;
     xhc[p] = A.x0;
@@ -520,9 +534,9 @@ __device__ __forceinline__ void simulate(const LevelArgs& A, const TableView& ta
     double z[1][NP];
     T zb[1];
     Uniforms<NP> cur, unused;
-    draw_uniforms<NP, 1, CHECKED>(kc, cur);
+    draw_uniforms<NP, 1, CHECKED>(kc, cur, lomin);
     gen_draws<Arith, TAB, kNeedExact, kBar, CHECKED, DUMP, 1, false, ZM>(
-        A, tab, s_math, ar, kc, u1, fk, local, valid, 0, cur, unused, z, zb);
+        A, tab, s_math, ar, kc, u1, lomin, fk, local, valid, 0, cur, unused, z, zb);
     if constexpr (kHat) hat_fine(z[0], 0);
     if constexpr (kBar) bar_fine(zb[0], 0);
   } else {
@@ -531,7 +545,7 @@ __device__ __forceinline__ void simulate(const LevelArgs& A, const TableView& ta
       // the batch after the last is drawn too (never consumed, its u == 1
       // bits never recorded): the price of a branch-free pipeline
       Uniforms<2 * G * NP> cur;
-      draw_uniforms<NP, 2 * G, CHECKED>(kc, cur);
+      draw_uniforms<NP, 2 * G, CHECKED>(kc, cur, lomin);
       if constexpr (kPipe) {
       // software pipeline: the legs of batch i run inside the Newton block of
       // batch i + 1 (one basic block: FP64/shared-load and FP32/integer work
@@ -541,7 +555,7 @@ __device__ __forceinline__ void simulate(const LevelArgs& A, const TableView& ta
       {
         Uniforms<2 * G * NP> next;
         gen_draws<Arith, TAB, kNeedExact, kBar, CHECKED, DUMP, 2 * G, true, ZM>(
-            A, tab, s_math, ar, kc, u1, fk, local, valid, 0, cur, next, zp, zbp);
+            A, tab, s_math, ar, kc, u1, lomin, fk, local, valid, 0, cur, next, zp, zbp);
         cur = next;
       }
       auto legs = [&](const double (&zl)[2 * G][NP], const T (&zbl)[2 * G], uint64_t m0) {
@@ -551,12 +565,15 @@ __device__ __forceinline__ void simulate(const LevelArgs& A, const TableView& ta
           coarse_step(zl[2 * g], zl[2 * g + 1], zbl[2 * g], zbl[2 * g + 1], n);
         }
       };
-      for (uint64_t m = G; m < halves; m += G) {
+      // 32-bit trip counter (m itself is only read by the checked and dump
+      // instances): two loop instructions instead of six
+      for (uint64_t m = G; m < halves;)
+      for (uint32_t trips = trip_count(halves - m, G); trips != 0; --trips, m += G) {
         double z[2 * G][NP];
         T zb[2 * G];
         Uniforms<2 * G * NP> next;
         gen_draws<Arith, TAB, kNeedExact, kBar, CHECKED, DUMP, 2 * G, true, ZM>(
-            A, tab, s_math, ar, kc, u1, fk, local, valid, 2 * m, cur, next, z, zb,
+            A, tab, s_math, ar, kc, u1, lomin, fk, local, valid, 2 * m, cur, next, z, zb,
             [&]() { legs(zp, zbp, m - G); });
         cur = next;
 #pragma unroll
@@ -568,12 +585,13 @@ __device__ __forceinline__ void simulate(const LevelArgs& A, const TableView& ta
       }
       legs(zp, zbp, halves - G);
       } else {
-      for (uint64_t m = 0; m < halves; m += G) {
+      for (uint64_t m = 0; m < halves;)
+      for (uint32_t trips = trip_count(halves - m, G); trips != 0; --trips, m += G) {
         double z[2 * G][NP];
         T zb[2 * G];
         Uniforms<2 * G * NP> next;
         gen_draws<Arith, TAB, kNeedExact, kBar, CHECKED, DUMP, 2 * G, true, ZM>(
-            A, tab, s_math, ar, kc, u1, fk, local, valid, 2 * m, cur, next, z, zb);
+            A, tab, s_math, ar, kc, u1, lomin, fk, local, valid, 2 * m, cur, next, z, zb);
         cur = next;
 #pragma unroll
         for (int g = 0; g < G; ++g) {
@@ -587,9 +605,9 @@ __device__ __forceinline__ void simulate(const LevelArgs& A, const TableView& ta
         double z[2][NP];
         T zb[2];
         Uniforms<2 * NP> cur, unused;
-        draw_uniforms<NP, 2, CHECKED>(kc, cur);
+        draw_uniforms<NP, 2, CHECKED>(kc, cur, lomin);
         gen_draws<Arith, TAB, kNeedExact, kBar, CHECKED, DUMP, 2, false, ZM>(
-            A, tab, s_math, ar, kc, u1, fk, local, valid, 2 * m, cur, unused, z, zb);
+            A, tab, s_math, ar, kc, u1, lomin, fk, local, valid, 2 * m, cur, unused, z, zb);
         coarse_step(z[0], z[1], zb[0], zb[1], 2 * m);
       }
     }
@@ -606,7 +624,8 @@ __device__ __forceinline__ void simulate(const LevelArgs& A, const TableView& ta
     R.bc[p] = (kBar && kCoarse && A.level > 0) ? ar.get(xbc, p) : 0.0;
     R.fk[p] = fk[p];
     const bool hat_bad = kHat && (nonfinite64(R.hf[p]) || nonfinite64(R.hc[p]));
-    R.suspect[p] = u1[p] || hat_bad || ((bad_f >> p) & 1u) || ((bad_c >> p) & 1u);
+    R.suspect[p] = u1[p] || (!CHECKED && lomin[p] <= 1u) || hat_bad || ((bad_f >> p) & 1u) ||
+                   ((bad_c >> p) & 1u);
   }
   R.range_bad = range.bad();
 }

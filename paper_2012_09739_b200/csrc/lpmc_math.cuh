@@ -104,6 +104,12 @@ LPMC_HD double from_bits(uint64_t b) {
 #endif
 }
 
+// neg ? -x : x as one XOR on the high word (a select of the sign mask and a
+// LOP3 instead of a DADD and two selects).
+LPMC_HD double flip_sign(double x, bool neg) {
+  return from_bits(bits(x) ^ (neg ? 0x8000000000000000ull : 0ull));
+}
+
 // 1/d to ~1 ulp: hardware seed (MUFU.RCP64H) + two Newton steps.
 LPMC_HD double rcp_refined(double d) {
 #ifdef __CUDA_ARCH__
@@ -690,7 +696,7 @@ __device__ __forceinline__ void phi_inv_direct_multi(const double (&v)[D], uint3
 #pragma unroll
   for (int d = 0; d < D; ++d) {
     if (any_tail && tail[d]) z[d] = phi_inv_lower_tail(v[d]);
-    z[d] = (neg >> d) & 1u ? -z[d] : z[d];
+    z[d] = flip_sign(z[d], (neg >> d) & 1u);
   }
 }
 
