@@ -507,12 +507,26 @@ lpmc_status build_spec(const lpmc_gbm* model, int32_t level, const lpmc_precisio
     int e = 0;
     return v > 0.0 && std::frexp(v, &e) == 0.5;
   };
+  // The carrier legs fold the same way (step_hat_pw): the carrier's own dt,
+  // 2dt, sqrt(dt) must be powers of two as well, and mu, sigma and the folded
+  // products far inside the binary64 range (RangeF64's argument).
+  auto mid_range = [](double v) {
+    const double a = std::fabs(v);
+    return v == 0.0 || (a >= 0x1p-200 && a <= 0x1p200);
+  };
+  const bool hat_ok = pow2(A.dtf) && pow2(A.sdtf) && pow2(A.dtc) && mid_range(A.mu) &&
+                      mid_range(A.sigma) && std::fabs(A.mu * A.dtc) <= 0x1p10 &&
+                      std::fabs(A.sigma * A.sdtf) <= 0x1p10 && mid_range(A.mu * A.dtf) &&
+                      mid_range(A.sigma * A.sdtf);
   if ((s.arith == BarArith::kF32 || s.arith == BarArith::kF32Round) && pow2(low[3]) &&
-      pow2(low[4]) && pow2(low[5])) {
+      pow2(low[4]) && pow2(low[5]) && hat_ok) {
     A.bar_pow2 = 1;
     A.mu_dtf_l = low[0] * low[3];  // exact: a power-of-two scaling
     A.mu_dtc_l = low[0] * low[5];
     A.sg_sdt_l = low[1] * low[4];
+    A.hat_mu_dtf = A.mu * A.dtf;
+    A.hat_mu_dtc = A.mu * A.dtc;
+    A.hat_sg_sdt = A.sigma * A.sdtf;
   }
   const uint64_t n_chunks = (n_paths + kChunkPaths - 1) / kChunkPaths;
   s.chunk_begin = 0;

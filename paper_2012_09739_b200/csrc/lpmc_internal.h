@@ -87,6 +87,9 @@ struct LevelArgs {
   // the products mu dt, mu 2dt, sigma sqrt(dt), exact
   int32_t bar_pow2 = 0;
   double mu_dtf_l = 0.0, mu_dtc_l = 0.0, sg_sdt_l = 0.0;
+  // the same products for the carrier legs (bar_pow2 also proves the
+  // carrier's dt, 2dt, sqrt(dt) powers of two; step_hat_pw)
+  double hat_mu_dtf = 0.0, hat_mu_dtc = 0.0, hat_sg_sdt = 0.0;
 };
 
 // Failure key: the path in the high bits (atomicMin finds the lowest failing

@@ -279,6 +279,43 @@ __device__ __forceinline__ void step_hat(const LevelArgs& A, double (&x)[NP], do
   }
 }
 
+// The carrier legs with power-of-two steps folded into the model constants
+// (LevelArgs::bar_pow2 also proves the carrier's dt, 2dt, sqrt(dt) powers of
+// two and mu, sigma, their products inside [2^-200, 2^200]):
+//   drift  R(R(mu x) dt)         = R(x (mu dt))
+//   fine   R(R(R(sigma x) s) z)  = R(R(x (sigma s)) z)
+//   coarse dW = R(R(s z0) + R(s z1)) = s R(z0 + z1),
+//          R(R(sigma x) dW)      = R(R(x (sigma s)) R(z0 + z1))
+// bitwise while every intermediate is normal or zero, which RangeF64 proves
+// once per coarse step (|x| in [2^-300, 2^300] there; two fine steps move |x|
+// by factors in [2^-53, 2^11] or to exactly 0, where both forms give 0).  A
+// path that leaves the range is replayed in the reference's own form
+// (replay_checked).  Two fewer FP64 operations per fine step, three per coarse
+// step -- and an FP64 instruction costs two issue slots on sm_100a.
+// zs = z (fine) or R(z0 + z1) (coarse).
+template <int NP>
+__device__ __forceinline__ void step_hat_pw(double (&x)[NP], double mu_dt, double sg_sdt,
+                                            const double (&zs)[NP]) {
+#pragma unroll
+  for (int p = 0; p < NP; ++p) {
+    const double xp = x[p];
+    const double drift = __dmul_rn(xp, mu_dt);
+    const double diff = __dmul_rn(__dmul_rn(xp, sg_sdt), zs[p]);
+    x[p] = __dadd_rn(xp, __dadd_rn(drift, diff));
+  }
+}
+
+// |x| in [2^-300, 2^300] <=> (high word of |x|) - hw(2^-300) < hw(2^300) -
+// hw(2^-300) unsigned; zero, subnormal and non-finite values are outside.
+struct RangeF64 {
+  static constexpr uint32_t kLo = (1023u - 300u) << 20, kHi = (1023u + 300u) << 20;
+  uint32_t worst = 0u;
+  __device__ void track(double x) {
+    worst = max(worst, (static_cast<uint32_t>(__double2hiint(x)) & 0x7fffffffu) - kLo);
+  }
+  __device__ bool bad() const { return worst >= kHi - kLo; }
+};
+
 // em_step / em_step_kahan and the _dw forms (sde.hpp:60-116), bar precision
 template <class Arith, bool KAHAN, bool CHECKED>
 __device__ __forceinline__ void step_bar(const Arith& ar, typename Arith::Range& range,
@@ -449,8 +486,15 @@ __device__ __forceinline__ void simulate(const LevelArgs& A, const TableView& ta
   const T mu_dtf = kPw ? ar.c(A.mu_dtf_l, 0) : T{};
   const T mu_dtc = kPw ? ar.c(A.mu_dtc_l, 0) : T{};
   const T sg_sdt = kPw ? ar.c(A.sg_sdt_l, 0) : T{};
+  RangeF64 hrange[NP];
+  const double h_mu_dtf = kPw ? A.hat_mu_dtf : 0.0, h_mu_dtc = kPw ? A.hat_mu_dtc : 0.0;
+  const double h_sg_sdt = kPw ? A.hat_sg_sdt : 0.0;
   auto hat_fine = [&](const double (&z)[NP], uint64_t n) {
-    step_hat<NP, CHECKED>(A, xhf, A.dtf, z, true, fk, n, kStageHatFine);
+    if constexpr (kPw) {
+      step_hat_pw<NP>(xhf, h_mu_dtf, h_sg_sdt, z);
+    } else {
+      step_hat<NP, CHECKED>(A, xhf, A.dtf, z, true, fk, n, kStageHatFine);
+    }
   };
   auto bar_fine = [&](T zb, uint64_t n) {
     if constexpr (kPw) {
@@ -462,12 +506,23 @@ __device__ __forceinline__ void simulate(const LevelArgs& A, const TableView& ta
   };
   // coarse legs: dW = sqrt_dt z0 + sqrt_dt z1 in each precision (sde.hpp:259-264)
   auto coarse = [&](const double (&z0)[NP], const double (&z1)[NP], T zb0, T zb1, uint64_t n) {
-    if constexpr (kHat && !kFineOnly) {
+    if constexpr (kHat && !kFineOnly && kPw) {
+      double zs[NP];
+#pragma unroll
+      for (int p = 0; p < NP; ++p) zs[p] = __dadd_rn(z0[p], z1[p]);
+      step_hat_pw<NP>(xhc, h_mu_dtc, h_sg_sdt, zs);
+#pragma unroll
+      for (int p = 0; p < NP; ++p) hrange[p].track(xhc[p]);
+    } else if constexpr (kHat && !kFineOnly) {
       double dw[NP];
 #pragma unroll
       for (int p = 0; p < NP; ++p)
         dw[p] = __dadd_rn(__dmul_rn(A.sdtf, z0[p]), __dmul_rn(A.sdtf, z1[p]));
       step_hat<NP, CHECKED>(A, xhc, A.dtc, dw, false, fk, n, kStageHatCoarse);
+    }
+    if constexpr (kHat && kPw) {  // once per coarse step (see RangeF64)
+#pragma unroll
+      for (int p = 0; p < NP; ++p) hrange[p].track(xhf[p]);
     }
     if constexpr (kBar && !kFineOnly && kPw) {
       step_bar_pw<Arith, KAHAN>(ar, range, xbc, cmpc, mu_dtc, sg_sdt, ar.add(zb0, zb1));
@@ -624,8 +679,9 @@ __device__ __forceinline__ void simulate(const LevelArgs& A, const TableView& ta
     R.bc[p] = (kBar && kCoarse && A.level > 0) ? ar.get(xbc, p) : 0.0;
     R.fk[p] = fk[p];
     const bool hat_bad = kHat && (nonfinite64(R.hf[p]) || nonfinite64(R.hc[p]));
-    R.suspect[p] = u1[p] || (!CHECKED && lomin[p] <= 1u) || hat_bad || ((bad_f >> p) & 1u) ||
-                   ((bad_c >> p) & 1u);
+    const bool hat_range = kHat && kPw && A.level > 0 && hrange[p].bad();
+    R.suspect[p] = u1[p] || (!CHECKED && lomin[p] <= 1u) || hat_bad || hat_range ||
+                   ((bad_f >> p) & 1u) || ((bad_c >> p) & 1u);
   }
   R.range_bad = range.bad();
 }

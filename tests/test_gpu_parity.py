@@ -84,6 +84,26 @@ def test_device_erfc_core_equals_host(gpu):
     assert np.array_equal(bits(dev), bits(host))
 
 
+def test_device_direct_table_equals_host(gpu):
+    """The device's exact inverse CDF inside the direct table's range is the
+    host evaluation that test_math_host.py checks against mpmath, bitwise
+    (same IEEE operation sequence), reflection included; below the table it
+    is the Halley step on the erfc core, within the same bound."""
+    rng = np.random.default_rng(8)
+    b = rng.integers(0, 1 << 53, 40000, dtype=np.uint64)
+    u = b.astype(np.float64) * 2.0 ** -53 + 2.0 ** -54  # the sampler's grid
+    edges = np.array([2.0 ** -(e + 1) * (1 + k / 16) for e in range(1, 15) for k in range(16)])
+    u = np.concatenate([u, edges, np.nextafter(edges, 0.0), 1.0 - edges, [0.5]])
+    u = u[(u > 0) & (u < 1)]
+    v = np.minimum(u, 1.0 - u)
+    dev = gpu.device_inv_cdf(u)
+    host = np.array([gpu.api.phi_inv_direct_core(x) for x in v], dtype=object)
+    inside = np.array([h is not None for h in host])
+    assert inside.mean() > 0.99 and np.array_equal(inside, v >= 2.0 ** -15)
+    want = np.where(u[inside] > 0.5, -1.0, 1.0) * host[inside].astype(np.float64)
+    assert np.array_equal(bits(dev[inside]), bits(want))
+
+
 def test_exact_z_agreement_report(gpu, ref):
     """Bitwise agreement of the device exact Gaussians with glibc's, for the
     product path and for the reference's formula on libdevice (context)."""
@@ -285,6 +305,30 @@ def test_pow2_step_folding_bitexact(gpu, oracle, level, m, approx, kahan, legs, 
         got = gpu.run_coupled_paths(model, level, sp, tb, kahan, n, 5, level << 40, **ext)
         want = oracle.tree_from_values(dh, db, legs={"all": 3, "bar": 2, "fine": 3}[legs])
         assert [got.d_hat.state(), got.d_bar.state(), got.d_four.state()] == want, horizon
+
+
+@pytest.mark.parametrize("level", [2, 6])
+@pytest.mark.parametrize("m", [23, 10])
+def test_pow2_step_folding_sign_changes(gpu, oracle, level, m):
+    """Power-of-two step folding (step_bar_pw, step_hat_pw) with sigma = 3:
+    states change sign and magnitude by orders of magnitude within a path;
+    the production moments still equal the unfolded dump kernel's per-path
+    values reduced by the restated tree, bitwise (a launch that leaves the
+    native fp32 range is re-run in the exact emulation, which is unfolded)."""
+    n = 4000
+    model = gpu.make_gbm(0.05, 3.0, 1.0, 1.0)
+    sp, tb = spec(gpu, m), table(gpu, "linear:16")
+    out = gpu.simulate_paths(model, level, sp, tb, False, n, 7, level << 40)
+    assert (out[:, 0] < 0).any() and (out[:, 2] < 0).any()
+    cfg = oracle.config(level=level, mantissa_bits=m, approx="linear:16", kahan=False, seed=7,
+                        sigma=3.0)
+    own, _, _ = oracle.simulate(cfg, level << 40, n)
+    assert np.array_equal(bits(out[:, 2:]), bits(own[:, 2:]))
+    dh = out[:, 0] - out[:, 1]
+    db = out[:, 2] - out[:, 3]
+    got = gpu.run_coupled_paths(model, level, sp, tb, False, n, 7, level << 40)
+    assert [got.d_hat.state(), got.d_bar.state(), got.d_four.state()] == \
+        oracle.tree_from_values(dh, db)
 
 
 @pytest.mark.parametrize("reduce,n", [("tree", 64 * 262144 + 1000),      # > one 64-chunk slice

@@ -168,3 +168,41 @@ def test_top_draw_raises_at_its_step(gpu, ref, exact_z, sched, m, ieee, approx, 
                                    exact_z=exact_z)
         assert ei.value.path_index == base + path
         assert ei.value.step == ctr
+
+
+# ---- the smallest draw (b = 0, u = 2^-54) ----------------------------------
+# 1 - u rounds to 1, so the approximate transform's v = 1 - fl(1 - u) is 0:
+# the reference maps it to the clamped tail (invcdf_approx.hpp:47-49, :61),
+# the dyadic-linear device code reads its last tail record (the index of v ==
+# 0 wraps; lpmc_device.cuh approx_inv).  The exact transform takes the path
+# below the direct table.  Schedules, precisions and table kinds as above.
+@pytest.mark.gpu
+@pytest.mark.parametrize("sched", ["fused", "warp_per_path"])
+@pytest.mark.parametrize("m,ieee,approx,kahan", SPECIAL_PRECS, ids=SPECIAL_IDS)
+def test_bottom_draw_mid_path(gpu, oracle, sched, m, ieee, approx, kahan):
+    level, base, n, path, ctr = 6, 1000, 300, 77, 21
+    if ieee and sched == "warp_per_path":
+        pytest.skip("half2 legs run two paths per thread (fused schedule only)")
+    seed = seed_for_draw(0, base + path, ctr)
+    assert stream_draw(seed, base + path, ctr) == 0
+    assert oracle.uniforms(seed, base + path, 1, ctr)[0] == 2.0 ** -54
+    model = gpu.make_gbm()
+    sp = gpu.PrecisionSpec(m, ieee)
+    tb = None if approx == "exact" else gpu.InvCdfApprox.parse(approx)
+    out, z = gpu.simulate_paths(model, level, sp, tb, kahan, n, seed, base, want_z=True,
+                                schedule=sched)
+    cfg = oracle.config(level=level, mantissa_bits=m, approx=approx, kahan=kahan, seed=seed,
+                        ieee_half=ieee)
+    own, zo, fails = oracle.simulate(cfg, base, n, want_z=True)
+    assert not fails
+    assert abs(z[path, ctr] - zo[path, ctr]) <= 4 * 2.0 ** -52 * abs(zo[path, ctr])
+    assert zo[path, ctr] < -8.0
+    rep, _, _ = oracle.simulate(cfg, base, n, z_in=z)
+    assert np.array_equal(bits(out), bits(rep))
+    if approx != "exact":  # bar legs: the oracle's own run, incl. the tail value
+        assert np.array_equal(bits(out[:, 2:]), bits(own[:, 2:]))
+    got = gpu.run_coupled_paths(model, level, sp, tb, kahan, n, seed, base, schedule=sched)
+    dh = out[:, 0] - out[:, 1]
+    db = out[:, 2] - out[:, 3]
+    assert [got.d_hat.state(), got.d_bar.state(), got.d_four.state()] == \
+        oracle.tree_from_values(dh, db)
