@@ -222,11 +222,21 @@ def cpu_baseline_sample() -> dict:
 
 
 # ------------------------------------------------------------- roofline -----
+# FP64 operations per fine path-step of the reference's
+# algorithm (FMA-free source-level count): RNG 2 + exact Z ~130 + approximate
+# Z 5 + carrier legs 11.5.
+ALGORITHMIC_FP64_PER_PATH_STEP = 148.5
+
+
 def roofline(L, per_cfg_ms, cfgs, n_local, clk, peaks, n_sm):
-    """North-star roofline of the dominant kernel: FP64 lane-ops/s achieved
-    (ncu-counted FP64 lane-ops per fine path-step x live path-steps/s) against
-    the measured FP64 peak; the multi-pipe view (FP64, issue, shared-memory
-    crossbar) is kept under multi_pipe."""
+    """Roofline of the dominant kernel (no HBM or tensor bound: state lives in
+    registers).  frac = executed FP64 lane-ops/s (ncu-counted per fine
+    path-step x live path-steps/s) / measured FP64 peak -- the north-star
+    figure, which falls when FP64 work is removed.  algorithmic = the
+    contract's definition (SURVEY 8(d)'s per-unit figure x units / time).
+    dispatch = the resource that binds the kernel: the SM sub-partition's
+    issue/dispatch port, where an FP64 warp-instruction occupies two slots
+    (profiles/r02_dispatch_model.md)."""
     from paper_2012_09739_b200.build import kernel_source_hash
     dom = max(cfgs, key=lambda c: statistics.mean(per_cfg_ms[c]))
     dom_ms = statistics.mean(per_cfg_ms[dom])
@@ -245,6 +255,11 @@ def roofline(L, per_cfg_ms, cfgs, n_local, clk, peaks, n_sm):
     if prof.get("warp_inst_per_path_step"):
         pipes["issue"] = {"demand_per_path_step": prof["warp_inst_per_path_step"],
                           "peak_per_s": 4.0 * n_sm * sm_hz, "unit": "warp-instructions"}
+    if prof.get("warp_inst_per_path_step") and prof.get("fp64_warp_inst_per_path_step"):
+        pipes["dispatch"] = {"demand_per_path_step": prof["warp_inst_per_path_step"] +
+                             prof["fp64_warp_inst_per_path_step"],
+                             "peak_per_s": 4.0 * n_sm * sm_hz,
+                             "unit": "dispatch slots (an FP64 warp-instruction takes two)"}
     if prof.get("smem_wavefronts_per_path_step"):
         pipes["smem"] = {"demand_per_path_step": prof["smem_wavefronts_per_path_step"],
                          "peak_per_s": 1.0 * n_sm * sm_hz, "unit": "shared-memory wavefronts"}
@@ -252,10 +267,17 @@ def roofline(L, per_cfg_ms, cfgs, n_local, clk, peaks, n_sm):
         p["ceiling_path_steps_per_s"] = p["peak_per_s"] / p["demand_per_path_step"]
         p["frac"] = rate / p["ceiling_path_steps_per_s"]
     kernel = f"level_kernel level {dom[0]} {dom[1]} (all legs, call payoff, linear:16)"
+    alg = ALGORITHMIC_FP64_PER_PATH_STEP * rate
+    algorithmic = {"fp64_ops_per_path_step": ALGORITHMIC_FP64_PER_PATH_STEP,
+                   "achieved": alg / 1e12, "frac": alg / peaks["fp64_ops_per_s"],
+                   "note": "SURVEY.md 8(d) count of the reference's algorithm (Acklam + Newton on "
+                           "libm erfc/exp ~130 FP64 per Gaussian); > 1 because the device "
+                           "computes the same Gaussians from a direct table in 10"}
     if "fp64" not in pipes:
         return {"bound": "fp64", "achieved": None, "peak": peaks["fp64_ops_per_s"] / 1e12,
                 "unit": "TFLOP/s", "frac": None, "traffic": None, "kernel": kernel,
-                "path_steps_per_s": rate, "note": "per-path-step demands not profiled"}
+                "path_steps_per_s": rate, "algorithmic": algorithmic,
+                "note": "per-path-step demands not profiled"}
     achieved = pipes["fp64"]["demand_per_path_step"] * rate  # FP64 lane-ops/s
     bind = min(pipes, key=lambda k: pipes[k]["ceiling_path_steps_per_s"])
     return {
@@ -266,22 +288,25 @@ def roofline(L, per_cfg_ms, cfgs, n_local, clk, peaks, n_sm):
         "fp64_lane_ops_per_path_step": pipes["fp64"]["demand_per_path_step"],
         "demands": os.path.relpath(DEMANDS, ROOT), "demands_stale": stale,
         "kernel_source_hash": src_hash,
-        # the FP64 pipe takes a warp-instruction every 2 cycles per SMSP, issue 1 per cycle:
-        # with this instruction mix the FP64 fraction cannot exceed 2 x its issue share
-        "fp64_frac_at_full_issue": min(1.0, 2.0 * pipes["fp64"]["demand_per_path_step"] /
-                                       (32.0 * pipes["issue"]["demand_per_path_step"]))
-        if "issue" in pipes else None,
+        "algorithmic": algorithmic,
+        # an FP64 warp-instruction holds the sub-partition's dispatch port for two cycles:
+        # with this instruction mix the FP64 fraction cannot exceed 2 N64 / (N + N64)
+        "fp64_frac_at_full_dispatch": 2.0 * prof["fp64_warp_inst_per_path_step"] /
+        pipes["dispatch"]["demand_per_path_step"] if "dispatch" in pipes else None,
+        "dispatch_frac": pipes["dispatch"]["frac"] if "dispatch" in pipes else None,
         "multi_pipe": {"binding": bind, "frac": pipes[bind]["frac"],
                        "ceiling_path_steps_per_s": pipes[bind]["ceiling_path_steps_per_s"],
                        "pipes": pipes, "co_limits": prof.get("co_limits")},
         "note": "no HBM or tensor bound: per-path state lives in registers (traffic = DRAM bytes "
-                "of one launch, ncu). achieved = FP64 lane-ops per fine path-step (ncu "
+                "of one launch, ncu). achieved = executed FP64 lane-ops per fine path-step (ncu "
                 "sm__sass_thread_inst_executed_op_{dadd,dmul,dfma}, one lane-op per DFMA as the "
                 "pipe issues it) x the dominant launch's path-steps/s from CUDA events; peak = "
                 "FP64 lane-op rate measured live on this GPU (lpmc_measure_pipe_peaks; "
-                "MEASURED_PEAKS.json has no FP64 figure), in 1e12 lane-ops/s. "
-                "fp64_frac_at_full_issue = the FP64 fraction this instruction mix would reach "
-                "at 100 % issue (FP64 pipe: one warp-instruction per 2 cycles per SMSP). "
+                "MEASURED_PEAKS.json has no FP64 figure), in 1e12 lane-ops/s. frac falls when "
+                "FP64 work is removed (round 2 cut the exact Gaussian from 40 to 10 FP64 "
+                "operations and the kernel got 1.5x faster); algorithmic uses SURVEY 8(d)'s "
+                "count instead. dispatch_frac = used / available dispatch slots, an FP64 "
+                "warp-instruction counted twice: the resource that binds this kernel. "
                 "demands_stale = the profiled kernel sources differ from this build."}
 
 

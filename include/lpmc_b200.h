@@ -329,6 +329,21 @@ lpmc_status lpmc_measure_pipe_peaks(int32_t device, double* out4, lpmc_error* er
 lpmc_status lpmc_device_math(int32_t op, const double* in, uint64_t n,
                              const lpmc_invcdf_table* table, double* out,
                              const lpmc_options* opts, lpmc_error* err);
+/*
+ * Which arithmetic the production launch of a run uses for the low-precision
+ * legs (a host decision, no device needed): the low byte is 0 carrier
+ * (binary64), 1 native fp32, 2 fp32-carried rounding to m+1 bits, 3 binary64
+ * with integer rounding, 4 IEEE binary16 pairs; LPMC_ARITH_POW2_FOLDED: power-
+ * of-two steps folded into the model constants; LPMC_ARITH_NATIVE_BINARY16:
+ * the m = 10 legs run on native binary16 with static scales (paths that leave
+ * its guard are replayed in arithmetic 2).  All of them are bitwise the
+ * reference's softfloat.hpp:69-111 semantics; the choice only affects speed.
+ */
+#define LPMC_ARITH_POW2_FOLDED 0x100
+#define LPMC_ARITH_NATIVE_BINARY16 0x200
+lpmc_status lpmc_bar_arithmetic(const lpmc_gbm* model, int32_t level, const lpmc_precision* prec,
+                                const lpmc_invcdf_table* table, int32_t kahan,
+                                const lpmc_options* opts, int32_t* out, lpmc_error* err);
 /* Host evaluation of the same erfc core (bitwise equal to op 3). */
 double lpmc_erfc_core(double t);
 /*

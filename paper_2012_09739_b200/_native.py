@@ -165,6 +165,8 @@ SIGNATURES = {
     "lpmc_device_inv_cdf": (_i32, [_dp, _u64, _P(InvCdfTable), _dp, _P(Options), _P(Error)]),
     "lpmc_measure_pipe_peaks": (_i32, [_i32, _dp, _P(Error)]),
     "lpmc_device_math": (_i32, [_i32, _dp, _u64, _P(InvCdfTable), _dp, _P(Options), _P(Error)]),
+    "lpmc_bar_arithmetic": (_i32, [_P(Gbm), _i32, _P(Precision), _P(InvCdfTable), _i32,
+                                   _P(Options), _P(_i32), _P(Error)]),
     "lpmc_erfc_core": (C.c_double, [C.c_double]),
     "lpmc_phi_inv_direct_core": (C.c_double, [C.c_double, _P(_i32)]),
     "lpmc_glibc_math": (C.c_double, [_i32, C.c_double, _P(_i32)]),

@@ -607,6 +607,22 @@ def erfc_core(t: float) -> float:
     return float(N.load().lpmc_erfc_core(float(t)))
 
 
+def bar_arithmetic(model: SdeModel, level: int, spec_low: PrecisionSpec,
+                   approx: Optional[InvCdfApprox], kahan: bool, **ext) -> dict:
+    """The arithmetic a production launch of this run uses for the low-precision
+    legs (lpmc_bar_arithmetic; a host decision, no device needed)."""
+    out = C.c_int32(0)
+    err = N.Error()
+    opts = _options(**ext)
+    N.check(N.load().lpmc_bar_arithmetic(C.byref(_gbm_c(model)), int(level),
+                                         C.byref(spec_low._c()), _table_ptr(approx),
+                                         int(bool(kahan)), C.byref(opts), C.byref(out),
+                                         C.byref(err)), err)
+    names = ["carrier", "fp32", "fp32-round", "fp64-round", "half2-ieee"]
+    return {"arith": names[out.value & 0xff], "pow2_folded": bool(out.value & 0x100),
+            "native_binary16": bool(out.value & 0x200)}
+
+
 def phi_inv_direct_core(v: float) -> Optional[float]:
     """Host evaluation of the direct table of the default exact inverse CDF
     (bitwise the device's value) for v = min(u, 1 - u) in [2^-15, 1/2]; None

@@ -32,12 +32,12 @@ CXX_FLAGS = ["-O2", "-ffp-contract=off", "-fno-fast-math", "-std=c++17", "-fPIC"
              "-Wextra", f"-I{CUDA_HOME}/include"]
 
 SOURCES_CU = ["lpmc_kernels.cu", "lpmc_level_carrier.cu", "lpmc_level_f32.cu",
-              "lpmc_level_f32r.cu", "lpmc_level_f64r.cu", "lpmc_level_half2.cu",
+              "lpmc_level_f32r.cu", "lpmc_level_f64r.cu", "lpmc_level_half2.cu", "lpmc_level_h16.cu",
               "lpmc_probe.cu", "lpmc_wpp_carrier.cu", "lpmc_wpp_f32.cu", "lpmc_wpp_f32r.cu",
               "lpmc_wpp_f64r.cu"]
 SOURCES_CXX = ["lpmc_host.cpp"]
 HEADERS = ["lpmc_internal.h", "lpmc_math.cuh", "lpmc_math_coef.h", "lpmc_math_coef_w8.h",
-           "lpmc_math_coef_w4.h", "lpmc_x0f_coef.h", "lpmc_glibc.cuh", "lpmc_glibc_coef.h", "lpmc_device.cuh",
+           "lpmc_math_coef_w4.h", "lpmc_x0f_coef.h", "lpmc_direct_coef.h", "lpmc_glibc.cuh", "lpmc_glibc_coef.h", "lpmc_device.cuh",
            "lpmc_level.cuh", os.path.join("..", "..", "include", "lpmc_b200.h")]
 
 

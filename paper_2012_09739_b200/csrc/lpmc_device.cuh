@@ -295,6 +295,8 @@ struct ArithCarrier {  // m >= 52
   using T = double;
   using Range = RangeNone;
   static constexpr int NP = 1;
+  static constexpr bool kScaled = false;  // see ArithHalfScaled
+  using Replay = ArithCarrier;
   static constexpr bool kIeee = false;
   static constexpr bool kPair = false;  // no packed fp32 pairs (see ArithF32)
   static constexpr bool kPow2 = false;  // no power-of-two step folding (see step_bar_pw)
@@ -313,6 +315,8 @@ struct ArithF32 {  // m == 23, native
   using T = float;
   using Range = RangeF32;
   static constexpr int NP = 1;
+  static constexpr bool kScaled = false;  // see ArithHalfScaled
+  using Replay = ArithF32;
   static constexpr bool kIeee = false;
   // mul2: two independent products of one leg step in one FFMA2 (bitwise
   // the two scalar products)
@@ -343,6 +347,8 @@ struct ArithF32Round {  // m <= 10: fp32 op (correctly rounded), then RNE to m+1
   using T = float;
   using Range = RangeF32;
   static constexpr int NP = 1;
+  static constexpr bool kScaled = false;  // see ArithHalfScaled
+  using Replay = ArithF32Round;
   static constexpr bool kIeee = false;
   uint32_t d, half_m1, keep;
   uint32_t d64;
@@ -414,6 +420,8 @@ struct ArithF64Round {  // any m < 52: binary64 op, then integer RNE (exact emul
   using T = double;
   using Range = RangeNone;
   static constexpr int NP = 1;
+  static constexpr bool kScaled = false;  // see ArithHalfScaled
+  using Replay = ArithF64Round;
   static constexpr bool kIeee = false;
   static constexpr bool kPair = false;
   static constexpr bool kPow2 = false;
@@ -438,6 +446,8 @@ struct ArithHalf2 {  // native IEEE binary16, two paths per thread
   using T = __half2;
   using Range = RangeNone;
   static constexpr int NP = 2;
+  static constexpr bool kScaled = false;  // see ArithHalfScaled
+  using Replay = ArithHalf2;
   static constexpr bool kIeee = true;
   static constexpr bool kPair = false;  // already two paths per half2 op
   static constexpr bool kPow2 = false;
@@ -460,6 +470,104 @@ struct ArithHalf2 {  // native IEEE binary16, two paths per thread
     const uint32_t b = *reinterpret_cast<const uint32_t*>(&x);
     return (((b & 0x7c00u) == 0x7c00u) ? 1u : 0u) | (((b & 0x7c000000u) == 0x7c000000u) ? 2u : 0u);
   }
+};
+
+// The reference's m = 10 emulation (RNE to 11 significant bits, unbounded
+// exponent; softfloat.hpp:69-111) on NATIVE binary16 arithmetic: one HMUL2 /
+// HFMA2 per reference operation instead of an fp32 operation plus a
+// three-operation Veltkamp split.  binary16's exponent range is far narrower
+// than the values of a step (mu x dt ~ 1e-5 is subnormal), so every quantity
+// is carried with a static power-of-two scale chosen on the host (LevelArgs::
+// hs_*; scaling by a power of two commutes with rounding while the scaled
+// value is a normal binary16 number).  With mu_l = mu_m 2^e_mu, sigma_l =
+// sg_m 2^e_sg, sqrt_dt_l = sdt_m 2^e_sdt (mantissas in [1, 2): exact binary16),
+// dt_l = 2^e_dt, the approximate Gaussian delivered as zs = R(z) 2^kz (the
+// table's c0, c1 are pre-scaled at staging; the conversion F2F.F16.F64 is the
+// reference's one rounding), e_d = e_sg + e_sdt - kz:
+//   a = R(x mu_m)                          = R(mu_l x) 2^-e_mu
+//   c = R(R(x sg_m) sdt_m)                 = R(R(sigma_l x) sqrt_dt_l) 2^-(e_sg+e_sdt)
+//   e = R(c zs)                            = diff 2^-e_d
+//   i = fma(a, P1, e),  P1 = 2^(e_mu+e_dt-e_d) = 4   (kz is chosen for this)
+//                                          = R(drift + diff) 2^-e_d
+//   x' = fma(i, P2, x), P2 = 2^e_d         = R(x + inc)
+// and the coarse step with dW 2^(kz-e_sdt) = R(R(sdt_m zs0) + R(sdt_m zs1)),
+// P1c = 8 (2 dt).  Exactness ("native binary16"):
+//  * |x| in [2^-4, 2^14) before and after every step (RangeH, per update)
+//    -- then a, R(x sg_m), c are normal;
+//  * zs is a normal binary16 number (RangeH::trackz, per draw), so
+//    R(sdt_m zs) is normal and carries the reference's 11 bits; dW, a sum of
+//    multiples of 2^-24, is exact whenever it is below 2^-14;
+//  * e may be subnormal (fewer than 11 bits): then |e| < 2^-14 <= 2^-10 |x|,
+//    below half an ulp of a P1 (>= 4 |x| 2^-12), so i = a P1 whatever e's
+//    last bits are; i itself is a sum of multiples of 2^-24, exact whenever
+//    it is below 2^-14; x' = fma(i, P2, x) rounds the exact x + inc once.
+// Overflow gives inf, which is absorbing and caught at the end of the path.
+// A path that fails any of these is replayed in the fp32-carried emulation
+// (Replay = ArithF32Round, bitwise the reference), so the result never
+// depends on the guard -- only the speed does (measured rate of replays:
+// below 1e-3 of the paths at level 12).  No Kahan (the emulation instance
+// serves it), dyadic-linear tables or none.
+struct RangeH {
+  // |x| in [2^-4, 2^14) <=> (bits(|x|) - bits(2^-4)) < bits(2^14) - bits(2^-4) unsigned
+  static constexpr uint32_t kLo = (15u - 4u) << 10, kHi = (15u + 14u) << 10;
+  uint32_t worst = 0u;
+  __half zmin = __ushort_as_half(0x7bffu);
+  __device__ void track(__half x) {
+    worst = max(worst, (static_cast<uint32_t>(__half_as_ushort(x)) & 0x7fffu) - kLo);
+  }
+  __device__ void trackz(__half zs) { zmin = __hmin(zmin, __habs(zs)); }
+  __device__ void track(float) {}
+  __device__ void track(double) {}
+  __device__ bool bad() const {
+    return worst >= kHi - kLo || __half_as_ushort(zmin) < 0x0400u;
+  }
+};
+
+struct ArithHalfScaled {
+  using T = __half;
+  using Range = RangeH;
+  using Replay = ArithF32Round;
+  static constexpr int NP = 1;
+  static constexpr bool kScaled = true;
+  static constexpr bool kIeee = false;
+  static constexpr bool kPair = false;
+  static constexpr bool kPow2 = true;  // PW instances fold the carrier legs (step_hat_pw)
+  __half mu_m, sg_m, sdt_m, p1, p1c, p2;
+  double zscale;
+  __device__ explicit ArithHalfScaled(const LevelArgs& A)
+      : mu_m(__ushort_as_half(A.hs_mu)), sg_m(__ushort_as_half(A.hs_sigma)),
+        sdt_m(__ushort_as_half(A.hs_sdt)), p1(__ushort_as_half(A.hs_p1)),
+        p1c(__ushort_as_half(A.hs_p1c)), p2(__ushort_as_half(A.hs_p2)), zscale(A.hs_zscale) {}
+  __device__ T c(double, uint16_t bits) const { return __ushort_as_half(bits); }  // x0 (exact)
+  __device__ T zero() const { return __ushort_as_half(0u); }
+  // z arrives pre-scaled by 2^kz from the scaled table copy; exact Gaussians
+  // (no table) are scaled here
+  __device__ T lift(const double (&z)[1]) const { return __double2half(z[0]); }
+  __device__ T lift_exact(const double (&z)[1]) const { return __double2half(__dmul_rn(z[0], zscale)); }
+  __device__ double get(T x, int) const { return static_cast<double>(__half2float(x)); }
+  __device__ uint32_t bad(T x) const {
+    return (__half_as_ushort(x) & 0x7c00u) == 0x7c00u ? 1u : 0u;
+  }
+  // em_step (sde.hpp:60-68)
+  __device__ void fine(T& x, T zs) const {
+    const T a = __hmul_rn(x, mu_m);
+    const T c = __hmul_rn(__hmul_rn(x, sg_m), sdt_m);
+    const T e = __hmul_rn(c, zs);
+    const T i = __hfma(a, p1, e);
+    x = __hfma(i, p2, x);
+  }
+  // em_step_dw (sde.hpp:70-79) with dW = sqrt_dt z0 + sqrt_dt z1 (sde.hpp:261-264)
+  __device__ void coarse(T& x, T zs0, T zs1) const {
+    const T dw = __hadd_rn(__hmul_rn(sdt_m, zs0), __hmul_rn(sdt_m, zs1));
+    const T a = __hmul_rn(x, mu_m);
+    const T e = __hmul_rn(__hmul_rn(x, sg_m), dw);
+    const T i = __hfma(a, p1c, e);
+    x = __hfma(i, p2, x);
+  }
+  // unused generic interface (step_bar is never instantiated for this policy)
+  __device__ T mul(T a, T b) const { return __hmul_rn(a, b); }
+  __device__ T add(T a, T b) const { return __hadd_rn(a, b); }
+  __device__ T sub(T a, T b) const { return __hsub_rn(a, b); }
 };
 
 // --------------------------------------------------------- block tree ------

@@ -107,6 +107,23 @@ uint16_t half_bits(double x) {
   return static_cast<uint16_t>(sign | (ef << 10) | (static_cast<int>(r) - 1024));
 }
 
+double half_value(uint16_t h) {  // binary16 pattern -> double (finite patterns)
+  const int e = (h >> 10) & 0x1f;
+  const int f = h & 0x3ff;
+  const double mag = e == 0 ? std::ldexp(static_cast<double>(f), -24)
+                            : std::ldexp(static_cast<double>(f + 1024), e - 25);
+  return (h & 0x8000) ? -mag : mag;
+}
+
+// v as a binary16 pattern if it is exactly representable (finite), else false
+bool exact_half(double v, uint16_t* out) {
+  if (!std::isfinite(v)) return false;
+  const uint16_t h = half_bits(v);
+  if ((h & 0x7c00) == 0x7c00 || half_value(h) != v) return false;
+  *out = h;
+  return true;
+}
+
 // gauss_legendre (quadrature.hpp:17-41): Newton on the Legendre recurrence.
 void gauss_legendre_rule(int n, std::vector<double>& x_out, std::vector<double>& w_out) {
   x_out.assign(n, 0.0);
@@ -527,6 +544,43 @@ lpmc_status build_spec(const lpmc_gbm* model, int32_t level, const lpmc_precisio
     A.hat_mu_dtf = A.mu * A.dtf;
     A.hat_mu_dtc = A.mu * A.dtc;
     A.hat_sg_sdt = A.sigma * A.sdtf;
+  }
+  // m = 10 on native binary16 with static power-of-two scales
+  // (dev::ArithHalfScaled): dt and 2dt powers of two, every mantissa and
+  // scale factor an exact binary16 number, P1 = 4 by the choice of kz, the
+  // scaled Gaussians far from binary16's overflow, x0 inside the guard.
+  if (s.arith == BarArith::kF32Round && m == 10 && pow2(low[3]) && low[5] == 2.0 * low[3] &&
+      low[0] != 0.0 && low[1] != 0.0 && low[4] > 0.0) {
+    int e_mu = 0, e_sg = 0, e_sdt = 0, e_dt = 0;
+    const double mu_m = 2.0 * std::frexp(low[0], &e_mu);  // mantissa in [1, 2), sign kept
+    const double sg_m = 2.0 * std::frexp(low[1], &e_sg);
+    const double sdt_m = 2.0 * std::frexp(low[4], &e_sdt);
+    std::frexp(low[3], &e_dt);
+    e_mu -= 1, e_sg -= 1, e_sdt -= 1, e_dt -= 1;
+    const int kz = 2 - e_mu - e_dt + e_sg + e_sdt;  // P1 = 2^(e_mu + e_dt - e_d) = 4
+    const int e_d = e_sg + e_sdt - kz;
+    double zmax = 8.5;  // exact Gaussians of draws u >= 2^-54
+    if (s.has_table) {
+      zmax = std::fabs(s.table.tail);
+      const size_t rec = s.table.dyadic ? kDyadicRecord : static_cast<size_t>(s.table.stride);
+      const size_t nrec = s.table.dyadic ? kDyadicRecords : static_cast<size_t>(s.table.K);
+      for (size_t j = 0; j < nrec; ++j) {
+        const double* r = s.table.rows.data() + rec * j;
+        zmax = std::max(zmax, std::fabs(r[2]) + std::fabs(r[3]));
+      }
+    }
+    uint16_t hx0 = 0;
+    const bool ok = kz >= 0 && kz <= 13 && std::ldexp(zmax, kz) <= 30000.0 && e_d >= -24 &&
+                    e_d <= 14 && exact_half(mu_m, &A.hs_mu) && exact_half(sg_m, &A.hs_sigma) &&
+                    exact_half(sdt_m, &A.hs_sdt) && exact_half(std::ldexp(1.0, e_d), &A.hs_p2) &&
+                    exact_half(low[2], &hx0) && hx0 == A.h_x0 && std::fabs(low[2]) >= 0x1p-4 &&
+                    std::fabs(low[2]) < 0x1p14;
+    if (ok) {
+      A.hs_native = 1;
+      A.hs_p1 = 0x4400;   // 4
+      A.hs_p1c = 0x4800;  // 8 (2 dt)
+      A.hs_zscale = std::ldexp(1.0, kz);
+    }
   }
   const uint64_t n_chunks = (n_paths + kChunkPaths - 1) / kChunkPaths;
   s.chunk_begin = 0;
@@ -1987,6 +2041,23 @@ lpmc_status lpmc_device_inv_cdf(const double* u, uint64_t n, const lpmc_invcdf_t
 double lpmc_erfc_core(double t) {
   if (!(t >= 0.0 && t < math::kFastTMax)) return std::erfc(t);
   return math::erfc_fast(t, math::kMathTableHost);
+}
+
+lpmc_status lpmc_bar_arithmetic(const lpmc_gbm* model, int32_t level, const lpmc_precision* prec,
+                                const lpmc_invcdf_table* table, int32_t kahan,
+                                const lpmc_options* opts, int32_t* out, lpmc_error* err) {
+  if (out == nullptr) return fail(err, LPMC_INVALID_ARGUMENT, "null argument");
+  RunSpec s;
+  const lpmc_status st = build_spec(model, level, prec, table, kahan, 256, 1, 0, opts, &s, err);
+  if (st != LPMC_OK) return st;
+  LevelArgs A = s.args;
+  // the dispatcher's view: a table pointer is set at launch
+  static const double kSome = 0.0;
+  A.table = s.has_table ? &kSome : nullptr;
+  *out = static_cast<int32_t>(s.arith) | (A.bar_pow2 ? LPMC_ARITH_POW2_FOLDED : 0) |
+         (s.arith == BarArith::kF32Round && use_native_half(A, kahan != 0, false)
+              ? LPMC_ARITH_NATIVE_BINARY16 : 0);
+  return ok(err);
 }
 
 double lpmc_phi_inv_direct_core(double v, int32_t* in_table) {

@@ -90,6 +90,12 @@ struct LevelArgs {
   // the same products for the carrier legs (bar_pow2 also proves the
   // carrier's dt, 2dt, sqrt(dt) powers of two; step_hat_pw)
   double hat_mu_dtf = 0.0, hat_mu_dtc = 0.0, hat_sg_sdt = 0.0;
+  // m = 10 legs on native binary16 with static scales (dev::ArithHalfScaled;
+  // host-proved, hs_native = 1): binary16 bit patterns of the mantissas of
+  // mu_l, sigma_l, sqrt_dt_l, of P1, P1c, P2, and 2^kz
+  int32_t hs_native = 0;
+  uint16_t hs_mu = 0, hs_sigma = 0, hs_sdt = 0, hs_p1 = 0, hs_p1c = 0, hs_p2 = 0;
+  double hs_zscale = 1.0;
 };
 
 // Failure key: the path in the high bits (atomicMin finds the lowest failing
@@ -101,6 +107,16 @@ constexpr int err_step_bits_for(int level) { return level > 22 ? level : 22; }
 inline LPMC_KEY_HD unsigned long long err_key_of(uint64_t path, uint32_t kind, uint64_t step,
                                                  int bits) {
   return (path << (bits + 2)) | (static_cast<uint64_t>(kind) << bits) | step;
+}
+
+// Production launches of the m = 10 emulation that run on native binary16
+// (dev::ArithHalfScaled): the host proved the scales (hs_native), no Kahan, no
+// dump, fast exact Gaussians, a dyadic-linear table or none.  Everything
+// else, and every path that leaves the native guard, runs the fp32-carried
+// emulation.
+inline bool use_native_half(const LevelArgs& A, bool kahan, bool dump) {
+  return A.hs_native != 0 && !kahan && !dump && A.exact_z == 0 && A.legs != 1 &&
+         (A.table == nullptr || (A.dyadic != 0 && A.table_simple != 0 && A.degree == 1));
 }
 
 struct LaunchResult {
@@ -152,11 +168,13 @@ cudaError_t launch_level_f32(const LevelArgs& A, bool kahan, bool dump, void* st
 cudaError_t launch_level_f32r(const LevelArgs& A, bool kahan, bool dump, void* stream);
 cudaError_t launch_level_f64r(const LevelArgs& A, bool kahan, bool dump, void* stream);
 cudaError_t launch_level_half2(const LevelArgs& A, bool kahan, bool dump, void* stream);
+cudaError_t launch_level_h16(const LevelArgs& A, void* stream);  // dev::ArithHalfScaled
 cudaError_t configure_level_carrier();
 cudaError_t configure_level_f32();
 cudaError_t configure_level_f32r();
 cudaError_t configure_level_f64r();
 cudaError_t configure_level_half2();
+cudaError_t configure_level_h16();
 cudaError_t configure_probe();
 // warp-per-path instances (lpmc_wpp_*.cu; NP == 1 arithmetics)
 cudaError_t launch_wpp_carrier(const LevelArgs& A, bool kahan, void* stream);

@@ -1,3 +1,4 @@
+#include <cstdlib>
 // Reduction, diagnostic and peak kernels, and the dispatch to the level
 // kernels (lpmc_level_*.cu, one translation unit per bar arithmetic).
 //
@@ -257,6 +258,7 @@ int configure_kernels() {
   if (e == cudaSuccess) e = configure_level_f32r();
   if (e == cudaSuccess) e = configure_level_f64r();
   if (e == cudaSuccess) e = configure_level_half2();
+  if (e == cudaSuccess) e = configure_level_h16();
   if (e == cudaSuccess) e = configure_probe();
   if (e == cudaSuccess) e = configure_wpp_carrier();
   if (e == cudaSuccess) e = configure_wpp_f32();
@@ -291,7 +293,17 @@ LaunchResult launch_paths(const LevelArgs& A, BarArith arith, bool kahan, bool d
   switch (arith) {
     case BarArith::kCarrier: e = launch_level_carrier(A, kahan, dump, stream); break;
     case BarArith::kF32: e = launch_level_f32(A, kahan, dump, stream); break;
-    case BarArith::kF32Round: e = launch_level_f32r(A, kahan, dump, stream); break;
+    case BarArith::kF32Round:
+      // m = 10 on native binary16 (dev::ArithHalfScaled) where the host proved
+      // the scales: production launches without Kahan, fast exact Gaussians,
+      // dyadic-linear tables or none; everything else on the fp32-carried
+      // emulation, which also replays the paths that leave the native guard
+      if (use_native_half(A, kahan, dump) && std::getenv("LPMC_NO_NATIVE_HALF") == nullptr) {
+        e = launch_level_h16(A, stream);
+      } else {
+        e = launch_level_f32r(A, kahan, dump, stream);
+      }
+      break;
     case BarArith::kF64Round: e = launch_level_f64r(A, kahan, dump, stream); break;
     case BarArith::kHalf2: e = launch_level_half2(A, kahan, dump, stream); break;
   }

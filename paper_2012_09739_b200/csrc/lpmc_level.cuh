@@ -254,7 +254,13 @@ __device__ __forceinline__ void gen_draws(const LevelArgs& A, const TableView& t
         zl[p] = z[h][p];
       }
     }
-    if constexpr (BAR) zb[h] = ar.lift(zl);
+    if constexpr (BAR) {
+      if constexpr (Arith::kScaled && TAB == kTabNone) {
+        zb[h] = ar.lift_exact(zl);  // exact Gaussians: scaled here (tables are pre-scaled)
+      } else {
+        zb[h] = ar.lift(zl);
+      }
+    }
   }
 }
 
@@ -497,7 +503,11 @@ __device__ __forceinline__ void simulate(const LevelArgs& A, const TableView& ta
     }
   };
   auto bar_fine = [&](T zb, uint64_t n) {
-    if constexpr (kPw) {
+    if constexpr (Arith::kScaled) {  // native binary16 with static scales
+      range.trackz(zb);
+      ar.fine(xbf, zb);
+      range.track(xbf);
+    } else if constexpr (kPw) {
       step_bar_pw<Arith, KAHAN>(ar, range, xbf, cmpf, mu_dtf, sg_sdt, zb);
     } else {
       step_bar<Arith, KAHAN, CHECKED>(ar, range, xbf, cmpf, mu_l, sg_l, dtf_l, sdtf_l, zb, true,
@@ -524,7 +534,10 @@ __device__ __forceinline__ void simulate(const LevelArgs& A, const TableView& ta
 #pragma unroll
       for (int p = 0; p < NP; ++p) hrange[p].track(xhf[p]);
     }
-    if constexpr (kBar && !kFineOnly && kPw) {
+    if constexpr (kBar && !kFineOnly && Arith::kScaled) {
+      ar.coarse(xbc, zb0, zb1);
+      range.track(xbc);
+    } else if constexpr (kBar && !kFineOnly && kPw) {
       step_bar_pw<Arith, KAHAN>(ar, range, xbc, cmpc, mu_dtc, sg_sdt, ar.add(zb0, zb1));
     } else if constexpr (kBar && !kFineOnly && !kJoint) {
       T dw;
@@ -680,10 +693,12 @@ __device__ __forceinline__ void simulate(const LevelArgs& A, const TableView& ta
     R.fk[p] = fk[p];
     const bool hat_bad = kHat && (nonfinite64(R.hf[p]) || nonfinite64(R.hc[p]));
     const bool hat_range = kHat && kPw && A.level > 0 && hrange[p].bad();
-    R.suspect[p] = u1[p] || (!CHECKED && lomin[p] <= 1u) || hat_bad || hat_range ||
+    // native binary16: a path outside the guard is replayed in the emulation
+    const bool bar_range = Arith::kScaled && kBar && range.bad();
+    R.suspect[p] = u1[p] || (!CHECKED && lomin[p] <= 1u) || hat_bad || hat_range || bar_range ||
                    ((bad_f >> p) & 1u) || ((bad_c >> p) & 1u);
   }
-  R.range_bad = range.bad();
+  R.range_bad = Arith::kScaled ? false : range.bad();
 }
 
 // Exact replay of this thread's paths (only for suspects: a u == 1 or
@@ -767,10 +782,24 @@ __global__ void __launch_bounds__(level_threads<Arith, LEGS, TAB, ZM>(), level_c
       stage_fast(kPersist ? s_dyn : s_static);
     }
   }
-  TableView tab{};
+  TableView tab{};      // the reference's table (the replay's, for scaled arithmetics)
+  TableView tab_run{};  // the table the unchecked pass evaluates
   if constexpr (TAB != kTabNone) {
     for (int i = threadIdx.x; i < A.table_words; i += blockDim.x) s_table[i] = A.table[i];
     tab = TableView{s_table, A.table_stride, A.K, A.degree, A.dyadic, A.table_simple, A.tail};
+    tab_run = tab;
+    if constexpr (Arith::kScaled) {
+      // second copy with c0, c1 (and the tail records' value) scaled by 2^kz:
+      // exact, and the scaled polynomial value is the value scaled
+      static_assert(TAB == kTabDyadicLinear, "scaled arithmetics: dyadic-linear tables");
+      double* s2 = s_table + A.table_words;
+      for (int i = threadIdx.x; i < A.table_words; i += blockDim.x) {
+        const double w = A.table[i];
+        s2[i] = (i % kDyadicRecord) >= 2 ? w * A.hs_zscale : w;
+      }
+      tab_run = TableView{s2, A.table_stride, A.K, A.degree, A.dyadic, A.table_simple,
+                          A.tail * A.hs_zscale};
+    }
   }
   __syncthreads();
 
@@ -794,14 +823,14 @@ __global__ void __launch_bounds__(level_threads<Arith, LEGS, TAB, ZM>(), level_c
   }
 
   PathEnd<NP> R;
-  simulate<Arith, KAHAN, LEGS, TAB, false, DUMP, ZM, PW>(A, tab, s_math, local, valid, R);
+  simulate<Arith, KAHAN, LEGS, TAB, false, DUMP, ZM, PW>(A, tab_run, s_math, local, valid, R);
 
   bool any_suspect = false;
 #pragma unroll
   for (int p = 0; p < NP; ++p) any_suspect |= valid[p] && R.suspect[p];
   if (any_suspect) {  // rare: exact values and first failure (serial order)
     const bool range_bad = R.range_bad;
-    replay_checked<Arith, KAHAN, LEGS, TAB, ZM>(A, tab, s_math, local, valid, R);
+    replay_checked<typename Arith::Replay, KAHAN, LEGS, TAB, ZM>(A, tab, s_math, local, valid, R);
     R.range_bad |= range_bad;
 #pragma unroll
     for (int p = 0; p < NP; ++p) {
@@ -1046,7 +1075,9 @@ template <class Arith, bool KAHAN, int LEGS, int TAB, bool DUMP, int ZM>
 cudaError_t launch_one(const LevelArgs& A, cudaStream_t s) {
   constexpr bool kPersist = level_persistent<LEGS, TAB, ZM>();
   constexpr int kThreads = level_threads<Arith, LEGS, TAB, ZM>();
-  const size_t smem = (TAB != kTabNone ? static_cast<size_t>(A.table_words) * sizeof(double) : 0) +
+  const size_t smem = (TAB != kTabNone ? static_cast<size_t>(A.table_words) * sizeof(double) *
+                                             (Arith::kScaled ? 2 : 1)
+                                       : 0) +
                       (kPersist ? static_cast<size_t>(kFastWords) * sizeof(double) : 0);
   unsigned grid = static_cast<unsigned>(A.n_batches);
   if constexpr (kPersist) {  // one CTA per SM, each group looping over batches

@@ -107,6 +107,8 @@ def demands(path: str, path_steps: float, note: str) -> str:
         "ncu_duration_ms": dur,
         "fp64_lane_ops_per_path_step": round(fp64 / path_steps, 3),
         "warp_inst_per_path_step": round(v["smsp__inst_executed.sum"] / path_steps, 4),
+        "fp64_warp_inst_per_path_step": round(
+            v.get("sm__inst_executed_pipe_fp64.sum", 0.0) / path_steps, 4),
         "smem_wavefronts_per_path_step": round(
             v.get("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", 0.0) / path_steps, 4),
         "dram_bytes_per_launch": v.get("dram__bytes_read.sum", 0.0) + v.get("dram__bytes_write.sum", 0.0),
@@ -122,7 +124,8 @@ def demands(path: str, path_steps: float, note: str) -> str:
             "bank_conflicts": v.get("l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum"),
         },
         "definition": "ncu --set full of one launch: FP64 lane-ops = sm__sass_thread_inst_executed_"
-                      "op_{dadd,dmul,dfma}_pred_on.sum, warp-instructions = smsp__inst_executed.sum, "
+                      "op_{dadd,dmul,dfma}_pred_on.sum, warp-instructions = smsp__inst_executed.sum (FP64 pipe: "
+                      "sm__inst_executed_pipe_fp64.sum), "
                       "shared-memory wavefronts = l1tex__data_pipe_lsu_wavefronts_mem_shared.sum, "
                       "each / fine path-steps of the launch; DRAM = dram__bytes_read.sum + "
                       "dram__bytes_write.sum",
