@@ -494,9 +494,15 @@ struct ArithHalf2 {  // native IEEE binary16, two paths per thread
 // P1c = 8 (2 dt).  Exactness ("native binary16"):
 //  * |x| in [2^-4, 2^14) before and after every step (RangeH, per update)
 //    -- then a, R(x sg_m), c are normal;
-//  * zs is a normal binary16 number (RangeH::trackz, per draw), so
-//    R(sdt_m zs) is normal and carries the reference's 11 bits; dW, a sum of
-//    multiples of 2^-24, is exact whenever it is below 2^-14;
+//  * a scaled Gaussian below 2^-14 is subnormal and carries fewer than 11
+//    bits.  In the fine step that only perturbs a subnormal e (next item).
+//    In the coarse dW = R(w0 + w1), w = R(sdt_m zs), it is absorbed when the
+//    other term is at least 2^-2 (|w| < 2^-13.5 is below half an ulp of it),
+//    so a harmful pair has |w0 w1| < 2^-15.5; RangeH::trackw flags the coarse
+//    steps with |R(w0 w1)| < 2^-15 (probability ~2e-9 per step; a first
+//    version that flagged every pair below 2^-2 replayed 5e-4 of the level-12
+//    paths, 14 % of the batches, and gave the native gain back).  dW itself,
+//    a sum of multiples of 2^-24, is exact whenever it is below 2^-14;
 //  * e may be subnormal (fewer than 11 bits): then |e| < 2^-14 <= 2^-10 |x|,
 //    below half an ulp of a P1 (>= 4 |x| 2^-12), so i = a P1 whatever e's
 //    last bits are; i itself is a sum of multiples of 2^-24, exact whenever
@@ -507,24 +513,37 @@ struct ArithHalf2 {  // native IEEE binary16, two paths per thread
 // depends on the guard -- only the speed does (measured rate of replays:
 // below 1e-3 of the paths at level 12).  No Kahan (the emulation instance
 // serves it), dyadic-linear tables or none.
+// State of ArithHalfScaled: X = (x_fine, x_coarse) in one binary16 pair; the
+// guard tracks both lanes at once (packed min / max of |X|) and, per coarse
+// step, the larger of the two scaled increments.  NaN is invisible to min / max and
+// inf to nothing: non-finite states are absorbing and caught at the end of
+// the path (bad()).
 struct RangeH {
-  // |x| in [2^-4, 2^14) <=> (bits(|x|) - bits(2^-4)) < bits(2^14) - bits(2^-4) unsigned
-  static constexpr uint32_t kLo = (15u - 4u) << 10, kHi = (15u + 14u) << 10;
-  uint32_t worst = 0u;
-  __half zmin = __ushort_as_half(0x7bffu);
-  __device__ void track(__half x) {
-    worst = max(worst, (static_cast<uint32_t>(__half_as_ushort(x)) & 0x7fffu) - kLo);
+  __half2 lo = __halves2half2(__ushort_as_half(0x7bffu), __ushort_as_half(0x7bffu));
+  __half2 hi = __halves2half2(__ushort_as_half(0u), __ushort_as_half(0u));
+  __half wmin = __ushort_as_half(0x7bffu);  // min over coarse steps of |R(w0 w1)|
+  __device__ void track(__half2 X) {
+    const __half2 a = __habs2(X);
+    lo = __hmin2(lo, a);
+    hi = __hmax2(hi, a);
   }
-  __device__ void trackz(__half zs) { zmin = __hmin(zmin, __habs(zs)); }
+  __device__ void trackw(__half2 w) {
+    wmin = __hmin(wmin, __habs(__hmul_rn(__low2half(w), __high2half(w))));
+  }
   __device__ void track(float) {}
   __device__ void track(double) {}
+  // |x| in [2^-4, 2^14) on both lanes; every coarse step had |w0 w1| >= 2^-15
   __device__ bool bad() const {
-    return worst >= kHi - kLo || __half_as_ushort(zmin) < 0x0400u;
+    const uint32_t l = *reinterpret_cast<const uint32_t*>(&lo);
+    const uint32_t h = *reinterpret_cast<const uint32_t*>(&hi);
+    constexpr uint32_t kLo = (15u - 4u) << 10, kHi = (15u + 14u) << 10;
+    return (l & 0xffffu) < kLo || (l >> 16) < kLo || (h & 0xffffu) >= kHi || (h >> 16) >= kHi ||
+           __half_as_ushort(wmin) < 0x0200u;  // 2^-15 (a binary16 subnormal: 512 2^-24)
   }
 };
 
 struct ArithHalfScaled {
-  using T = __half;
+  using T = __half2;  // states: (fine, coarse); Gaussians: low lane
   using Range = RangeH;
   using Replay = ArithF32Round;
   static constexpr int NP = 1;
@@ -532,42 +551,84 @@ struct ArithHalfScaled {
   static constexpr bool kIeee = false;
   static constexpr bool kPair = false;
   static constexpr bool kPow2 = true;  // PW instances fold the carrier legs (step_hat_pw)
-  __half mu_m, sg_m, sdt_m, p1, p1c, p2;
+  __half2 musg, mu2, sg2, sdt2, sdt_one, p1_2, p1_p1c, p2_2;
   double zscale;
-  __device__ explicit ArithHalfScaled(const LevelArgs& A)
-      : mu_m(__ushort_as_half(A.hs_mu)), sg_m(__ushort_as_half(A.hs_sigma)),
-        sdt_m(__ushort_as_half(A.hs_sdt)), p1(__ushort_as_half(A.hs_p1)),
-        p1c(__ushort_as_half(A.hs_p1c)), p2(__ushort_as_half(A.hs_p2)), zscale(A.hs_zscale) {}
-  __device__ T c(double, uint16_t bits) const { return __ushort_as_half(bits); }  // x0 (exact)
-  __device__ T zero() const { return __ushort_as_half(0u); }
+  __device__ explicit ArithHalfScaled(const LevelArgs& A) : zscale(A.hs_zscale) {
+    const __half mu = __ushort_as_half(A.hs_mu), sg = __ushort_as_half(A.hs_sigma);
+    const __half sd = __ushort_as_half(A.hs_sdt), one = __ushort_as_half(0x3c00u);
+    const __half p1 = __ushort_as_half(A.hs_p1), p1c = __ushort_as_half(A.hs_p1c);
+    const __half p2 = __ushort_as_half(A.hs_p2);
+    musg = __halves2half2(mu, sg);
+    mu2 = __halves2half2(mu, mu);
+    sg2 = __halves2half2(sg, sg);
+    sdt2 = __halves2half2(sd, sd);
+    sdt_one = __halves2half2(sd, one);
+    p1_2 = __halves2half2(p1, p1);
+    p1_p1c = __halves2half2(p1, p1c);
+    p2_2 = __halves2half2(p2, p2);
+  }
+  __device__ T c(double, uint16_t bits) const {  // x0 (exact): both legs start there
+    const __half h = __ushort_as_half(bits);
+    return __halves2half2(h, h);
+  }
+  __device__ T zero() const { return __halves2half2(__ushort_as_half(0u), __ushort_as_half(0u)); }
   // z arrives pre-scaled by 2^kz from the scaled table copy; exact Gaussians
   // (no table) are scaled here
-  __device__ T lift(const double (&z)[1]) const { return __double2half(z[0]); }
-  __device__ T lift_exact(const double (&z)[1]) const { return __double2half(__dmul_rn(z[0], zscale)); }
-  __device__ double get(T x, int) const { return static_cast<double>(__half2float(x)); }
+  __device__ T lift(const double (&z)[1]) const {
+    const __half h = __double2half(z[0]);
+    return __halves2half2(h, h);
+  }
+  __device__ T lift_exact(const double (&z)[1]) const {
+    const __half h = __double2half(__dmul_rn(z[0], zscale));
+    return __halves2half2(h, h);
+  }
+  __device__ double get(T x, int lane) const {
+    return static_cast<double>(__half2float(lane == 0 ? __low2half(x) : __high2half(x)));
+  }
   __device__ uint32_t bad(T x) const {
-    return (__half_as_ushort(x) & 0x7c00u) == 0x7c00u ? 1u : 0u;
+    const uint32_t b = *reinterpret_cast<const uint32_t*>(&x);
+    return ((b & 0x7c00u) == 0x7c00u || (b & 0x7c000000u) == 0x7c000000u) ? 1u : 0u;
   }
-  // em_step (sde.hpp:60-68)
-  __device__ void fine(T& x, T zs) const {
-    const T a = __hmul_rn(x, mu_m);
-    const T c = __hmul_rn(__hmul_rn(x, sg_m), sdt_m);
-    const T e = __hmul_rn(c, zs);
-    const T i = __hfma(a, p1, e);
-    x = __hfma(i, p2, x);
+  // em_step (sde.hpp:60-68) of the fine leg (lane 0 of X); returns the new
+  // x_fine in both lanes
+  __device__ T fine_value(T X, T zs) const {
+    const T xf = __low2half2(X);
+    const T ab = __hmul2_rn(xf, musg);                      // (R(x mu_m), R(x sg_m))
+    const T cc = __hmul2_rn(__high2half2(ab), sdt2);        // R(R(x sg_m) sdt_m)
+    const T e = __hmul2_rn(cc, __low2half2(zs));
+    const T i = __hfma2(__low2half2(ab), p1_2, e);
+    return __hfma2(i, p2_2, xf);
   }
-  // em_step_dw (sde.hpp:70-79) with dW = sqrt_dt z0 + sqrt_dt z1 (sde.hpp:261-264)
-  __device__ void coarse(T& x, T zs0, T zs1) const {
-    const T dw = __hadd_rn(__hmul_rn(sdt_m, zs0), __hmul_rn(sdt_m, zs1));
-    const T a = __hmul_rn(x, mu_m);
-    const T e = __hmul_rn(__hmul_rn(x, sg_m), dw);
-    const T i = __hfma(a, p1c, e);
-    x = __hfma(i, p2, x);
+  // one fine step alone (level 0, the two-way sampler): lane 1 is kept
+  __device__ void fine(T& X, T zs, Range& r) const {
+    const T xf1 = fine_value(X, zs);
+    X = __halves2half2(__low2half(xf1), __high2half(X));
+    r.track(X);
+  }
+  // fine step n (zs0), then fine step n + 1 (zs1) and the coarse step as one
+  // pair: em_step and em_step_dw (sde.hpp:60-79) with dW = sqrt_dt z0 +
+  // sqrt_dt z1 (sde.hpp:261-264); the coarse lane multiplies by an exact 1
+  // where the fine lane takes sdt_m
+  __device__ void coarse_step(T& X, T zs0, T zs1, Range& r) const {
+    const T Z = __halves2half2(__low2half(zs0), __low2half(zs1));
+    const T xf1 = fine_value(X, zs0);
+    r.track(xf1);
+    const T X1 = __halves2half2(__low2half(xf1), __high2half(X));
+    const T a = __hmul2_rn(X1, mu2);
+    const T b = __hmul2_rn(X1, sg2);
+    const T w = __hmul2_rn(Z, sdt2);                                   // (w0, w1)
+    r.trackw(w);
+    const T dw = __hadd2_rn(__low2half2(w), __high2half2(w));          // both lanes
+    const T cc = __hmul2_rn(b, sdt_one);                               // (R(b sdt_m), b)
+    const T e = __hmul2_rn(cc, __halves2half2(__high2half(Z), __low2half(dw)));  // (zs1, dW)
+    const T i = __hfma2(a, p1_p1c, e);
+    X = __hfma2(i, p2_2, X1);
+    r.track(X);
   }
   // unused generic interface (step_bar is never instantiated for this policy)
-  __device__ T mul(T a, T b) const { return __hmul_rn(a, b); }
-  __device__ T add(T a, T b) const { return __hadd_rn(a, b); }
-  __device__ T sub(T a, T b) const { return __hsub_rn(a, b); }
+  __device__ T mul(T a, T b) const { return __hmul2_rn(a, b); }
+  __device__ T add(T a, T b) const { return __hadd2_rn(a, b); }
+  __device__ T sub(T a, T b) const { return __hsub2_rn(a, b); }
 };
 
 // --------------------------------------------------------- block tree ------

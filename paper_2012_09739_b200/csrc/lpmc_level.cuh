@@ -13,6 +13,7 @@
 // its first failing step in the reference's serial order.
 #pragma once
 
+#include <cstdio>
 #include <type_traits>
 
 #include "lpmc_device.cuh"
@@ -503,10 +504,8 @@ __device__ __forceinline__ void simulate(const LevelArgs& A, const TableView& ta
     }
   };
   auto bar_fine = [&](T zb, uint64_t n) {
-    if constexpr (Arith::kScaled) {  // native binary16 with static scales
-      range.trackz(zb);
-      ar.fine(xbf, zb);
-      range.track(xbf);
+    if constexpr (Arith::kScaled) {  // native binary16 with static scales: xbf = (fine, coarse)
+      ar.fine(xbf, zb, range);
     } else if constexpr (kPw) {
       step_bar_pw<Arith, KAHAN>(ar, range, xbf, cmpf, mu_dtf, sg_sdt, zb);
     } else {
@@ -535,8 +534,7 @@ __device__ __forceinline__ void simulate(const LevelArgs& A, const TableView& ta
       for (int p = 0; p < NP; ++p) hrange[p].track(xhf[p]);
     }
     if constexpr (kBar && !kFineOnly && Arith::kScaled) {
-      ar.coarse(xbc, zb0, zb1);
-      range.track(xbc);
+      // both bar legs were stepped as one pair in coarse_step below
     } else if constexpr (kBar && !kFineOnly && kPw) {
       step_bar_pw<Arith, KAHAN>(ar, range, xbc, cmpc, mu_dtc, sg_sdt, ar.add(zb0, zb1));
     } else if constexpr (kBar && !kFineOnly && !kJoint) {
@@ -565,6 +563,11 @@ __device__ __forceinline__ void simulate(const LevelArgs& A, const TableView& ta
       }
       step_bar_joint<Arith, KAHAN>(ar, range, xbf, xbc, cmpf, cmpc, mu_l, sg_l, dtf_l, sdtf_l,
                                    dtc_l, zb0, zb1, fk, n);
+    } else if constexpr (Arith::kScaled && kBar && !kFineOnly) {
+      if constexpr (kHat) hat_fine(z0, n);
+      if constexpr (kHat) hat_fine(z1, n + 1);
+      coarse(z0, z1, zb0, zb1, n + 1);  // the hat leg only
+      ar.coarse_step(xbf, zb0, zb1, range);
     } else {
       if constexpr (kHat) hat_fine(z0, n);
       if constexpr (kBar) bar_fine(zb0, n);
@@ -682,6 +685,7 @@ __device__ __forceinline__ void simulate(const LevelArgs& A, const TableView& ta
   }
 
   constexpr bool kCoarse = !kFineOnly;
+  if constexpr (Arith::kScaled) xbc = xbf;  // one pair (fine, coarse): lane 1 is the coarse leg
   const uint32_t bad_f = kBar ? ar.bad(xbf) : 0u;
   const uint32_t bad_c = (kBar && kCoarse && A.level > 0) ? ar.bad(xbc) : 0u;
 #pragma unroll
@@ -689,7 +693,7 @@ __device__ __forceinline__ void simulate(const LevelArgs& A, const TableView& ta
     R.hf[p] = kHat ? xhf[p] : 0.0;
     R.hc[p] = (kHat && kCoarse && A.level > 0) ? xhc[p] : 0.0;
     R.bf[p] = kBar ? ar.get(xbf, p) : 0.0;
-    R.bc[p] = (kBar && kCoarse && A.level > 0) ? ar.get(xbc, p) : 0.0;
+    R.bc[p] = (kBar && kCoarse && A.level > 0) ? ar.get(xbc, Arith::kScaled ? 1 : p) : 0.0;
     R.fk[p] = fk[p];
     const bool hat_bad = kHat && (nonfinite64(R.hf[p]) || nonfinite64(R.hc[p]));
     const bool hat_range = kHat && kPw && A.level > 0 && hrange[p].bad();
@@ -697,6 +701,18 @@ __device__ __forceinline__ void simulate(const LevelArgs& A, const TableView& ta
     const bool bar_range = Arith::kScaled && kBar && range.bad();
     R.suspect[p] = u1[p] || (!CHECKED && lomin[p] <= 1u) || hat_bad || hat_range || bar_range ||
                    ((bad_f >> p) & 1u) || ((bad_c >> p) & 1u);
+#ifdef LPMC_TRACE_REPLAY
+    if (!CHECKED && R.suspect[p]) {
+      if constexpr (Arith::kScaled) {
+        printf("suspect path %llu: u1 %d lomin %u hat_bad %d hat_range %d bar_range %d bad %u %u lo %08x hi %08x wmin %04x\n",
+               static_cast<unsigned long long>(local[p]), int(u1[p]), lomin[p], int(hat_bad),
+               int(hat_range), int(bar_range), bad_f, bad_c,
+               *reinterpret_cast<const uint32_t*>(&range.lo),
+               *reinterpret_cast<const uint32_t*>(&range.hi),
+               static_cast<unsigned>(__half_as_ushort(range.wmin)));
+      }
+    }
+#endif
   }
   R.range_bad = Arith::kScaled ? false : range.bad();
 }
@@ -829,6 +845,10 @@ __global__ void __launch_bounds__(level_threads<Arith, LEGS, TAB, ZM>(), level_c
 #pragma unroll
   for (int p = 0; p < NP; ++p) any_suspect |= valid[p] && R.suspect[p];
   if (any_suspect) {  // rare: exact values and first failure (serial order)
+#ifdef LPMC_TRACE_REPLAY  // debugging only: which paths are replayed
+    printf("replay path %llu batch %llu\n", static_cast<unsigned long long>(local[0]),
+           static_cast<unsigned long long>(slot_b));
+#endif
     const bool range_bad = R.range_bad;
     replay_checked<typename Arith::Replay, KAHAN, LEGS, TAB, ZM>(A, tab, s_math, local, valid, R);
     R.range_bad |= range_bad;
