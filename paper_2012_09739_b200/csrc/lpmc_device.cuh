@@ -92,7 +92,16 @@ struct TableView {
   const double* base;
   int stride, K, degree, dyadic, simple;
   double tail;
+  uint32_t saddr = 0;  // shared-space address of `base` (the level kernel's reversed copy)
 };
+
+// 128-bit load from a shared-space address (no generic-to-shared conversion
+// in the hot loop: the address is a uniform base plus the record offset)
+__device__ __forceinline__ math::D2 lds2(uint32_t saddr) {
+  math::D2 r;
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(r.a), "=d"(r.b) : "r"(saddr));
+  return r;
+}
 
 // InvCdfApprox::operator() (invcdf_approx.hpp:44-90).
 //  * dyadic tables (K <= 32, w_max = K+1): the reference's j = floor(-log2 v)
@@ -117,27 +126,36 @@ enum : int { kTabNone = 0, kTabDyadicLinear = 1, kTabGeneric = 2 };
 template <bool EXACT_HALF = true, int TAB = kTabGeneric>
 __device__ __forceinline__ double approx_inv(const TableView& t, double u, bool lower) {
   const double up = lower ? 1.0 - u : u;  // fl(1-u) for the lower half (:47-49)
-  const double v = 1.0 - up;              // exact (Sterbenz)
   double r;
   if constexpr (TAB == kTabDyadicLinear) {
-    // floor(-log2 v) = 1022 - e', e' the biased exponent of the next double
-    // below v (v = 2^k drops a binade, anything else stays): j = fl - 1 =
-    // 1021 - e' from one 64-bit decrement and a shift.  Records j >= K are
-    // the host's tail records (c0 = tail, c1 = 0: tail + 0 * 0 = tail), so
-    // neither the reference's clamp nor its tail test needs an instruction.
-    // v == 0 (u == 1, where the reference throws and the path is replayed
-    // checked; or the smallest draw u = 2^-54, whose 1 - u rounds to 1 and
-    // which the reference maps to the tail value): vb - 1 wraps, the
-    // unsigned min sends it to the last tail record.
-    const uint64_t vb = static_cast<uint64_t>(__double_as_longlong(v));
-    const uint32_t eb = static_cast<uint32_t>((vb - 1) >> 52);
+    // floor(-log2 v), v = 1 - u' (exact, Sterbenz), needs the binade of v with
+    // an exact power of two counted into the binade below.  u' and v sit on
+    // the 2^-53 grid, so (1 - 2^-53) - u' = v - 2^-53 is exact and has that
+    // binade: a power of two drops into the binade below, any other grid
+    // point of a binade stays (it is at least one grid step above the
+    // binade's start).  v = 2^-53 gives 0 (exponent field 0: the last tail
+    // record, which is the reference's j = 52), v = 0 (u' == 1: u == 1, where
+    // the reference throws and the path is replayed checked; or the smallest
+    // draw u = 2^-54, whose 1 - u rounds to 1 and which the reference maps to
+    // the tail value) gives -2^-53, whose sign bit sends the unsigned minimum
+    // to the last tail record too.  One FP64 subtraction and a shift instead
+    // of a subtraction, a 64-bit decrement and a shift.  Records j >= K are the
+    // host's tail records (c0 = tail, c1 = 0: tail + 0 * s = tail), so neither
+    // the reference's clamp nor its tail test needs an instruction.
+    const double vm = __dsub_rn(0x1.fffffffffffffp-1, up);
+    const uint32_t eb = static_cast<uint32_t>(__double2hiint(vm)) >> 20;
     const uint32_t j = min(1021u - eb, static_cast<uint32_t>(kDyadicRecords - 1));
     const double* b = t.base + 6 * j;
     const math::D2 cw = math::load2(b);
     const math::D2 c01 = math::load2(b + 2);
     const double s = __fma_rn(up, cw.b, cw.a);
     r = __dadd_rn(c01.a, __dmul_rn(c01.b, s));
-  } else if (t.dyadic) {
+    r = math::flip_sign(r, lower);
+    if constexpr (EXACT_HALF) r = u == 0.5 ? 0.0 : r;
+    return r;
+  }
+  const double v = 1.0 - up;              // exact (Sterbenz)
+  if (t.dyadic) {
     const uint64_t vb = static_cast<uint64_t>(__double_as_longlong(v));
     const int e = static_cast<int>(vb >> 52) - 1023;
     const int fl = (vb & 0xFFFFFFFFFFFFFull) == 0 ? -e : -e - 1;  // floor(-log2 v) >= 1
@@ -190,6 +208,31 @@ __device__ __forceinline__ double approx_inv(const TableView& t, double u, bool 
   r = math::flip_sign(r, lower);
   if constexpr (EXACT_HALF) r = u == 0.5 ? 0.0 : r;
   return r;
+}
+
+// The dyadic-linear evaluation of the unchecked hot loop from the
+// reflected draw: up = u > 1/2 ? u : fl(1 - u), sgn = 0x80000000 where the
+// result is negated (u < 1/2), both shared with the exact transform.
+// t is the kernel's REVERSED copy of the dyadic table (kRunCopyRecords
+// records, staged by the level kernel): record r = e' - 969 holds interval
+// j = 52 - r for r <= 52 (e' the biased exponent of v - 2^-53, see
+// approx_inv), record 53 the tail value -- so the index is one shift-add and
+// one unsigned minimum with immediates (v - 2^-53 <= 0: the wrapped or
+// sign-carrying e' lands on record 53 or record 0, both tail records).
+constexpr int kRunCopyRecords = kDyadicRecords + 1;
+constexpr int kRunCopyWords = kRunCopyRecords * kDyadicRecord;
+__device__ __forceinline__ int run_copy_source(int r) {  // forward record of reversed record r
+  return r < kDyadicRecords ? kDyadicRecords - 1 - r : kDyadicRecords - 1;
+}
+__device__ __forceinline__ double approx_inv_up(const TableView& t, double up, uint32_t sgn) {
+  const double vm = __dsub_rn(0x1.fffffffffffffp-1, up);  // see approx_inv
+  const uint32_t r = min((static_cast<uint32_t>(__double2hiint(vm)) >> 20) - (1021u - 52u),
+                         static_cast<uint32_t>(kRunCopyRecords - 1));
+  const uint32_t b = t.saddr + r * (kDyadicRecord * 8u);
+  const math::D2 cw = lds2(b);
+  const math::D2 c01 = lds2(b + 16u);
+  const double s = __fma_rn(up, cw.b, cw.a);
+  return math::flip_sign_mask(__dadd_rn(c01.a, __dmul_rn(c01.b, s)), sgn);
 }
 
 template <bool EXACT_HALF = true, int TAB = kTabGeneric>

@@ -2065,7 +2065,8 @@ double lpmc_phi_inv_direct_core(double v, int32_t* in_table) {
   double z = std::nan("");
   if (v > 0.0 && v <= 0.5) z = math::phi_inv_direct(v, math::DirectTab{math::kDirectHost}, &tail);
   if (in_table != nullptr) *in_table = tail ? 0 : 1;
-  return tail ? std::nan("") : z;
+  // the table holds the upper half, -Phi^-1(v); +0 at v == 1/2 (gaussian.hpp:62)
+  return tail ? std::nan("") : (z == 0.0 ? 0.0 : -z);
 }
 
 static_assert(LPMC_EXACT_Z_FAST == 0 && LPMC_EXACT_Z_GLIBC == 1, "dev::kZFast / kZGlibc");

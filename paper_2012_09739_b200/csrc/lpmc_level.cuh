@@ -114,8 +114,14 @@ __device__ __forceinline__ void stage_fast(double* s) {
   for (int i = threadIdx.x; i < kFastWords; i += blockDim.x)
     s[i] = math::kDirectTable[math::lane_direct_source(i)];
 }
+// per-thread view (copy = lane % 8); the shared-space address goes through a
+// volatile move so that ptxas keeps it in a register instead of re-deriving
+// it (S2R SR_TID, S2UR SR_CgaCtaId, ULEA, ...) in every loop iteration
 __device__ __forceinline__ FastTab fast_tab(const double* s) {
-  return FastTab{s + 2 * static_cast<int>(threadIdx.x & (math::kLaneCopies - 1))};
+  const double* t = s + 2 * static_cast<int>(threadIdx.x & (math::kLaneCopies - 1));
+  uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(t)), pinned;
+  asm volatile("mov.u32 %0, %1;" : "=r"(pinned) : "r"(a));
+  return FastTab{t, pinned};
 }
 #else
 using FastTab = math::DirectTab;
@@ -152,10 +158,30 @@ __device__ __forceinline__ WppTab wpp_tab(const double* s) { return fast_tab(s);
 // Exact-Gaussian mode of a level instance (values of LPMC_EXACT_Z_*).
 enum : int { kZFast = 0, kZGlibc = 1 };
 
+// Shared-space address of p, computed once: the volatile move keeps ptxas
+// from re-deriving it (S2R SR_CgaCtaId, LEA, ...) inside the hot loop.
+__device__ __forceinline__ uint32_t pinned_saddr(const void* p) {
+  uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(p)), out;
+  asm volatile("mov.u32 %0, %1;" : "=r"(out) : "r"(a));
+  return out;
+}
+
+// Instances whose unchecked pass reads the reversed (and, for the native
+// binary16 arithmetic, pre-scaled) copy of the dyadic table (approx_inv_up).
+template <int TAB, bool DUMP, int ZM>
+__host__ __device__ constexpr bool run_copy() {
+#ifdef LPMC_HALLEY_Z
+  return false;
+#else
+  return TAB == kTabDyadicLinear && !DUMP && ZM != kZGlibc;
+#endif
+}
+
 template <class Arith, int TAB, bool NEED_EXACT, bool BAR, bool CHECKED, bool DUMP, int H,
           bool PREFETCH, int ZM, class Mid = math::NoMid>
 __device__ __forceinline__ void gen_draws(const LevelArgs& A, const TableView& tab,
-                                          const double* s_math, const Arith& ar,
+                                          const double* s_math, const FastTab& lt,
+                                          const Arith& ar,
                                           uint64_t (&kc)[Arith::NP], bool (&u1)[Arith::NP],
                                           uint32_t (&lomin)[Arith::NP],
                                           uint64_t (&fk)[Arith::NP],
@@ -184,6 +210,15 @@ __device__ __forceinline__ void gen_draws(const LevelArgs& A, const TableView& t
       }
     }
   double zz[D];
+  double up[D];      // reflected draws of the approximate transform (fast exact mode)
+  uint32_t sgn[D];   // common sign mask of both transforms (fast exact mode)
+  // unchecked production instances with a dyadic-linear table evaluate it
+  // from the reflected draw and the kernel's reversed table copy
+  constexpr bool kShared = run_copy<TAB, DUMP, ZM>() && !CHECKED
+#ifdef LPMC_HALLEY_Z
+                           && false
+#endif
+      ;
   if constexpr (NEED_EXACT && ZM == kZGlibc) {
     if constexpr (PREFETCH) draw_uniforms<NP, H, CHECKED>(kc, next, lomin);
     glibc::inv_cdf_multi<D>(u, zz, s_math);
@@ -191,12 +226,34 @@ __device__ __forceinline__ void gen_draws(const LevelArgs& A, const TableView& t
   } else if constexpr (NEED_EXACT) {
     double v[D], x0[D];
     uint32_t neg = 0;
+#if !defined(LPMC_HALLEY_Z)
+    // Reflection without compares or selects: q = u - 1/2 is exact (u is an
+    // odd multiple of 2^-54 below 1/2 and a multiple of 2^-53 above, so the
+    // difference has at most 53 bits), v = 1/2 - |q| = min(u, 1 - u) exactly
+    // (gaussian.hpp:63), and the approximate transform's reflected draw
+    // u > 1/2 ? u : fl(1 - u) (invcdf_approx.hpp:47-49) is fl(1 - v) in both
+    // half-planes (exact above 1/2, the reference's own rounding below).  The
+    // sign bit of q is the common sign mask of both transforms (the direct
+    // table holds the upper half, like the approximate transform); u == 1/2
+    // gives q = +0, hence v = up = 1/2, mask 0 and the reference's +0.
+    // Three FP64 operations and two LOP3 instead of a subtraction, a compare,
+    // four selects of register halves and a mask select.
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+      const double q = __dsub_rn(u[d], 0.5);
+      sgn[d] = static_cast<uint32_t>(__double2hiint(q)) & 0x80000000u;
+      v[d] = __dsub_rn(0.5, fabs(q));
+      up[d] = __dsub_rn(1.0, v[d]);
+    }
+    (void)neg;
+#else
 #pragma unroll
     for (int d = 0; d < D; ++d) {
       const bool ng = u[d] > 0.5;
       v[d] = ng ? 1.0 - u[d] : u[d];  // exact (gaussian.hpp:63)
       neg |= (ng ? 1u : 0u) << d;
     }
+#endif
 #if !defined(LPMC_HALLEY_Z)
     (void)x0;
     if constexpr (CHECKED) {
@@ -204,26 +261,23 @@ __device__ __forceinline__ void gen_draws(const LevelArgs& A, const TableView& t
       // the flat layout): the same table straight from global memory
       const math::DirectTab gt{math::kDirectTable};
       if constexpr (PREFETCH) draw_uniforms<NP, H, CHECKED>(kc, next, lomin);
-      math::phi_inv_direct_multi<D>(v, neg, zz, gt, mid);
+      math::phi_inv_direct_multi<D>(v, sgn, zz, gt, mid);
     } else {
-      const FastTab lt = fast_tab(s_math);  // staged by stage_fast
 #if defined(LPMC_DIRECT_MID_FIRST)  // legs, then the RNG, then the polynomials
       mid();
       if constexpr (PREFETCH) draw_uniforms<NP, H, CHECKED>(kc, next, lomin);
-      math::phi_inv_direct_multi<D>(v, neg, zz, lt);
+      math::phi_inv_direct_multi<D>(v, sgn, zz, lt);
 #else  // the previous batch's legs in the polynomials' basic block
       if constexpr (PREFETCH) draw_uniforms<NP, H, CHECKED>(kc, next, lomin);
-      math::phi_inv_direct_multi<D>(v, neg, zz, lt, mid);
+      math::phi_inv_direct_multi<D>(v, sgn, zz, lt, mid);
 #endif
     }
 #elif !defined(LPMC_MID_LATE)  // the previous batch's legs run beside the fp32 initial guesses
-    const FastTab lt = fast_tab(s_math);  // staged by stage_fast
     mid();
     math::phi_inv_stage1<D>(v, x0);
     if constexpr (PREFETCH) draw_uniforms<NP, H, CHECKED>(kc, next, lomin);
     math::phi_inv_stage2<D, CHECKED>(v, x0, neg, cur.half, zz, lt);
 #else
-    const FastTab lt = fast_tab(s_math);  // staged by stage_fast
     math::phi_inv_stage1<D>(v, x0);
     if constexpr (PREFETCH) draw_uniforms<NP, H, CHECKED>(kc, next, lomin);
     math::phi_inv_stage2<D, CHECKED>(v, x0, neg, cur.half, zz, lt, mid);
@@ -233,6 +287,14 @@ __device__ __forceinline__ void gen_draws(const LevelArgs& A, const TableView& t
     mid();
 #pragma unroll
     for (int d = 0; d < D; ++d) zz[d] = 0.0;
+    if constexpr (kShared) {  // the reflection of the exact branch above (same comments)
+#pragma unroll
+      for (int d = 0; d < D; ++d) {
+        const double q = __dsub_rn(u[d], 0.5);
+        sgn[d] = static_cast<uint32_t>(__double2hiint(q)) & 0x80000000u;
+        up[d] = __dsub_rn(1.0, __dsub_rn(0.5, fabs(q)));
+      }
+    }
   }
 #pragma unroll
   for (int h = 0; h < H; ++h) {
@@ -246,7 +308,9 @@ __device__ __forceinline__ void gen_draws(const LevelArgs& A, const TableView& t
           A.z_out[local[p] * (1ull << A.level) + n0 + h] = z[h][p];
         }
       }
-      if constexpr (TAB != kTabNone) {
+      if constexpr (kShared) {
+        zl[p] = approx_inv_up(tab, up[h * NP + p], sgn[h * NP + p]);
+      } else if constexpr (TAB != kTabNone) {
         // lower = !(u > 1/2): one half-plane test for both transforms (at
         // u == 1/2 both selections of 1 - u and u coincide and the result is
         // the exact 0 of EXACT_HALF / the replay)
@@ -466,6 +530,10 @@ __device__ __forceinline__ void simulate(const LevelArgs& A, const TableView& ta
   constexpr bool kNeedExact = kHat || TAB == kTabNone;
 
   const Arith ar(A);
+  // the fast mode's table view, once per path batch (its shared-space address
+  // is pinned in a register, fast_tab)
+  FastTab lt{};
+  if constexpr (kNeedExact && ZM == kZFast) lt = fast_tab(s_math);
   typename Arith::Range range;
   uint64_t kc[NP];
   bool u1[NP];
@@ -607,7 +675,7 @@ __device__ __forceinline__ void simulate(const LevelArgs& A, const TableView& ta
     Uniforms<NP> cur, unused;
     draw_uniforms<NP, 1, CHECKED>(kc, cur, lomin);
     gen_draws<Arith, TAB, kNeedExact, kBar, CHECKED, DUMP, 1, false, ZM>(
-        A, tab, s_math, ar, kc, u1, lomin, fk, local, valid, 0, cur, unused, z, zb);
+        A, tab, s_math, lt, ar, kc, u1, lomin, fk, local, valid, 0, cur, unused, z, zb);
     if constexpr (kHat) hat_fine(z[0], 0);
     if constexpr (kBar) bar_fine(zb[0], 0);
   } else {
@@ -626,7 +694,7 @@ __device__ __forceinline__ void simulate(const LevelArgs& A, const TableView& ta
       {
         Uniforms<2 * G * NP> next;
         gen_draws<Arith, TAB, kNeedExact, kBar, CHECKED, DUMP, 2 * G, true, ZM>(
-            A, tab, s_math, ar, kc, u1, lomin, fk, local, valid, 0, cur, next, zp, zbp);
+            A, tab, s_math, lt, ar, kc, u1, lomin, fk, local, valid, 0, cur, next, zp, zbp);
         cur = next;
       }
       auto legs = [&](const double (&zl)[2 * G][NP], const T (&zbl)[2 * G], uint64_t m0) {
@@ -638,13 +706,15 @@ __device__ __forceinline__ void simulate(const LevelArgs& A, const TableView& ta
       };
       // 32-bit trip counter (m itself is only read by the checked and dump
       // instances): two loop instructions instead of six
-      for (uint64_t m = G; m < halves;)
-      for (uint32_t trips = trip_count(halves - m, G); trips != 0; --trips, m += G) {
+      for (uint64_t m0 = G; m0 < halves;) {
+      const uint32_t trips = trip_count(halves - m0, G);
+      for (uint32_t it = 0; it < trips; ++it) {
+        const uint64_t m = m0 + static_cast<uint64_t>(it) * G;  // dead in production instances
         double z[2 * G][NP];
         T zb[2 * G];
         Uniforms<2 * G * NP> next;
         gen_draws<Arith, TAB, kNeedExact, kBar, CHECKED, DUMP, 2 * G, true, ZM>(
-            A, tab, s_math, ar, kc, u1, lomin, fk, local, valid, 2 * m, cur, next, z, zb,
+            A, tab, s_math, lt, ar, kc, u1, lomin, fk, local, valid, 2 * m, cur, next, z, zb,
             [&]() { legs(zp, zbp, m - G); });
         cur = next;
 #pragma unroll
@@ -654,21 +724,27 @@ __device__ __forceinline__ void simulate(const LevelArgs& A, const TableView& ta
           for (int p = 0; p < NP; ++p) zp[i][p] = z[i][p];
         }
       }
+      m0 += static_cast<uint64_t>(trips) * G;
+      }
       legs(zp, zbp, halves - G);
       } else {
-      for (uint64_t m = 0; m < halves;)
-      for (uint32_t trips = trip_count(halves - m, G); trips != 0; --trips, m += G) {
+      for (uint64_t m0 = 0; m0 < halves;) {
+      const uint32_t trips = trip_count(halves - m0, G);
+      for (uint32_t it = 0; it < trips; ++it) {
+        const uint64_t m = m0 + static_cast<uint64_t>(it) * G;  // dead in production instances
         double z[2 * G][NP];
         T zb[2 * G];
         Uniforms<2 * G * NP> next;
         gen_draws<Arith, TAB, kNeedExact, kBar, CHECKED, DUMP, 2 * G, true, ZM>(
-            A, tab, s_math, ar, kc, u1, lomin, fk, local, valid, 2 * m, cur, next, z, zb);
+            A, tab, s_math, lt, ar, kc, u1, lomin, fk, local, valid, 2 * m, cur, next, z, zb);
         cur = next;
 #pragma unroll
         for (int g = 0; g < G; ++g) {
           const uint64_t n = 2 * (m + g);
           coarse_step(z[2 * g], z[2 * g + 1], zb[2 * g], zb[2 * g + 1], n);
         }
+      }
+      m0 += static_cast<uint64_t>(trips) * G;
       }
       }
     } else {  // fewer coarse steps than one batch: one coarse step at a time
@@ -678,7 +754,7 @@ __device__ __forceinline__ void simulate(const LevelArgs& A, const TableView& ta
         Uniforms<2 * NP> cur, unused;
         draw_uniforms<NP, 2, CHECKED>(kc, cur, lomin);
         gen_draws<Arith, TAB, kNeedExact, kBar, CHECKED, DUMP, 2, false, ZM>(
-            A, tab, s_math, ar, kc, u1, lomin, fk, local, valid, 2 * m, cur, unused, z, zb);
+            A, tab, s_math, lt, ar, kc, u1, lomin, fk, local, valid, 2 * m, cur, unused, z, zb);
         coarse_step(z[0], z[1], zb[0], zb[1], 2 * m);
       }
     }
@@ -790,7 +866,10 @@ __global__ void __launch_bounds__(level_threads<Arith, LEGS, TAB, ZM>(), level_c
   constexpr int kStaged = ZM == kZGlibc ? kMathWords : kFastWords;
   __shared__ __align__(16) double s_static[(kNeedExact && !kPersist) ? kStaged : 2];
   const double* s_math = kPersist ? s_dyn : s_static;
-  double* s_table = s_dyn + (kPersist ? kFastWords : 0);
+  // [direct table (persistent)] [reversed copy (run_copy instances)] [the table]:
+  // the unchecked pass's copy sits at a compile-time offset
+  double* s_run = s_dyn + (kPersist ? kFastWords : 0);
+  double* s_table = s_run + (run_copy<TAB, DUMP, ZM>() ? kRunCopyWords : 0);
   if constexpr (kNeedExact) {
     if constexpr (ZM == kZGlibc) {
       stage_math(s_static, kStaged);
@@ -804,17 +883,25 @@ __global__ void __launch_bounds__(level_threads<Arith, LEGS, TAB, ZM>(), level_c
     for (int i = threadIdx.x; i < A.table_words; i += blockDim.x) s_table[i] = A.table[i];
     tab = TableView{s_table, A.table_stride, A.K, A.degree, A.dyadic, A.table_simple, A.tail};
     tab_run = tab;
-    if constexpr (Arith::kScaled) {
-      // second copy with c0, c1 (and the tail records' value) scaled by 2^kz:
-      // exact, and the scaled polynomial value is the value scaled
-      static_assert(TAB == kTabDyadicLinear, "scaled arithmetics: dyadic-linear tables");
-      double* s2 = s_table + A.table_words;
-      for (int i = threadIdx.x; i < A.table_words; i += blockDim.x) {
-        const double w = A.table[i];
-        s2[i] = (i % kDyadicRecord) >= 2 ? w * A.hs_zscale : w;
+    static_assert(!Arith::kScaled || TAB == kTabDyadicLinear,
+                  "scaled arithmetics: dyadic-linear tables");
+    if constexpr (run_copy<TAB, DUMP, ZM>()) {
+      // the unchecked pass's copy: records reversed (approx_inv_up) and, for
+      // the native binary16 arithmetic, c0, c1 (and the tail records' value)
+      // scaled by 2^kz -- exact, and the scaled polynomial value is the value
+      // scaled
+      double* s2 = s_run;
+      for (int i = threadIdx.x; i < kRunCopyWords; i += blockDim.x) {
+        const int w = i % kDyadicRecord;
+        double val = A.table[run_copy_source(i / kDyadicRecord) * kDyadicRecord + w];
+        if constexpr (Arith::kScaled) {
+          if (w >= 2) val *= A.hs_zscale;
+        }
+        s2[i] = val;
       }
       tab_run = TableView{s2, A.table_stride, A.K, A.degree, A.dyadic, A.table_simple,
-                          A.tail * A.hs_zscale};
+                          Arith::kScaled ? A.tail * A.hs_zscale : A.tail,
+                          pinned_saddr(s2)};
     }
   }
   __syncthreads();
@@ -1095,9 +1182,8 @@ template <class Arith, bool KAHAN, int LEGS, int TAB, bool DUMP, int ZM>
 cudaError_t launch_one(const LevelArgs& A, cudaStream_t s) {
   constexpr bool kPersist = level_persistent<LEGS, TAB, ZM>();
   constexpr int kThreads = level_threads<Arith, LEGS, TAB, ZM>();
-  const size_t smem = (TAB != kTabNone ? static_cast<size_t>(A.table_words) * sizeof(double) *
-                                             (Arith::kScaled ? 2 : 1)
-                                       : 0) +
+  const size_t smem = (TAB != kTabNone ? static_cast<size_t>(A.table_words) * sizeof(double) : 0) +
+                      (run_copy<TAB, DUMP, ZM>() ? kRunCopyWords * sizeof(double) : 0) +
                       (kPersist ? static_cast<size_t>(kFastWords) * sizeof(double) : 0);
   unsigned grid = static_cast<unsigned>(A.n_batches);
   if constexpr (kPersist) {  // one CTA per SM, each group looping over batches
@@ -1157,7 +1243,8 @@ template <class Arith, bool KAHAN, int LEGS, bool DUMP, int ZM>
 cudaError_t configure_tabs() {
   // persistent instances add the lane-private direct table
   constexpr int kGen = kMaxDynSmem + (level_persistent<LEGS, kTabGeneric, ZM>() ? kFastWords * 8 : 0);
-  constexpr int kDyn = kMaxDynSmem + (level_persistent<LEGS, kTabDyadicLinear, ZM>() ? kFastWords * 8 : 0);
+  constexpr int kDyn = kMaxDynSmem + (level_persistent<LEGS, kTabDyadicLinear, ZM>() ? kFastWords * 8 : 0) +
+                       kRunCopyWords * 8;
   cudaError_t e = cudaFuncSetAttribute(level_kernel<Arith, KAHAN, LEGS, kTabGeneric, DUMP, ZM>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, kGen);
   if (e != cudaSuccess) return e;

@@ -19,7 +19,7 @@ cudaError_t launch_legs(const LevelArgs& A, cudaStream_t s) {
 template <int LEGS, int TAB, bool PW>
 cudaError_t configure_inst() {
   constexpr int kBytes = (dev::level_persistent<LEGS, TAB, dev::kZFast>() ? dev::kFastWords * 8 : 0) +
-                         2 * kDyadicRecord * kDyadicRecords * 8;
+                         (kDyadicRecord * kDyadicRecords + dev::kRunCopyWords) * 8;
   return cudaFuncSetAttribute(
       dev::level_kernel<dev::ArithHalfScaled, false, LEGS, TAB, false, dev::kZFast, PW>,
       cudaFuncAttributeMaxDynamicSharedMemorySize, kBytes);

@@ -109,6 +109,11 @@ LPMC_HD double from_bits(uint64_t b) {
 LPMC_HD double flip_sign(double x, bool neg) {
   return from_bits(bits(x) ^ (neg ? 0x8000000000000000ull : 0ull));
 }
+// x with the high word XORed by `mask` (0 or 0x80000000, computed once per
+// draw and shared by both transforms)
+LPMC_HD double flip_sign_mask(double x, uint32_t mask) {
+  return from_bits(bits(x) ^ (static_cast<uint64_t>(mask) << 32));
+}
 
 // 1/d to ~1 ulp: hardware seed (MUFU.RCP64H) + two Newton steps.
 LPMC_HD double rcp_refined(double d) {
@@ -313,15 +318,33 @@ struct DirectTab {
 };
 struct LaneDirectTab {
   const double* t;  // copy c (base + 2 c)
+  uint32_t saddr;   // its shared-space address (device: loads without a generic pointer)
   static constexpr int kRec = kDirectRow * kLaneCopies;
   static constexpr int kStep = kLaneCopies;
 };
+// quad q (0..4) of record j
+LPMC_HD D2 direct_quad(const DirectTab& tab, uint32_t j, int q) {
+  return load2(tab.t + j * DirectTab::kRec + 2 * q);
+}
+LPMC_HD D2 direct_quad(const LaneDirectTab& tab, uint32_t j, int q) {
+#ifdef __CUDA_ARCH__
+  D2 r;
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];"
+               : "=d"(r.a), "=d"(r.b)
+               : "r"(tab.saddr + j * (LaneDirectTab::kRec * 8u) + q * (LaneDirectTab::kStep * 16u)));
+  return r;
+#else
+  return load2(tab.t + j * LaneDirectTab::kRec + 2 * q * LaneDirectTab::kStep);
+#endif
+}
 constexpr int kLaneDirectWords = kDirectWords * kLaneCopies;
 // source word of lane-layout word i: 16 doubles = 8 copies of one quad
 LPMC_HD int lane_direct_source(int i) { return 2 * (i >> 4) + (i & 1); }
 
-// Phi^-1(v) for v in [2^-(B+1), 1/2] (v == 1/2: the all-zero record, +0
-// exactly, gaussian.hpp:62).  Record index = exponent and top S mantissa
+// -Phi^-1(v) = Phi^-1(1 - v) >= 0 for v in [2^-(B+1), 1/2] (v == 1/2: the
+// all-zero record, +0 exactly, gaussian.hpp:62): the table holds the upper
+// half, so the exact and the approximate transform (invcdf_approx.hpp:47-49)
+// flip their signs on the same predicate, u < 1/2.  Record index = exponent and top S mantissa
 // bits of v; t = v - midpoint is exact (both in one binade; the midpoint is
 // v's bit pattern with the low mantissa bits replaced by 100...0).
 // *tail: v below the table (probability 2^-B per draw); the value returned
@@ -334,12 +357,11 @@ LPMC_HD double phi_inv_direct(double v, const V& tab, bool* tail) {
   const uint32_t idx = (hi >> kDirectShift) - kDirectBase;
   *tail = idx >= static_cast<uint32_t>(kDirectN);  // below the table: idx wrapped
   const uint32_t j = idx < static_cast<uint32_t>(kDirectN - 1) ? idx : static_cast<uint32_t>(kDirectN - 1);
-  const double* r = tab.t + j * V::kRec;
   const uint32_t hc = (hi & ~((1u << kDirectShift) - 1u)) | (1u << (kDirectShift - 1));
   const double t = v - from_bits(static_cast<uint64_t>(hc) << 32);
-  constexpr int S = V::kStep;
-  const D2 a = load2(r), b = load2(r + 2 * S), c = load2(r + 4 * S), d = load2(r + 6 * S);
-  const D2 e = load2(r + 8 * S);  // c0_lo, c0_hi
+  const D2 a = direct_quad(tab, j, 0), b = direct_quad(tab, j, 1), c = direct_quad(tab, j, 2);
+  const D2 d = direct_quad(tab, j, 3);
+  const D2 e = direct_quad(tab, j, 4);  // c0_lo, c0_hi
   double p = fmad(a.a, t, a.b);
   p = fmad(p, t, b.a);
   p = fmad(p, t, b.b);
@@ -679,13 +701,15 @@ struct NoMid {
 };
 
 // exact_inv_cdf for D reflected draws from the direct table: polynomial
-// evaluation for all, the tail fix-up behind one combined branch, sign (bit d
-// of `neg`: u > 1/2).  u == 1/2 needs no special case (the zero record).
-// `mid` runs in the same basic block as the polynomial evaluations.
+// evaluation for all, the tail fix-up behind one combined branch, sign: the
+// table holds the upper half, so the value is negated where sgn[d] =
+// 0x80000000 (u < 1/2) and kept where it is 0.  u == 1/2 needs no special
+// case (the zero record, +0 with sgn 0).  `mid` runs in the same basic block
+// as the polynomial evaluations.
 template <int D, class V, class Mid = NoMid>
-__device__ __forceinline__ void phi_inv_direct_multi(const double (&v)[D], uint32_t neg,
-                                                     double (&z)[D], const V& tab,
-                                                     Mid&& mid = Mid{}) {
+__device__ __forceinline__ void phi_inv_direct_multi(const double (&v)[D],
+                                                     const uint32_t (&sgn)[D], double (&z)[D],
+                                                     const V& tab, Mid&& mid = Mid{}) {
   bool tail[D];
 #pragma unroll
   for (int d = 0; d < D; ++d) z[d] = phi_inv_direct(v[d], tab, &tail[d]);
@@ -693,11 +717,13 @@ __device__ __forceinline__ void phi_inv_direct_multi(const double (&v)[D], uint3
   bool any_tail = false;
 #pragma unroll
   for (int d = 0; d < D; ++d) any_tail |= tail[d];
+  if (any_tail) {  // one rare region for all D draws
 #pragma unroll
-  for (int d = 0; d < D; ++d) {
-    if (any_tail && tail[d]) z[d] = phi_inv_lower_tail(v[d]);
-    z[d] = flip_sign(z[d], (neg >> d) & 1u);
+    for (int d = 0; d < D; ++d)
+      if (tail[d]) z[d] = -phi_inv_lower_tail(v[d]);
   }
+#pragma unroll
+  for (int d = 0; d < D; ++d) z[d] = flip_sign_mask(z[d], sgn[d]);
 }
 
 // `mid` runs between the Newton block and the slow-path fix-ups, in the
@@ -734,13 +760,13 @@ template <int D, class V>
 __device__ __forceinline__ void phi_inv_multi_direct(const double (&u)[D], double (&z)[D],
                                                      const V& tab) {
   double v[D];
-  uint32_t neg = 0;
+  uint32_t sgn[D];
 #pragma unroll
   for (int d = 0; d < D; ++d) {
     v[d] = u[d] > 0.5 ? 1.0 - u[d] : u[d];  // exact (gaussian.hpp:63)
-    neg |= (u[d] > 0.5 ? 1u : 0u) << d;
+    sgn[d] = u[d] < 0.5 ? 0x80000000u : 0u;  // u == 1/2: +0 (gaussian.hpp:62)
   }
-  phi_inv_direct_multi<D>(v, neg, z, tab);
+  phi_inv_direct_multi<D>(v, sgn, z, tab);
 }
 template <int D>
 __device__ __forceinline__ void phi_inv_multi(const double (&u)[D], double (&z)[D],

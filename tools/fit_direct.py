@@ -1,7 +1,8 @@
 """Fit the direct piecewise-polynomial table of the fast exact Gaussian
 (paper_2012_09739_b200/csrc/lpmc_direct_coef.h) with mpmath at 50 digits.
 
-Phi^-1 on the lower half, v = min(u, 1 - u) in [2^-(B+1), 1/2), is cut the
+-Phi^-1 on the lower half (the upper quantile Phi^-1(1 - v) > 0), v =
+min(u, 1 - u) in [2^-(B+1), 1/2), is cut the
 way the paper cuts its approximate transforms, but to binary64 accuracy:
 every binade [2^-(k+1), 2^-k), k = 1..B, into 2^S equal sub-intervals, a
 degree-DEG polynomial in t = v - v_c on each (v_c the sub-interval's
@@ -47,13 +48,20 @@ def ndtri_lower(v):
     return -mp.sqrt(2) * mp.erfinv(1 - 2 * v)
 
 
+def table_value(v):
+    """What the table stores: -Phi^-1(v) = Phi^-1(1 - v) > 0 for v < 1/2, so
+    that the exact and the approximate transform (which evaluates the upper
+    half, invcdf_approx.hpp:47-49) flip their signs on the same predicate."""
+    return -ndtri_lower(v)
+
+
 def fit_interval(a, b):
     """Monomial coefficients (ascending, in t = v - (a+b)/2) of the
     interpolant of Phi^-1 at DEG+1 Chebyshev nodes of [a, b]."""
     n = DEG + 1
     mid, half = (a + b) / 2, (b - a) / 2
     xs = [mp.cos(mp.pi * (2 * i + 1) / (2 * n)) for i in range(n)]
-    fs = [ndtri_lower(mid + half * x) for x in xs]
+    fs = [table_value(mid + half * x) for x in xs]
     V = mp.matrix(n, n)
     for i, x in enumerate(xs):
         for j in range(n):
@@ -121,7 +129,7 @@ def check(n=20000):
         t = mp.mpf(vf) - mp.mpf(vc)
         assert t == fl(t)
         z = eval_record(recs[idx], t)
-        zt = ndtri_lower(mp.mpf(vf))
+        zt = table_value(mp.mpf(vf))
         phi = mp.exp(-zt * zt / 2) / mp.sqrt(2 * mp.pi)
         unit = eps * (mp.mpf(vf) / phi + abs(zt))
         worst = max(worst, abs(z - zt) / unit)
@@ -135,7 +143,7 @@ def main():
     n = len(recs)
     out = ["// Generated by tools/fit_direct.py (mpmath, 50 digits).  Do not edit.",
            "#pragma once", "",
-           "// Phi^-1(v), v in [2^-(B+1), 1/2]: B binades x 2^S sub-intervals, degree DEG in",
+           "// -Phi^-1(v) = Phi^-1(1 - v) >= 0, v in [2^-(B+1), 1/2]: B binades x 2^S sub-intervals, degree DEG in",
            "// t = v - midpoint; record = c_DEG..c_1, c0_lo, c0_hi (+ padding), index order =",
            "// increasing v, last record (all zero) = v == 1/2.",
            f"#define LPMC_DIRECT_B {B}", f"#define LPMC_DIRECT_S {S}",
