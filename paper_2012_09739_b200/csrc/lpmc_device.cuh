@@ -145,6 +145,7 @@ __device__ __forceinline__ double approx_inv(const TableView& t, double u, bool 
     const double vm = __dsub_rn(0x1.fffffffffffffp-1, up);
     const uint32_t eb = static_cast<uint32_t>(__double2hiint(vm)) >> 20;
     const uint32_t j = min(1021u - eb, static_cast<uint32_t>(kDyadicRecords - 1));
+    LPMC_DCHECK(j < static_cast<uint32_t>(kDyadicRecords));
     const double* b = t.base + 6 * j;
     const math::D2 cw = math::load2(b);
     const math::D2 c01 = math::load2(b + 2);
@@ -228,6 +229,7 @@ __device__ __forceinline__ double approx_inv_up(const TableView& t, double up, u
   const double vm = __dsub_rn(0x1.fffffffffffffp-1, up);  // see approx_inv
   const uint32_t r = min((static_cast<uint32_t>(__double2hiint(vm)) >> 20) - (1021u - 52u),
                          static_cast<uint32_t>(kRunCopyRecords - 1));
+  LPMC_DCHECK(r < static_cast<uint32_t>(kRunCopyRecords) && t.saddr != 0u);
   const uint32_t b = t.saddr + r * (kDyadicRecord * 8u);
   const math::D2 cw = lds2(b);
   const math::D2 c01 = lds2(b + 16u);

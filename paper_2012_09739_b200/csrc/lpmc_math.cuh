@@ -357,6 +357,7 @@ LPMC_HD double phi_inv_direct(double v, const V& tab, bool* tail) {
   const uint32_t idx = (hi >> kDirectShift) - kDirectBase;
   *tail = idx >= static_cast<uint32_t>(kDirectN);  // below the table: idx wrapped
   const uint32_t j = idx < static_cast<uint32_t>(kDirectN - 1) ? idx : static_cast<uint32_t>(kDirectN - 1);
+  LPMC_DCHECK(j < static_cast<uint32_t>(kDirectN));
   const uint32_t hc = (hi & ~((1u << kDirectShift) - 1u)) | (1u << (kDirectShift - 1));
   const double t = v - from_bits(static_cast<uint64_t>(hc) << 32);
   const D2 a = direct_quad(tab, j, 0), b = direct_quad(tab, j, 1), c = direct_quad(tab, j, 2);
