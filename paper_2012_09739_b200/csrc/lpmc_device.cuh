@@ -555,9 +555,8 @@ struct ArithHalf2 {  // native IEEE binary16, two paths per thread
 // Overflow gives inf, which is absorbing and caught at the end of the path.
 // A path that fails any of these is replayed in the fp32-carried emulation
 // (Replay = ArithF32Round, bitwise the reference), so the result never
-// depends on the guard -- only the speed does (measured rate of replays:
-// below 1e-3 of the paths at level 12).  No Kahan (the emulation instance
-// serves it), dyadic-linear tables or none.
+// depends on the guard -- only the speed does.  With or without Kahan
+// compensation (ArithHalfScaled::kahan), dyadic-linear tables or none.
 // State of ArithHalfScaled: X = (x_fine, x_coarse) in one binary16 pair; the
 // guard tracks both lanes at once (packed min / max of |X|) and, per coarse
 // step, the larger of the two scaled increments.  NaN is invisible to min / max and
@@ -596,9 +595,12 @@ struct ArithHalfScaled {
   static constexpr bool kIeee = false;
   static constexpr bool kPair = false;
   static constexpr bool kPow2 = true;  // PW instances fold the carrier legs (step_hat_pw)
-  __half2 musg, mu2, sg2, sdt2, sdt_one, p1_2, p1_p1c, p2_2;
+  __half2 musg, mu2, sg2, sdt2, sdt_one, p1_2, p1_p1c, p2_2, q1_2, q2_2;
   double zscale;
   __device__ explicit ArithHalfScaled(const LevelArgs& A) : zscale(A.hs_zscale) {
+    const __half q1 = __ushort_as_half(A.hs_q1), q2 = __ushort_as_half(A.hs_q2);
+    q1_2 = __halves2half2(q1, q1);
+    q2_2 = __halves2half2(q2, q2);
     const __half mu = __ushort_as_half(A.hs_mu), sg = __ushort_as_half(A.hs_sigma);
     const __half sd = __ushort_as_half(A.hs_sdt), one = __ushort_as_half(0x3c00u);
     const __half p1 = __ushort_as_half(A.hs_p1), p1c = __ushort_as_half(A.hs_p1c);
@@ -634,31 +636,60 @@ struct ArithHalfScaled {
     const uint32_t b = *reinterpret_cast<const uint32_t*>(&x);
     return ((b & 0x7c00u) == 0x7c00u || (b & 0x7c000000u) == 0x7c000000u) ? 1u : 0u;
   }
-  // em_step (sde.hpp:60-68) of the fine leg (lane 0 of X); returns the new
-  // x_fine in both lanes
-  __device__ T fine_value(T X, T zs) const {
+  // kahan_accumulate (sde.hpp:85-92) on scaled values: the increment is
+  // inc = i P2 and the compensation is carried as cs = comp / P2, so
+  //   ys = R(i - cs)                   = R(inc - comp) / P2
+  //   s  = fma(ys, P2, x)              = R(sum + y)
+  //   t  = R(s - x)                      (a multiple of 2^-14: normal or 0)
+  //   cs = fma(t Q1, Q2, -ys), Q1 Q2 = 1 / P2   = R(R(s - x) - y) / P2
+  // (t Q1 is an exact scaling; 1/P2 may exceed binary16's range, hence two
+  // factors).  Differences below 2^-14 are multiples of 2^-24 and exact, in
+  // the reference as well (they have at most 10 bits).  Returns s.
+  __device__ T kahan(T x, T i, T& cs) const {
+    const T ys = __hsub2_rn(i, cs);
+    const T s = __hfma2(ys, p2_2, x);
+    const T t = __hsub2_rn(s, x);
+    cs = __hfma2(__hmul2_rn(t, q1_2), q2_2, __hneg2(ys));
+    return s;
+  }
+  // em_step / em_step_kahan (sde.hpp:60-68, :95-104) of the fine leg (lane 0
+  // of X, lane 0 of the compensation pair); returns the new x_fine in both
+  // lanes (and, with Kahan, the new compensation in both lanes of csf)
+  template <bool KAHAN>
+  __device__ T fine_value(T X, T zs, T& csf) const {
     const T xf = __low2half2(X);
     const T ab = __hmul2_rn(xf, musg);                      // (R(x mu_m), R(x sg_m))
     const T cc = __hmul2_rn(__high2half2(ab), sdt2);        // R(R(x sg_m) sdt_m)
     const T e = __hmul2_rn(cc, __low2half2(zs));
     const T i = __hfma2(__low2half2(ab), p1_2, e);
-    return __hfma2(i, p2_2, xf);
+    if constexpr (KAHAN) {
+      csf = __low2half2(csf);
+      return kahan(xf, i, csf);
+    } else {
+      return __hfma2(i, p2_2, xf);
+    }
   }
   // one fine step alone (level 0, the two-way sampler): lane 1 is kept
-  __device__ void fine(T& X, T zs, Range& r) const {
-    const T xf1 = fine_value(X, zs);
+  template <bool KAHAN>
+  __device__ void fine(T& X, T& CS, T zs, Range& r) const {
+    T csf = CS;
+    const T xf1 = fine_value<KAHAN>(X, zs, csf);
     X = __halves2half2(__low2half(xf1), __high2half(X));
+    if constexpr (KAHAN) CS = __halves2half2(__low2half(csf), __high2half(CS));
     r.track(X);
   }
   // fine step n (zs0), then fine step n + 1 (zs1) and the coarse step as one
   // pair: em_step and em_step_dw (sde.hpp:60-79) with dW = sqrt_dt z0 +
   // sqrt_dt z1 (sde.hpp:261-264); the coarse lane multiplies by an exact 1
   // where the fine lane takes sdt_m
-  __device__ void coarse_step(T& X, T zs0, T zs1, Range& r) const {
+  template <bool KAHAN>
+  __device__ void coarse_step(T& X, T& CS, T zs0, T zs1, Range& r) const {
     const T Z = __halves2half2(__low2half(zs0), __low2half(zs1));
-    const T xf1 = fine_value(X, zs0);
+    T csf = CS;
+    const T xf1 = fine_value<KAHAN>(X, zs0, csf);
     r.track(xf1);
     const T X1 = __halves2half2(__low2half(xf1), __high2half(X));
+    if constexpr (KAHAN) CS = __halves2half2(__low2half(csf), __high2half(CS));
     const T a = __hmul2_rn(X1, mu2);
     const T b = __hmul2_rn(X1, sg2);
     const T w = __hmul2_rn(Z, sdt2);                                   // (w0, w1)
@@ -667,7 +698,11 @@ struct ArithHalfScaled {
     const T cc = __hmul2_rn(b, sdt_one);                               // (R(b sdt_m), b)
     const T e = __hmul2_rn(cc, __halves2half2(__high2half(Z), __low2half(dw)));  // (zs1, dW)
     const T i = __hfma2(a, p1_p1c, e);
-    X = __hfma2(i, p2_2, X1);
+    if constexpr (KAHAN) {
+      X = kahan(X1, i, CS);
+    } else {
+      X = __hfma2(i, p2_2, X1);
+    }
     r.track(X);
   }
   // unused generic interface (step_bar is never instantiated for this policy)

@@ -569,8 +569,13 @@ lpmc_status build_spec(const lpmc_gbm* model, int32_t level, const lpmc_precisio
         zmax = std::max(zmax, std::fabs(r[2]) + std::fabs(r[3]));
       }
     }
+    // 1 / P2 = 2^-e_d as two binary16 powers of two (the Kahan compensation)
+    const int q1e = -e_d > 12 ? 12 : -e_d;
+    const int q2e = -e_d - q1e;
     uint16_t hx0 = 0;
-    const bool ok = kz >= 0 && kz <= 13 && std::ldexp(zmax, kz) <= 30000.0 && e_d >= -24 &&
+    const bool ok = exact_half(std::ldexp(1.0, q1e), &A.hs_q1) &&
+                    exact_half(std::ldexp(1.0, q2e), &A.hs_q2) && q1e >= -10 && q2e >= 0 &&
+                    kz >= 0 && kz <= 13 && std::ldexp(zmax, kz) <= 30000.0 && e_d >= -24 &&
                     e_d <= 14 && exact_half(mu_m, &A.hs_mu) && exact_half(sg_m, &A.hs_sigma) &&
                     exact_half(sdt_m, &A.hs_sdt) && exact_half(std::ldexp(1.0, e_d), &A.hs_p2) &&
                     exact_half(low[2], &hx0) && hx0 == A.h_x0 && std::fabs(low[2]) >= 0x1p-4 &&

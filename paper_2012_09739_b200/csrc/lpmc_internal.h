@@ -95,6 +95,7 @@ struct LevelArgs {
   // mu_l, sigma_l, sqrt_dt_l, of P1, P1c, P2, and 2^kz
   int32_t hs_native = 0;
   uint16_t hs_mu = 0, hs_sigma = 0, hs_sdt = 0, hs_p1 = 0, hs_p1c = 0, hs_p2 = 0;
+  uint16_t hs_q1 = 0, hs_q2 = 0;  // Q1 Q2 = 1 / P2 (the Kahan compensation's scale)
   double hs_zscale = 1.0;
 };
 
@@ -110,12 +111,13 @@ inline LPMC_KEY_HD unsigned long long err_key_of(uint64_t path, uint32_t kind, u
 }
 
 // Production launches of the m = 10 emulation that run on native binary16
-// (dev::ArithHalfScaled): the host proved the scales (hs_native), no Kahan, no
+// (dev::ArithHalfScaled): the host proved the scales (hs_native), no
 // dump, fast exact Gaussians, a dyadic-linear table or none.  Everything
 // else, and every path that leaves the native guard, runs the fp32-carried
 // emulation.
 inline bool use_native_half(const LevelArgs& A, bool kahan, bool dump) {
-  return A.hs_native != 0 && !kahan && !dump && A.exact_z == 0 && A.legs != 1 &&
+  (void)kahan;  // with or without Kahan compensation
+  return A.hs_native != 0 && !dump && A.exact_z == 0 && A.legs != 1 &&
          (A.table == nullptr || (A.dyadic != 0 && A.table_simple != 0 && A.degree == 1));
 }
 
@@ -168,7 +170,7 @@ cudaError_t launch_level_f32(const LevelArgs& A, bool kahan, bool dump, void* st
 cudaError_t launch_level_f32r(const LevelArgs& A, bool kahan, bool dump, void* stream);
 cudaError_t launch_level_f64r(const LevelArgs& A, bool kahan, bool dump, void* stream);
 cudaError_t launch_level_half2(const LevelArgs& A, bool kahan, bool dump, void* stream);
-cudaError_t launch_level_h16(const LevelArgs& A, void* stream);  // dev::ArithHalfScaled
+cudaError_t launch_level_h16(const LevelArgs& A, bool kahan, void* stream);  // dev::ArithHalfScaled
 cudaError_t configure_level_carrier();
 cudaError_t configure_level_f32();
 cudaError_t configure_level_f32r();

@@ -295,11 +295,11 @@ LaunchResult launch_paths(const LevelArgs& A, BarArith arith, bool kahan, bool d
     case BarArith::kF32: e = launch_level_f32(A, kahan, dump, stream); break;
     case BarArith::kF32Round:
       // m = 10 on native binary16 (dev::ArithHalfScaled) where the host proved
-      // the scales: production launches without Kahan, fast exact Gaussians,
-      // dyadic-linear tables or none; everything else on the fp32-carried
+      // the scales: production launches, fast exact Gaussians, dyadic-linear
+      // tables or none; everything else on the fp32-carried
       // emulation, which also replays the paths that leave the native guard
       if (use_native_half(A, kahan, dump) && std::getenv("LPMC_NO_NATIVE_HALF") == nullptr) {
-        e = launch_level_h16(A, stream);
+        e = launch_level_h16(A, kahan, stream);
       } else {
         e = launch_level_f32r(A, kahan, dump, stream);
       }

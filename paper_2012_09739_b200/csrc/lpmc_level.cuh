@@ -573,7 +573,7 @@ __device__ __forceinline__ void simulate(const LevelArgs& A, const TableView& ta
   };
   auto bar_fine = [&](T zb, uint64_t n) {
     if constexpr (Arith::kScaled) {  // native binary16 with static scales: xbf = (fine, coarse)
-      ar.fine(xbf, zb, range);
+      ar.template fine<KAHAN>(xbf, cmpf, zb, range);  // cmpf = (comp_fine, comp_coarse) / P2
     } else if constexpr (kPw) {
       step_bar_pw<Arith, KAHAN>(ar, range, xbf, cmpf, mu_dtf, sg_sdt, zb);
     } else {
@@ -635,7 +635,7 @@ __device__ __forceinline__ void simulate(const LevelArgs& A, const TableView& ta
       if constexpr (kHat) hat_fine(z0, n);
       if constexpr (kHat) hat_fine(z1, n + 1);
       coarse(z0, z1, zb0, zb1, n + 1);  // the hat leg only
-      ar.coarse_step(xbf, zb0, zb1, range);
+      ar.template coarse_step<KAHAN>(xbf, cmpf, zb0, zb1, range);
     } else {
       if constexpr (kHat) hat_fine(z0, n);
       if constexpr (kBar) bar_fine(zb0, n);
