@@ -508,6 +508,20 @@ __device__ __forceinline__ void step_bar_joint(const Arith& ar, typename Arith::
                                 kStageBarFine);
 }
 
+// Does the stream of path `local` hold a draw with u == 1 (b = 2^53 - 1) or
+// u == 1/2 (b = 2^52) among this level's 2^level draws?  Out of line: runs
+// only for the paths the low-word prefilter flagged.
+static __device__ __noinline__ bool has_special_draw(const LevelArgs& A, uint64_t local) {
+  uint64_t kc = path_key(A.seed_key, A.path_base + local) + A.counter0 * kCounterStep;
+  const uint64_t n = 1ull << A.level;
+  bool found = false;
+  for (uint64_t i = 0; i < n; ++i) {
+    const uint64_t b = next_draw(kc);
+    found |= b == kTopDraw || b == kHalfDraw;
+  }
+  return found;
+}
+
 // iterations of a loop over `left` coarse steps, `g` per iteration, capped
 // so that they fit 32 bits (the caller loops again)
 __device__ __forceinline__ uint32_t trip_count(uint64_t left, int g) {
@@ -775,7 +789,15 @@ __device__ __forceinline__ void simulate(const LevelArgs& A, const TableView& ta
     const bool hat_range = kHat && kPw && A.level > 0 && hrange[p].bad();
     // native binary16: a path outside the guard is replayed in the emulation
     const bool bar_range = Arith::kScaled && kBar && range.bad();
-    R.suspect[p] = u1[p] || (!CHECKED && lomin[p] <= 1u) || hat_bad || hat_range || bar_range ||
+    // the low-word prefilter fired (2^-31 per draw): regenerate the path's
+    // draws (RNG only, ~1/20 of a checked replay) and replay only if one of
+    // them really is u == 1 or u == 1/2 -- at level 16 and above the filter's
+    // false positives would otherwise cost whole-group replays
+    bool special = false;
+    if constexpr (!CHECKED) {
+      if (lomin[p] <= 1u) special = has_special_draw(A, local[p]);
+    }
+    R.suspect[p] = u1[p] || special || hat_bad || hat_range || bar_range ||
                    ((bad_f >> p) & 1u) || ((bad_c >> p) & 1u);
 #ifdef LPMC_TRACE_REPLAY
     if (!CHECKED && R.suspect[p]) {
