@@ -1,16 +1,26 @@
-// The coupled level sampler: simulate_coupled (sde.hpp:211-284) for 256
-// paths per CTA (one path per thread, two for the IEEE-half2 legs), reduced
-// to per-batch central moments in the same CTA.
+// The coupled level sampler: simulate_coupled (sde.hpp:211-284) for batches
+// of 256 paths (one path per thread, two for the IEEE-half2 legs), each
+// reduced to per-batch central moments by the threads that simulated it.
+// Instances that draw exact Gaussians in the fast mode are persistent: one
+// 768-thread CTA per SM, three 256-path groups looping over batches on their
+// own named barriers, the direct inverse-CDF table in eight lane-private
+// shared-memory copies (lpmc_math.cuh); the others run one batch per CTA.
 //
-// Hot loop per coarse step m (two fine draws):
-//   RNG for both draws -> exact Gaussians for both (phi_inv_multi: branch-free
-//   central Acklam, one warp-uniform tail pass, interleaved Newton) ->
-//   approximate Gaussians -> fine legs x2 -> coarse legs.
-// State stays in registers.  Failure bookkeeping in the hot loop is two
-// bits (a u == 1 draw; a native-range excursion); non-finite values are
-// absorbing, so a non-finite end state <=> a non-finite operation somewhere.
-// Only a path that may have failed is replayed (noinline, CHECKED) to find
-// its first failing step in the reference's serial order.
+// Hot loop per coarse step (two fine draws), software-pipelined across
+// batches:
+//   legs of the previous batch -> RNG for the next batch -> reflection of
+//   both draws (three exact FP64 subtractions, no compares or selects) ->
+//   exact Gaussians (direct table, one rare out-of-line tail call) ->
+//   approximate Gaussians (reversed dyadic table copy) -> rounding into the
+//   bar precision.
+// State stays in registers.  Failure bookkeeping in the hot loop is a
+// running minimum over the draws' low words (a superset of the u == 1 and
+// u == 1/2 draws) and the range guards of the folded / native arithmetics;
+// non-finite values are absorbing, so a non-finite end state <=> a
+// non-finite operation somewhere.  Only a path that may have failed or left
+// a guard is replayed (noinline, CHECKED, in the reference's own operation
+// order) to find its values and its first failing step in the reference's
+// serial order.
 #pragma once
 
 #include <cstdio>

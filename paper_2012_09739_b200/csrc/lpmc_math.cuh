@@ -1,14 +1,24 @@
-// Device math for the exact Gaussian: the reference's Acklam + one Newton
-// step (gaussian.hpp:26-65), restated for the sm_100a issue budget.
+// Device math for the exact Gaussian (gaussian.hpp:26-65: Acklam's rational
+// + one Newton step on libm's erfc), restated for the sm_100a issue budget.
+//
+// Round 2: the default transform is ONE TABLE LOOKUP -- phi_inv_direct: a
+// degree-8 polynomial of Phi^-1 on 16 sub-intervals per binade of
+// v = min(u, 1 - u) (tools/fit_direct.py, lpmc_direct_coef.h), 10 FP64
+// operations per draw, 0.42 eps (v/pdf + |z|) from the true value
+// (DirectTab: flat; LaneDirectTab: eight lane-private copies, conflict-free
+// gathers in the persistent level kernel).  Draws below the table (v < 2^-15,
+// 6e-5 of them) take round 1's transform, which the rest of this header
+// describes, out of line (phi_inv_lower_tail); -DLPMC_HALLEY_Z rebuilds it
+// everywhere (A/B).
 //
 // Why not libdevice: its erfc/exp keep their polynomial coefficients as
 // 64-bit literals, which ptxas rematerialises through uniform moves on every
 // loop iteration (136 UMOV per warp-step, 24% of all issue slots in the v0
 // kernel, profiles/r01_v0_summary.md), and their range branches diverge.
 // Here every coefficient is a constant-bank operand (__constant__) or a
-// shared-memory load, and the hot path has one branch (Acklam's tail).
+// shared-memory load.
 //
-// Accuracy design:
+// Round 1's transform ("below the table"):
 //  * The reference refines Acklam's x0 (1.15e-9) by one Newton step.  Here
 //    x0 comes from an fp32 polynomial in log2(v (1 - v)) (~4e-7 relative,
 //    tools/fit_x0f.py) and one Halley step x0 - r (1 - x0 r / 2),
@@ -22,15 +32,15 @@
 //    hi + lo (tools/fit_math.py).  1/pdf is sqrt(2 pi) 2^-k / p(r): the same
 //    exponential, no second exp, no division.  Table indices come from the
 //    low words of shifted FMAs (no F2I/I2F conversions).
-//  * t >= kDevTMax (6.5: u < 1e-20, never drawn by the sampler; 3 with the
-//    lane-private table layout, LaneTab below) takes a libdevice slow path
-//    out of line.
+//  * t >= kDevTMax (6.5: u < 1e-20, never drawn by the sampler) takes a
+//    libdevice slow path out of line.
 //  * -DLPMC_X0_ACKLAM restores Acklam's binary64 x0 + Newton (A/B only,
 //    tools/gpu_ab_x0.sh).
 //
-// All functions are __host__ __device__ so tests/cpp/math_accuracy.cpp can
-// check the erfc core on the CPU against mpmath; the core uses only IEEE
-// fma/mul/add and integer bit operations, hence is bitwise the same there.
+// All functions are __host__ __device__ so the host hooks (lpmc_erfc_core,
+// lpmc_phi_inv_direct_core; tests/test_math_host.py) can check them on the
+// CPU against mpmath; they use only IEEE fma/mul/add and integer bit
+// operations, hence are bitwise the same there.
 #pragma once
 
 #include <cstdint>
