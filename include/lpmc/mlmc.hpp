@@ -115,6 +115,27 @@ inline CoupledMoments run_coupled_paths(const SdeModel& model, int level,
   return m;
 }
 
+// Extension (diagnostic, no device needed): the arithmetic a production
+// launch of run_coupled_paths uses for the low-precision legs -- low byte 0
+// carrier, 1 native fp32, 2 fp32-carried rounding, 3 binary64 rounding, 4 IEEE
+// half2; LPMC_ARITH_POW2_FOLDED / LPMC_ARITH_NATIVE_BINARY16 flags
+// (lpmc_bar_arithmetic, include/lpmc_b200.h).  The choice never changes a
+// result.
+inline int bar_arithmetic(const SdeModel& model, int level, const PrecisionSpec& spec_low,
+                          const InvCdfApprox* approx, bool kahan,
+                          const DeviceOptions& options = {}) {
+  const lpmc_gbm g = detail::gbm_of(model);
+  const lpmc_precision p = spec_low.c_abi();
+  const lpmc_options o = options.c_abi();
+  lpmc_invcdf_table t{};
+  if (approx != nullptr) t = approx->c_abi();
+  std::int32_t out = 0;
+  lpmc_error err{};
+  detail::throw_status(
+      lpmc_bar_arithmetic(&g, level, &p, approx ? &t : nullptr, kahan ? 1 : 0, &o, &out, &err), err);
+  return out;
+}
+
 namespace detail {
 inline LevelStats stats_from_c(const lpmc_level_stats& s) {
   LevelStats r;

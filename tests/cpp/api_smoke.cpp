@@ -110,6 +110,18 @@ int main(int argc, char** argv) {
     CHECK(ExperimentConfig{}.paths_for_level(11) == 2500);
   }
 
+  {  // extension: which arithmetic the low-precision legs run on (host decision)
+    const SdeModel gbm = make_gbm(0.05, 0.2, 1.0, 1.0);
+    const InvCdfApprox lin = InvCdfApprox::build(InvCdfApprox::Kind::linear, 16);
+    const int h = bar_arithmetic(gbm, 12, PrecisionSpec::fp16(), &lin, false);
+    CHECK((h & 0xff) == 2 && (h & LPMC_ARITH_NATIVE_BINARY16) && (h & LPMC_ARITH_POW2_FOLDED));
+    const int k = bar_arithmetic(gbm, 11, PrecisionSpec::fp16(), &lin, true);
+    CHECK((k & LPMC_ARITH_NATIVE_BINARY16) && !(k & LPMC_ARITH_POW2_FOLDED));
+    const int f = bar_arithmetic(gbm, 12, PrecisionSpec::fp32(), &lin, false);
+    CHECK((f & 0xff) == 1 && !(f & LPMC_ARITH_NATIVE_BINARY16) && (f & LPMC_ARITH_POW2_FOLDED));
+    CHECK((bar_arithmetic(gbm, 6, PrecisionSpec::carrier(), nullptr, false) & 0xff) == 0);
+  }
+
   if (host_only) {
     std::printf(g_fail ? "host-only FAILED\n" : "host-only ok\n");
     return g_fail ? 1 : 0;
