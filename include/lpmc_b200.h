@@ -336,11 +336,13 @@ lpmc_status lpmc_device_math(int32_t op, const double* in, uint64_t n,
  * with integer rounding, 4 IEEE binary16 pairs; LPMC_ARITH_POW2_FOLDED: power-
  * of-two steps folded into the model constants; LPMC_ARITH_NATIVE_BINARY16:
  * the m = 10 legs run on native binary16 with static scales (paths that leave
- * its guard are replayed in arithmetic 2).  All of them are bitwise the
+ * its guard are replayed in arithmetic 2); LPMC_ARITH_NATIVE_BFLOAT16: the
+ * m = 7 legs run on native bfloat16.  All of them are bitwise the
  * reference's softfloat.hpp:69-111 semantics; the choice only affects speed.
  */
 #define LPMC_ARITH_POW2_FOLDED 0x100
 #define LPMC_ARITH_NATIVE_BINARY16 0x200
+#define LPMC_ARITH_NATIVE_BFLOAT16 0x400 /* the m = 7 legs on native bfloat16 */
 lpmc_status lpmc_bar_arithmetic(const lpmc_gbm* model, int32_t level, const lpmc_precision* prec,
                                 const lpmc_invcdf_table* table, int32_t kahan,
                                 const lpmc_options* opts, int32_t* out, lpmc_error* err);

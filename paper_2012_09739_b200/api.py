@@ -620,7 +620,8 @@ def bar_arithmetic(model: SdeModel, level: int, spec_low: PrecisionSpec,
                                          C.byref(err)), err)
     names = ["carrier", "fp32", "fp32-round", "fp64-round", "half2-ieee"]
     return {"arith": names[out.value & 0xff], "pow2_folded": bool(out.value & 0x100),
-            "native_binary16": bool(out.value & 0x200)}
+            "native_binary16": bool(out.value & 0x200),
+            "native_bfloat16": bool(out.value & 0x400)}
 
 
 def phi_inv_direct_core(v: float) -> Optional[float]:

@@ -32,7 +32,7 @@ CXX_FLAGS = ["-O2", "-ffp-contract=off", "-fno-fast-math", "-std=c++17", "-fPIC"
              "-Wextra", f"-I{CUDA_HOME}/include"]
 
 SOURCES_CU = ["lpmc_kernels.cu", "lpmc_level_carrier.cu", "lpmc_level_f32.cu",
-              "lpmc_level_f32r.cu", "lpmc_level_f64r.cu", "lpmc_level_half2.cu", "lpmc_level_h16.cu",
+              "lpmc_level_f32r.cu", "lpmc_level_f64r.cu", "lpmc_level_half2.cu", "lpmc_level_h16.cu", "lpmc_level_bf16.cu",
               "lpmc_probe.cu", "lpmc_wpp_carrier.cu", "lpmc_wpp_f32.cu", "lpmc_wpp_f32r.cu",
               "lpmc_wpp_f64r.cu"]
 SOURCES_CXX = ["lpmc_host.cpp"]

@@ -9,6 +9,7 @@
 //   MomentAccumulator add/merge     stats.hpp:15-54
 #pragma once
 
+#include <cuda_bf16.h>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
@@ -319,6 +320,7 @@ __device__ __forceinline__ float hi2(uint64_t v) {
 // or overflow); otherwise the host re-runs
 // the level in the exact kF64Round emulation.
 struct RangeNone {
+  __device__ void track(__nv_bfloat16) {}
   __device__ void track(double) {}
   __device__ void track(float) {}
   __device__ void track(__half2) {}
@@ -514,6 +516,54 @@ struct ArithHalf2 {  // native IEEE binary16, two paths per thread
   __device__ uint32_t bad(T x) const {
     const uint32_t b = *reinterpret_cast<const uint32_t*>(&x);
     return (((b & 0x7c00u) == 0x7c00u) ? 1u : 0u) | (((b & 0x7c000000u) == 0x7c000000u) ? 2u : 0u);
+  }
+};
+
+// The reference's m = 7 (bf16: RNE to 8 significant bits, unbounded exponent)
+// on NATIVE bfloat16 arithmetic: bfloat16 has fp32's exponent range, so the
+// native fp32 policies' range guard ([2^-32, 2^33) states, host-bounded
+// constants: no intermediate is subnormal or overflows) makes one
+// HMUL2.BF16 / HADD2.BF16 per reference operation exact -- no scaling, unlike
+// binary16 below -- instead of an fp32 operation plus a three-operation
+// Veltkamp split.  Production launches in the fast mode; dumps, glibc mode
+// and the warp-per-path schedule run the fp32-carried emulation
+// (ArithF32Round), which also replays suspect paths; a launch that leaves the
+// range is re-run in the binary64 emulation like the other native policies.
+struct RangeBf16 {
+  static constexpr uint32_t kLo = 0x2f80u, kHi = 0x5000u;  // 2^-32, 2^33 (top halves of fp32)
+  uint32_t worst = 0u;
+  __device__ void track(__nv_bfloat16 x) {
+    worst = max(worst, (static_cast<uint32_t>(__bfloat16_as_ushort(x)) & 0x7fffu) - kLo);
+  }
+  __device__ bool bad() const { return worst >= kHi - kLo; }
+};
+
+struct ArithBf16 {
+  using T = __nv_bfloat16;
+  using Range = RangeBf16;
+  using Replay = ArithF32Round;
+  static constexpr int NP = 1;
+  static constexpr bool kScaled = false;
+  static constexpr bool kIeee = false;
+  static constexpr bool kPair = false;
+  static constexpr bool kPow2 = true;  // native range guard: step_bar_pw is exact
+  double split64;  // 2^45 + 1: Veltkamp's splitter for R(z) in binary64
+  __device__ explicit ArithBf16(const LevelArgs&) : split64(35184372088833.0) {}
+  // constants are already rounded to 8 bits on the host: exact conversions
+  __device__ T c(double d, uint16_t) const { return __float2bfloat16_rn(static_cast<float>(d)); }
+  __device__ T zero() const { return __ushort_as_bfloat16(0u); }
+  __device__ T mul(T a, T b) const { return __hmul_rn(a, b); }
+  __device__ T add(T a, T b) const { return __hadd_rn(a, b); }
+  __device__ T sub(T a, T b) const { return __hsub_rn(a, b); }
+  // R(z) from the full binary64 value: one rounding (softfloat.hpp:69) by
+  // Veltkamp's split in binary64, then exact conversions
+  __device__ T lift(const double (&z)[1]) const {
+    const double c = __dmul_rn(z[0], split64);
+    return __float2bfloat16_rn(__double2float_rn(__dsub_rn(c, __dsub_rn(c, z[0]))));
+  }
+  __device__ double get(T x, int) const { return static_cast<double>(__bfloat162float(x)); }
+  __device__ uint32_t bad(T x) const {
+    return (__bfloat16_as_ushort(x) & 0x7f80u) == 0x7f80u ? 1u : 0u;
   }
 };
 

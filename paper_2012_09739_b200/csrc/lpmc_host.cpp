@@ -2061,7 +2061,9 @@ lpmc_status lpmc_bar_arithmetic(const lpmc_gbm* model, int32_t level, const lpmc
   A.table = s.has_table ? &kSome : nullptr;
   *out = static_cast<int32_t>(s.arith) | (A.bar_pow2 ? LPMC_ARITH_POW2_FOLDED : 0) |
          (s.arith == BarArith::kF32Round && use_native_half(A, kahan != 0, false)
-              ? LPMC_ARITH_NATIVE_BINARY16 : 0);
+              ? LPMC_ARITH_NATIVE_BINARY16 : 0) |
+         (s.arith == BarArith::kF32Round && use_native_bf16(A, false) ? LPMC_ARITH_NATIVE_BFLOAT16
+                                                                      : 0);
   return ok(err);
 }
 

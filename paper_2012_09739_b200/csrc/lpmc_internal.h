@@ -121,6 +121,13 @@ inline bool use_native_half(const LevelArgs& A, bool kahan, bool dump) {
          (A.table == nullptr || (A.dyadic != 0 && A.table_simple != 0 && A.degree == 1));
 }
 
+// Production launches of the m = 7 emulation that run on native bfloat16
+// (dev::ArithBf16): fast exact Gaussians, no dump.  bfloat16 has fp32's
+// exponent range, so the native fp32 range guard is the whole condition.
+inline bool use_native_bf16(const LevelArgs& A, bool dump) {
+  return A.mantissa_bits == 7 && !dump && A.exact_z == 0 && A.legs != 1;
+}
+
 struct LaunchResult {
   int cuda_error;  // cudaError_t
   int kernels;     // kernels enqueued
@@ -170,13 +177,15 @@ cudaError_t launch_level_f32(const LevelArgs& A, bool kahan, bool dump, void* st
 cudaError_t launch_level_f32r(const LevelArgs& A, bool kahan, bool dump, void* stream);
 cudaError_t launch_level_f64r(const LevelArgs& A, bool kahan, bool dump, void* stream);
 cudaError_t launch_level_half2(const LevelArgs& A, bool kahan, bool dump, void* stream);
-cudaError_t launch_level_h16(const LevelArgs& A, bool kahan, void* stream);  // dev::ArithHalfScaled
+cudaError_t launch_level_h16(const LevelArgs& A, bool kahan, void* stream);
+cudaError_t launch_level_bf16(const LevelArgs& A, bool kahan, void* stream);  // dev::ArithBf16  // dev::ArithHalfScaled
 cudaError_t configure_level_carrier();
 cudaError_t configure_level_f32();
 cudaError_t configure_level_f32r();
 cudaError_t configure_level_f64r();
 cudaError_t configure_level_half2();
 cudaError_t configure_level_h16();
+cudaError_t configure_level_bf16();
 cudaError_t configure_probe();
 // warp-per-path instances (lpmc_wpp_*.cu; NP == 1 arithmetics)
 cudaError_t launch_wpp_carrier(const LevelArgs& A, bool kahan, void* stream);

@@ -259,6 +259,7 @@ int configure_kernels() {
   if (e == cudaSuccess) e = configure_level_f64r();
   if (e == cudaSuccess) e = configure_level_half2();
   if (e == cudaSuccess) e = configure_level_h16();
+  if (e == cudaSuccess) e = configure_level_bf16();
   if (e == cudaSuccess) e = configure_probe();
   if (e == cudaSuccess) e = configure_wpp_carrier();
   if (e == cudaSuccess) e = configure_wpp_f32();
@@ -300,6 +301,8 @@ LaunchResult launch_paths(const LevelArgs& A, BarArith arith, bool kahan, bool d
       // emulation, which also replays the paths that leave the native guard
       if (use_native_half(A, kahan, dump) && std::getenv("LPMC_NO_NATIVE_HALF") == nullptr) {
         e = launch_level_h16(A, kahan, stream);
+      } else if (use_native_bf16(A, dump) && std::getenv("LPMC_NO_NATIVE_BF16") == nullptr) {
+        e = launch_level_bf16(A, kahan, stream);  // m = 7 on native bfloat16 (dev::ArithBf16)
       } else {
         e = launch_level_f32r(A, kahan, dump, stream);
       }
