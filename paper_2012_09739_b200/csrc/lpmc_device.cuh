@@ -338,15 +338,30 @@ struct RangeF32 {
   __device__ bool bad() const { return worst >= kHi - kLo; }
 };
 
+// Guard of the folded binary64 legs (step_hat_pw, and step_bar_pw on the
+// carrier arithmetic): |x| in [2^-300, 2^300] <=> (high word of |x|) - hw(2^-300) < hw(2^300) -
+// hw(2^-300) unsigned; zero, subnormal and non-finite values are outside.
+struct RangeF64 {
+  static constexpr uint32_t kLo = (1023u - 300u) << 20, kHi = (1023u + 300u) << 20;
+  uint32_t worst = 0u;
+  __device__ void track(double x) {
+    worst = max(worst, (static_cast<uint32_t>(__double2hiint(x)) & 0x7fffffffu) - kLo);
+  }
+  __device__ bool bad() const { return worst >= kHi - kLo; }
+};
+
 struct ArithCarrier {  // m >= 52
   using T = double;
-  using Range = RangeNone;
+  using Range = RangeF64;  // only the folded instances (PW) depend on it
   static constexpr int NP = 1;
   static constexpr bool kScaled = false;  // see ArithHalfScaled
   using Replay = ArithCarrier;
+  static constexpr bool kRangeReplays = true;  // a path outside the guard is replayed (else: the launch is re-run)
   static constexpr bool kIeee = false;
   static constexpr bool kPair = false;  // no packed fp32 pairs (see ArithF32)
-  static constexpr bool kPow2 = false;  // no power-of-two step folding (see step_bar_pw)
+  // power-of-two step folding like the carrier (hat) legs: exact inside
+  // RangeF64, checked on every state update; a path outside is replayed
+  static constexpr bool kPow2 = true;
   __device__ explicit ArithCarrier(const LevelArgs&) {}
   __device__ T c(double d, uint16_t) const { return d; }
   __device__ T zero() const { return 0.0; }
@@ -364,6 +379,7 @@ struct ArithF32 {  // m == 23, native
   static constexpr int NP = 1;
   static constexpr bool kScaled = false;  // see ArithHalfScaled
   using Replay = ArithF32;
+  static constexpr bool kRangeReplays = false;  // a path outside the guard is replayed (else: the launch is re-run)
   static constexpr bool kIeee = false;
   // mul2: two independent products of one leg step in one FFMA2 (bitwise
   // the two scalar products)
@@ -396,6 +412,7 @@ struct ArithF32Round {  // m <= 10: fp32 op (correctly rounded), then RNE to m+1
   static constexpr int NP = 1;
   static constexpr bool kScaled = false;  // see ArithHalfScaled
   using Replay = ArithF32Round;
+  static constexpr bool kRangeReplays = false;  // a path outside the guard is replayed (else: the launch is re-run)
   static constexpr bool kIeee = false;
   uint32_t d, half_m1, keep;
   uint32_t d64;
@@ -469,6 +486,7 @@ struct ArithF64Round {  // any m < 52: binary64 op, then integer RNE (exact emul
   static constexpr int NP = 1;
   static constexpr bool kScaled = false;  // see ArithHalfScaled
   using Replay = ArithF64Round;
+  static constexpr bool kRangeReplays = false;  // a path outside the guard is replayed (else: the launch is re-run)
   static constexpr bool kIeee = false;
   static constexpr bool kPair = false;
   static constexpr bool kPow2 = false;
@@ -495,6 +513,7 @@ struct ArithHalf2 {  // native IEEE binary16, two paths per thread
   static constexpr int NP = 2;
   static constexpr bool kScaled = false;  // see ArithHalfScaled
   using Replay = ArithHalf2;
+  static constexpr bool kRangeReplays = false;  // a path outside the guard is replayed (else: the launch is re-run)
   static constexpr bool kIeee = true;
   static constexpr bool kPair = false;  // already two paths per half2 op
   static constexpr bool kPow2 = false;
@@ -544,6 +563,7 @@ struct ArithBf16 {
   using Replay = ArithF32Round;
   static constexpr int NP = 1;
   static constexpr bool kScaled = false;
+  static constexpr bool kRangeReplays = false;  // a path outside the guard is replayed (else: the launch is re-run)
   static constexpr bool kIeee = false;
   static constexpr bool kPair = false;
   static constexpr bool kPow2 = true;  // native range guard: step_bar_pw is exact
@@ -642,6 +662,7 @@ struct ArithHalfScaled {
   using Replay = ArithF32Round;
   static constexpr int NP = 1;
   static constexpr bool kScaled = true;
+  static constexpr bool kRangeReplays = true;  // a path outside the guard is replayed (else: the launch is re-run)
   static constexpr bool kIeee = false;
   static constexpr bool kPair = false;
   static constexpr bool kPow2 = true;  // PW instances fold the carrier legs (step_hat_pw)

@@ -535,8 +535,12 @@ lpmc_status build_spec(const lpmc_gbm* model, int32_t level, const lpmc_precisio
                       mid_range(A.sigma) && std::fabs(A.mu * A.dtc) <= 0x1p10 &&
                       std::fabs(A.sigma * A.sdtf) <= 0x1p10 && mid_range(A.mu * A.dtf) &&
                       mid_range(A.sigma * A.sdtf);
-  if ((s.arith == BarArith::kF32 || s.arith == BarArith::kF32Round) && pow2(low[3]) &&
-      pow2(low[4]) && pow2(low[5]) && hat_ok) {
+  // (binary64 bar legs -- the carrier arithmetic -- fold under the same proof)
+  const bool carrier_ok = s.arith == BarArith::kCarrier && mid_range(low[0]) &&
+                          mid_range(low[1]) && mid_range(low[2]) && low[2] != 0.0 &&
+                          mid_range(low[0] * low[3]) && mid_range(low[1] * low[4]);
+  if ((s.arith == BarArith::kF32 || s.arith == BarArith::kF32Round || carrier_ok) &&
+      pow2(low[3]) && pow2(low[4]) && pow2(low[5]) && hat_ok) {
     A.bar_pow2 = 1;
     A.mu_dtf_l = low[0] * low[3];  // exact: a power-of-two scaling
     A.mu_dtc_l = low[0] * low[5];

@@ -386,17 +386,6 @@ __device__ __forceinline__ void step_hat_pw(double (&x)[NP], double mu_dt, doubl
   }
 }
 
-// |x| in [2^-300, 2^300] <=> (high word of |x|) - hw(2^-300) < hw(2^300) -
-// hw(2^-300) unsigned; zero, subnormal and non-finite values are outside.
-struct RangeF64 {
-  static constexpr uint32_t kLo = (1023u - 300u) << 20, kHi = (1023u + 300u) << 20;
-  uint32_t worst = 0u;
-  __device__ void track(double x) {
-    worst = max(worst, (static_cast<uint32_t>(__double2hiint(x)) & 0x7fffffffu) - kLo);
-  }
-  __device__ bool bad() const { return worst >= kHi - kLo; }
-};
-
 // em_step / em_step_kahan and the _dw forms (sde.hpp:60-116), bar precision
 template <class Arith, bool KAHAN, bool CHECKED>
 __device__ __forceinline__ void step_bar(const Arith& ar, typename Arith::Range& range,
@@ -475,7 +464,10 @@ __device__ __forceinline__ void step_bar_pw(const Arith& ar, typename Arith::Ran
   } else {
     x = ar.add(xp, inc);
   }
-  range.track(x);
+  // the binary64 (carrier) legs are checked once per coarse step, like the
+  // hat legs (RangeF64's argument); the native fp32 / bfloat16 legs on every
+  // update
+  if constexpr (!Arith::kRangeReplays) range.track(x);
 }
 
 // One coarse step of both bar legs with packed fp32 pairs (Arith::kPair):
@@ -559,6 +551,11 @@ __device__ __forceinline__ void simulate(const LevelArgs& A, const TableView& ta
   FastTab lt{};
   if constexpr (kNeedExact && ZM == kZFast) lt = fast_tab(s_math);
   typename Arith::Range range;
+  // The carrier arithmetic needs its guard only where steps are folded
+  // (step_bar_pw); its unfolded steps track into an object nobody reads.
+  typename Arith::Range range_unread;
+  typename Arith::Range& unfolded_range =
+      (Arith::kRangeReplays && !Arith::kScaled) ? range_unread : range;
   uint64_t kc[NP];
   bool u1[NP];
   uint32_t lomin[NP];
@@ -601,7 +598,7 @@ __device__ __forceinline__ void simulate(const LevelArgs& A, const TableView& ta
     } else if constexpr (kPw) {
       step_bar_pw<Arith, KAHAN>(ar, range, xbf, cmpf, mu_dtf, sg_sdt, zb);
     } else {
-      step_bar<Arith, KAHAN, CHECKED>(ar, range, xbf, cmpf, mu_l, sg_l, dtf_l, sdtf_l, zb, true,
+      step_bar<Arith, KAHAN, CHECKED>(ar, unfolded_range, xbf, cmpf, mu_l, sg_l, dtf_l, sdtf_l, zb, true,
                                       fk, n, kStageBarFine);
     }
   };
@@ -625,6 +622,10 @@ __device__ __forceinline__ void simulate(const LevelArgs& A, const TableView& ta
 #pragma unroll
       for (int p = 0; p < NP; ++p) hrange[p].track(xhf[p]);
     }
+    if constexpr (kBar && kPw && Arith::kRangeReplays && !Arith::kScaled) {
+      range.track(xbf);  // folded binary64 bar legs: the same guard, the same cadence
+      if constexpr (!kFineOnly) range.track(xbc);
+    }
     if constexpr (kBar && !kFineOnly && Arith::kScaled) {
       // both bar legs were stepped as one pair in coarse_step below
     } else if constexpr (kBar && !kFineOnly && kPw) {
@@ -637,7 +638,7 @@ __device__ __forceinline__ void simulate(const LevelArgs& A, const TableView& ta
       } else {
         dw = ar.add(ar.mul(sdtf_l, zb0), ar.mul(sdtf_l, zb1));
       }
-      step_bar<Arith, KAHAN, CHECKED>(ar, range, xbc, cmpc, mu_l, sg_l, dtc_l, sdtf_l, dw, false,
+      step_bar<Arith, KAHAN, CHECKED>(ar, unfolded_range, xbc, cmpc, mu_l, sg_l, dtc_l, sdtf_l, dw, false,
                                       fk, n, kStageBarCoarse);
     }
   };
@@ -798,7 +799,7 @@ __device__ __forceinline__ void simulate(const LevelArgs& A, const TableView& ta
     const bool hat_bad = kHat && (nonfinite64(R.hf[p]) || nonfinite64(R.hc[p]));
     const bool hat_range = kHat && kPw && A.level > 0 && hrange[p].bad();
     // native binary16: a path outside the guard is replayed in the emulation
-    const bool bar_range = Arith::kScaled && kBar && range.bad();
+    const bool bar_range = Arith::kRangeReplays && kBar && range.bad();
     // the low-word prefilter fired (2^-31 per draw): regenerate the path's
     // draws (RNG only, ~1/20 of a checked replay) and replay only if one of
     // them really is u == 1 or u == 1/2 -- at level 16 and above the filter's
@@ -822,7 +823,7 @@ __device__ __forceinline__ void simulate(const LevelArgs& A, const TableView& ta
     }
 #endif
   }
-  R.range_bad = Arith::kScaled ? false : range.bad();
+  R.range_bad = Arith::kRangeReplays ? false : range.bad();
 }
 
 // Exact replay of this thread's paths (only for suspects: a u == 1 or
@@ -968,7 +969,7 @@ __global__ void __launch_bounds__(level_threads<Arith, LEGS, TAB, ZM>(), level_c
     printf("replay path %llu batch %llu\n", static_cast<unsigned long long>(local[0]),
            static_cast<unsigned long long>(slot_b));
 #endif
-    const bool range_bad = R.range_bad;
+    const bool range_bad = R.range_bad;  // (false for the arithmetics whose guards replay)
     replay_checked<typename Arith::Replay, KAHAN, LEGS, TAB, ZM>(A, tab, s_math, local, valid, R);
     R.range_bad |= range_bad;
 #pragma unroll
@@ -1192,7 +1193,8 @@ constexpr int kMaxDynSmem = (kTableRows * kMaxTableK + 1) * 8;  // + 1 / step_w
 // (non-dump) fast-mode launches of the native fp32 arithmetics with bar legs.
 template <class Arith, int LEGS, bool DUMP, int ZM>
 constexpr bool has_pw() {
-  return Arith::kPow2 && !DUMP && ZM == kZFast && LEGS != 1;
+  // hat-only launches (LEGS == 1) exist for the carrier arithmetic only
+  return Arith::kPow2 && !DUMP && ZM == kZFast && (LEGS != 1 || Arith::kRangeReplays);
 }
 
 // SMs of the current device (cached per device ordinal).
@@ -1318,8 +1320,15 @@ cudaError_t configure_one() {
 template <class Arith, bool DUMP>
 cudaError_t configure_hat_only() {
   if constexpr (level_persistent<1, kTabNone, kZFast>()) {
-    return cudaFuncSetAttribute(level_kernel<Arith, false, 1, kTabNone, DUMP, kZFast>,
-                                cudaFuncAttributeMaxDynamicSharedMemorySize, kFastWords * 8);
+    cudaError_t e = cudaFuncSetAttribute(level_kernel<Arith, false, 1, kTabNone, DUMP, kZFast>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         kFastWords * 8);
+    if constexpr (has_pw<Arith, 1, DUMP, kZFast>()) {
+      if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(level_kernel<Arith, false, 1, kTabNone, DUMP, kZFast, true>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, kFastWords * 8);
+    }
+    return e;
   } else {
     return cudaSuccess;
   }

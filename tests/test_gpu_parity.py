@@ -274,7 +274,9 @@ def test_moments_bitexact_on_device_paths(gpu, oracle, level, m, approx, kahan, 
 @pytest.mark.parametrize("level", [2, 4, 6, 12])
 @pytest.mark.parametrize("m,approx,kahan", [(23, "linear:16", False), (23, "linear:16", True),
                                              (10, "linear:16", False), (10, "cubic:64", True),
-                                             (10, "exact", False), (23, "exact", True)])
+                                             (10, "exact", False), (23, "exact", True),
+                                             (52, "linear:16", False), (52, "cubic:64", True),
+                                             (52, "exact", False)])
 @pytest.mark.parametrize("legs,payoff", [("all", "call"), ("bar", "terminal"),
                                          ("fine", "terminal")])
 def test_pow2_step_folding_bitexact(gpu, oracle, level, m, approx, kahan, legs, payoff):
@@ -307,8 +309,29 @@ def test_pow2_step_folding_bitexact(gpu, oracle, level, m, approx, kahan, legs, 
         assert [got.d_hat.state(), got.d_bar.state(), got.d_four.state()] == want, horizon
 
 
+@pytest.mark.parametrize("level", [0, 2, 6, 12])
+def test_pow2_step_folding_hat_only(gpu, oracle, level):
+    """BASELINE config 1's shape (carrier legs only, exact Gaussians): the
+    production launch folds the power-of-two steps (step_hat_pw), the dump
+    kernel does not; its per-path values reduced by the restated tree must
+    equal the production moments bitwise, and a horizon of 0.75 takes the
+    unfolded kernel as a control."""
+    n = 3000 if level < 12 else 600
+    for horizon in (1.0, 0.75):
+        model = gpu.make_gbm(0.05, 0.2, 1.0, horizon)
+        sp = gpu.PrecisionSpec(52, False)
+        assert gpu.api.bar_arithmetic(model, level, sp, None, False,
+                                      legs="hat")["pow2_folded"] == (horizon == 1.0 and
+                                                                     level % 2 == 0)
+        out = gpu.simulate_paths(model, level, sp, None, False, n, 5, level << 40, legs="hat")
+        dh = out[:, 0] - (out[:, 1] if level > 0 else 0.0)
+        got = gpu.run_coupled_paths(model, level, sp, None, False, n, 5, level << 40, legs="hat")
+        want = oracle.tree_from_values(dh, np.zeros_like(dh), legs=1)
+        assert [got.d_hat.state(), got.d_bar.state(), got.d_four.state()] == want, horizon
+
+
 @pytest.mark.parametrize("level", [2, 6])
-@pytest.mark.parametrize("m", [23, 10])
+@pytest.mark.parametrize("m", [23, 10, 52])
 def test_pow2_step_folding_sign_changes(gpu, oracle, level, m):
     """Power-of-two step folding (step_bar_pw, step_hat_pw) with sigma = 3:
     states change sign and magnitude by orders of magnitude within a path;
