@@ -12,6 +12,7 @@
 #include <algorithm>
 #include <array>
 #include <cmath>
+#include <cstdlib>
 #include <cstdint>
 #include <cstdio>
 #include <cstring>
@@ -549,6 +550,8 @@ lpmc_status build_spec(const lpmc_gbm* model, int32_t level, const lpmc_precisio
     A.hat_mu_dtc = A.mu * A.dtc;
     A.hat_sg_sdt = A.sigma * A.sdtf;
   }
+  // A/B and stress checks (tools/stress_native.py): the unfolded kernels
+  if (A.bar_pow2 != 0 && std::getenv("LPMC_NO_POW2") != nullptr) A.bar_pow2 = 0;
   // m = 10 on native binary16 with static power-of-two scales
   // (dev::ArithHalfScaled): dt and 2dt powers of two, every mantissa and
   // scale factor an exact binary16 number, P1 = 4 by the choice of kz, the
