@@ -8,7 +8,7 @@ Workload (BASELINE.json configs[3], "C4" -- the largest single-GPU config):
 nested-MLMC four-way difference P_f,exact - P_c,exact - P_f,approx + P_c,approx
 for GBM dS = 0.05 S dt + 0.2 S dW, S0 = 1, T = 1, European call payoff
 max(S_T - 1, 0); exact Gaussians in fp64 (hat legs) and approximate ones
-(linear:16 table) in the reference's fp16 (m = 10, emulated) and fp32 (bar
+(linear:16 table) in the reference's fp16 (m = 10 semantics, run on native binary16) and fp32 (bar
 legs); levels 0..12; 2^24 paths per level per GPU (weak scaling; --scaling
 strong keeps 2^24 paths per level in total; --paths changes either).  Every path runs all four
 coupled legs and all three moment families (estimate_level_stats semantics,
@@ -51,7 +51,7 @@ STRIKE = 1.0
 APPROX = "linear:16"
 WORKLOAD = ("BASELINE config 4: nested-MLMC 4-way difference, GBM(mu=0.05, sigma=0.2, S0=1, T=1), "
             "European call payoff max(S_T-1,0), exact fp64 Gaussians + linear:16 approximate "
-            "Gaussians in fp16 (reference m=10 emulation) and fp32, no Kahan, levels 0..12, "
+            "Gaussians in fp16 (the reference's m=10 semantics) and fp32, no Kahan, levels 0..12, "
             "2^24 paths per level, all four coupled legs -> d_hat, d_bar, d_four moments")
 DEMANDS = os.path.join(ROOT, "profiles", "r02_c4_l12_demands.json")
 CPU_SAMPLE = 1 << 15  # >= 256 paths x threads x 8 at 16 threads
@@ -508,7 +508,7 @@ def main():
            "data": "synthetic (seeded counter-based RNG; no dataset)",
            "config": {"workload": WORKLOAD,
                       "paths_per_level": n_total, "paths_per_level_per_gpu": n_local,
-                      "levels": "0..12", "precisions": ["fp16 (m=10, reference emulation)", "fp32"],
+                      "levels": "0..12", "precisions": ["fp16 (the reference's m=10 semantics, on native binary16 with static scales)", "fp32"],
                       "kahan": False, "approx": APPROX, "payoff": "call, strike 1",
                       "legs": "all", "reduce": "tree",
                       "path_bases": "fp16: l<<40, fp32: l<<40 | 2<<36 (experiments.hpp:185-194)",
