@@ -32,6 +32,11 @@
  *   lpmc_step_error_probe       <- step_error_probe        include/lpmc/sde.hpp:297-344
  *   lpmc_density_histogram      <- the histogram loop of run_density_report
  *                                  include/lpmc/experiments.hpp:276-285
+ * Diagnostics without a reference counterpart: lpmc_bar_arithmetic (which
+ * arithmetic a run's low-precision legs use: native fp32 / bfloat16 /
+ * binary16, fp32- or binary64-carried rounding -- all bitwise
+ * softfloat.hpp:69-111), lpmc_device_math, lpmc_erfc_core,
+ * lpmc_phi_inv_direct_core, lpmc_glibc_math, lpmc_measure_pipe_peaks.
  *
  * Error contract: every entry point returns an lpmc_status.  The values map
  * one-to-one onto the exception types the reference throws
