@@ -107,3 +107,39 @@ def test_direct_table_edges(lib):
             if below < 2.0 ** -15:
                 continue
             assert lib.api.phi_inv_direct_core(below) <= lib.api.phi_inv_direct_core(a)
+
+
+# ---- index arithmetic of the level kernel's dyadic-table lookup -------------
+def test_reversed_dyadic_index_matches_reference_index():
+    """approx_inv_up (lpmc_device.cuh) reads record r = e' - 969 of a reversed
+    table copy, e' the biased exponent of (1 - 2^-53) - u', with an unsigned
+    minimum at 53; record r <= 52 holds interval j = 52 - r.  For every
+    reflected draw u' in [1/2, 1] on the 2^-53 grid this must be the
+    reference's j = floor(-log2(1 - u')) - 1 (invcdf_approx.hpp:52-66), with
+    v = 0 and v = 2^-53 landing on tail records.  Checked at every binade
+    edge +-48 grid steps and on random grid points (numpy bit arithmetic, the
+    same operations as the device's)."""
+    g = 2.0 ** -53
+    pts = [0.5, 1.0, 1.0 - g, 1.0 - 2 * g]
+    for k in range(1, 53):
+        edge = 1.0 - 2.0 ** -k  # u' where v = 2^-k exactly
+        pts += [edge + i * g for i in range(-48, 49) if 0.5 <= edge + i * g <= 1.0]
+    rng = np.random.default_rng(17)
+    pts += list(0.5 + rng.integers(0, 1 << 52, 20000).astype(np.float64) * g)
+    up = np.array(pts, dtype=np.float64)
+    vm = np.float64(1.0 - g) - up  # exact: both on the 2^-53 grid
+    hi = (vm.view(np.uint64) >> np.uint64(32)).astype(np.uint64)
+    r = np.minimum(((hi >> np.uint64(20)) - np.uint64(969)) & np.uint64(0xFFFFFFFF), np.uint64(53))
+    v = 1.0 - up  # exact
+    for ri, vi in zip(r.tolist(), v.tolist()):
+        if vi == 0.0:
+            assert ri == 53  # u' == 1: a tail record (the sign bit of vm wraps the index)
+            continue
+        m, e = math.frexp(vi)  # vi = m 2^e, m in [1/2, 1)
+        fl = -e + 1 if m == 0.5 else -e  # floor(-log2 v)
+        j = fl - 1
+        assert 0 <= j <= 52
+        if vi == g:  # vm == 0: exponent field 0 wraps onto record 53, a copy of j = 52 (tail)
+            assert j == 52 and ri == 53
+            continue
+        assert ri == 52 - j, (vi, ri, j)
